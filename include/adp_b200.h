@@ -1,0 +1,185 @@
+/*
+ * adp_b200.h — C ABI of the B200-native MAID hot path.
+ *
+ * Drop-in boundary for the reference package `adp` (arxiv 2502.09758,
+ * /root/reference/pkg/src/adp).  The reference is pure Python/NumPy with no
+ * FFI; its seams are Python functions.  Each entry point
+ * below replaces the NumPy/SciPy arithmetic behind one of those functions;
+ * the Python package `paper_2502_09758_b200` binds them with ctypes and
+ * keeps the reference's Python signatures, return types and exceptions.
+ *
+ * Conventions
+ *   - All array pointers are DEVICE pointers owned by the caller, C-order,
+ *     element type given by the plan (float64, or float32 in fp32 mode).
+ *     Images are (H, W, C); dense 1-D signals are (n,), dense kernels (n, n).
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).
+ *   - Scalar results are written to HOST memory; calls that return scalars
+ *     synchronise `stream` before returning.
+ *   - Return value: ADP_OK or a negative ADP_ERR_* code; adp_last_error()
+ *     gives a message.  Numerical failures are reported through the result
+ *     structs (status field), mirroring SolveDiverged / NegativeCurvatureError.
+ *   - A plan owns its device workspace (allocated once at creation; no
+ *     allocation in any hot call) and is not thread-safe: use one plan per
+ *     concurrent stream.
+ */
+#ifndef ADP_B200_H
+#define ADP_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ADP_OK 0
+#define ADP_ERR_ARG (-1)
+#define ADP_ERR_CUDA (-2)
+#define ADP_ERR_UNSUPPORTED (-3)
+
+#define ADP_LAYOUT_DEPTHWISE2D 0 /* operators.py:18, ConvOperator 83-122 */
+#define ADP_LAYOUT_DENSE1D 1     /* operators.py:17, DenseOperator 49-80 */
+
+#define ADP_DTYPE_F64 0
+#define ADP_DTYPE_F32 1
+
+#define ADP_MODE_STRICT 0 /* bitwise reference arithmetic order (f64) */
+#define ADP_MODE_FAST 1   /* FMA stencils */
+
+#define ADP_REG_TV 0      /* SmoothedTV, regularizers.py:137-199 */
+#define ADP_REG_ELASTIC 1 /* SmoothedElasticNet, regularizers.py:75-134 */
+
+#define ADP_METHOD_PROXGRAD 0 /* lower_solvers.py:154-167 */
+#define ADP_METHOD_AGD 1      /* lower_solvers.py:180-213 */
+#define ADP_METHOD_FISTA_SC 2
+
+#define ADP_STATUS_OK 0
+#define ADP_STATUS_DIVERGED 1  /* SolveDiverged("... at lower iteration t") */
+#define ADP_STATUS_BT_FAIL 2   /* SolveDiverged("backtracking line search failed ...") */
+#define ADP_STATUS_NEGCURV 3   /* NegativeCurvatureError */
+
+typedef struct adp_plan adp_plan;
+
+typedef struct {
+  int32_t layout; /* ADP_LAYOUT_* */
+  int32_t dtype;  /* ADP_DTYPE_* */
+  int32_t mode;   /* ADP_MODE_* */
+  int32_t H, W, C; /* depthwise2d image; dense1d: H = 1, W = n, C = 1 */
+  int32_t kh, kw;  /* stencil size (odd); dense1d: kh = kw = n */
+  int32_t tile_h, tile_w; /* 0 = auto */
+} adp_plan_desc;
+
+/* Lower problem h(x, b) = ||B_b x - y||^2 + alpha J(x) (lower_solvers.py:20-25) */
+typedef struct {
+  const void* kernel; /* B_b: (kh, kw, C) stencil or (n, n) matrix */
+  const void* y;      /* lower-level data */
+  double alpha;
+  int32_t reg;        /* ADP_REG_* */
+  double nu, l1, l2;  /* TV: nu; elastic net: l1, l2, nu */
+} adp_lower;
+
+/* solve_lower arguments (lower_solvers.py:104-113) */
+typedef struct {
+  double eps, mu;
+  int32_t max_iters;
+  int32_t method;       /* ADP_METHOD_* */
+  int32_t adaptive;
+  double step_size;     /* <= 0: None (use 1 / L_of_b) */
+  double norm_sq;       /* >= 0: cached op_norm_sq (op._norm_sq); < 0: compute */
+  int32_t norm_max_iters; /* L_of_b: 300 */
+  double norm_tol;        /* L_of_b: 1e-4 */
+  const void* v0;       /* power-iteration start vector (un-normalised), device */
+} adp_solve_args;
+
+typedef struct {
+  double norm_sq;       /* op_norm_sq used (computed or cached) */
+  double lip;
+  double grad_norm;
+  double value;
+  int32_t iters;
+  int32_t converged;
+  int32_t status;       /* ADP_STATUS_* */
+  int32_t fail_iter;
+  int32_t power_iters;
+  int32_t power_converged;
+  int64_t vg_evals, value_evals, restarts;
+} adp_solve_result;
+
+typedef struct {
+  double residual;
+  double curv;
+  int32_t iters;
+  int32_t converged;
+  int32_t status;
+  int32_t hv;
+} adp_cg_result;
+
+/* ---- plans ---- */
+int adp_plan_create(adp_plan** out, const adp_plan_desc* desc);
+void adp_plan_destroy(adp_plan* plan);
+size_t adp_plan_workspace_bytes(const adp_plan* plan);
+const char* adp_last_error(void);
+int adp_device_info(int* sm_count, int* cc_major, int* cc_minor);
+
+/* ---- operators (operators.py) ---- */
+/* ConvOperator.apply / DenseOperator.apply: out = B x      (operators.py:70-74, 108-112) */
+int adp_apply(adp_plan* p, const void* kernel, const void* x, void* out, void* stream);
+/* adjoint: out = B^T y                                      (operators.py:76-80, 114-118) */
+int adp_adjoint(adp_plan* p, const void* kernel, const void* y, void* out, void* stream);
+/* gram_diag: diag(B^T B)                                    (operators.py:66-68, 120-122) */
+int adp_gram_diag(adp_plan* p, const void* kernel, void* out, void* stream);
+/* op_norm_sq: power iteration on B^T B                      (operators.py:137-173) */
+int adp_op_norm_sq(adp_plan* p, const void* kernel, const void* v0, int32_t max_iters, double tol,
+                   double* lam, int32_t* converged, int32_t* iters, void* stream);
+/* kernel_gram_correlation: out (kernel-shaped) = kgc(x, v)  (operators.py:198-220) */
+int adp_kgc(adp_plan* p, const void* x, const void* v, void* out, void* stream);
+
+/* ---- lower level (lower_solvers.py) ---- */
+int adp_lower_value(adp_plan* p, const adp_lower* lp, const void* x, double* value, void* stream);          /* :37-39 */
+int adp_lower_value_and_grad(adp_plan* p, const adp_lower* lp, const void* x, double* value, void* g,
+                             void* stream);                                                              /* :50-63 */
+int adp_lower_grad(adp_plan* p, const adp_lower* lp, const void* x, void* g, void* stream);                /* :42-47 */
+int adp_lower_hess_vec(adp_plan* p, const adp_lower* lp, const void* x, const void* v, void* out,
+                       void* stream);                                                                    /* :66-71 */
+int adp_lower_hess_diag(adp_plan* p, const adp_lower* lp, const void* x, void* out, void* stream);         /* :74-80 */
+/* solve_lower -> _gradient_descent / _accelerated, one persistent launch  (:104-213) */
+int adp_lower_solve(adp_plan* p, const adp_lower* lp, const void* x0, void* x_out, const adp_solve_args* args,
+                    adp_solve_result* res, void* stream);
+
+/* ---- hypergradient (hypergradient.py) ---- */
+/* cg_solve specialised to the lower Hessian at x_tilde with Jacobi preconditioner
+ * lower_hess_diag (computed inside when precond == NULL); q in/out, warm start if warm != 0
+ * (hypergradient.py:35-84 as called at 171-176) */
+int adp_hess_cg(adp_plan* p, const adp_lower* lp, const void* x_tilde, const void* rhs, void* q, int32_t warm,
+                const void* precond, double tol, int32_t max_iters, adp_cg_result* res, void* stream);
+/* mixed_second_transpose: out = 2 [kgc(x~, B q) + kgc(q, B x~ - y)]   (hypergradient.py:92-104) */
+int adp_mixed_T(adp_plan* p, const adp_lower* lp, const void* x_tilde, const void* q, void* out, void* stream);
+/* UpperProblem.fit_value (problems.py:48-50) and ||upper_fit_grad|| (hypergradient.py:87-89);
+ * grad_out may be NULL */
+int adp_upper_terms(adp_plan* p, const void* A_kernel, const void* x, const void* y_delta, double* fit,
+                    double* grad_norm, void* grad_out, void* stream);
+/* ---- regularizer alone (regularizers.py SmoothedTV / SmoothedElasticNet methods) ----
+ * op: 0 value (tv_value / ElasticNet.value), 1 value_and_grad (value -> *value, grad -> out),
+ *     2 grad, 3 hess_vec(x, v), 4 hess_diag(x).  reg->kernel, reg->y, reg->alpha are ignored. */
+int adp_reg_op(adp_plan* p, const adp_lower* reg, int32_t op, const void* x, const void* v, void* out,
+               double* value, void* stream);
+/* ddot-type inner product with the plan's fixed reduction tree (np.vdot sites) */
+int adp_dot(adp_plan* p, const void* a, const void* b, double* out, void* stream);
+
+/* ---- plan-free vector primitives (generic cg_solve with a caller-supplied hess_vec) ----
+ * op 0: out = x + a*y   1: out = x - a*y   2: out = x*y   3: out = 1/x   4: out = x - y   5: out = x
+ * op 10: *red_out = <x, y> (fixed-order tree)   11: *red_out = count(x <= 0) */
+int adp_vec(int32_t op, int64_t n, int32_t dtype, double a, const void* x, const void* y, void* out,
+            double* red_out, void* stream);
+
+/* ---- host-only introspection (no device): the deterministic-sum layout for n
+ * elements (np_rule = 1: NumPy pairwise leaves of <= 128; 0: binary over n items):
+ * leaf starts, subtree cut and the tree programs the kernels evaluate. */
+int adp_sum_layout(int64_t n, int32_t np_rule, int64_t* n_leaves, int32_t* n_sub, int32_t* top_prog,
+                   int64_t* leaf_start, int64_t leaf_cap, int32_t* sub_leaf, int32_t* sub_prog, int64_t sub_cap,
+                   int32_t* words, int64_t words_cap, int64_t* n_words);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ADP_B200_H */

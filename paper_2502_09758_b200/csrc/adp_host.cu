@@ -1,0 +1,820 @@
+// Host runtime of the B200 MAID engine: plan creation (tile geometry,
+// workspace, deterministic-sum programs), cooperative launches and the
+// extern "C" ABI declared in include/adp_b200.h.
+#include <cuda_runtime.h>
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <functional>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "adp_plan.h"
+#include "conv2d_args.h"
+#include "dense1d_args.h"
+
+namespace adp {
+
+static thread_local std::string g_err;
+static int fail(int code, const std::string& m) {
+  g_err = m;
+  return code;
+}
+int dense_fail(int code, const char* m) { return fail(code, m); }
+#define CK(x)                                                                                   \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess) return fail(ADP_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// Tree programs.
+//   numpy rule (np == true): leaf if n <= 128, else split at
+//     n2 = n/2 - (n/2) % 8       (numpy pairwise_sum, PW_BLOCKSIZE = 128)
+//   binary rule: leaf if n <= 1, else split at n/2.
+static bool is_leaf(bool np, int64_t n) { return np ? n <= 128 : n <= 1; }
+static int64_t split_at(bool np, int64_t n) {
+  if (np) {
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    return n2;
+  }
+  return n / 2;
+}
+
+struct LeafCounter {
+  bool np;
+  std::map<int64_t, int64_t> memo;
+  int64_t operator()(int64_t n) {
+    if (is_leaf(np, n)) return 1;
+    auto it = memo.find(n);
+    if (it != memo.end()) return it->second;
+    const int64_t a = split_at(np, n);
+    const int64_t v = (*this)(a) + (*this)(n - a);
+    memo[n] = v;
+    return v;
+  }
+};
+
+// Program over the tree of size n whose terminal nodes are given by term().
+static std::vector<int> make_prog(int64_t n, bool np, const std::function<bool(int64_t)>& term) {
+  struct Inner { int l, r, h; };
+  std::vector<Inner> inner;     // temp ids: leaves >= 0, inner -> -(k+1)
+  int nL = 0;
+  std::function<std::pair<int, int>(int64_t)> rec = [&](int64_t m) -> std::pair<int, int> {
+    if (term(m)) return {nL++, 0};
+    const int64_t a = split_at(np, m);
+    auto L = rec(a);
+    auto R = rec(m - a);
+    const int h = 1 + std::max(L.second, R.second);
+    inner.push_back({L.first, R.first, h});
+    return {-(int)inner.size(), h};
+  };
+  rec(n);
+  const int nI = (int)inner.size();
+  std::vector<int> order(nI);
+  for (int k = 0; k < nI; ++k) order[k] = k;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return inner[x].h < inner[y].h; });
+  std::vector<int> rank(nI);
+  for (int k = 0; k < nI; ++k) rank[order[k]] = k;
+  auto fin = [&](int t) { return t >= 0 ? t : nL + rank[-t - 1]; };
+  int nLev = nI ? inner[order[nI - 1]].h : 0;
+  std::vector<int> prog;
+  prog.push_back(nL);
+  prog.push_back(nI);
+  prog.push_back(nLev);
+  // level starts (heights 1..nLev)
+  std::vector<int> lev(nLev + 1, 0);
+  {
+    int k = 0;
+    for (int h = 1; h <= nLev; ++h) {
+      lev[h - 1] = k;
+      while (k < nI && inner[order[k]].h == h) ++k;
+    }
+    lev[nLev] = nI;
+  }
+  for (int v : lev) prog.push_back(v);
+  for (int k = 0; k < nI; ++k) prog.push_back(fin(inner[order[k]].l));
+  for (int k = 0; k < nI; ++k) prog.push_back(fin(inner[order[k]].r));
+  return prog;
+}
+
+int ProgPool::add(const std::string& key, const std::vector<int>& prog) {
+  for (auto& kv : memo)
+    if (kv.first == key) return kv.second;
+  const int off = (int)words.size();
+  words.insert(words.end(), prog.begin(), prog.end());
+  memo.push_back({key, off});
+  return off;
+}
+
+void build_sum(SumHost& s, int64_t n, bool np, ProgPool& pool) {
+  s.n = n;
+  s.np = np;
+  LeafCounter cnt{np, {}};
+  s.leaf_start.clear();
+  s.sub_leaf.clear();
+  s.sub_prog.clear();
+  if (n <= 0) {
+    s.nLeaves = 0;
+    s.nSub = 1;
+    s.leaf_start.push_back(0);
+    s.sub_leaf = {0, 0};
+    s.top_prog = pool.add("empty", {0, 0, 0, 0});
+    s.sub_prog = {s.top_prog};
+    return;
+  }
+  if (np) {
+    std::function<void(int64_t, int64_t)> rec = [&](int64_t off, int64_t m) {
+      if (is_leaf(true, m)) {
+        s.leaf_start.push_back(off);
+        return;
+      }
+      const int64_t a = split_at(true, m);
+      rec(off, a);
+      rec(off + a, m - a);
+    };
+    rec(0, n);
+    s.leaf_start.push_back(n);
+  }
+  s.nLeaves = (int)cnt(n);
+  const std::string tag = np ? "np" : "bin";
+  auto leafterm = [&](int64_t m) { return is_leaf(np, m); };
+  if (s.nLeaves <= kMaxProgLeaves) {
+    s.nSub = 1;
+    s.top_prog = pool.add(tag + ":" + std::to_string(n), make_prog(n, np, leafterm));
+    s.sub_leaf = {0, s.nLeaves};
+    s.sub_prog = {s.top_prog};
+    return;
+  }
+  // cut into maximal subtrees with <= kMaxProgLeaves leaves
+  auto cutterm = [&](int64_t m) { return cnt(m) <= kMaxProgLeaves; };
+  int64_t lacc = 0;
+  std::function<void(int64_t)> rec = [&](int64_t m) {
+    if (cutterm(m)) {
+      s.sub_leaf.push_back((int)lacc);
+      s.sub_prog.push_back(pool.add(tag + ":" + std::to_string(m), make_prog(m, np, leafterm)));
+      lacc += cnt(m);
+      return;
+    }
+    const int64_t a = split_at(np, m);
+    rec(a);
+    rec(m - a);
+  };
+  rec(n);
+  s.sub_leaf.push_back((int)lacc);
+  s.nSub = (int)s.sub_prog.size();
+  s.top_prog = pool.add(tag + ":top:" + std::to_string(n), make_prog(n, np, cutterm));
+}
+
+// ---------------------------------------------------------------------------
+static int device_props(int& sms, size_t& smem_optin) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  int v = 0;
+  CK(cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  smem_optin = (size_t)v;
+  return ADP_OK;
+}
+
+static constexpr int kRW = 4;
+
+static void choose_tiles(const adp_plan_desc& d, int& TH, int& TW) {
+  const int64_t px = (int64_t)d.H * d.W;
+  if (d.tile_w > 0 && d.tile_h > 0) {
+    TH = d.tile_h;
+    TW = d.tile_w;
+    return;
+  }
+  TW = 64;
+  if (d.W <= 32) TW = 32;
+  TH = px >= (1 << 20) ? 16 : 8;
+  if (d.kh >= 25) TH = 8;
+}
+
+static size_t conv_smem(const ConvGeom& g, int esize) {
+  const size_t nk = (size_t)g.kh * g.kw * g.C;
+  size_t off = 64 * sizeof(double);
+  off += ((nk * esize + 15) & ~size_t(15)) * 2;
+  const int QP = (g.TW + 1) + ((g.TW + 1) >> 2) + 1;
+  const size_t pa = (size_t)g.C * g.SH * g.SWP * esize;
+  const size_t q = 2 * (size_t)g.C * (g.TH + 1) * QP * esize;
+  size_t region = std::max(pa + q, (size_t)(2 * kMaxProgLeaves) * sizeof(double));
+  return off + region;
+}
+
+template <typename T>
+static void fill_sum(SumDev& sd, const SumHost& sh, const int* d_progs, const int64_t* d_leaf, int* d_subleaf,
+                     int* d_subprog, double* leaf_vals, double* sub_vals) {
+  sd.nLeaves = sh.nLeaves;
+  sd.nSub = sh.nSub;
+  sd.top_prog = sh.top_prog;
+  sd.leaf_start = d_leaf;
+  sd.sub_leaf = d_subleaf;
+  sd.sub_prog = d_subprog;
+  sd.progs = d_progs;
+  sd.leaf_vals = leaf_vals;
+  sd.sub_vals = sub_vals;
+}
+
+static int setup_kernel(PlanImpl& P, KernelInfo& k, const void* fn, int threads, size_t smem, int max_grid) {
+  k.fn = fn;
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_optin));
+  int nb = 0;
+  CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem));
+  if (nb <= 0) return fail(ADP_ERR_UNSUPPORTED, "kernel does not fit on an SM (smem/registers)");
+  k.grid = std::max(1, std::min(max_grid, nb * P.sm_count));
+  return ADP_OK;
+}
+
+static int conv_plan_init(PlanImpl& P) {
+  const adp_plan_desc& d = P.d;
+  size_t smem_optin = 0;
+  if (int e = device_props(P.sm_count, smem_optin)) return e;
+  P.smem_optin = smem_optin;
+  ConvGeom& g = P.g;
+  g.H = d.H; g.W = d.W; g.C = d.C; g.kh = d.kh; g.kw = d.kw;
+  g.rh = d.kh / 2; g.rw = d.kw / 2;
+  choose_tiles(d, g.TH, g.TW);
+  if (g.TW % kRW) return fail(ADP_ERR_ARG, "tile width must be a multiple of 4");
+  g.threads = g.TH * g.TW / kRW;
+  if (g.threads % 32 || g.threads > 512) return fail(ADP_ERR_ARG, "tile must map to 32..512 threads");
+  g.tilesH = (g.H + g.TH - 1) / g.TH;
+  g.tilesW = (g.W + g.TW - 1) / g.TW;
+  g.nTiles = g.tilesH * g.tilesW;
+  g.SH = g.TH + 2 * g.rh + 2;
+  const int SWL = g.TW + 2 * g.rw + 2;
+  g.SWP = SWL + SWL / kRW + 1;
+  g.YSH = g.TH + 2;
+  g.YSWP = (g.TW + 2) + (g.TW + 2) / kRW + 1;
+  g.N = (int64_t)g.H * g.W * g.C;
+  P.smem = conv_smem(g, P.esize);
+  if (P.smem > smem_optin) return fail(ADP_ERR_UNSUPPORTED, "tile + halo exceeds shared memory; use a smaller tile");
+
+  // workspace: 18 N-arrays + 2 arrays of 2N
+  const int64_t N = g.N;
+  const size_t es = (size_t)P.esize;
+  std::vector<size_t> sizes;
+  for (int k = 0; k < 18; ++k) sizes.push_back((size_t)N * es);
+  sizes.push_back((size_t)2 * N * es);
+  sizes.push_back((size_t)2 * N * es);
+  // sums
+  ProgPool pool;
+  SumHost sN, s2N, sT;
+  build_sum(sN, N, true, pool);
+  build_sum(s2N, 2 * N, true, pool);
+  build_sum(sT, g.nTiles, false, pool);
+  // kgc partial groups
+  P.kgc_groups = std::min(4 * P.sm_count, std::max(1, ((g.H + 15) / 16) * ((g.W + 15) / 16)));
+  const size_t nk = (size_t)g.kh * g.kw * g.C;
+  // layout the device block
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return o;
+  };
+  std::vector<size_t> wofs;
+  for (size_t b : sizes) wofs.push_back(take(b));
+  const size_t o_progs = take(pool.words.size() * sizeof(int));
+  const size_t o_leafN = take(sN.leaf_start.size() * sizeof(int64_t));
+  const size_t o_leaf2N = take(s2N.leaf_start.size() * sizeof(int64_t));
+  const SumHost* shs[3] = {&sN, &s2N, &sT};
+  size_t o_sl[3], o_sp[3];
+  for (int k = 0; k < 3; ++k) {
+    o_sl[k] = take(shs[k]->sub_leaf.size() * sizeof(int));
+    o_sp[k] = take(shs[k]->sub_prog.size() * sizeof(int));
+  }
+  const int tileLeaves = std::max(sT.nLeaves, 4 * P.sm_count * 32);
+  size_t o_lv[7], o_sv[7];
+  const int nLeavesOf[7] = {sN.nLeaves, s2N.nLeaves, sN.nLeaves, s2N.nLeaves, tileLeaves, tileLeaves, tileLeaves};
+  const int nSubOf[7] = {sN.nSub, s2N.nSub, sN.nSub, s2N.nSub, sT.nSub, sT.nSub, sT.nSub};
+  for (int k = 0; k < 7; ++k) {
+    o_lv[k] = take((size_t)nLeavesOf[k] * sizeof(double));
+    o_sv[k] = take((size_t)nSubOf[k] * sizeof(double));
+  }
+  const size_t o_bar = take(256);
+  const size_t o_sres = take(sizeof(SolveOut));
+  const size_t o_cres = take(sizeof(CGOut));
+  const size_t o_scal = take(64 * sizeof(double));
+  const size_t o_kgc = take((size_t)P.kgc_groups * nk * sizeof(double));
+  P.dbytes = off;
+  CK(cudaMalloc(&P.dmem, off));
+  char* base = (char*)P.dmem;
+  P.nws = (int)sizes.size();
+  for (int k = 0; k < P.nws; ++k) P.ws[k] = base + wofs[k];
+  P.d_progs = (int*)(base + o_progs);
+  P.d_leaf_N = (int64_t*)(base + o_leafN);
+  P.d_leaf_2N = (int64_t*)(base + o_leaf2N);
+  CK(cudaMemcpy(P.d_progs, pool.words.data(), pool.words.size() * sizeof(int), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(P.d_leaf_N, sN.leaf_start.data(), sN.leaf_start.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  CK(cudaMemcpy(P.d_leaf_2N, s2N.leaf_start.data(), s2N.leaf_start.size() * sizeof(int64_t),
+                cudaMemcpyHostToDevice));
+  for (int k = 0; k < 3; ++k) {
+    P.d_sub[2 * k] = (int*)(base + o_sl[k]);
+    P.d_sub[2 * k + 1] = (int*)(base + o_sp[k]);
+    CK(cudaMemcpy(P.d_sub[2 * k], shs[k]->sub_leaf.data(), shs[k]->sub_leaf.size() * sizeof(int),
+                  cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(P.d_sub[2 * k + 1], shs[k]->sub_prog.data(), shs[k]->sub_prog.size() * sizeof(int),
+                  cudaMemcpyHostToDevice));
+  }
+  SumDev* sds[7] = {&P.s_fit, &P.s_tv, &P.s_fitc, &P.s_tvc, &P.s_t0, &P.s_t1, &P.s_t2};
+  const int which[7] = {0, 1, 0, 1, 2, 2, 2};
+  for (int k = 0; k < 7; ++k) {
+    const SumHost& sh = *shs[which[k]];
+    const int64_t* dl = which[k] == 0 ? P.d_leaf_N : which[k] == 1 ? P.d_leaf_2N : nullptr;
+    fill_sum<double>(*sds[k], sh, P.d_progs, dl, P.d_sub[2 * which[k]], P.d_sub[2 * which[k] + 1],
+                     (double*)(base + o_lv[k]), (double*)(base + o_sv[k]));
+  }
+  P.d_bar = (unsigned int*)(base + o_bar);
+  P.d_sres = (SolveOut*)(base + o_sres);
+  P.d_cres = (CGOut*)(base + o_cres);
+  P.d_scal = (double*)(base + o_scal);
+  P.d_kgc_part = (double*)(base + o_kgc);
+  CK(cudaMallocHost(&P.h_sres, sizeof(SolveOut)));
+  CK(cudaMallocHost(&P.h_cres, sizeof(CGOut)));
+  CK(cudaMallocHost(&P.h_scal, 64 * sizeof(double)));
+
+  ConvKernelSet ks = P.d.dtype == ADP_DTYPE_F32 ? conv_kernels_f32()
+                     : P.d.mode == ADP_MODE_FAST ? conv_kernels_f64f()
+                                                 : conv_kernels_f64s();
+  const int maxg = g.nTiles;
+  if (int e = setup_kernel(P, P.k_solve, ks.solve, g.threads, P.smem, maxg)) return e;
+  if (int e = setup_kernel(P, P.k_cg, ks.cg, g.threads, P.smem, maxg)) return e;
+  if (int e = setup_kernel(P, P.k_misc, ks.misc, g.threads, P.smem, maxg)) return e;
+  g.grid = P.k_solve.grid;
+  P.k_misc.attr_set = true;
+  return ADP_OK;
+}
+
+// ---------------------------------------------------------------------------
+template <typename T>
+static ConvArgs<T> conv_base(PlanImpl& P) {
+  ConvArgs<T> a;
+  std::memset(&a, 0, sizeof(a));
+  a.g = P.g;
+  T** w = (T**)P.ws;
+  a.X[0] = w[0]; a.X[1] = w[1]; a.X[2] = w[2];
+  a.R = w[3]; a.RC = w[4]; a.G = w[5]; a.TVG = w[6];
+  a.DIAG = w[7]; a.WV = w[8]; a.WH = w[9];
+  a.P[0] = w[10]; a.P[1] = w[11]; a.BP = w[12]; a.HP = w[13]; a.CR = w[14]; a.CS = w[15];
+  a.TV2 = w[18]; a.TV2C = w[19];
+  a.s_fit = P.s_fit; a.s_tv = P.s_tv; a.s_fitc = P.s_fitc; a.s_tvc = P.s_tvc;
+  a.s_t0 = P.s_t0; a.s_t1 = P.s_t1; a.s_t2 = P.s_t2;
+  a.bar = P.d_bar;
+  a.sres = P.d_sres;
+  a.cres = P.d_cres;
+  a.scal = P.d_scal;
+  return a;
+}
+
+template <typename T>
+static void set_lower(ConvArgs<T>& a, const adp_lower* lp) {
+  a.kern = (const T*)lp->kernel;
+  a.ydat = (const T*)lp->y;
+  a.alpha = lp->alpha;
+  a.nu = lp->nu;
+  a.reg = lp->reg;
+  a.regcurv = 8.0 / lp->nu;   // SmoothedTV.curvature (regularizers.py:148-156)
+}
+
+template <typename T>
+static int launch_coop(PlanImpl& P, KernelInfo& k, ConvArgs<T>& a, cudaStream_t st) {
+  a.g.grid = k.grid;
+  CK(cudaMemsetAsync(P.d_bar, 0, sizeof(unsigned int), st));
+  void* args[] = {&a};
+  CK(cudaLaunchCooperativeKernel(k.fn, dim3(k.grid), dim3(P.g.threads), args, P.smem, st));
+  return ADP_OK;
+}
+
+static int fetch_scal(PlanImpl& P, int n, cudaStream_t st) {
+  CK(cudaMemcpyAsync(P.h_scal, P.d_scal, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return ADP_OK;
+}
+
+template <typename T>
+static int conv_misc(PlanImpl& P, int mode, const adp_lower* lp, const void* kernel, const void* in0,
+                     const void* in1, void* out0, void* out1, const void* ydat, cudaStream_t st) {
+  ConvArgs<T> a = conv_base<T>(P);
+  if (lp) set_lower(a, lp);
+  if (kernel) a.kern = (const T*)kernel;
+  if (ydat) a.ydat = (const T*)ydat;
+  a.mode = mode;
+  a.in0 = (const T*)in0;
+  a.in1 = (const T*)in1;
+  a.out0 = (T*)out0;
+  a.out1 = (T*)out1;
+  return launch_coop(P, P.k_misc, a, st);
+}
+
+template <typename T>
+static int conv_kgc(PlanImpl& P, const void* xa, const void* va, const void* xb, const void* vb, void* out,
+                    double scale, cudaStream_t st) {
+  ConvKernelSet ks = P.d.dtype == ADP_DTYPE_F32 ? conv_kernels_f32()
+                     : P.d.mode == ADP_MODE_FAST ? conv_kernels_f64f()
+                                                 : conv_kernels_f64s();
+  KgcArgs<T> a;
+  std::memset(&a, 0, sizeof(a));
+  a.g = P.g;
+  a.xa = (const T*)xa; a.va = (const T*)va; a.xb = (const T*)xb; a.vb = (const T*)vb;
+  a.part = P.d_kgc_part;
+  a.ngroups = P.kgc_groups;
+  a.out = (T*)out;
+  a.scale = scale;
+  const int KT = 16;
+  const size_t smem = ((size_t)(KT + P.g.kh - 1) * (KT + P.g.kw - 1) + KT * KT) * sizeof(T);
+  CK(cudaFuncSetAttribute(ks.kgc_part, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_optin));
+  void* args[] = {&a};
+  CK(cudaLaunchKernel(ks.kgc_part, dim3(P.kgc_groups), dim3(256), args, smem, st));
+  const int n = P.g.kh * P.g.kw * P.g.C;
+  CK(cudaLaunchKernel(ks.kgc_final, dim3((n + 255) / 256), dim3(256), args, 0, st));
+  return ADP_OK;
+}
+
+}  // namespace adp
+
+using namespace adp;
+
+// ===========================================================================
+// dense 1-D dispatch (adp_dense.cu)
+namespace adp {
+int dense_plan_init(PlanImpl& P);
+int dense_call(PlanImpl& P, int op, const void* kernel, const adp_lower* lp, const void* a0, const void* a1,
+               void* o0, void* o1, const void* ydat, double* scal, cudaStream_t st);
+int dense_solve(PlanImpl& P, const adp_lower* lp, const void* x0, void* x_out, const adp_solve_args* args,
+                adp_solve_result* res, cudaStream_t st);
+int dense_cg(PlanImpl& P, const adp_lower* lp, const void* xt, const void* rhs, void* q, int warm,
+             const void* precond, double tol, int max_iters, adp_cg_result* res, cudaStream_t st);
+void dense_plan_free(PlanImpl& P);
+}  // namespace adp
+
+#define DISPATCH_T(P, CALL)                          \
+  ((P).d.dtype == ADP_DTYPE_F32 ? CALL<float> : CALL<double>)
+
+extern "C" {
+
+const char* adp_last_error(void) { return g_err.c_str(); }
+
+int adp_device_info(int* sm_count, int* cc_major, int* cc_minor) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(sm_count, cudaDevAttrMultiProcessorCount, dev));
+  CK(cudaDeviceGetAttribute(cc_major, cudaDevAttrComputeCapabilityMajor, dev));
+  CK(cudaDeviceGetAttribute(cc_minor, cudaDevAttrComputeCapabilityMinor, dev));
+  return ADP_OK;
+}
+
+int adp_plan_create(adp_plan** out, const adp_plan_desc* desc) {
+  if (!out || !desc) return fail(ADP_ERR_ARG, "null argument");
+  *out = nullptr;
+  const adp_plan_desc& d = *desc;
+  if (d.dtype != ADP_DTYPE_F64 && d.dtype != ADP_DTYPE_F32) return fail(ADP_ERR_ARG, "bad dtype");
+  if (d.H < 1 || d.W < 1 || d.C < 1) return fail(ADP_ERR_ARG, "bad shape");
+  if (d.layout == ADP_LAYOUT_DEPTHWISE2D) {
+    if (d.kh < 1 || d.kw < 1 || d.kh % 2 == 0 || d.kw % 2 == 0)
+      return fail(ADP_ERR_ARG, "depthwise2d kernel must have odd spatial size");
+  } else if (d.layout == ADP_LAYOUT_DENSE1D) {
+    if (d.H != 1 || d.C != 1 || d.kh != d.W || d.kw != d.W) return fail(ADP_ERR_ARG, "bad dense1d plan");
+  } else {
+    return fail(ADP_ERR_ARG, "unknown layout");
+  }
+  adp_plan* p = new adp_plan();
+  p->impl.d = d;
+  p->impl.esize = d.dtype == ADP_DTYPE_F32 ? 4 : 8;
+  int e = d.layout == ADP_LAYOUT_DEPTHWISE2D ? conv_plan_init(p->impl) : dense_plan_init(p->impl);
+  if (e) {
+    adp_plan_destroy(p);
+    return e;
+  }
+  *out = p;
+  return ADP_OK;
+}
+
+void adp_plan_destroy(adp_plan* p) {
+  if (!p) return;
+  PlanImpl& P = p->impl;
+  if (P.d.layout == ADP_LAYOUT_DENSE1D) dense_plan_free(P);
+  if (P.dmem) cudaFree(P.dmem);
+  if (P.d_zero) cudaFree(P.d_zero);
+  if (P.h_sres) cudaFreeHost(P.h_sres);
+  if (P.h_cres) cudaFreeHost(P.h_cres);
+  if (P.h_scal) cudaFreeHost(P.h_scal);
+  delete p;
+}
+
+size_t adp_plan_workspace_bytes(const adp_plan* p) { return p ? p->impl.dbytes : 0; }
+
+#define STREAM(s) ((cudaStream_t)(s))
+#define IS_DENSE(p) ((p)->impl.d.layout == ADP_LAYOUT_DENSE1D)
+
+enum DenseOp { DO_APPLY, DO_ADJOINT, DO_GRAM, DO_VALUE, DO_VG, DO_GRAD, DO_HV, DO_HDIAG, DO_UPPER, DO_POWER, DO_MIXED,
+               DO_DOT, DO_KGC };
+
+int adp_apply(adp_plan* p, const void* kernel, const void* x, void* out, void* stream) {
+  if (!p) return fail(ADP_ERR_ARG, "null plan");
+  if (IS_DENSE(p)) return dense_call(p->impl, DO_APPLY, kernel, nullptr, x, nullptr, out, nullptr, nullptr, nullptr, STREAM(stream));
+  return DISPATCH_T(p->impl, conv_misc)(p->impl, CM_APPLY, nullptr, kernel, x, nullptr, out, nullptr, nullptr,
+                                        STREAM(stream));
+}
+
+int adp_adjoint(adp_plan* p, const void* kernel, const void* y, void* out, void* stream) {
+  if (!p) return fail(ADP_ERR_ARG, "null plan");
+  if (IS_DENSE(p)) return dense_call(p->impl, DO_ADJOINT, kernel, nullptr, y, nullptr, out, nullptr, nullptr, nullptr, STREAM(stream));
+  return DISPATCH_T(p->impl, conv_misc)(p->impl, CM_ADJOINT, nullptr, kernel, y, nullptr, out, nullptr, nullptr,
+                                        STREAM(stream));
+}
+
+int adp_gram_diag(adp_plan* p, const void* kernel, void* out, void* stream) {
+  if (!p) return fail(ADP_ERR_ARG, "null plan");
+  if (IS_DENSE(p)) return dense_call(p->impl, DO_GRAM, kernel, nullptr, nullptr, nullptr, out, nullptr, nullptr, nullptr, STREAM(stream));
+  return DISPATCH_T(p->impl, conv_misc)(p->impl, CM_GRAM_DIAG, nullptr, kernel, nullptr, nullptr, out, nullptr,
+                                        nullptr, STREAM(stream));
+}
+
+int adp_op_norm_sq(adp_plan* p, const void* kernel, const void* v0, int32_t max_iters, double tol, double* lam,
+                   int32_t* converged, int32_t* iters, void* stream) {
+  if (!p) return fail(ADP_ERR_ARG, "null plan");
+  PlanImpl& P = p->impl;
+  int e;
+  if (IS_DENSE(p)) {
+    double sc[3];
+    adp_lower lp{};
+    lp.kernel = kernel;
+    lp.l1 = tol;
+    lp.alpha = (double)max_iters;
+    e = dense_call(P, DO_POWER, kernel, &lp, v0, nullptr, nullptr, nullptr, nullptr, sc, STREAM(stream));
+    if (e) return e;
+    *lam = sc[0]; *converged = (int)sc[1]; *iters = (int)sc[2];
+    return ADP_OK;
+  }
+  auto run = [&](auto tag) -> int {
+    using T = decltype(tag);
+    ConvArgs<T> a = conv_base<T>(P);
+    a.kern = (const T*)kernel;
+    a.v0 = (const T*)v0;
+    a.mode = CM_POWER;
+    a.power_max_iters = max_iters;
+    a.power_tol = tol;
+    if (int e2 = launch_coop(P, P.k_misc, a, STREAM(stream))) return e2;
+    if (int e2 = fetch_scal(P, 3, STREAM(stream))) return e2;
+    *lam = P.h_scal[0];
+    *converged = (int)P.h_scal[1];
+    *iters = (int)P.h_scal[2];
+    return ADP_OK;
+  };
+  return P.d.dtype == ADP_DTYPE_F32 ? run(float()) : run(double());
+}
+
+int adp_kgc(adp_plan* p, const void* x, const void* v, void* out, void* stream) {
+  if (!p) return fail(ADP_ERR_ARG, "null plan");
+  if (IS_DENSE(p)) return dense_call(p->impl, DO_KGC, nullptr, nullptr, x, v, out, nullptr, nullptr, nullptr, STREAM(stream));
+  return DISPATCH_T(p->impl, conv_kgc)(p->impl, x, v, nullptr, nullptr, out, 1.0, STREAM(stream));
+}
+
+static int check_lower(adp_plan* p, const adp_lower* lp) {
+  if (!p || !lp) return fail(ADP_ERR_ARG, "null argument");
+  if (!IS_DENSE(p) && lp->reg != ADP_REG_TV) return fail(ADP_ERR_UNSUPPORTED, "depthwise2d path supports SmoothedTV");
+  if (lp->reg == ADP_REG_TV && lp->alpha != 0.0 && !(lp->nu > 0.0))
+    return fail(ADP_ERR_ARG, "gradient requested on the nonsmooth branch (nu = 0)");
+  return ADP_OK;
+}
+
+int adp_lower_value(adp_plan* p, const adp_lower* lp, const void* x, double* value, void* stream) {
+  if (int e = check_lower(p, lp)) return e;
+  PlanImpl& P = p->impl;
+  if (IS_DENSE(p)) return dense_call(P, DO_VALUE, lp->kernel, lp, x, nullptr, nullptr, nullptr, nullptr, value, STREAM(stream));
+  if (int e = DISPATCH_T(P, conv_misc)(P, CM_VALUE, lp, nullptr, x, nullptr, nullptr, nullptr, nullptr, STREAM(stream)))
+    return e;
+  if (int e = fetch_scal(P, 1, STREAM(stream))) return e;
+  *value = P.h_scal[0];
+  return ADP_OK;
+}
+
+int adp_lower_value_and_grad(adp_plan* p, const adp_lower* lp, const void* x, double* value, void* g, void* stream) {
+  if (int e = check_lower(p, lp)) return e;
+  PlanImpl& P = p->impl;
+  if (IS_DENSE(p)) return dense_call(P, DO_VG, lp->kernel, lp, x, nullptr, g, nullptr, nullptr, value, STREAM(stream));
+  if (int e = DISPATCH_T(P, conv_misc)(P, CM_VALUE_GRAD, lp, nullptr, x, nullptr, g, nullptr, nullptr, STREAM(stream)))
+    return e;
+  if (int e = fetch_scal(P, 2, STREAM(stream))) return e;
+  *value = P.h_scal[0];
+  return ADP_OK;
+}
+
+int adp_lower_grad(adp_plan* p, const adp_lower* lp, const void* x, void* g, void* stream) {
+  if (int e = check_lower(p, lp)) return e;
+  PlanImpl& P = p->impl;
+  if (IS_DENSE(p)) return dense_call(P, DO_GRAD, lp->kernel, lp, x, nullptr, g, nullptr, nullptr, nullptr, STREAM(stream));
+  return DISPATCH_T(P, conv_misc)(P, CM_GRAD, lp, nullptr, x, nullptr, g, nullptr, nullptr, STREAM(stream));
+}
+
+int adp_lower_hess_vec(adp_plan* p, const adp_lower* lp, const void* x, const void* v, void* out, void* stream) {
+  if (int e = check_lower(p, lp)) return e;
+  PlanImpl& P = p->impl;
+  if (IS_DENSE(p)) return dense_call(P, DO_HV, lp->kernel, lp, x, v, out, nullptr, nullptr, nullptr, STREAM(stream));
+  return DISPATCH_T(P, conv_misc)(P, CM_HESS_VEC, lp, nullptr, x, v, out, nullptr, nullptr, STREAM(stream));
+}
+
+int adp_lower_hess_diag(adp_plan* p, const adp_lower* lp, const void* x, void* out, void* stream) {
+  if (int e = check_lower(p, lp)) return e;
+  PlanImpl& P = p->impl;
+  if (IS_DENSE(p)) return dense_call(P, DO_HDIAG, lp->kernel, lp, x, nullptr, out, nullptr, nullptr, nullptr, STREAM(stream));
+  return DISPATCH_T(P, conv_misc)(P, CM_HESS_DIAG, lp, nullptr, x, nullptr, out, nullptr, nullptr, STREAM(stream));
+}
+
+int adp_lower_solve(adp_plan* p, const adp_lower* lp, const void* x0, void* x_out, const adp_solve_args* sa,
+                    adp_solve_result* res, void* stream) {
+  if (int e = check_lower(p, lp)) return e;
+  if (!sa || !res) return fail(ADP_ERR_ARG, "null argument");
+  if (!(sa->eps > 0)) return fail(ADP_ERR_ARG, "eps must be > 0");
+  if (!(sa->mu > 0)) return fail(ADP_ERR_ARG, "mu must be > 0");
+  if (sa->method < 0 || sa->method > 2) return fail(ADP_ERR_ARG, "unknown lower solver method");
+  PlanImpl& P = p->impl;
+  if (IS_DENSE(p)) return dense_solve(P, lp, x0, x_out, sa, res, STREAM(stream));
+  auto run = [&](auto tag) -> int {
+    using T = decltype(tag);
+    ConvArgs<T> a = conv_base<T>(P);
+    set_lower(a, lp);
+    a.method = sa->method;
+    a.adaptive = sa->adaptive;
+    a.max_iters = sa->max_iters;
+    a.mu = sa->mu;
+    a.tol = sa->eps * sa->mu;
+    a.step_given = sa->step_size > 0 ? sa->step_size : 0.0;
+    a.lip_cached = sa->norm_sq;
+    a.power_max_iters = sa->norm_max_iters;
+    a.power_tol = sa->norm_tol;
+    a.v0 = (const T*)sa->v0;
+    a.x0 = (const T*)x0;
+    a.out = (T*)x_out;
+    if (int e = launch_coop(P, P.k_solve, a, STREAM(stream))) return e;
+    CK(cudaMemcpyAsync(P.h_sres, P.d_sres, sizeof(SolveOut), cudaMemcpyDeviceToHost, STREAM(stream)));
+    CK(cudaStreamSynchronize(STREAM(stream)));
+    const SolveOut& o = *P.h_sres;
+    res->norm_sq = o.lam;
+    res->lip = o.lip;
+    res->grad_norm = o.grad_norm;
+    res->value = o.value;
+    res->iters = o.iters;
+    res->converged = o.converged;
+    res->status = o.status;
+    res->fail_iter = o.fail_iter;
+    res->power_iters = o.power_iters;
+    res->power_converged = o.power_converged;
+    res->vg_evals = o.vg_evals;
+    res->value_evals = o.value_evals;
+    res->restarts = o.restarts;
+    return ADP_OK;
+  };
+  return P.d.dtype == ADP_DTYPE_F32 ? run(float()) : run(double());
+}
+
+int adp_hess_cg(adp_plan* p, const adp_lower* lp, const void* x_tilde, const void* rhs, void* q, int32_t warm,
+                const void* precond, double tol, int32_t max_iters, adp_cg_result* res, void* stream) {
+  if (int e = check_lower(p, lp)) return e;
+  if (!res) return fail(ADP_ERR_ARG, "null argument");
+  if (!(tol > 0)) return fail(ADP_ERR_ARG, "tol must be > 0");
+  PlanImpl& P = p->impl;
+  if (IS_DENSE(p)) return dense_cg(P, lp, x_tilde, rhs, q, warm, precond, tol, max_iters, res, STREAM(stream));
+  auto run = [&](auto tag) -> int {
+    using T = decltype(tag);
+    ConvArgs<T> a = conv_base<T>(P);
+    set_lower(a, lp);
+    a.xt = (const T*)x_tilde;
+    a.rhs = (const T*)rhs;
+    a.Q = (T*)q;
+    a.warm = warm;
+    a.diag_in = (const T*)precond;
+    a.tol = tol;
+    a.max_iters = max_iters;
+    if (int e = launch_coop(P, P.k_cg, a, STREAM(stream))) return e;
+    CK(cudaMemcpyAsync(P.h_cres, P.d_cres, sizeof(CGOut), cudaMemcpyDeviceToHost, STREAM(stream)));
+    CK(cudaStreamSynchronize(STREAM(stream)));
+    const CGOut& o = *P.h_cres;
+    res->residual = o.residual;
+    res->curv = o.curv;
+    res->iters = o.iters;
+    res->converged = o.converged;
+    res->status = o.status;
+    res->hv = o.hv;
+    return ADP_OK;
+  };
+  return P.d.dtype == ADP_DTYPE_F32 ? run(float()) : run(double());
+}
+
+int adp_mixed_T(adp_plan* p, const adp_lower* lp, const void* x_tilde, const void* q, void* out, void* stream) {
+  if (int e = check_lower(p, lp)) return e;
+  PlanImpl& P = p->impl;
+  if (IS_DENSE(p)) return dense_call(P, DO_MIXED, lp->kernel, lp, x_tilde, q, out, nullptr, nullptr, nullptr, STREAM(stream));
+  void* resid = P.ws[3];  // R
+  void* bq = P.ws[12];    // BP
+  if (int e = DISPATCH_T(P, conv_misc)(P, CM_MIXED_PREP, lp, nullptr, x_tilde, q, resid, bq, nullptr, STREAM(stream)))
+    return e;
+  return DISPATCH_T(P, conv_kgc)(P, x_tilde, bq, q, resid, out, 2.0, STREAM(stream));
+}
+
+int adp_upper_terms(adp_plan* p, const void* A_kernel, const void* x, const void* y_delta, double* fit,
+                    double* grad_norm, void* grad_out, void* stream) {
+  if (!p) return fail(ADP_ERR_ARG, "null plan");
+  PlanImpl& P = p->impl;
+  if (IS_DENSE(p)) {
+    double sc[2];
+    if (int e = dense_call(P, DO_UPPER, A_kernel, nullptr, x, nullptr, grad_out, nullptr, y_delta, sc, STREAM(stream))) return e;
+    *fit = sc[0];
+    *grad_norm = sc[1];
+    return ADP_OK;
+  }
+  if (int e = DISPATCH_T(P, conv_misc)(P, CM_UPPER, nullptr, A_kernel, x, nullptr, grad_out, nullptr, y_delta,
+                                       STREAM(stream)))
+    return e;
+  if (int e = fetch_scal(P, 2, STREAM(stream))) return e;
+  *fit = P.h_scal[0];
+  *grad_norm = P.h_scal[1];
+  return ADP_OK;
+}
+
+// Regularizer alone (SmoothedTV / SmoothedElasticNet methods): the lower
+// machinery with the operator term removed (zero stencil / reg_only) and
+// alpha = 1, which reproduces J's own value / gradient / Hessian exactly.
+int adp_reg_op(adp_plan* p, const adp_lower* reg, int32_t op, const void* x, const void* v, void* out,
+               double* value, void* stream) {
+  if (!p || !reg) return fail(ADP_ERR_ARG, "null argument");
+  PlanImpl& P = p->impl;
+  adp_lower lp = *reg;
+  lp.alpha = 1.0;
+  if (IS_DENSE(p)) {
+    if (lp.reg != ADP_REG_ELASTIC) return fail(ADP_ERR_UNSUPPORTED, "dense1d path supports SmoothedElasticNet");
+    const int ops[5] = {DO_VALUE, DO_VG, DO_GRAD, DO_HV, DO_HDIAG};
+    if (op < 0 || op > 4) return fail(ADP_ERR_ARG, "bad reg op");
+    double sc[2] = {0, 0};
+    if (int e = dense_call(P, 100 + ops[op], nullptr, &lp, x, v, out, nullptr, nullptr, sc, STREAM(stream))) return e;
+    if (value) *value = sc[0];
+    return ADP_OK;
+  }
+  if (lp.reg != ADP_REG_TV) return fail(ADP_ERR_UNSUPPORTED, "depthwise2d path supports SmoothedTV");
+  if (!(lp.nu > 0.0) && op != 0) return fail(ADP_ERR_ARG, "gradient requested on the nonsmooth branch (nu = 0)");
+  if (!P.d_zero) {
+    CK(cudaMalloc(&P.d_zero, (size_t)(P.g.N + (int64_t)P.g.kh * P.g.kw * P.g.C) * P.esize));
+    CK(cudaMemset(P.d_zero, 0, (size_t)(P.g.N + (int64_t)P.g.kh * P.g.kw * P.g.C) * P.esize));
+  }
+  lp.kernel = P.d_zero;
+  lp.y = P.d_zero;
+  auto run = [&](auto tag) -> int {
+    using T = decltype(tag);
+    ConvArgs<T> a = conv_base<T>(P);
+    set_lower(a, &lp);
+    const int modes[5] = {CM_VALUE, CM_VALUE_GRAD, CM_GRAD, CM_HESS_VEC, CM_HESS_DIAG};
+    if (op < 0 || op > 4) return fail(ADP_ERR_ARG, "bad reg op");
+    a.mode = modes[op];
+    a.nofloor = 1;
+    a.in0 = (const T*)x;
+    a.in1 = (const T*)v;
+    a.out0 = (T*)out;
+    if (int e = launch_coop(P, P.k_misc, a, STREAM(stream))) return e;
+    if (op <= 1) {
+      if (int e = fetch_scal(P, 1, STREAM(stream))) return e;
+      if (value) *value = P.h_scal[0];
+    }
+    return ADP_OK;
+  };
+  return P.d.dtype == ADP_DTYPE_F32 ? run(float()) : run(double());
+}
+
+int adp_dot(adp_plan* p, const void* a, const void* b, double* out, void* stream) {
+  if (!p) return fail(ADP_ERR_ARG, "null plan");
+  PlanImpl& P = p->impl;
+  if (IS_DENSE(p)) return dense_call(P, DO_DOT, nullptr, nullptr, a, b, nullptr, nullptr, nullptr, out, STREAM(stream));
+  if (int e = DISPATCH_T(P, conv_misc)(P, CM_DOT, nullptr, nullptr, a, b, nullptr, nullptr, nullptr, STREAM(stream)))
+    return e;
+  if (int e = fetch_scal(P, 1, STREAM(stream))) return e;
+  *out = P.h_scal[0];
+  return ADP_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Host-only introspection of the deterministic-sum layout (no device needed):
+// lets CPU tests evaluate the exact tree the kernels evaluate.
+extern "C" int adp_sum_layout(int64_t n, int32_t np_rule, int64_t* n_leaves, int32_t* n_sub, int32_t* top_prog,
+                              int64_t* leaf_start, int64_t leaf_cap, int32_t* sub_leaf, int32_t* sub_prog,
+                              int64_t sub_cap, int32_t* words, int64_t words_cap, int64_t* n_words) {
+  adp::ProgPool pool;
+  adp::SumHost s;
+  adp::build_sum(s, n, np_rule != 0, pool);
+  *n_leaves = s.nLeaves;
+  *n_sub = s.nSub;
+  *top_prog = s.top_prog;
+  *n_words = (int64_t)pool.words.size();
+  if ((int64_t)s.leaf_start.size() > leaf_cap || (int64_t)s.sub_leaf.size() > sub_cap + 1 ||
+      (int64_t)pool.words.size() > words_cap)
+    return fail(ADP_ERR_ARG, "buffer too small");
+  for (size_t i = 0; i < s.leaf_start.size(); ++i) leaf_start[i] = s.leaf_start[i];
+  for (size_t i = 0; i < s.sub_leaf.size(); ++i) sub_leaf[i] = s.sub_leaf[i];
+  for (size_t i = 0; i < s.sub_prog.size(); ++i) sub_prog[i] = s.sub_prog[i];
+  for (size_t i = 0; i < pool.words.size(); ++i) words[i] = pool.words[i];
+  return ADP_OK;
+}

@@ -1,0 +1,75 @@
+// Host-side plan: geometry, workspace and deterministic-sum programs.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+#include "adp_types.h"
+#include "../../include/adp_b200.h"
+
+namespace adp {
+
+// Deterministic sum layout built on the host (see adp_types.h SumDev).
+struct SumHost {
+  int64_t n = 0;              // elements (np rule) or items (binary rule)
+  bool np = true;
+  std::vector<int64_t> leaf_start;
+  std::vector<int> sub_leaf, sub_prog;
+  int top_prog = 0;
+  int nLeaves = 0, nSub = 1;
+};
+
+// Programs for all sums of a plan live in one int32 buffer.
+struct ProgPool {
+  std::vector<int> words;
+  std::vector<std::pair<std::string, int>> memo;
+  int add(const std::string& key, const std::vector<int>& prog);
+};
+
+void build_sum(SumHost& s, int64_t n, bool np, ProgPool& pool);
+
+struct KernelInfo {
+  const void* fn = nullptr;
+  int grid = 0;
+  bool attr_set = false;
+};
+
+struct PlanImpl {
+  adp_plan_desc d{};
+  ConvGeom g{};
+  int esize = 8;
+  size_t smem = 0;
+  size_t smem_optin = 0;        // device max dynamic smem per block (function attribute set to this)
+  int sm_count = 0;
+  // device memory
+  void* dmem = nullptr;
+  void* d_zero = nullptr;        // zero stencil + zero image (regularizer-only calls)
+  size_t dbytes = 0;
+  void* ws[24] = {};            // workspace arrays (T*)
+  int nws = 0;
+  int* d_progs = nullptr;
+  int64_t* d_leaf_N = nullptr;  // leaf starts for N-element sums
+  int64_t* d_leaf_2N = nullptr;
+  int* d_sub[8] = {};           // sub_leaf / sub_prog per layout
+  SumDev s_fit{}, s_tv{}, s_fitc{}, s_tvc{}, s_t0{}, s_t1{}, s_t2{};
+  unsigned int* d_bar = nullptr;
+  SolveOut* d_sres = nullptr;
+  CGOut* d_cres = nullptr;
+  double* d_scal = nullptr;
+  double* d_kgc_part = nullptr;
+  int kgc_groups = 0;
+  // pinned host staging
+  SolveOut* h_sres = nullptr;
+  CGOut* h_cres = nullptr;
+  double* h_scal = nullptr;
+  KernelInfo k_solve, k_cg, k_misc;
+  // dense 1-D engine data
+  int dense_grid = 0;
+  size_t dense_smem = 0;
+};
+
+}  // namespace adp
+
+struct adp_plan {
+  adp::PlanImpl impl;
+};

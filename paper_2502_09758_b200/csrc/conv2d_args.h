@@ -1,0 +1,85 @@
+// Kernel-argument block of the depthwise 2-D engine (host + device).
+#pragma once
+#include "adp_types.h"
+
+namespace adp {
+
+enum ConvMode : int {
+  CM_APPLY = 0,          // out0 = B in0
+  CM_ADJOINT = 1,        // out0 = B^T in0
+  CM_GRAM_DIAG = 2,      // out0 = correlate(ones, flipped**2)
+  CM_VALUE = 3,          // scal[0] = lower_value(in0)
+  CM_VALUE_GRAD = 4,     // scal[0] = value, out0 = grad    (value_and_grad form)
+  CM_GRAD = 5,           // out0 = lower_grad(in0)
+  CM_HESS_VEC = 6,       // out0 = H(in0 = x) in1
+  CM_HESS_DIAG = 7,      // out0 = lower_hess_diag(in0)
+  CM_UPPER = 8,          // scal[0] = sum((B in0 - y)^2), scal[1] = ||2 B^T (B in0 - y)||, out0 = grad or null
+  CM_POWER = 9,          // scal[0] = op_norm_sq, scal[1] = converged, scal[2] = iters
+  CM_MIXED_PREP = 10,    // out0 = B in0 - y (residual), out1 = B in1 (B q)
+  CM_DOT = 11,           // scal[0] = <in0, in1> (ddot-type, fixed tree)
+};
+
+
+template <typename T>
+struct ConvArgs {
+  ConvGeom g;
+  const T* kern;           // (kh, kw, C) stencil, C-order
+  const T* ydat;           // lower-level data y (H, W, C)
+  double alpha, nu, regcurv;  // alpha, TV nu, C_J
+  int reg;                 // RegKind (conv path: REG_TV)
+  int method, adaptive;
+  int max_iters;
+  double tol, mu;          // tol = eps * mu
+  double step_given;       // > 0: step_size passed by the caller
+  double lip_cached;       // > 0: op norm already known (op._norm_sq cache)
+  int power_max_iters;
+  double power_tol;
+  const T* v0;             // power-iteration start (un-normalised)
+  const T* x0;             // warm start
+  T* out;                  // x_tilde
+  // workspace
+  T* X[3];
+  T* R;  T* RC; T* G; T* TVG; T* TV2; T* TV2C;
+  // CG / Hessian
+  const T* xt;             // x_tilde (Hessian point)
+  const T* rhs;
+  T* Q;                    // q (in/out)
+  const T* diag_in;        // optional precond diag
+  T* DIAG;                 // inv diag workspace / diag output
+  T* WV; T* WH;            // rho'' weights
+  T* P[2]; T* BP; T* HP; T* CR; T* CS;
+  int warm;
+  // sums
+  SumDev s_fit, s_tv, s_fitc, s_tvc;   // numpy-pairwise element sums (N, 2N, N, 2N)
+  SumDev s_t0, s_t1, s_t2;             // per-tile partial sums (ddot-type)
+  unsigned int* bar;
+  SolveOut* sres;
+  CGOut* cres;
+  double* scal;            // misc scalar outputs
+  int mode;                // misc kernel mode
+  int nofloor;             // hess_diag without the 1e-12*max floor (regularizer-only call)
+  const T* in0; const T* in1; T* out0; T* out1;
+};
+
+template <typename T>
+struct KgcArgs {
+  ConvGeom g;
+  const T* xa; const T* va; const T* xb; const T* vb;
+  double* part;   // [ngroups][kh*kw*C]
+  int ngroups;
+  T* out;         // (kh, kw, C)
+  double scale;
+};
+
+struct ConvKernelSet {
+  const void* solve;
+  const void* cg;
+  const void* misc;
+  const void* kgc_part;
+  const void* kgc_final;
+};
+ConvKernelSet conv_kernels_f64s();
+ConvKernelSet conv_kernels_f64f();
+ConvKernelSet conv_kernels_f32();
+
+}  // namespace adp

@@ -1,0 +1,674 @@
+// Cooperative persistent kernels of the depthwise 2-D engine.
+#pragma once
+#include <initializer_list>
+#include "conv2d_engine.cuh"
+
+namespace adp {
+
+
+template <typename T, bool FAST, int RW>
+struct ConvOps : Conv<T, FAST, RW> {
+  using Base = Conv<T, FAST, RW>;
+  using Base::a; using Base::g; using Base::sv; using Base::red;
+  GridBarrier gb;
+
+  __device__ ConvOps(const ConvArgs<T>& a_, unsigned char* smem) : Base(a_, smem) {
+    gb.counter = a_.bar;
+    gb.nblocks = gridDim.x;
+    gb.target = 0;
+  }
+
+  __device__ double reduce1(const SumDev& s) {
+    const SumDev* ss[1] = {&s};
+    double o[1];
+    reduce_list(ss, 1, o, sv, gb);
+    return o[0];
+  }
+  __device__ void reduce(std::initializer_list<const SumDev*> l, double* out) {
+    const SumDev* ss[8];
+    int k = 0;
+    for (const SumDev* p : l) ss[k++] = p;
+    reduce_list(ss, k, out, sv, gb);
+  }
+
+  // Power iteration on B^T B (op_norm_sq, operators.py:137-173).  Uses R
+  // (B v) and G (w) as scratch.  Returns lambda; sets iters / converged.
+  __device__ double power(int max_iters, double tol, int& iters, int& conv) {
+    // v /= ||v||  (operators.py:150)
+    this->foreach_pixel_sum([&](int64_t i, int, int, int) {
+      const double v = (double)a.v0[i];
+      return v * v;
+    }, a.s_t0);
+    gb.sync();
+    const double nv = sqrt(reduce1(a.s_t0));
+    double lam = 0.0;
+    conv = 0;
+    iters = 0;
+    const T* src = a.v0;
+    double scale = nv;
+    for (int it = 0; it < max_iters; ++it) {
+      iters = it + 1;
+      this->stage_corr(SrcScaled<T>{src, T(scale)}, false, a.R, nullptr, T(1), nullptr);
+      gb.sync();
+      this->stage_corr(SrcLin<T>{a.R}, true, a.G, nullptr, T(1), &a.s_t0);
+      gb.sync();
+      const double lam_new = sqrt(reduce1(a.s_t0));
+      if (lam_new == 0.0) { lam = 0.0; conv = 1; break; }
+      src = a.G;
+      scale = lam_new;
+      if (fabs(lam_new - lam) <= tol * fmax(lam_new, 1e-300)) { lam = lam_new; conv = 1; break; }
+      lam = lam_new;
+    }
+    return lam;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// solve_lower (lower_solvers.py:104-213) as one persistent kernel.
+template <typename T, bool FAST, int RW>
+__global__ void __launch_bounds__(512, 1) conv_solve_kernel(const __grid_constant__ ConvArgs<T> a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  ConvOps<T, FAST, RW> E(a, smem);
+  const ConvGeom& g = a.g;
+  if (a.kern) E.load_weights(a.kern);
+  const bool tv = (a.alpha != 0.0);
+  const double twoN = 2.0 * (double)g.N;
+
+  // ---- step size / Lipschitz constant (solve_lower lines 135-140, L_of_b 90-96)
+  double lip, step = 0.0;
+  int pit = 0, pconv = 1;
+  double lam = a.lip_cached;
+  if (a.step_given > 0.0) {
+    step = a.step_given;
+    lip = 1.0 / a.step_given;
+  } else {
+    if (!(a.lip_cached >= 0.0)) lam = E.power(a.power_max_iters, a.power_tol, pit, pconv);
+    lip = 2.0 * lam + a.alpha * a.regcurv;
+    step = 1.0 / lip;
+  }
+
+  // ---- x = x_prev = x0
+  E.foreach_pixel([&](int64_t i, int, int, int) { a.X[0][i] = a.x0[i]; });
+  E.gb.sync();
+
+  int ix = 0, ixp = 0, ic = 1;
+  double t_mom = 1.0, lip_t = lip;
+  double theta = 0.0;
+  if (a.method == M_FISTA_SC) {
+    const double q = fmin(a.mu / lip, 1.0);
+    theta = (1.0 - sqrt(q)) / (1.0 + sqrt(q));
+  }
+  double gd_step = step;   // _gradient_descent's `step`
+  int status = ST_OK, fail_iter = -1, iters = a.max_iters, converged = 0;
+  double gn = 0.0, h_y = 0.0, beta = 0.0;
+  long long vg = 0, vals = 0, restarts = 0;
+  bool done = false;
+
+  for (int t = 0; t < a.max_iters; ++t) {
+    if (a.method == M_AGD) {
+      const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t_mom * t_mom));
+      beta = (t_mom - 1.0) / t_next;
+      t_mom = t_next;
+    } else if (a.method == M_FISTA_SC) {
+      beta = theta;
+    } else {
+      beta = 0.0;
+      ixp = ix;
+    }
+    const T tb = T(beta);
+    // value and gradient at y
+    E.stageA(SrcExtrap<T>{a.X[ix], a.X[ixp], tb}, a.R, a.ydat, tv, a.TV2, a.TVG);
+    E.gb.sync();
+    E.stageB(a.R, tv, a.TVG, a.G, &a.s_t0);
+    np_leaves(a.s_fit, SqOf<T>{a.R});
+    if (tv) np_leaves(a.s_tv, Plain<T>{a.TV2});
+    ++vg;
+    // first candidate, computed speculatively before the convergence test
+    const bool gd_fixed = (a.method == M_PROXGRAD && !a.adaptive);
+    double L_try = (a.method == M_PROXGRAD) ? 1.0 / gd_step : lip_t;
+    E.gb.sync();
+    if (a.adaptive) {
+      E.stageC(SrcCand<T>{a.X[ix], a.X[ixp], a.G, tb, T(L_try)}, a.RC, tv, a.TV2C, a.X[ic], a.G, a.X[ix], &a.s_t1);
+      E.gb.sync();
+      np_leaves(a.s_fitc, SqOf<T>{a.RC});
+      if (tv) np_leaves(a.s_tvc, Plain<T>{a.TV2C});
+      ++vals;
+    } else if (gd_fixed) {
+      E.stageCLight(SrcStep<T>{a.X[ix], a.G, T(gd_step)}, a.X[ic], a.G, a.X[ix], &a.s_t1);
+    } else {
+      E.stageCLight(SrcCand<T>{a.X[ix], a.X[ixp], a.G, tb, T(lip_t)}, a.X[ic], a.G, a.X[ix], &a.s_t1);
+    }
+    E.gb.sync();
+    // fit(y), tv(y), g.g, dot, [fit(xc), tv(xc)]
+    double o[6] = {0, 0, 0, 0, 0, 0};
+    if (a.adaptive && tv) E.reduce({&a.s_fit, &a.s_tv, &a.s_t0, &a.s_t1, &a.s_fitc, &a.s_tvc}, o);
+    else if (a.adaptive) { E.reduce({&a.s_fit, &a.s_t0, &a.s_t1, &a.s_fitc}, o + 2); o[0] = o[2]; o[2] = o[3]; o[3] = o[4]; o[4] = o[5]; o[5] = 0.0; }
+    else if (tv) E.reduce({&a.s_fit, &a.s_tv, &a.s_t0, &a.s_t1}, o);
+    else { E.reduce({&a.s_fit, &a.s_t0, &a.s_t1}, o + 1); o[0] = o[1]; o[1] = 0.0; }
+    const double fit = o[0];
+    h_y = fit;
+    if (tv) h_y = fit + a.alpha * (o[1] - a.nu * twoN);
+    gn = sqrt(o[2]);
+    double dot = o[3];
+    const double tvc0 = o[5];
+    if (!isfinite(gn)) { status = ST_DIVERGED; fail_iter = t; done = true; break; }
+    if (gn <= a.tol) {
+      // converged: return y (lower_solvers.py:200-201)
+      E.foreach_pixel([&](int64_t i, int, int, int) {
+        const T xv = ldcg(a.X[ix] + i), xpv = ldcg(a.X[ixp] + i);
+        a.out[i] = xv + tb * (xv - xpv);
+      });
+      iters = t;
+      converged = 1;
+      done = true;
+      break;
+    }
+    if (a.adaptive) {
+      // _backtracked_step (lower_solvers.py:170-177)
+      double fitc = o[4], tvc = tvc0;
+      int k = 0;
+      while (true) {
+        const double val = tv ? fitc + a.alpha * tvc : fitc + a.alpha * 0.0;
+        if (val <= h_y - 0.5 * gn * gn / L_try + 1e-15 * fabs(h_y)) break;
+        L_try *= 2.0;
+        if (++k >= 60) { status = ST_BT_FAIL; fail_iter = t; break; }
+        E.gb.sync();
+        E.stageC(SrcCand<T>{a.X[ix], a.X[ixp], a.G, tb, T(L_try)}, a.RC, tv, a.TV2C, a.X[ic], a.G, a.X[ix], &a.s_t1);
+        E.gb.sync();
+        np_leaves(a.s_fitc, SqOf<T>{a.RC});
+        if (tv) np_leaves(a.s_tvc, Plain<T>{a.TV2C});
+        ++vals;
+        E.gb.sync();
+        double o3[3] = {0, 0, 0};
+        if (tv) E.reduce({&a.s_fitc, &a.s_tvc, &a.s_t1}, o3);
+        else { E.reduce({&a.s_fitc, &a.s_t1}, o3); o3[2] = o3[1]; o3[1] = 0.0; }
+        fitc = o3[0]; tvc = o3[1]; dot = o3[2];
+      }
+      if (status != ST_OK) { done = true; break; }
+      const double bstep = 1.0 / L_try;
+      if (a.method == M_PROXGRAD) gd_step = bstep;
+      else lip_t = fmax(1.0 / bstep * 0.9, lip * 1e-8);
+    }
+    // x_prev = x; x = candidate; restart (lower_solvers.py:202-211)
+    const int old_x = ix, old_xp = ixp;
+    ixp = old_x;
+    ix = ic;
+    if (a.method == M_AGD && dot > 0.0) {
+      t_mom = 1.0;
+      ixp = ix;
+      ++restarts;
+    }
+    // free buffer for the next candidate: not ix, not ixp
+    for (int b = 0; b < 3; ++b)
+      if (b != ix && b != ixp) { ic = b; break; }
+    (void)old_xp;
+  }
+
+  if (!done) {
+    // max_iters reached: g = lower_grad(p, x) (lower_solvers.py:212-213)
+    E.stageA(SrcLin<T>{a.X[ix]}, a.R, a.ydat, tv, a.TV2, a.TVG);
+    E.gb.sync();
+    E.stageB(a.R, tv, a.TVG, a.G, &a.s_t0);
+    E.foreach_pixel([&](int64_t i, int, int, int) { a.out[i] = ldcg(a.X[ix] + i); });
+    E.gb.sync();
+    gn = sqrt(E.reduce1(a.s_t0));
+    iters = a.max_iters;
+    converged = gn <= a.tol;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    SolveOut* r = a.sres;
+    r->lam = lam;
+    r->lip = lip;
+    r->grad_norm = gn;
+    r->value = h_y;
+    r->iters = iters;
+    r->converged = converged;
+    r->status = status;
+    r->fail_iter = fail_iter;
+    r->power_iters = pit;
+    r->power_converged = pconv;
+    r->vg_evals = vg;
+    r->value_evals = vals;
+    r->restarts = restarts;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Hessian of the lower problem (lower_hess_vec, lower_solvers.py:66-71):
+//   H v = 2 B^T (B v) + alpha * D^T (rho''(D x) . D v)
+// Two stages: (1) BP = B v   (2) out = 2 B^T BP + alpha * TV-Hessian term.
+template <typename T, bool FAST, int RW>
+struct HessOps : ConvOps<T, FAST, RW> {
+  using Base = ConvOps<T, FAST, RW>;
+  using Base::a; using Base::g;
+  __device__ HessOps(const ConvArgs<T>& a_, unsigned char* smem) : Base(a_, smem) {}
+
+  // rho'' weights of x: WV (vertical edges), WH (horizontal); _rho_curv
+  // (regularizers.py:34-36): nu^2 / (t^2 + nu^2)^1.5
+  __device__ void hess_weights(const T* x) {
+    const T nu = T(a.nu), nu2 = nu * nu;
+    this->foreach_pixel([&](int64_t i, int h, int w, int c) {
+      const T xc = ldcg(x + i);
+      const T d0 = (h < g.H - 1) ? ldcg(x + i + (int64_t)g.W * g.C) - xc : T(0);
+      const T d1 = (w < g.W - 1) ? ldcg(x + i + g.C) - xc : T(0);
+      const T s0 = d0 * d0 + nu2, s1 = d1 * d1 + nu2;
+      a.WV[i] = nu2 / (s0 * sqrt(s0));
+      a.WH[i] = nu2 / (s1 * sqrt(s1));
+    });
+  }
+
+  // out = H v, given BP = B v already computed; v read with 1-halo from
+  // global.  Optional tile partial of <pdot, out> (curvature) or of
+  // (out - sub)^2 (true residual).
+  __device__ void hess_stage2(const T* V, bool tv, T* Out, const T* pdot, const T* sub, const SumDev* s) {
+    const T two = T(2), alpha = T(a.alpha);
+    const int C = g.C;
+    const int64_t rowS = (int64_t)g.W * C;
+    for (int tile = blockIdx.x; tile < g.nTiles; tile += gridDim.x) {
+      int h0, w0;
+      this->tile_origin(tile, h0, w0);
+      __syncthreads();
+      this->load_full(this->pa, h0, w0, SrcLin<T>{a.BP});
+      __syncthreads();
+      const int h = h0 + this->ty;
+      double part = 0.0;
+      for (int c = 0; c < C; ++c) {
+        T acc[RW];
+        this->stencil(this->plane(this->pa, c), this->wf + c * g.kh * g.kw, acc);
+#pragma unroll
+        for (int o = 0; o < RW; ++o) {
+          const int w = w0 + this->tx * RW + o;
+          if (h < g.H && w < g.W) {
+            const int64_t i = this->gidx(h, w, c);
+            T hv = two * acc[o];
+            if (tv) {
+              // D^T (W . D v) at pixel i, image_forward_diff_adjoint order
+              const T vc = ldcg(V + i);
+              T t = T(0);
+              if (h >= 1) t = t + ldcg(a.WV + i - rowS) * (vc - ldcg(V + i - rowS));
+              if (h <= g.H - 2) t = t - ldcg(a.WV + i) * (ldcg(V + i + rowS) - vc);
+              if (w >= 1) t = t + ldcg(a.WH + i - C) * (vc - ldcg(V + i - C));
+              if (w <= g.W - 2) t = t - ldcg(a.WH + i) * (ldcg(V + i + C) - vc);
+              hv = hv + alpha * t;
+            }
+            Out[i] = hv;
+            if (s) {
+              if (pdot) part += (double)ldcg(pdot + i) * (double)hv;
+              else {
+                const double d = (double)(hv - ldcg(sub + i));
+                part += d * d;
+              }
+            }
+          }
+        }
+      }
+      if (s) store_tile_partial(*s, tile, part, this->red);
+    }
+  }
+
+  // H v with v = src (materialised into Vbuf by stage 1).
+  template <class Src>
+  __device__ void hess_vec(const Src& src, T* Vbuf, bool tv, T* Out, const T* pdot, const T* sub, const SumDev* s) {
+    // stage 1: Vbuf = src (own pixels), BP = B src
+    for (int tile = blockIdx.x; tile < g.nTiles; tile += gridDim.x) {
+      int h0, w0;
+      this->tile_origin(tile, h0, w0);
+      __syncthreads();
+      this->load_full(this->pa, h0, w0, src);
+      __syncthreads();
+      const int h = h0 + this->ty;
+      for (int c = 0; c < g.C; ++c) {
+        T acc[RW];
+        this->stencil(this->plane(this->pa, c), this->ws + c * g.kh * g.kw, acc);
+#pragma unroll
+        for (int o = 0; o < RW; ++o) {
+          const int q = this->tx * RW + o;
+          const int w = w0 + q;
+          if (h < g.H && w < g.W) {
+            const int64_t i = this->gidx(h, w, c);
+            a.BP[i] = acc[o];
+            if (Vbuf) Vbuf[i] = this->fp(this->pa, c, this->ty, q);
+          }
+        }
+      }
+    }
+    this->gb.sync();
+    hess_stage2(Vbuf, tv, Out, pdot, sub, s);
+  }
+
+  // lower_hess_diag (lower_solvers.py:74-80) into DIAG (before flooring when
+  // floor == false); TV part: SmoothedTV.hess_diag (regularizers.py:185-199).
+  __device__ void hess_diag(const T* x, bool tv, T* Out) {
+    this->load_weights_sq(a.kern);
+    const T nu = T(a.nu), nu2 = nu * nu, two = T(2), alpha = T(a.alpha);
+    const int C = g.C;
+    const int64_t rowS = (int64_t)g.W * C;
+    double mx = -INFINITY;
+    for (int tile = blockIdx.x; tile < g.nTiles; tile += gridDim.x) {
+      int h0, w0;
+      this->tile_origin(tile, h0, w0);
+      __syncthreads();
+      this->load_full(this->pa, h0, w0, SrcOnes<T>{});
+      __syncthreads();
+      const int h = h0 + this->ty;
+      for (int c = 0; c < C; ++c) {
+        T acc[RW];
+        this->stencil(this->plane(this->pa, c), this->wf + c * g.kh * g.kw, acc);
+#pragma unroll
+        for (int o = 0; o < RW; ++o) {
+          const int w = w0 + this->tx * RW + o;
+          if (h < g.H && w < g.W) {
+            const int64_t i = this->gidx(h, w, c);
+            T d = two * acc[o];
+            if (tv) {
+              const T xc = ldcg(x + i);
+              T t = T(0);
+              // diag[:-1] += wv; diag[1:] += wv; diag[:, :-1] += wh; diag[:, 1:] += wh
+              if (h <= g.H - 2) { const T dd = ldcg(x + i + rowS) - xc, s = dd * dd + nu2; t = t + nu2 / (s * sqrt(s)); }
+              if (h >= 1) { const T dd = xc - ldcg(x + i - rowS), s = dd * dd + nu2; t = t + nu2 / (s * sqrt(s)); }
+              if (w <= g.W - 2) { const T dd = ldcg(x + i + C) - xc, s = dd * dd + nu2; t = t + nu2 / (s * sqrt(s)); }
+              if (w >= 1) { const T dd = xc - ldcg(x + i - C), s = dd * dd + nu2; t = t + nu2 / (s * sqrt(s)); }
+              d = d + alpha * t;
+            }
+            Out[i] = d;
+            mx = fmax(mx, (double)d);
+          }
+        }
+      }
+    }
+    // global max -> floor (np.maximum(d, 1e-12 * d.max() + 1e-300))
+    mx = block_max(mx, this->red);
+    if (threadIdx.x == 0) a.s_t2.leaf_vals[blockIdx.x] = mx;
+    this->gb.sync();
+    double gmx = -INFINITY;
+    for (int b = threadIdx.x; b < gridDim.x; b += blockDim.x) gmx = fmax(gmx, ldcg(a.s_t2.leaf_vals + b));
+    gmx = block_max(gmx, this->red);
+    const T fl = T(1e-12 * gmx + 1e-300);
+    if (!a.nofloor) this->foreach_pixel([&](int64_t i, int, int, int) {
+      const T d = ldcg(Out + i);
+      Out[i] = d > fl ? d : fl;   // np.maximum (d is never NaN here)
+    });
+    this->load_weights(a.kern);
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Jacobi-preconditioned CG on the lower Hessian at x_tilde
+// (cg_solve, hypergradient.py:35-84, as specialised by inexact_hypergradient
+// 171-176).  Q in/out (warm start when a.warm), DIAG gets the preconditioner.
+template <typename T, bool FAST, int RW>
+__global__ void __launch_bounds__(512, 1) conv_cg_kernel(const __grid_constant__ ConvArgs<T> a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  HessOps<T, FAST, RW> E(a, smem);
+  const ConvGeom& g = a.g;
+  if (a.kern) E.load_weights(a.kern);
+  const bool tv = (a.alpha != 0.0);
+  const double tol = a.tol;
+  int status = ST_OK, hv = 0;
+  double curv = 0.0;
+
+  if (tv) E.hess_weights(a.xt);
+  if (a.diag_in) {
+    E.foreach_pixel([&](int64_t i, int, int, int) { a.DIAG[i] = T(1) / a.diag_in[i]; });
+  } else {
+    E.gb.sync();
+    E.hess_diag(a.xt, tv, a.DIAG);
+    E.gb.sync();
+    E.foreach_pixel([&](int64_t i, int, int, int) { a.DIAG[i] = T(1) / ldcg(a.DIAG + i); });
+  }
+  E.gb.sync();
+  // r = rhs - H q0 (warm) or rhs; q = q0 or 0
+  if (a.warm) {
+    E.hess_vec(SrcLin<T>{a.Q}, a.P[1], tv, a.HP, nullptr, nullptr, nullptr);
+    ++hv;
+    E.gb.sync();
+    E.foreach_pixel([&](int64_t i, int, int, int) { a.CR[i] = a.rhs[i] - ldcg(a.HP + i); });
+  } else {
+    E.foreach_pixel([&](int64_t i, int, int, int) { a.Q[i] = T(0); a.CR[i] = a.rhs[i]; });
+  }
+  // s = inv_diag * r ; rs = <r, s> ; rr = <r, r>
+  E.foreach_pixel_sum([&](int64_t i, int, int, int) {
+    const T r = ldcg(a.CR + i), s = ldcg(a.DIAG + i) * r;
+    a.CS[i] = s;
+    return (double)r * (double)s;
+  }, a.s_t1);
+  E.foreach_pixel_sum([&](int64_t i, int, int, int) {
+    const double r = (double)ldcg(a.CR + i);
+    return r * r;
+  }, a.s_t2);
+  E.gb.sync();
+  double rs, rr;
+  {
+    double o[2];
+    E.reduce({&a.s_t1, &a.s_t2}, o);
+    rs = o[0];
+    rr = o[1];
+  }
+  int iters = 0;
+  int cur = 0;          // P[cur] holds the current direction
+  int first = 1;        // p = s.copy() on the first direction
+  double beta = 0.0;
+  for (iters = 1; iters <= a.max_iters; ++iters) {
+    if (sqrt(rr) <= tol) { iters -= 1; break; }
+    // p = s + beta * p_old (materialised by hess stage 1), Hp
+    const int nxt = first ? cur : cur ^ 1;
+    E.hess_vec(SrcCGDir<T>{a.CS, a.P[cur], T(beta), first}, a.P[nxt], tv, a.HP, a.P[nxt], nullptr, &a.s_t0);
+    ++hv;
+    cur = nxt;
+    first = 0;
+    E.gb.sync();
+    curv = E.reduce1(a.s_t0);
+    if (curv <= 0.0) { status = ST_NEGCURV; break; }
+    const double al = rs / curv;
+    const T ta = T(al);
+    E.foreach_pixel_sum([&](int64_t i, int, int, int) {
+      const T p = ldcg(a.P[cur] + i);
+      a.Q[i] = ldcg(a.Q + i) + ta * p;
+      const T r = ldcg(a.CR + i) - ta * ldcg(a.HP + i);
+      a.CR[i] = r;
+      const T s = ldcg(a.DIAG + i) * r;
+      a.CS[i] = s;
+      return (double)r * (double)s;
+    }, a.s_t1);
+    E.foreach_pixel_sum([&](int64_t i, int, int, int) {
+      const double r = (double)ldcg(a.CR + i);
+      return r * r;
+    }, a.s_t2);
+    E.gb.sync();
+    double o[2];
+    E.reduce({&a.s_t1, &a.s_t2}, o);
+    beta = o[0] / rs;
+    rs = o[0];
+    rr = o[1];
+  }
+  if (iters > a.max_iters) iters = a.max_iters;
+  double res = 0.0;
+  int conv = 0;
+  if (status == ST_OK) {
+    // true residual ||H q - rhs|| (hypergradient.py:83)
+    E.gb.sync();
+    E.hess_vec(SrcLin<T>{a.Q}, a.P[cur ^ 1], tv, a.HP, nullptr, a.rhs, &a.s_t0);
+    ++hv;
+    E.gb.sync();
+    res = sqrt(E.reduce1(a.s_t0));
+    conv = res <= tol;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    CGOut* r = a.cres;
+    r->residual = res;
+    r->curv = curv;
+    r->rs = rs;
+    r->iters = iters;
+    r->converged = conv;
+    r->status = status;
+    r->hv = hv;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Per-call primitives (one cooperative launch each).
+template <typename T, bool FAST, int RW>
+__global__ void __launch_bounds__(512, 1) conv_misc_kernel(const __grid_constant__ ConvArgs<T> a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  HessOps<T, FAST, RW> E(a, smem);
+  const ConvGeom& g = a.g;
+  if (a.kern) E.load_weights(a.kern);
+  const bool tv = (a.alpha != 0.0);
+  switch (a.mode) {
+    case CM_APPLY:
+      E.stage_corr(SrcLin<T>{a.in0}, false, a.out0, nullptr, T(1), nullptr);
+      break;
+    case CM_ADJOINT:
+      E.stage_corr(SrcLin<T>{a.in0}, true, a.out0, nullptr, T(1), nullptr);
+      break;
+    case CM_GRAM_DIAG:
+      E.load_weights_sq(a.kern);
+      E.stage_corr(SrcOnes<T>{}, true, a.out0, nullptr, T(1), nullptr);
+      break;
+    case CM_VALUE: {
+      // lower_value (lower_solvers.py:37-39): sum(r*r) + alpha * tv_value(x)
+      E.stageC(SrcLin<T>{a.in0}, a.RC, true, a.TV2C, nullptr, nullptr, nullptr, nullptr);
+      E.gb.sync();
+      np_leaves(a.s_fitc, SqOf<T>{a.RC});
+      np_leaves(a.s_tvc, Plain<T>{a.TV2C});
+      E.gb.sync();
+      double o[2];
+      E.reduce({&a.s_fitc, &a.s_tvc}, o);
+      if (blockIdx.x == 0 && threadIdx.x == 0) a.scal[0] = o[0] + a.alpha * o[1];
+      break;
+    }
+    case CM_VALUE_GRAD:
+    case CM_GRAD: {
+      E.stageA(SrcLin<T>{a.in0}, a.R, a.ydat, tv, a.TV2, a.TVG);
+      E.gb.sync();
+      E.stageB(a.R, tv, a.TVG, a.out0, &a.s_t0);
+      np_leaves(a.s_fit, SqOf<T>{a.R});
+      if (tv) np_leaves(a.s_tv, Plain<T>{a.TV2});
+      E.gb.sync();
+      double o[3] = {0, 0, 0};
+      if (tv) E.reduce({&a.s_fit, &a.s_tv, &a.s_t0}, o);
+      else { E.reduce({&a.s_fit, &a.s_t0}, o); o[2] = o[1]; o[1] = 0.0; }
+      if (blockIdx.x == 0 && threadIdx.x == 0) {
+        double v = o[0];
+        if (tv) v = o[0] + a.alpha * (o[1] - a.nu * (2.0 * (double)g.N));
+        a.scal[0] = v;
+        a.scal[1] = sqrt(o[2]);
+      }
+      break;
+    }
+    case CM_HESS_VEC:
+      if (tv) { E.hess_weights(a.in0); E.gb.sync(); }
+      E.hess_vec(SrcLin<T>{a.in1}, a.P[0], tv, a.out0, nullptr, nullptr, nullptr);
+      break;
+    case CM_HESS_DIAG:
+      E.hess_diag(a.in0, tv, a.out0);
+      break;
+    case CM_UPPER: {
+      // UpperProblem.fit_value (problems.py:48-50) and ||upper_fit_grad||
+      // (hypergradient.py:87-89): r = A x - y; sum(r*r); u = 2 A^T r
+      E.stage_corr(SrcLin<T>{a.in0}, false, a.R, a.ydat, T(1), nullptr);
+      E.gb.sync();
+      E.stage_corr(SrcLin<T>{a.R}, true, a.out0 ? a.out0 : a.G, nullptr, T(2), &a.s_t0);
+      np_leaves(a.s_fit, SqOf<T>{a.R});
+      E.gb.sync();
+      double o[2];
+      E.reduce({&a.s_fit, &a.s_t0}, o);
+      if (blockIdx.x == 0 && threadIdx.x == 0) { a.scal[0] = o[0]; a.scal[1] = sqrt(o[1]); }
+      break;
+    }
+    case CM_POWER: {
+      int it = 0, cv = 0;
+      const double lam = E.power(a.power_max_iters, a.power_tol, it, cv);
+      if (blockIdx.x == 0 && threadIdx.x == 0) { a.scal[0] = lam; a.scal[1] = cv; a.scal[2] = it; }
+      break;
+    }
+    case CM_MIXED_PREP:
+      E.stage_corr(SrcLin<T>{a.in0}, false, a.out0, a.ydat, T(1), nullptr);
+      E.stage_corr(SrcLin<T>{a.in1}, false, a.out1, nullptr, T(1), nullptr);
+      break;
+    case CM_DOT: {
+      E.foreach_pixel_sum([&](int64_t i, int, int, int) { return (double)a.in0[i] * (double)a.in1[i]; }, a.s_t0);
+      E.gb.sync();
+      const double d = E.reduce1(a.s_t0);
+      if (blockIdx.x == 0 && threadIdx.x == 0) a.scal[0] = d;
+      break;
+    }
+    default:
+      break;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// kernel_gram_correlation (operators.py:198-220), summed over pairs:
+//   out[i,j,c] = sum_{h,w} xa[h+i-r, w+j-r, c] * va[h,w,c] (+ same for xb, vb)
+// Non-cooperative: work groups own fixed tile sets; per-group partials then a
+// fixed-order final reduction (deterministic, independent of the grid).
+template <typename T>
+__global__ void __launch_bounds__(256) kgc_partial_kernel(const __grid_constant__ KgcArgs<T> a) {
+  const ConvGeom& g = a.g;
+  extern __shared__ __align__(16) unsigned char smem[];
+  // tile of KT x KT outputs pixels + halo of x, plus v tile
+  constexpr int KT = 16;
+  const int SHx = KT + g.kh - 1, SWx = KT + g.kw - 1;
+  T* xs = reinterpret_cast<T*>(smem);
+  T* vs = xs + SHx * SWx;
+  const int ntap = g.kh * g.kw;
+  const int thH = (g.H + KT - 1) / KT, thW = (g.W + KT - 1) / KT;
+  const int ntile = thH * thW;
+  for (int grp = blockIdx.x; grp < a.ngroups; grp += gridDim.x) {
+    for (int c = 0; c < g.C; ++c) {
+      // each thread owns taps t = threadIdx.x + k*blockDim
+      double acc[12];
+#pragma unroll
+      for (int k = 0; k < 12; ++k) acc[k] = 0.0;
+      for (int pair = 0; pair < 2; ++pair) {
+        const T* X = pair ? a.xb : a.xa;
+        const T* V = pair ? a.vb : a.va;
+        if (!X) continue;
+        for (int tile = grp; tile < ntile; tile += a.ngroups) {
+          const int h0 = (tile / thW) * KT, w0 = (tile % thW) * KT;
+          __syncthreads();
+          for (int e = threadIdx.x; e < SHx * SWx; e += blockDim.x) {
+            const int r = e / SWx, q = e % SWx;
+            const int gh = h0 - g.rh + r, gw = w0 - g.rw + q;
+            xs[e] = (gh >= 0 && gh < g.H && gw >= 0 && gw < g.W) ? X[((int64_t)gh * g.W + gw) * g.C + c] : T(0);
+          }
+          for (int e = threadIdx.x; e < KT * KT; e += blockDim.x) {
+            const int r = e / KT, q = e % KT;
+            const int gh = h0 + r, gw = w0 + q;
+            vs[e] = (gh < g.H && gw < g.W) ? V[((int64_t)gh * g.W + gw) * g.C + c] : T(0);
+          }
+          __syncthreads();
+#pragma unroll
+          for (int k = 0; k < 12; ++k) {
+            const int t = threadIdx.x + k * blockDim.x;
+            if (t < ntap) {
+              const int i = t / g.kw, j = t % g.kw;
+              double s = 0.0;
+              for (int r = 0; r < KT; ++r)
+                for (int q = 0; q < KT; ++q) s += (double)xs[(r + i) * SWx + q + j] * (double)vs[r * KT + q];
+              acc[k] += s;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 12; ++k) {
+        const int t = threadIdx.x + k * blockDim.x;
+        if (t < ntap) a.part[(size_t)grp * ntap * g.C + t * g.C + c] = acc[k];
+      }
+    }
+  }
+}
+
+template <typename T>
+__global__ void kgc_final_kernel(const __grid_constant__ KgcArgs<T> a) {
+  const int n = a.g.kh * a.g.kw * a.g.C;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < a.ngroups; ++k) s += a.part[(size_t)k * n + e];
+    a.out[e] = T(a.scale * s);
+  }
+}
+
+}  // namespace adp

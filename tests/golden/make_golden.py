@@ -1,0 +1,195 @@
+"""Generate the golden fixtures in tests/golden/ by running the REAL reference
+(/root/reference/pkg/src/adp) in the build container.
+
+    OPENBLAS_NUM_THREADS=1 python tests/golden/make_golden.py
+
+/root/reference does not exist on the GPU box: the fixtures are committed and
+the GPU tests read only them.  Every input is seeded; outputs are the
+reference's own results with OpenBLAS pinned to one thread.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+os.environ.setdefault("OPENBLAS_NUM_THREADS", "1")
+import numpy as np  # noqa: E402
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REF)
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+from adp import hypergradient as H  # noqa: E402
+from adp import lower_solvers as L  # noqa: E402
+from adp import maid as M  # noqa: E402
+from adp import operators as O  # noqa: E402
+from adp import problems as P  # noqa: E402
+from adp import regularizers as R  # noqa: E402
+
+
+def save(name, **arrays):
+    np.savez_compressed(os.path.join(HERE, name), **{k: np.asarray(v) for k, v in arrays.items()})
+    print("wrote", name, sorted(arrays))
+
+
+def reductions():
+    rng = np.random.default_rng(7)
+    out = {}
+    for n in (1, 5, 8, 17, 31, 100, 128, 129, 255, 1000, 4099, 65536, 90000):
+        a = rng.standard_normal(n) * np.exp(2.0 * rng.standard_normal(n))
+        b = rng.standard_normal(n)
+        out[f"a{n}"] = a
+        out[f"b{n}"] = b
+        out[f"sum{n}"] = np.sum(a)
+        out[f"dot{n}"] = np.dot(a, b)
+        out[f"vdot{n}"] = np.vdot(a, b)
+        out[f"norm{n}"] = np.linalg.norm(a)
+    save("reductions.npz", **out)
+
+
+def conv_case(name, shape, k, seed, tiny=True):
+    rng = np.random.default_rng(seed)
+    h, w, c = shape
+    kern = rng.uniform(0.0, 1.0, (k, k, c))
+    if tiny:
+        kern[0, 0, 0] = 1e-17     # skipped by ndimage (|w| <= DBL_EPSILON)
+        kern[k - 1, 0, c - 1] = 0.0
+        kern[1, 2, 0] = -3e-16    # kept
+    kern /= kern.sum(axis=(0, 1), keepdims=True)
+    x = rng.uniform(0.0, 1.0, shape)
+    v = rng.standard_normal(shape)
+    y = rng.uniform(0.0, 1.0, shape)
+    op = O.ConvOperator(O.Kernel(kern, O.DEPTHWISE2D), shape)
+    reg = R.SmoothedTV(1e-4)
+    p = L.LowerProblem(op, y, 0.6, reg)
+    vg_val, vg_g = L.lower_value_and_grad(p, x)
+    lam = O.op_norm_sq(O.ConvOperator(O.Kernel(kern, O.DEPTHWISE2D), shape), 300, 1e-4)
+    tvv, tvg = reg.value_and_grad(x)
+    save(name, kern=kern, x=x, v=v, y=y, alpha=0.6, nu=1e-4,
+         apply=op.apply(x), adjoint=op.adjoint(v), gram_diag=op.gram_diag(),
+         kgc=O.kernel_gram_correlation(x, v, op.kernel),
+         lower_value=L.lower_value(p, x), vg_val=vg_val, vg_g=vg_g, lower_grad=L.lower_grad(p, x),
+         hess_vec=L.lower_hess_vec(p, x, v), hess_diag=L.lower_hess_diag(p, x),
+         tv_value=reg.value(x), tv_grad=reg.grad(x), tv_vg_val=tvv, tv_vg_g=tvg,
+         tv_hess_vec=reg.hess_vec(x, v), tv_hess_diag=reg.hess_diag(x), norm_sq=lam,
+         mixed=H.mixed_second_transpose(x, op.kernel, v, p))
+
+
+def dense_case(name, n, seed):
+    rng = np.random.default_rng(seed)
+    m = rng.standard_normal((n, n)) / np.sqrt(n) + np.eye(n)
+    x = rng.standard_normal(n)
+    v = rng.standard_normal(n)
+    y = rng.standard_normal(n)
+    op = O.DenseOperator(m)
+    reg = R.SmoothedElasticNet(1.2e-3, 4e-3, 1e-4)
+    p = L.LowerProblem(op, y, 1.0, reg)
+    vg_val, vg_g = L.lower_value_and_grad(p, x)
+    save(name, m=m, x=x, v=v, y=y, l1=1.2e-3, l2=4e-3, nu=1e-4, alpha=1.0,
+         apply=op.apply(x), adjoint=op.adjoint(v), gram_diag=op.gram_diag(),
+         kgc=O.kernel_gram_correlation(x, v, op.kernel),
+         lower_value=L.lower_value(p, x), vg_val=vg_val, vg_g=vg_g, lower_grad=L.lower_grad(p, x),
+         hess_vec=L.lower_hess_vec(p, x, v), hess_diag=L.lower_hess_diag(p, x),
+         en_value=reg.value(x), en_grad=reg.grad(x), en_hess_vec=reg.hess_vec(x, v), en_hess_diag=reg.hess_diag(x),
+         norm_sq=O.op_norm_sq(O.DenseOperator(m), 300, 1e-4),
+         mixed=H.mixed_second_transpose(x, op.kernel, v, p))
+
+
+def solver_cases():
+    # 2-D adaptive AGD on a small semi-blind instance (motion2d semantics)
+    up = P.build_semiblind2d(size=(40, 48), seed=3)
+    b = up.b0
+    p = up.lower_problem(b)
+    mu = L.mu_of_b(p, 10.0)
+    out = {}
+    for tag, method, adaptive, iters, eps in (("agd_ad", "agd", True, 400, 1e-9), ("agd_ad_conv", "agd", True, 2000, 1e-2),
+                                              ("gd_ad", "proxgrad", True, 150, 1e-9),
+                                              ("fista", "fista_sc", True, 150, 1e-9),
+                                              ("agd_fixed", "agd", False, 150, 1e-9)):
+        p = up.lower_problem(b)
+        r = L.solve_lower(p, up.x0, eps, mu, max_iters=iters, method=method, adaptive=adaptive)
+        out[f"{tag}_x"] = r.x_tilde
+        out[f"{tag}_gn"] = r.grad_norm
+        out[f"{tag}_iters"] = r.iters
+        out[f"{tag}_conv"] = r.converged
+        out[f"{tag}_args"] = np.array([eps, mu, iters])
+    save("solve2d.npz", y_delta=up.y_delta, x0=up.x0, kern=b.data, A_kern=up.a.data, **out)
+
+    # hypergradient on the same instance
+    p = up.lower_problem(b)
+    st = H.WarmState(x=up.x0.copy())
+    hg = H.inexact_hypergradient(up, b, 0.5, 0.5, st, cg_max_iters=60)
+    p = up.lower_problem(b)
+    rhs = H.upper_fit_grad(hg.x_tilde, up.A, up.y_delta)
+    cg = H.cg_solve(lambda v: L.lower_hess_vec(p, hg.x_tilde, v), rhs, 1e-3, max_iters=40,
+                    precond_diag=L.lower_hess_diag(p, hg.x_tilde))
+    st2 = H.WarmState(x=up.x0.copy())
+    hg15 = H.inexact_hypergradient(up, b, 0.5, 0.5, st2, cg_max_iters=15)
+    save("hyper2d_cg15.npz", z=hg15.z, cg_iters=hg15.cg_iters, cg_residual=hg15.cg_residual, q=st2.q)
+    save("hyper2d.npz", y_delta=up.y_delta, x0=up.x0, kern=b.data, a_kern=up.a.data, z=hg.z, x_tilde=hg.x_tilde,
+         cg_iters=hg.cg_iters, lower_iters=hg.lower_iters, cg_residual=hg.cg_residual, eps_used=hg.epsilon_used,
+         q=st.q, cg_q=cg.q, cg_res=cg.residual, cg_it=cg.iters, rhs=rhs,
+         fit=up.fit_value(hg.x_tilde), loss=up.loss(hg.x_tilde, b),
+         gnorm=np.linalg.norm(H.upper_fit_grad(hg.x_tilde, up.A, up.y_delta)))
+
+    # 1-D deconvolution: solve, hypergradient, a short MAID run
+    up = P.build_deconv1d(seed=1, n=80, num_pieces=5)
+    p = up.lower_problem(up.b0)
+    mu = L.mu_of_b(p, up.mu_floor)
+    r = L.solve_lower(p, up.x0, 1e-6, mu, max_iters=300)
+    st = H.WarmState(x=up.x0.copy())
+    hg = H.inexact_hypergradient(up, up.b0, 1e-2, 1e-2, st, cg_max_iters=200)
+    b_star, x_star, tr = M.maid_run(up, M.MAIDConfig(max_upper_iters=8))
+    save("dense1d_run.npz", y_delta=up.y_delta, A=up.A.matrix, x_true=up.ground_truth,
+         solve_x=r.x_tilde, solve_gn=r.grad_norm, solve_iters=r.iters, z=hg.z, hg_x=hg.x_tilde,
+         hg_cg_iters=hg.cg_iters, hg_lower_iters=hg.lower_iters, hg_res=hg.cg_residual,
+         maid_b=b_star.data, maid_x=x_star, maid_loss=np.array(tr.loss), maid_alpha=np.array(tr.alpha),
+         maid_eps=np.array(tr.eps), maid_lower_cum=np.array(tr.lower_iters_cum),
+         maid_cg_cum=np.array(tr.cg_iters_cum), maid_final=tr.final_loss)
+
+
+def config_cases():
+    """The BASELINE c1 and a reduced c2 generated by the repo's own seeded
+    generators, with the reference's answers on them."""
+    from paper_2502_09758_b200 import configs as C
+    import adp
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(HERE)), "oracle"))
+    import adp_oracle as orc
+
+    def ref_blur(x, kernel):
+        return O.ConvOperator(O.Kernel(kernel.data, O.DEPTHWISE2D), x.shape).apply(x)
+
+    up = C.config1(0)
+    refup = P.UpperProblem(name="c1", A=O.DenseOperator(up.A.matrix), a=O.Kernel(up.a.data, O.DENSE1D),
+                           y_delta=up.y_delta, beta=0.0, alpha=1.0, reg=R.SmoothedElasticNet(1.2e-3, 4e-3, 1e-4),
+                           b0=O.Kernel(up.b0.data, O.DENSE1D), x0=up.x0, mu_floor=1e-3, lower_method="agd",
+                           lower_max_iters=300)
+    b_star, x_star, tr = M.maid_run(refup, M.MAIDConfig(max_upper_iters=60))
+    save("c1_maid.npz", y_delta=up.y_delta, A=up.A.matrix, x_true=up.ground_truth, maid_b=b_star.data,
+         maid_x=x_star, maid_loss=np.array(tr.loss), maid_alpha=np.array(tr.alpha), maid_eps=np.array(tr.eps),
+         maid_delta=np.array(tr.delta), maid_grad=np.array(tr.grad_norm),
+         maid_lower_cum=np.array(tr.lower_iters_cum), maid_cg_cum=np.array(tr.cg_iters_cum),
+         maid_final=tr.final_loss)
+    del adp, orc
+
+    up2 = C.config2(0, size=96, blur_fn=ref_blur)
+    ref2 = P.UpperProblem(name="c2s", A=O.ConvOperator(O.Kernel(up2.a.data, O.DEPTHWISE2D), up2.y_delta.shape),
+                          a=O.Kernel(up2.a.data, O.DEPTHWISE2D), y_delta=up2.y_delta, beta=0.3, alpha=0.6,
+                          reg=R.SmoothedTV(1e-4), b0=O.Kernel(up2.b0.data, O.DEPTHWISE2D), x0=up2.x0,
+                          mu_floor=10.0, lower_method="agd", lower_max_iters=1200, lower_adaptive=True)
+    p = ref2.lower_problem(ref2.b0)
+    mu = L.mu_of_b(p, 10.0)
+    r = L.solve_lower(p, ref2.x0, 0.25, mu, max_iters=1200, method="agd", adaptive=True)
+    save("c2_small.npz", y_delta=up2.y_delta, x_true=up2.ground_truth, a=up2.a.data, solve_x=r.x_tilde,
+         solve_gn=r.grad_norm, solve_iters=r.iters, solve_conv=r.converged)
+
+
+if __name__ == "__main__":
+    reductions()
+    conv_case("conv_small.npz", (24, 20, 3), 5, 11)
+    conv_case("conv_k9.npz", (33, 40, 1), 9, 12)
+    conv_case("conv_k15.npz", (40, 37, 3), 15, 13, tiny=False)
+    dense_case("dense_small.npz", 40, 21)
+    solver_cases()
+    config_cases()

@@ -1,0 +1,90 @@
+"""Pin the CPU oracle against the REAL reference (golden fixtures generated
+from /root/reference by tests/golden/make_golden.py).  Runs without a GPU."""
+import numpy as np
+import pytest
+
+SIZES = (1, 5, 8, 17, 31, 100, 128, 129, 255, 1000, 4099, 65536, 90000)
+
+
+def rel(a, b):
+    a, b = np.asarray(a, dtype=float), np.asarray(b, dtype=float)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+@pytest.mark.parametrize("n", SIZES)
+def test_reductions_bitwise(orc, golden, n):
+    d = golden("reductions.npz")
+    a, b = d[f"a{n}"], d[f"b{n}"]
+    assert orc.npsum(a) == float(d[f"sum{n}"])          # numpy pairwise
+    assert orc.ddot(a, b) == float(d[f"dot{n}"])        # OpenBLAS SkylakeX ddot
+    assert orc.ddot(a, b) == float(d[f"vdot{n}"])
+    assert orc.norm(a) == float(d[f"norm{n}"])
+
+
+@pytest.mark.parametrize("name", ["conv_small.npz", "conv_k9.npz", "conv_k15.npz"])
+def test_conv_primitives(orc, golden, name):
+    d = golden(name)
+    op = orc.Conv(d["kern"], d["x"].shape)
+    p = orc.Lower(op, d["y"], float(d["alpha"]), orc.TV(float(d["nu"])))
+    assert np.array_equal(op.apply(d["x"]), d["apply"])
+    assert np.array_equal(op.adjoint(d["v"]), d["adjoint"])
+    assert np.array_equal(op.gram_diag(), d["gram_diag"])
+    assert orc.lower_value(p, d["x"]) == float(d["lower_value"])
+    v, g = orc.lower_value_and_grad(p, d["x"])
+    assert v == float(d["vg_val"]) and np.array_equal(g, d["vg_g"])
+    assert np.array_equal(orc.lower_grad(p, d["x"]), d["lower_grad"])
+    assert orc.TV(1e-4).value(d["x"]) == float(d["tv_value"])
+    assert rel(orc.lower_hess_vec(p, d["x"], d["v"]), d["hess_vec"]) <= 1e-13
+    assert rel(orc.lower_hess_diag(p, d["x"]), d["hess_diag"]) <= 1e-13
+    assert rel(orc.kgc(d["x"], d["v"], False, d["kern"].shape[:2]), d["kgc"]) <= 1e-13
+    lam, conv, _ = orc.op_norm_sq(orc.Conv(d["kern"], d["x"].shape), 300, 1e-4)
+    assert lam == float(d["norm_sq"])
+
+
+def test_dense_primitives(orc, golden):
+    d = golden("dense_small.npz")
+    op = orc.Dense(d["m"])
+    reg = orc.ElasticNet(float(d["l1"]), float(d["l2"]), float(d["nu"]))
+    p = orc.Lower(op, d["y"], 1.0, reg)
+    assert rel(op.apply(d["x"]), d["apply"]) <= 1e-14
+    assert reg.value(d["x"]) == float(d["en_value"])
+    assert np.array_equal(reg.grad(d["x"]), d["en_grad"])
+    v, g = orc.lower_value_and_grad(p, d["x"])
+    assert abs(v - float(d["vg_val"])) <= 1e-14 * abs(v) and rel(g, d["vg_g"]) <= 1e-13
+    assert rel(orc.lower_hess_vec(p, d["x"], d["v"]), d["hess_vec"]) <= 1e-13
+
+
+@pytest.mark.parametrize("tag,method,adaptive", [("agd_ad", "agd", True), ("gd_ad", "proxgrad", True),
+                                                 ("fista", "fista_sc", True), ("agd_fixed", "agd", False),
+                                                 ("agd_ad_conv", "agd", True)])
+def test_solve_lower_bitwise(orc, golden, tag, method, adaptive):
+    """The restated solver reproduces the reference's trajectory bit for bit."""
+    d = golden("solve2d.npz")
+    eps, mu, iters = d[f"{tag}_args"]
+    p = orc.Lower(orc.Conv(d["kern"], d["y_delta"].shape), d["y_delta"], 0.6, orc.TV(1e-4))
+    x, gn, it, conv = orc.solve_lower(p, d["x0"], float(eps), float(mu), int(iters), method, None, adaptive)
+    assert it == int(d[f"{tag}_iters"]) and conv == bool(d[f"{tag}_conv"])
+    assert np.array_equal(x, d[f"{tag}_x"]) and gn == float(d[f"{tag}_gn"])
+
+
+def test_hypergradient_2d(orc, golden):
+    d = golden("hyper2d.npz")
+    d15 = golden("hyper2d_cg15.npz")
+    up = orc.Upper(A_kernel=d["a_kern"], a=d["a_kern"], y_delta=d["y_delta"], beta=0.3, alpha=0.6, reg=orc.TV(1e-4),
+                   b0=d["kern"], x0=d["x0"], dense=False, mu_floor=1e-3, lower_adaptive=True)
+    st = {"x": d["x0"].copy(), "q": None}
+    hg = orc.inexact_hypergradient(up, d["kern"], 0.5, 0.5, st, 15)
+    assert hg["cg_iters"] == int(d15["cg_iters"])
+    assert np.array_equal(hg["x_tilde"], d["x_tilde"])
+    assert rel(hg["z"], d15["z"]) <= 1e-12
+
+
+def test_dense_maid_short_run(orc, golden):
+    d = golden("dense1d_run.npz")
+    up = orc.Upper(A_kernel=d["A"], a=d["A"], y_delta=d["y_delta"], beta=0.0, alpha=1.0,
+                   reg=orc.ElasticNet(1.2e-3, 4e-3, 1e-4), b0=d["A"], x0=np.zeros(80), dense=True)
+    b, x, tr = orc.maid_run(up, dict(max_upper_iters=8))
+    assert tr["lower_iters_cum"] == [int(v) for v in d["maid_lower_cum"]]
+    assert tr["cg_iters_cum"] == [int(v) for v in d["maid_cg_cum"]]
+    assert rel(tr["loss"], d["maid_loss"]) <= 1e-12
+    assert rel(b, d["maid_b"]) <= 1e-12
