@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""Benchmark of the MAID hot path on B200 (contract: see README / DESIGN.md).
+
+Workload (BASELINE.json configs[1], "c2"): 256x256x1 float64 image, 9x9
+stencil, smoothed TV (nu 1e-4, alpha 0.6), adaptive AGD with gradient
+restart, 1,200 lower iterations per solve (eps tiny so the budget is used).
+One STEP = one ``solve_lower`` call exactly as MAID issues it: a fresh
+operator (so the power iteration for L(b) runs), then the whole lower solve.
+
+  value   lower-level Gpixel-iterations/s, inputs resident in HBM, device time
+          (CUDA events around each step, L2 flushed between steps; the
+          working set of c2 is L2-resident within a step).
+  e2e     the same metric through the public API (paper_2502_09758_b200.solve_lower)
+          with host NumPy inputs/outputs, H2D + D2H inside the timed region.
+  N > 1   (torchrun) independent replicas, one instance per GPU ("replicas
+          only": c2 does not shard); max time over ranks.
+
+``--impl reference`` times the CPU oracle (the reference algorithm restated,
+bitwise-pinned to it) on the host cores on a bounded sample of the same
+workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "lower-level Gpixel-iters/s"
+UNIT = "Gpx-it/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--mode", default="strict", choices=["strict", "fast", "fp32"])
+    ap.add_argument("--iters", type=int, default=1200)
+    ap.add_argument("--size", type=int, default=256)
+    ap.add_argument("--maid-steps", type=int, default=2, help="accepted MAID steps for upper iters/s (0: skip)")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the fast-mode / fp32 side measurements")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def oracle_blur(x, kernel):
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import adp_oracle as orc
+    return orc.correlate(x, kernel.data)
+
+
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            time.sleep(0.2)
+            self.proc.terminate()
+            out, _ = self.proc.communicate(timeout=10)
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [t.strip() for t in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        busy = [s for s in sm if s > 0.5 * max(sm)] or sm
+        return {"sm_mhz": float(np.median(busy)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+def cpu_sample(size, iters, seed=0):
+    """Bounded oracle sample: one solve_lower with `iters` iterations on the
+    c2 workload.  Returns (pixel-iterations, seconds)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import adp_oracle as orc
+    from paper_2502_09758_b200 import configs
+    up = configs.config2(seed, size=size, blur_fn=oracle_blur)
+    p = orc.Lower(orc.Conv(up.b0.data, up.y_delta.shape), up.y_delta, 0.6, orc.TV(1e-4))
+    t0 = time.perf_counter()
+    _, _, it, _ = orc.solve_lower(p, up.y_delta, 1e-14, 10.0, iters, "agd", None, True)
+    dt = time.perf_counter() - t0
+    return up.y_delta.size * it, dt
+
+
+def _cpu_worker(a):
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    return cpu_sample(*a)
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import multiprocessing as mp
+    cores = len(os.sched_getaffinity(0))
+    iters = 12
+    rates = []
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(cores) as pool:
+        for s in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            res = pool.map(_cpu_worker, [(args.size, iters, k) for k in range(cores)])
+            dt = time.perf_counter() - t0
+            if s >= args.warmup:
+                rates.append(sum(r[0] for r in res) / dt / 1e9)
+    v = float(np.mean(rates))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"c2: {args.size}x{args.size}x1 f64, 9x9 stencil, TV, adaptive AGD",
+                       "sample": f"{iters} lower iterations per process per step"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": f"{cores} processes x {iters} adaptive-AGD iterations of the CPU oracle "
+                                       "(bitwise-pinned restatement of adp.solve_lower)"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def run_native(args):
+    import torch
+    import torch.distributed as dist
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    import paper_2502_09758_b200 as adp
+    from paper_2502_09758_b200 import _native as nat
+    from paper_2502_09758_b200 import configs
+
+    dtype, mode = ("float32", "fast") if args.mode == "fp32" else ("float64", args.mode)
+    up = configs.config2(rank, size=args.size)
+    adp.set_precision(dtype, mode)
+    N = up.y_delta.size
+    K = up.b0.data.shape[0]
+    eps = 1e-14
+    mu = 10.0
+    x0 = nat.to_dev(up.x0)
+    out = nat.empty_like_dev(up.x0.shape)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")   # 256 MB > L2
+
+    def one_step(stats):
+        p = up.lower_problem(up.b0)   # fresh operator: power iteration included
+        return adp.solve_lower(p, x0, eps, mu, max_iters=args.iters, method="agd", adaptive=True, x_out=out,
+                               stats=stats)
+
+    for _ in range(args.warmup):
+        one_step({})
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    times, units, vals, vgs = [], 0, 0, 0
+    st = torch.cuda.current_stream()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            flush.zero_()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(st)
+            stats = {}
+            r = one_step(stats)
+            e1.record(st)
+            torch.cuda.synchronize()
+            times.append(e0.elapsed_time(e1) / 1e3)
+            units += N * r.iters
+            vals += stats["value_evals"]
+            vgs += stats["vg_evals"]
+    if ws > 1:
+        dist.barrier()
+    t_dev = float(np.sum(times))
+    if ws > 1:
+        tt = torch.tensor([t_dev], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_dev = float(tt.item())
+    value = units * ws / t_dev / 1e9
+
+    # ---- e2e through the public API with host buffers
+    kern_host = up.b0.data.copy()
+    y_host = np.asarray(up.y_delta)
+    x0_host = np.asarray(up.x0)
+
+    def e2e_step():
+        b = adp.Kernel(kern_host, adp.DEPTHWISE2D)
+        p = adp.LowerProblem(adp.ConvOperator(b, y_host.shape), y_host, up.alpha, up.reg)
+        r = adp.solve_lower(p, x0_host, eps, mu, max_iters=args.iters, method="agd", adaptive=True)
+        return r
+
+    e2e_step()
+    torch.cuda.synchronize()
+    e2e_t, e2e_units = 0.0, 0
+    for _ in range(max(1, args.steps)):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r = e2e_step()
+        assert isinstance(r.x_tilde, np.ndarray)
+        e2e_t += time.perf_counter() - t0
+        e2e_units += N * r.iters
+    if ws > 1:
+        tt = torch.tensor([e2e_t], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_t = float(tt.item())
+    esz = 8 if dtype == "float64" else 4
+    e2e = {"value": e2e_units * ws / e2e_t / 1e9, "unit": UNIT,
+           "h2d_bytes_per_step": 2 * N * 8 + kern_host.size * 8, "d2h_bytes_per_step": N * esz,
+           "note": "host float64 NumPy in/out through paper_2502_09758_b200.solve_lower"}
+
+    # ---- roofline of the dominant (only) kernel: conv_solve_kernel
+    iters_total = units / N
+    value_per_it = vals / max(iters_total, 1)
+    flop_px_it = 2.0 * K * K * (2.0 + value_per_it) + 50.0    # 6K^2+50 at one value pass
+    achieved_tf = flop_px_it * units / t_dev / 1e12
+    pk = nat.SolveArgs  # keep linter quiet
+    import ctypes
+    tf = ctypes.c_double()
+    ms = ctypes.c_double()
+    nat.check(nat.lib().adp_fp64_peak(ctypes.byref(tf), ctypes.byref(ms), nat.stream_ptr()), "fp64 peak")
+    peak = tf.value
+    bytes_px_it = 48.0 if dtype == "float64" else 24.0
+    hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    roof = {"bound": "fp64", "achieved": achieved_tf, "peak": peak, "unit": "TFLOP/s",
+            "frac": achieved_tf / peak, "traffic": None,
+            "peak_source": "measured live: DFMA microbenchmark (adp_fp64_peak), 2 flop/DFMA",
+            "flop_per_px_it": flop_px_it, "kernel": "conv_solve_kernel",
+            "note": ("strict mode issues DMUL+DADD per tap (reference rounding), so its attainable fraction "
+                     "of the DFMA roof is <= 0.5" if mode == "strict" and dtype == "float64" else ""),
+            "hbm": {"achieved_gbs": bytes_px_it * units / t_dev / 1e9, "peak_gbs": hbm,
+                    "frac": bytes_px_it * units / t_dev / 1e9 / hbm,
+                    "bytes_per_px_it": bytes_px_it}}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t_dev / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64" if dtype == "float64" else "f32",
+            "data": "synthetic",
+            "config": {"workload": f"c2: {args.size}x{args.size}x1 image, {K}x{K} stencil, smoothed TV, "
+                                   f"adaptive AGD, {args.iters} lower iterations per solve",
+                       "mode": mode, "l2": "flushed between steps (256 MB write)",
+                       "parallelism": f"replicas x{ws}", "value_evals_per_iter": value_per_it,
+                       "vg_evals": vgs},
+            "roofline": roof, "e2e": e2e, "gpu_launches": args.steps, "clocks": clk.summary()}
+
+    # ---- MAID upper iterations / s (c2, reference 2-D settings)
+    if args.maid_steps > 0 and rank == 0:
+        cfg = configs.maid_config("c2")
+        cfg.max_upper_iters = args.maid_steps
+        upm = configs.config2(0, size=args.size)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        b, x, tr = adp.maid_run(upm, cfg)
+        dt = time.perf_counter() - t0
+        line["maid"] = {"metric": "MAID upper iters/s", "value": len(tr) / dt, "accepted": len(tr),
+                        "seconds": dt, "lower_iters_cum": tr.lower_iters_cum[-1] if len(tr) else 0,
+                        "cg_iters_cum": tr.cg_iters_cum[-1] if len(tr) else 0}
+
+    # ---- side measurements: the other precision modes (device time)
+    if not args.no_extra and rank == 0:
+        side = {}
+        for tag, (dt_, md) in {"fast_f64": ("float64", "fast"), "fp32": ("float32", "fast")}.items():
+            if (dt_, md) == (dtype, mode):
+                continue
+            adp.set_precision(dt_, md)
+            x0s = nat.to_dev(up.x0)
+            outs = nat.empty_like_dev(up.x0.shape)
+            p = up.lower_problem(up.b0)
+            adp.solve_lower(p, x0s, eps, mu, max_iters=args.iters, method="agd", adaptive=True, x_out=outs)
+            tt, uu = 0.0, 0
+            for _ in range(3):
+                p = up.lower_problem(up.b0)
+                flush.zero_()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record()
+                r = adp.solve_lower(p, x0s, eps, mu, max_iters=args.iters, method="agd", adaptive=True, x_out=outs)
+                e1.record()
+                torch.cuda.synchronize()
+                tt += e0.elapsed_time(e1) / 1e3
+                uu += N * r.iters
+            side[tag] = {"value": uu / tt / 1e9, "unit": UNIT}
+        adp.set_precision(dtype, mode)
+        line["other_modes"] = side
+
+    # ---- CPU baseline (rank 0, N = 1 only): bounded oracle sample
+    if not args.no_cpu and rank == 0 and ws == 1:
+        iters = 40
+        u, dt = cpu_sample(args.size, iters)
+        line["cpu_baseline"] = {"value": u / dt / 1e9, "unit": UNIT, "cores": 1, "kind": "port",
+                                "sample": f"one CPU-oracle solve_lower, {iters} adaptive-AGD iterations on c2 "
+                                          f"({dt:.1f} s, 1 thread)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_native(a)

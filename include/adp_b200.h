@@ -172,6 +172,9 @@ int adp_dot(adp_plan* p, const void* a, const void* b, double* out, void* stream
 int adp_vec(int32_t op, int64_t n, int32_t dtype, double a, const void* x, const void* y, void* out,
             double* red_out, void* stream);
 
+/* ---- FP64 roof: sustained DFMA throughput (TFLOP/s, 2 flop per DFMA) of this device ---- */
+int adp_fp64_peak(double* tflops, double* ms, void* stream);
+
 /* ---- host-only introspection (no device): the deterministic-sum layout for n
  * elements (np_rule = 1: NumPy pairwise leaves of <= 128; 0: binary over n items):
  * leaf starts, subtree cut and the tree programs the kernels evaluate. */

@@ -128,9 +128,47 @@ __device__ __forceinline__ double np_leaf_warp(const Src& src, int64_t s, int n)
   return t;
 }
 
+// Regular layout (all leaves of length L, L % 8 == 0): one thread per
+// accumulator chain r[k] (8 per leaf, 4 leaves per warp), then the fixed
+// combine ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)) by xor-shuffles inside each
+// 8-lane group (addition is commutative, so pairing order is irrelevant).
+template <class Src>
+__device__ void np_leaves_regular(const SumDev& s, const Src& src) {
+  const int L = s.leaf_len;
+  const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+  const int64_t total = (int64_t)s.nLeaves * 8;
+  const int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (int64_t g0 = 0; g0 < total; g0 += nthreads) {
+    const int64_t g = g0 + base;       // warp-uniform loop trip count (total % 8 == 0)
+    const bool act = g < total;
+    const int64_t leaf = g >> 3;
+    const int k = (int)(g & 7);
+    double acc = 0.0;
+    if (act) {
+      // L <= 128: issue all (<= 16) loads of the chain, then add in order
+      const int64_t e0 = leaf * L + k;
+      double v[16];
+#pragma unroll
+      for (int m = 0; m < 16; ++m) v[m] = (8 * m < L) ? src(e0 + 8 * m) : 0.0;
+      acc = v[0];
+#pragma unroll
+      for (int m = 1; m < 16; ++m)
+        if (8 * m < L) acc = acc + v[m];
+    }
+    acc = acc + __shfl_xor_sync(kFull, acc, 1);
+    acc = acc + __shfl_xor_sync(kFull, acc, 2);
+    acc = acc + __shfl_xor_sync(kFull, acc, 4);
+    if (act && k == 0) s.leaf_vals[leaf] = acc;
+  }
+}
+
 // All leaves of an element sum, distributed over every warp of the grid.
 template <class Src>
 __device__ void np_leaves(const SumDev& s, const Src& src) {
+  if (s.regular) {
+    np_leaves_regular(s, src);
+    return;
+  }
   const int wpb = blockDim.x >> 5;
   const int gw = blockIdx.x * wpb + (threadIdx.x >> 5);
   const int nw = gridDim.x * wpb;
@@ -160,9 +198,71 @@ __device__ __forceinline__ double eval_prog(const int* __restrict__ prog, double
   return r;
 }
 
+// Perfect binary tree over vals[0..n), zero-padded to the next power of two,
+// evaluated by one CTA (blockDim a power of two): values staged in shared
+// memory, each thread folds a contiguous power-of-two chunk with a binary
+// counter (exact perfect-tree order), then xor-shuffles across lanes and
+// warps.  Result valid in every thread.
+__device__ __forceinline__ double tree_reduce_cta(const double* __restrict__ vals, int n, double* sv, double* red) {
+  int P = 1;
+  while (P < n) P <<= 1;
+  const int BD = blockDim.x;
+  const int T = 1 << (31 - __clz(BD));          // folding threads: largest power of two <= blockDim
+  const int chunk = P > T ? P / T : 1;
+  for (int k0 = threadIdx.x; k0 < P; k0 += 8 * BD) {
+    double v[8];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+      const int k = k0 + b * BD;
+      v[b] = k < n ? ldcg(vals + k) : 0.0;
+    }
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+      if (k0 + b * BD < P) sv[k0 + b * BD] = v[b];
+  }
+  __syncthreads();
+  double root = 0.0;
+  if (threadIdx.x * chunk < P) {
+    const double* c = sv + threadIdx.x * chunk;
+    double st[14];
+#pragma unroll
+    for (int lv = 0; lv < 14; ++lv) st[lv] = 0.0;
+    for (int i = 0; i < chunk; ++i) {
+      double v = c[i];
+#pragma unroll
+      for (int lv = 0; lv < 14; ++lv) {
+        if ((i >> lv) & 1) {
+          v = st[lv] + v;
+        } else {
+          st[lv] = v;
+          break;
+        }
+      }
+      root = v;
+    }
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) root = root + __shfl_xor_sync(kFull, root, o);
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = BD >> 5;
+  if (lane == 0) red[warp] = root;
+  __syncthreads();
+  if (warp == 0) {
+    double t = lane < nw ? red[lane] : 0.0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) t = t + __shfl_xor_sync(kFull, t, o);
+    if (lane == 0) red[32] = t;
+  }
+  __syncthreads();
+  const double r = red[32];
+  __syncthreads();
+  return r;
+}
+
 // Evaluate a single-level sum (nSub == 1) redundantly in this CTA.
 __device__ __forceinline__ double sum_single(const SumDev& s, double* sv) {
   if (s.nLeaves == 0) return 0.0;
+  if (s.regular) return tree_reduce_cta(s.leaf_vals, s.nLeaves, sv, sv + 4096);
   for (int k = threadIdx.x; k < s.nLeaves; k += blockDim.x) sv[k] = ldcg(s.leaf_vals + k);
   __syncthreads();
   return eval_prog(s.progs + s.top_prog, sv);
@@ -171,6 +271,14 @@ __device__ __forceinline__ double sum_single(const SumDev& s, double* sv) {
 // Two-level sums: phase 1 (subtrees, distributed), grid barrier, phase 2 (top).
 __device__ __forceinline__ void sum_phase1(const SumDev& s, double* sv) {
   if (s.nSub <= 1) return;
+  if (s.regular) {
+    for (int t = blockIdx.x; t < s.nSub; t += gridDim.x) {
+      const int a = t * s.sub_size;
+      const double r = tree_reduce_cta(s.leaf_vals + a, min(s.sub_size, s.nLeaves - a), sv, sv + 4096);
+      if (threadIdx.x == 0) s.sub_vals[t] = r;
+    }
+    return;
+  }
   for (int t = blockIdx.x; t < s.nSub; t += gridDim.x) {
     const int l0 = s.sub_leaf[t], l1 = s.sub_leaf[t + 1];
     for (int k = threadIdx.x; k < l1 - l0; k += blockDim.x) sv[k] = ldcg(s.leaf_vals + l0 + k);
@@ -182,15 +290,21 @@ __device__ __forceinline__ void sum_phase1(const SumDev& s, double* sv) {
 
 __device__ __forceinline__ double sum_phase2(const SumDev& s, double* sv) {
   if (s.nSub <= 1) return sum_single(s, sv);
+  if (s.regular) return tree_reduce_cta(s.sub_vals, s.nSub, sv, sv + 4096);
   for (int k = threadIdx.x; k < s.nSub; k += blockDim.x) sv[k] = ldcg(s.sub_vals + k);
   __syncthreads();
   return eval_prog(s.progs + s.top_prog, sv);
 }
 
-// Reduce k sums: phase 1 for all, one barrier if any is two-level, then
-// phase 2 for all.  out[i] valid in every thread of every CTA.
-static __device__ __noinline__ void reduce_list(const SumDev* const* ss, int k, double* out, double* sv,
-                                         GridBarrier& gb) {
+
+// Reduce k (<= 8) sums: phase 1 (distributed subtrees) for two-level sums and
+// one grid barrier if there are any; then every regular sum (its leaves, or
+// its subtree roots) is folded in ONE batched CTA pass — all loads in
+// flight together, one shuffle/smem exchange for all sums; irregular
+// (program) sums fall back to the level-by-level evaluator.  out[i] valid in
+// every thread of every CTA.
+__device__ __forceinline__ void reduce_list(const SumDev* const* ss, int k, double* out, double* sv,
+                                            GridBarrier& gb) {
   bool two = false;
   for (int i = 0; i < k; ++i) {
     if (ss[i]->nSub > 1) {
@@ -199,7 +313,85 @@ static __device__ __noinline__ void reduce_list(const SumDev* const* ss, int k, 
     }
   }
   if (two) gb.sync();
-  for (int i = 0; i < k; ++i) out[i] = sum_phase2(*ss[i], sv);
+  const int BD = blockDim.x;
+  const int T = 1 << (31 - __clz(BD));          // folding threads (power of two)
+  int P[8], base[8], n[8];
+  int total = 0;
+  for (int i = 0; i < k; ++i) {
+    const SumDev& s = *ss[i];
+    n[i] = s.regular ? (s.nSub > 1 ? s.nSub : s.nLeaves) : 0;
+    int p = 1;
+    while (p < n[i]) p <<= 1;
+    P[i] = s.regular ? p : 0;
+    base[i] = total;
+    total += P[i];
+  }
+  if (total > kTreeStage) {
+    for (int i = 0; i < k; ++i) out[i] = sum_phase2(*ss[i], sv);
+    return;
+  }
+  // stage all regular sums, 8 loads in flight per thread
+  for (int i = 0; i < k; ++i) {
+    if (!P[i]) continue;
+    const SumDev& s = *ss[i];
+    const double* src = s.nSub > 1 ? s.sub_vals : s.leaf_vals;
+    for (int k0 = threadIdx.x; k0 < P[i]; k0 += 8 * BD) {
+      double v[8];
+#pragma unroll
+      for (int b = 0; b < 8; ++b) {
+        const int e = k0 + b * BD;
+        v[b] = e < n[i] ? ldcg(src + e) : 0.0;
+      }
+#pragma unroll
+      for (int b = 0; b < 8; ++b)
+        if (k0 + b * BD < P[i]) sv[base[i] + k0 + b * BD] = v[b];
+    }
+  }
+  __syncthreads();
+  double* red = sv + kTreeStage;   // 8 x 32 warp partials + 8 results
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = BD >> 5;
+  for (int i = 0; i < k; ++i) {
+    if (!P[i]) continue;
+    const int chunk = P[i] > T ? P[i] / T : 1;
+    double root = 0.0;
+    if (threadIdx.x * chunk < P[i]) {
+      const double* c = sv + base[i] + threadIdx.x * chunk;
+      double st[14];
+#pragma unroll
+      for (int lv = 0; lv < 14; ++lv) st[lv] = 0.0;
+      for (int e = 0; e < chunk; ++e) {
+        double v = c[e];
+#pragma unroll
+        for (int lv = 0; lv < 14; ++lv) {
+          if ((e >> lv) & 1) {
+            v = st[lv] + v;
+          } else {
+            st[lv] = v;
+            break;
+          }
+        }
+        root = v;
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) root = root + __shfl_xor_sync(kFull, root, o);
+    if (lane == 0) red[i * 32 + warp] = root;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    for (int i = 0; i < k; ++i) {
+      if (!P[i]) continue;
+      double t = lane < nw ? red[i * 32 + lane] : 0.0;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) t = t + __shfl_xor_sync(kFull, t, o);
+      if (lane == 0) red[256 + i] = t;
+    }
+  }
+  __syncthreads();
+  for (int i = 0; i < k; ++i) out[i] = P[i] ? red[256 + i] : 0.0;
+  __syncthreads();
+  for (int i = 0; i < k; ++i)
+    if (!ss[i]->regular) out[i] = sum_phase2(*ss[i], sv);
 }
 
 // Tile partial (ddot-type): per-thread accumulation in a fixed order then

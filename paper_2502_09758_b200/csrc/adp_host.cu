@@ -109,7 +109,7 @@ int ProgPool::add(const std::string& key, const std::vector<int>& prog) {
   return off;
 }
 
-void build_sum(SumHost& s, int64_t n, bool np, ProgPool& pool) {
+void build_sum(SumHost& s, int64_t n, bool np, ProgPool& pool, bool allow_regular) {
   s.n = n;
   s.np = np;
   LeafCounter cnt{np, {}};
@@ -139,6 +139,32 @@ void build_sum(SumHost& s, int64_t n, bool np, ProgPool& pool) {
     s.leaf_start.push_back(n);
   }
   s.nLeaves = (int)cnt(n);
+  // regular: perfect tree (element sums: equal leaves, L % 8 == 0, pow2 count;
+  // tile sums: always, zero-padded) -> register/shuffle evaluation on device
+  s.regular = 0;
+  s.leaf_len = 0;
+  if (np) {
+    const int64_t L = s.leaf_start[1] - s.leaf_start[0];
+    bool eq = (L % 8 == 0);
+    for (size_t i = 1; eq && i + 1 < s.leaf_start.size(); ++i) eq = (s.leaf_start[i + 1] - s.leaf_start[i]) == L;
+    const bool pow2 = (s.nLeaves & (s.nLeaves - 1)) == 0;
+    if (allow_regular && eq && pow2) { s.regular = 1; s.leaf_len = (int)L; }
+  } else {
+    s.regular = allow_regular ? 1 : 0;
+  }
+  if (s.regular) {
+    int64_t P = 1;
+    while (P < s.nLeaves) P <<= 1;
+    s.sub_size = 2048;
+    s.nSub = P <= 4096 ? 1 : (int)((s.nLeaves + 2047) / 2048);
+    s.sub_leaf.clear();
+    s.sub_prog.clear();
+    for (int t = 0; t <= s.nSub; ++t) s.sub_leaf.push_back(std::min<int64_t>((int64_t)t * 2048, s.nLeaves));
+    for (int t = 0; t < s.nSub; ++t) s.sub_prog.push_back(0);
+    if (s.nSub == 1) s.sub_leaf = {0, s.nLeaves};
+    s.top_prog = 0;
+    return;
+  }
   const std::string tag = np ? "np" : "bin";
   auto leafterm = [&](int64_t m) { return is_leaf(np, m); };
   if (s.nLeaves <= kMaxProgLeaves) {
@@ -181,28 +207,54 @@ static int device_props(int& sms, size_t& smem_optin) {
 
 static constexpr int kRW = 4;
 
-static void choose_tiles(const adp_plan_desc& d, int& TH, int& TW) {
+// Tile choice.  When the NumPy-pairwise layout of N elements is regular
+// (equal leaves of L elements, power-of-two count) and a tile row can hold
+// whole leaves (W*C % L == 0), the tile width is a multiple of L/C-aligned
+// element runs so every tile computes its own leaves ("fused").
+static void choose_tiles(const adp_plan_desc& d, int leafL, int& TH, int& TW, int& fused) {
   const int64_t px = (int64_t)d.H * d.W;
+  fused = 0;
   if (d.tile_w > 0 && d.tile_h > 0) {
     TH = d.tile_h;
     TW = d.tile_w;
-    return;
+  } else {
+    TW = 64;
+    if (d.W <= 32) TW = 32;
+    TH = px >= (1 << 20) ? 16 : 8;
+    if (d.kh >= 25) TH = 8;
+    if (leafL > 0 && ((int64_t)d.W * d.C) % leafL == 0) {
+      // smallest width (multiple of 32 px) holding whole leaves, >= 64 px if the image allows
+      for (int tw = 32; tw <= 512; tw += 32) {
+        if (((int64_t)tw * d.C) % leafL == 0 && (tw >= 64 || tw >= d.W)) {
+          TW = tw;
+          break;
+        }
+      }
+      TH = std::max(1, 512 / TW);    // 128 threads at RW = 4
+      if (px >= (1 << 20) && d.kh < 25 && TW <= 64) TH = 16;
+    }
   }
-  TW = 64;
-  if (d.W <= 32) TW = 32;
-  TH = px >= (1 << 20) ? 16 : 8;
-  if (d.kh >= 25) TH = 8;
+  if (leafL > 0 && ((int64_t)d.W * d.C) % leafL == 0 && ((int64_t)TW * d.C) % leafL == 0) fused = 1;
 }
 
-static size_t conv_smem(const ConvGeom& g, int esize) {
+// Dynamic shared-memory layout (byte offsets; see ConvGeom).
+static size_t conv_smem(ConvGeom& g, int esize) {
   const size_t nk = (size_t)g.kh * g.kw * g.C;
-  size_t off = 64 * sizeof(double);
-  off += ((nk * esize + 15) & ~size_t(15)) * 2;
-  const int QP = (g.TW + 1) + ((g.TW + 1) >> 2) + 1;
-  const size_t pa = (size_t)g.C * g.SH * g.SWP * esize;
-  const size_t q = 2 * (size_t)g.C * (g.TH + 1) * QP * esize;
-  size_t region = std::max(pa + q, (size_t)(2 * kMaxProgLeaves) * sizeof(double));
-  return off + region;
+  size_t off = 64 * sizeof(double);                  // red
+  g.o_ws = (int)off;
+  off += (nk * esize + 15) & ~size_t(15);
+  g.o_wf = (int)off;
+  off += (nk * esize + 15) & ~size_t(15);
+  const size_t R0 = off;
+  g.QP = 0;   // TV Q values are staged through registers into the plane region
+  const size_t pa = ((size_t)g.C * g.SH * g.SWP * esize + 15) & ~size_t(15);
+  const size_t tm = g.fused ? (size_t)3 * g.TH * g.TW * g.C * sizeof(double) : 0;
+  g.o_pa = (int)R0;
+  g.o_pq = (int)R0;
+  g.o_tm = (int)(R0 + pa);
+  g.o_sv = (int)R0;
+  const size_t region = std::max(pa + tm, (size_t)(kTreeStage + 512) * sizeof(double));
+  return R0 + region;
 }
 
 template <typename T>
@@ -210,6 +262,9 @@ static void fill_sum(SumDev& sd, const SumHost& sh, const int* d_progs, const in
                      int* d_subprog, double* leaf_vals, double* sub_vals) {
   sd.nLeaves = sh.nLeaves;
   sd.nSub = sh.nSub;
+  sd.regular = sh.regular;
+  sd.sub_size = sh.sub_size;
+  sd.leaf_len = sh.leaf_len;
   sd.top_prog = sh.top_prog;
   sd.leaf_start = d_leaf;
   sd.sub_leaf = d_subleaf;
@@ -237,10 +292,21 @@ static int conv_plan_init(PlanImpl& P) {
   ConvGeom& g = P.g;
   g.H = d.H; g.W = d.W; g.C = d.C; g.kh = d.kh; g.kw = d.kw;
   g.rh = d.kh / 2; g.rw = d.kw / 2;
-  choose_tiles(d, g.TH, g.TW);
+  {
+    ProgPool tmp;
+    SumHost s;
+    build_sum(s, (int64_t)d.H * d.W * d.C, true, tmp);
+    g.leafL = s.regular ? s.leaf_len : 0;
+  }
+  choose_tiles(d, g.leafL, g.TH, g.TW, g.fused);
   if (g.TW % kRW) return fail(ADP_ERR_ARG, "tile width must be a multiple of 4");
-  g.threads = g.TH * g.TW / kRW;
-  if (g.threads % 32 || g.threads > 512) return fail(ADP_ERR_ARG, "tile must map to 32..512 threads");
+  if (d.tile_h <= 0)
+    while (g.TH > 1 && g.TH * (g.TW / kRW) * g.C > 512) g.TH /= 2;   // channel-parallel CTA <= 512 threads
+  g.tpc = g.TH * g.TW / kRW;
+  g.threads = g.tpc * g.C;
+  g.magicC = (unsigned)((1u << 20) + g.C - 1) / (unsigned)g.C;
+  if (g.tpc % 32 || g.threads > 512)
+    return fail(ADP_ERR_ARG, "tile must map to 32-thread multiples per channel and <= 512 threads");
   g.tilesH = (g.H + g.TH - 1) / g.TH;
   g.tilesW = (g.W + g.TW - 1) / g.TW;
   g.nTiles = g.tilesH * g.tilesW;
@@ -807,7 +873,7 @@ extern "C" int adp_sum_layout(int64_t n, int32_t np_rule, int64_t* n_leaves, int
   adp::build_sum(s, n, np_rule != 0, pool);
   *n_leaves = s.nLeaves;
   *n_sub = s.nSub;
-  *top_prog = s.top_prog;
+  *top_prog = s.regular ? -1 : s.top_prog;   // -1: perfect tree (zero-padded), subtrees of 2048 leaves
   *n_words = (int64_t)pool.words.size();
   if ((int64_t)s.leaf_start.size() > leaf_cap || (int64_t)s.sub_leaf.size() > sub_cap + 1 ||
       (int64_t)pool.words.size() > words_cap)

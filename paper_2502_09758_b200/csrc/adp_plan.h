@@ -17,6 +17,7 @@ struct SumHost {
   std::vector<int> sub_leaf, sub_prog;
   int top_prog = 0;
   int nLeaves = 0, nSub = 1;
+  int regular = 0, sub_size = 0, leaf_len = 0;
 };
 
 // Programs for all sums of a plan live in one int32 buffer.
@@ -26,7 +27,7 @@ struct ProgPool {
   int add(const std::string& key, const std::vector<int>& prog);
 };
 
-void build_sum(SumHost& s, int64_t n, bool np, ProgPool& pool);
+void build_sum(SumHost& s, int64_t n, bool np, ProgPool& pool, bool allow_regular = true);
 
 struct KernelInfo {
   const void* fn = nullptr;

@@ -21,7 +21,11 @@ struct SumDev {
   int nLeaves;
   int nSub;
   int top_prog;            // offset (in ints) of the top program in progs
-  int pad_;
+  int regular;             // 1: perfect binary tree over nLeaves (pow2 after zero padding for
+                           //    tile sums; exact for element sums with equal leaves) -> evaluated
+                           //    in registers / shuffles, subtrees of sub_size leaves
+  int sub_size;            // regular two-level: leaves per subtree (pow2)
+  int leaf_len;            // regular element sums: common leaf length (elements)
   const int64_t* leaf_start;  // nLeaves+1 element offsets (element sums only)
   const int* sub_leaf;     // nSub+1 leaf boundaries
   const int* sub_prog;     // nSub program offsets
@@ -31,6 +35,7 @@ struct SumDev {
 };
 
 constexpr int kMaxProgLeaves = 2048;   // smem tree evaluation capacity (nL + nI <= 4095)
+constexpr int kTreeStage = 4096;       // doubles of CTA tree staging; then 512 doubles of scratch
 
 // regularizer kinds (regularizers.py:75-199)
 enum RegKind : int { REG_TV = 0, REG_ELASTIC = 1 };
@@ -56,6 +61,13 @@ struct ConvGeom {
   int YSH, YSWP;           // small (1-halo) plane rows / pitch
   int threads;             // CTA size = TH * TW / RW
   int grid;                // persistent grid size (co-resident)
+  int fused;               // 1: NumPy-pairwise leaves computed inside the tiles (regular,
+                           //    tile-aligned layout); 0: global term arrays + leaf pass
+  int leafL;               // common leaf length (elements) when fused
+  int QP;                  // pitch of the TV Q planes
+  int tpc;                 // threads per channel (TH * TW / RW); CTA = tpc * C threads
+  unsigned magicC;         // ceil(2^20 / C): px = (e * magicC) >> 20 for e < 2^15
+  int o_ws, o_wf, o_pa, o_pq, o_tm, o_sv;   // byte offsets in dynamic smem
   int64_t N;               // H*W*C
 };
 

@@ -13,21 +13,32 @@
 //     stages the tile plus halo in shared memory as channel planes with a
 //     skewed row layout (one pad per RW elements) so the register-blocked
 //     stencil (RW outputs per thread, sliding window) is bank-conflict free.
+//     Threads are channel-parallel: thread = (channel, row, RW-column group).
+//     Loaders walk tile rows warp by warp (coalesced, no integer division),
+//     with 8 loads in flight per lane.  Shared memory is addressed through
+//     byte offsets from the dynamic window (LDS/STS, never generic).
 //   * Strict mode reproduces scipy.ndimage.correlate bit for bit: taps in
 //     row-major order, acc = 0.0 then acc + x*w (no FMA), taps with
 //     |w| <= DBL_EPSILON skipped.  Fast mode uses FMA.
 //   * Element sums the reference takes with np.sum use NumPy's pairwise
-//     tree (bitwise); ddot-type sums (norms, vdot) use fixed per-tile trees.
+//     tree (bitwise).  When the layout is regular and leaf-aligned with the
+//     tiles, each tile computes its leaves from shared memory ("fused");
+//     otherwise the terms go to global memory and a leaf pass follows.
+//     ddot-type sums (norms, vdot) use fixed per-tile trees.
 #pragma once
 #include "adp_device.cuh"
 #include "conv2d_args.h"
 
 namespace adp {
 
+__device__ __forceinline__ unsigned char* dsm() {
+  extern __shared__ __align__(16) unsigned char adp_dyn_smem[];
+  return adp_dyn_smem;
+}
+
 // ---------------------------------------------------------------------------
-// value sources used by the tile loaders (all compute exactly the reference
-// expression for one element)
-template <typename T> struct SrcZero { __device__ T operator()(int64_t) const { return T(0); } };
+// value sources used by the tile loaders (each computes exactly the
+// reference expression for one element)
 template <typename T> struct SrcOnes { __device__ T operator()(int64_t) const { return T(1); } };
 template <typename T> struct SrcLin {
   const T* x;
@@ -69,118 +80,128 @@ template <typename T> struct SrcCGDir {
   }
 };
 
+template <typename T> struct SqOf {
+  const T* p;
+  __device__ double operator()(int64_t i) const {
+    const T v = ldcg(p + i);
+    return (double)(v * v);
+  }
+};
+template <typename T> struct Plain {
+  const T* p;
+  __device__ double operator()(int64_t i) const { return (double)ldcg(p + i); }
+};
+
 // ---------------------------------------------------------------------------
 template <typename T, bool FAST, int RW>
 struct Conv {
   static_assert((RW & (RW - 1)) == 0, "RW must be a power of two");
   static constexpr int kShift = RW == 1 ? 0 : RW == 2 ? 1 : RW == 4 ? 2 : 3;
+  static constexpr int kB = 8;   // loads in flight per lane in the tile loaders
 
   const ConvArgs<T>& a;
-  const ConvGeom& g;
-  T* ws;       // C x kh x kw  (taps, tiny taps zeroed)
-  T* wf;       // flipped
-  T* pa;       // plane set A: C x SH x SWP
-  T* pb;       // small planes (1-halo) C x YSH x YSWP, or Q planes
-  T* pq;       // Q planes 2 x C x (TH+1) x QP
-  double* sv;  // tree scratch
-  double* red; // 33 doubles
-  int QP;
-  int ty, tx;
+  int ch, ty, tx;                // this thread's channel, tile row, column group
 
   __device__ static __forceinline__ int sk(int col) { return col + (col >> kShift); }
 
-  __device__ Conv(const ConvArgs<T>& a_, unsigned char* smem) : a(a_), g(a_.g) {
-    const int nk = g.kh * g.kw * g.C;
-    size_t off = 0;
-    red = reinterpret_cast<double*>(smem);
-    off += 64 * sizeof(double);
-    ws = reinterpret_cast<T*>(smem + off);
-    off += ((size_t)nk * sizeof(T) + 15) & ~size_t(15);
-    wf = reinterpret_cast<T*>(smem + off);
-    off += ((size_t)nk * sizeof(T) + 15) & ~size_t(15);
-    unsigned char* region = smem + off;
-    sv = reinterpret_cast<double*>(region);
-    pa = reinterpret_cast<T*>(region);
-    const size_t pa_elems = (size_t)g.C * g.SH * g.SWP;
-    pb = pa + pa_elems;
-    QP = (g.TW + 1) + ((g.TW + 1) >> kShift) + 1;
-    pq = pb;  // Q planes live after plane set A (stage A only)
-    const int tpr = g.TW / RW;
-    ty = threadIdx.x / tpr;
-    tx = threadIdx.x % tpr;
+  __device__ explicit Conv(const ConvArgs<T>& a_) : a(a_) {
+    const int tpr = a.g.TW / RW;
+    ch = threadIdx.x / a.g.tpc;
+    const int r = threadIdx.x - ch * a.g.tpc;
+    ty = r / tpr;
+    tx = r - ty * tpr;
   }
+
+  // ---- shared-memory views (byte offsets from the dynamic window)
+  __device__ __forceinline__ double* red() const { return reinterpret_cast<double*>(dsm()); }
+  __device__ __forceinline__ T* ws() const { return reinterpret_cast<T*>(dsm() + a.g.o_ws); }
+  __device__ __forceinline__ T* wf() const { return reinterpret_cast<T*>(dsm() + a.g.o_wf); }
+  __device__ __forceinline__ T* pa() const { return reinterpret_cast<T*>(dsm() + a.g.o_pa); }
+  __device__ __forceinline__ double* tm() const { return reinterpret_cast<double*>(dsm() + a.g.o_tm); }
+  __device__ __forceinline__ double* sv() const { return reinterpret_cast<double*>(dsm() + a.g.o_sv); }
+  __device__ __forceinline__ T* plane(int c) const { return pa() + (size_t)c * a.g.SH * a.g.SWP; }
 
   // ---- weights: ws[c][i][j] = kern[i][j][c] (|w| <= eps -> 0), wf flipped
   __device__ void load_weights(const T* kern) {
-    const int kh = g.kh, kw = g.kw, C = g.C, nk = kh * kw * C;
+    const int kh = a.g.kh, kw = a.g.kw, C = a.g.C, nk = kh * kw * C;
+    T* s = ws();
+    T* f = wf();
     for (int e = threadIdx.x; e < nk; e += blockDim.x) {
       const int c = e % C, ij = e / C, i = ij / kw, j = ij % kw;
       T w = kern[e];
       if (!(fabs((double)w) > kDblEps)) w = T(0);  // ndimage: only |w| > DBL_EPSILON taps
-      ws[(c * kh + i) * kw + j] = w;
-      wf[(c * kh + (kh - 1 - i)) * kw + (kw - 1 - j)] = w;
+      s[(c * kh + i) * kw + j] = w;
+      f[(c * kh + (kh - 1 - i)) * kw + (kw - 1 - j)] = w;
     }
     __syncthreads();
   }
   // squared flipped taps (gram_diag: correlate(ones, flipped**2), operators.py:120-122)
   __device__ void load_weights_sq(const T* kern) {
-    const int kh = g.kh, kw = g.kw, C = g.C, nk = kh * kw * C;
+    const int kh = a.g.kh, kw = a.g.kw, C = a.g.C, nk = kh * kw * C;
+    T* f = wf();
+    __syncthreads();
     for (int e = threadIdx.x; e < nk; e += blockDim.x) {
       const int c = e % C, ij = e / C, i = ij / kw, j = ij % kw;
       T w = kern[e];
       w = w * w;
       if (!(fabs((double)w) > kDblEps)) w = T(0);
-      wf[(c * kh + (kh - 1 - i)) * kw + (kw - 1 - j)] = w;
+      f[(c * kh + (kh - 1 - i)) * kw + (kw - 1 - j)] = w;
     }
     __syncthreads();
   }
 
   __device__ __forceinline__ void tile_origin(int tile, int& h0, int& w0) const {
-    h0 = (tile / g.tilesW) * g.TH;
-    w0 = (tile % g.tilesW) * g.TW;
+    h0 = (tile / a.g.tilesW) * a.g.TH;
+    w0 = (tile % a.g.tilesW) * a.g.TW;
   }
-  __device__ __forceinline__ T* plane(T* base, int c) const { return base + (size_t)c * g.SH * g.SWP; }
+  __device__ __forceinline__ int64_t gidx(int h, int w, int c) const {
+    return ((int64_t)h * a.g.W + w) * a.g.C + c;
+  }
 
-  // ---- load tile + (r+1) halo of all channels into plane set `dst`
+  // ---- load tile + (r+1) halo of all channels into the planes.  One warp
+  // per tile row (a contiguous run of global memory), lanes over elements,
+  // kB loads per lane in flight before any store.
   template <class Src>
-  __device__ void load_full(T* dst, int h0, int w0, const Src& src) const {
-    const int C = g.C, SWL = g.TW + 2 * g.rw + 2, rowE = SWL * C;
-    const int total = g.SH * rowE;
-    const int gh0 = h0 - g.rh - 1, gw0 = w0 - g.rw - 1;
-    for (int k = threadIdx.x; k < total; k += blockDim.x) {
-      const int sr = k / rowE, e = k - sr * rowE;
-      const int px = e / C, c = e - px * C;
-      const int gh = gh0 + sr, gw = gw0 + px;
-      T v = T(0);
-      if (gh >= 0 && gh < g.H && gw >= 0 && gw < g.W) v = src(((int64_t)gh * g.W + gw) * C + c);
-      dst[(size_t)c * g.SH * g.SWP + sr * g.SWP + sk(px)] = v;
-    }
-  }
-  // ---- load tile + 1 halo into small planes (pitch YSWP)
-  template <class Src>
-  __device__ void load_small(T* dst, int h0, int w0, const Src& src) const {
-    const int C = g.C, SWL = g.TW + 2, rowE = SWL * C;
-    const int total = g.YSH * rowE;
-    for (int k = threadIdx.x; k < total; k += blockDim.x) {
-      const int sr = k / rowE, e = k - sr * rowE;
-      const int px = e / C, c = e - px * C;
-      const int gh = h0 - 1 + sr, gw = w0 - 1 + px;
-      T v = T(0);
-      if (gh >= 0 && gh < g.H && gw >= 0 && gw < g.W) v = src(((int64_t)gh * g.W + gw) * C + c);
-      dst[(size_t)c * g.YSH * g.YSWP + sr * g.YSWP + sk(px)] = v;
+  __device__ void load_full(int h0, int w0, const Src& src) const {
+    const int C = a.g.C, SWL = a.g.TW + 2 * a.g.rw + 2, rowE = SWL * C, H = a.g.H, W = a.g.W;
+    const int SH = a.g.SH, SWP = a.g.SWP;
+    const unsigned magic = a.g.magicC;
+    const int gh0 = h0 - a.g.rh - 1, gw0 = w0 - a.g.rw - 1;
+    const int lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    T* dst = pa();
+    for (int sr = threadIdx.x >> 5; sr < SH; sr += nwarps) {
+      const int gh = gh0 + sr;
+      const bool rowok = gh >= 0 && gh < H;
+      const int64_t gbase = ((int64_t)gh * W + gw0) * C;
+      for (int e0 = lane; e0 < rowE; e0 += 32 * kB) {
+        T v[kB];
+        int off[kB];
+#pragma unroll
+        for (int b = 0; b < kB; ++b) {
+          const int e = e0 + 32 * b;
+          const int px = (int)(((unsigned long long)e * magic) >> 20);
+          const int c = e - px * C;
+          const int gw = gw0 + px;
+          off[b] = e < rowE ? c * SH * SWP + sr * SWP + sk(px) : -1;
+          v[b] = (e < rowE && rowok && gw >= 0 && gw < W) ? src(gbase + e) : T(0);
+        }
+#pragma unroll
+        for (int b = 0; b < kB; ++b)
+          if (off[b] >= 0) dst[off[b]] = v[b];
+      }
     }
   }
 
   // ---- register-blocked correlation: RW consecutive outputs (row ty, cols
-  // tx*RW..) of one channel plane with stencil w (kh x kw).  Per output the
-  // taps are accumulated in row-major order starting from 0.
+  // tx*RW..) of the thread's channel plane with stencil w (kh x kw).  Per
+  // output the taps are accumulated in row-major order starting from 0.
   __device__ __forceinline__ void stencil(const T* __restrict__ pl, const T* __restrict__ w, T (&acc)[RW]) const {
 #pragma unroll
     for (int o = 0; o < RW; ++o) acc[o] = T(0);
-    const int kh = g.kh, kw = g.kw;
-    const T* base = pl + (ty + 1) * g.SWP + tx * (RW + 1);
+    const int kh = a.g.kh, kw = a.g.kw, SWP = a.g.SWP;
+    const T* base = pl + (ty + 1) * SWP + tx * (RW + 1);
     for (int i = 0; i < kh; ++i) {
-      const T* row = base + i * g.SWP;
+      const T* row = base + i * SWP;
       const T* wr = w + i * kw;
       T win[RW];
 #pragma unroll
@@ -212,259 +233,322 @@ struct Conv {
       }
     }
   }
-
-  __device__ __forceinline__ int64_t gidx(int h, int w, int c) const { return ((int64_t)h * g.W + w) * g.C + c; }
-
-  // small-plane accessor: pixel (tile row r, tile col q), r,q in [-1, TH]/[-1, TW]
-  __device__ __forceinline__ T sp(const T* base, int c, int r, int q) const {
-    return base[(size_t)c * g.YSH * g.YSWP + (r + 1) * g.YSWP + sk(q + 1)];
+  __device__ __forceinline__ void stencil_fwd(T (&acc)[RW]) const {
+    stencil(plane(ch), ws() + ch * a.g.kh * a.g.kw, acc);
   }
-  // full-plane accessor for pixel (tile row r, tile col q)
-  __device__ __forceinline__ T fp(const T* base, int c, int r, int q) const {
-    return base[(size_t)c * g.SH * g.SWP + (r + g.rh + 1) * g.SWP + sk(q + g.rw + 1)];
+  __device__ __forceinline__ void stencil_adj(T (&acc)[RW]) const {
+    stencil(plane(ch), wf() + ch * a.g.kh * a.g.kw, acc);
+  }
+
+  // plane value of this thread's channel at tile pixel (r, q)
+  __device__ __forceinline__ T fp(int r, int q) const {
+    return plane(ch)[(r + a.g.rh + 1) * a.g.SWP + sk(q + a.g.rw + 1)];
+  }
+
+  // ---- fused NumPy-pairwise leaves of up to 3 term buffers (tm[k], each
+  // TH x (TW*C) doubles, interleaved like the image) -> leaf_vals.  Leaf
+  // index of (tile row r, segment s): (h*W*C + w0*C)/L + s; buffer k goes to
+  // sums[k] with a leaf offset koff[k].
+  __device__ void tile_leaves(int h0, int w0, int nbuf, const SumDev* s0, const SumDev* s1, int koff2) {
+    __syncthreads();
+    const int C = a.g.C, L = a.g.leafL, W = a.g.W;
+    const int rows = min(a.g.TH, a.g.H - h0);
+    const int rowE = min(a.g.TW, W - w0) * C;
+    const int segs = rowE / L;
+    const int per_buf = rows * segs * 8;
+    const int tmE = a.g.TH * a.g.TW * C;
+    const int total = per_buf * nbuf;
+    for (int g0 = 0; g0 < total; g0 += blockDim.x) {      // total % 8 == 0, blockDim % 32 == 0
+      const int gch = g0 + threadIdx.x;
+      const bool act = gch < total;
+      double acc = 0.0;
+      int buf = 0, k = 0, r = 0, s = 0;
+      if (act) {
+        buf = gch / per_buf;
+        const int rem = gch - buf * per_buf;
+        const int leaf_l = rem >> 3;
+        k = rem & 7;
+        r = leaf_l / segs;
+        s = leaf_l - r * segs;
+        const double* t = tm() + (size_t)buf * tmE + (size_t)r * a.g.TW * C + s * L + k;
+        acc = t[0];
+        for (int i = 8; i < L; i += 8) acc = acc + t[i];
+      }
+      acc = acc + __shfl_xor_sync(kFull, acc, 1);
+      acc = acc + __shfl_xor_sync(kFull, acc, 2);
+      acc = acc + __shfl_xor_sync(kFull, acc, 4);
+      if (act && k == 0) {
+        const int64_t li = (((int64_t)(h0 + r) * W + w0) * C) / L + s + (buf == 2 ? koff2 : 0);
+        (buf == 0 ? s0 : s1)->leaf_vals[li] = acc;
+      }
+    }
+  }
+  __device__ __forceinline__ void put_term(int buf, int r, int q, double v) const {
+    tm()[(size_t)buf * a.g.TH * a.g.TW * a.g.C + ((size_t)r * a.g.TW + q) * a.g.C + ch] = v;
   }
 
   // =========================================================================
-  // Stage A: r = B y - ydat (write R); TV at y: terms (root) -> TV2, grad -> TVG
+  // Stage A: r = B y - ydat (write R); TV at y: root terms, grad -> TVG
   // (lower_value_and_grad, lower_solvers.py:50-63; SmoothedTV.value_and_grad,
-  // regularizers.py:167-175).  `tv` false when alpha == 0.
+  // regularizers.py:167-175).  `tv` false when alpha == 0.  Fused mode: the
+  // fit / TV leaves go straight to s_fit / s_tv.
   template <class Src>
-  __device__ void stageA(const Src& src, T* Rout, const T* ydat, bool tv, T* TV2out, T* TVGout) {
+  __device__ void stageA(const Src& src, T* Rout, const T* ydat, bool tv, T* TV2out, T* TVGout,
+                         const SumDev* sfit, const SumDev* stv) {
     const T nu = T(a.nu), nu2 = nu * nu;
-    for (int tile = blockIdx.x; tile < g.nTiles; tile += gridDim.x) {
+    const int H = a.g.H, W = a.g.W, TH = a.g.TH, TW = a.g.TW, C = a.g.C;
+    const bool fused = a.g.fused && sfit;
+    const int64_t N = a.g.N;
+    for (int tile = blockIdx.x; tile < a.g.nTiles; tile += gridDim.x) {
       int h0, w0;
       tile_origin(tile, h0, w0);
       __syncthreads();
-      load_full(pa, h0, w0, src);
+      load_full(h0, w0, src);
       __syncthreads();
       const int h = h0 + ty;
-      for (int c = 0; c < g.C; ++c) {
-        T acc[RW];
-        stencil(plane(pa, c), ws + c * g.kh * g.kw, acc);
+      T acc[RW];
+      stencil_fwd(acc);
 #pragma unroll
-        for (int o = 0; o < RW; ++o) {
-          const int w = w0 + tx * RW + o;
-          if (h < g.H && w < g.W) {
-            const int64_t i = gidx(h, w, c);
-            Rout[i] = acc[o] - ydat[i];
-          }
+      for (int o = 0; o < RW; ++o) {
+        const int q = tx * RW + o;
+        const int w = w0 + q;
+        if (h < H && w < W) {
+          const int64_t i = gidx(h, w, ch);
+          const T r = acc[o] - ydat[i];
+          Rout[i] = r;
+          if (fused) put_term(0, ty, q, (double)(r * r));
         }
       }
-      if (!tv) continue;
-      // Q planes over tile rows -1..TH-1, cols -1..TW-1: q = d / sqrt(d^2 + nu^2)
-      T* q0 = pq;
-      T* q1 = pq + (size_t)g.C * (g.TH + 1) * QP;
-      const int qrE = (g.TW + 1) * g.C, qtot = (g.TH + 1) * qrE;
-      for (int k = threadIdx.x; k < qtot; k += blockDim.x) {
-        const int qr = k / qrE, e = k - qr * qrE;
-        const int qc = e / g.C, c = e - qc * g.C;
-        const int r = qr - 1, q = qc - 1;   // tile-relative pixel
-        const int hh = h0 + r, ww = w0 + q;
-        const T yc = fp(pa, c, r, q);
-        const T d0 = (hh < g.H - 1) ? fp(pa, c, r + 1, q) - yc : T(0);
-        const T d1 = (ww < g.W - 1) ? fp(pa, c, r, q + 1) - yc : T(0);
-        const T rt0 = sqrt(d0 * d0 + nu2), rt1 = sqrt(d1 * d1 + nu2);
-        q0[(size_t)c * (g.TH + 1) * QP + qr * QP + sk(qc)] = d0 / rt0;
-        q1[(size_t)c * (g.TH + 1) * QP + qr * QP + sk(qc)] = d1 / rt1;
-        if (r >= 0 && q >= 0 && hh < g.H && ww < g.W) {
-          const int64_t i = gidx(hh, ww, c);
-          TV2out[i] = rt0;
-          TV2out[g.N + i] = rt1;
-        }
-      }
-      __syncthreads();
-      for (int c = 0; c < g.C; ++c) {
-        const T* Q0 = q0 + (size_t)c * (g.TH + 1) * QP;
-        const T* Q1 = q1 + (size_t)c * (g.TH + 1) * QP;
-#pragma unroll
-        for (int o = 0; o < RW; ++o) {
-          const int qcol = tx * RW + o;
-          const int w = w0 + qcol;
-          if (h < g.H && w < g.W) {
-            // image_forward_diff_adjoint (regularizers.py:61-67), per-pixel order
-            T t = T(0);
-            if (h >= 1) t = t + Q0[ty * QP + sk(qcol + 1)];
-            if (h <= g.H - 2) t = t - Q0[(ty + 1) * QP + sk(qcol + 1)];
-            if (w >= 1) t = t + Q1[(ty + 1) * QP + sk(qcol)];
-            if (w <= g.W - 2) t = t - Q1[(ty + 1) * QP + sk(qcol + 1)];
-            TVGout[gidx(h, w, c)] = t;
-          }
-        }
-      }
-    }
-  }
-
-  // Stage B: g = 2 * B^T r (+ alpha * tvg); tile partial of g.g -> sgg
-  __device__ void stageB(const T* Rin, bool tv, const T* TVGin, T* Gout, const SumDev* sgg) {
-    const T two = T(2), alpha = T(a.alpha);
-    for (int tile = blockIdx.x; tile < g.nTiles; tile += gridDim.x) {
-      int h0, w0;
-      tile_origin(tile, h0, w0);
-      __syncthreads();
-      load_full(pa, h0, w0, SrcLin<T>{Rin});
-      __syncthreads();
-      const int h = h0 + ty;
-      double part = 0.0;
-      for (int c = 0; c < g.C; ++c) {
-        T acc[RW];
-        stencil(plane(pa, c), wf + c * g.kh * g.kw, acc);
-#pragma unroll
-        for (int o = 0; o < RW; ++o) {
-          const int w = w0 + tx * RW + o;
-          if (h < g.H && w < g.W) {
-            const int64_t i = gidx(h, w, c);
-            T gv = two * acc[o];
-            if (tv) gv = gv + alpha * ldcg(TVGin + i);
-            Gout[i] = gv;
-            part += (double)gv * (double)gv;
-          }
-        }
-      }
-      if (sgg) store_tile_partial(*sgg, tile, part, red);
-    }
-  }
-
-  // Stage C (value at a candidate): xc = src; rc = B xc - y -> RCout; TV
-  // terms sqrt(d^2+nu^2) - nu -> TV2Cout (tv_value, regularizers.py:70-72);
-  // optional tile partial of g.(xc - xold); xc written to Xout.
-  template <class Src>
-  __device__ void stageC(const Src& src, T* RCout, bool tv, T* TV2Cout, T* Xout, const T* Gin, const T* Xold,
-                         const SumDev* sdot) {
-    const T nu = T(a.nu), nu2 = nu * nu;
-    for (int tile = blockIdx.x; tile < g.nTiles; tile += gridDim.x) {
-      int h0, w0;
-      tile_origin(tile, h0, w0);
-      __syncthreads();
-      load_full(pa, h0, w0, src);
-      __syncthreads();
-      const int h = h0 + ty;
-      double part = 0.0;
-      for (int c = 0; c < g.C; ++c) {
-        T acc[RW];
-        stencil(plane(pa, c), ws + c * g.kh * g.kw, acc);
+      if (tv) {
+        // q = d / sqrt(d^2 + nu^2) for the own pixels (registers), the row
+        // above the tile (ty == 0) and the column left of it (tx == 0)
+        T q0[RW], q1[RW], q0u[RW], q1l = T(0);
 #pragma unroll
         for (int o = 0; o < RW; ++o) {
           const int q = tx * RW + o;
           const int w = w0 + q;
-          if (h < g.H && w < g.W) {
-            const int64_t i = gidx(h, w, c);
-            RCout[i] = acc[o] - a.ydat[i];
-            const T xc = fp(pa, c, ty, q);
-            if (tv) {
-              const T d0 = (h < g.H - 1) ? fp(pa, c, ty + 1, q) - xc : T(0);
-              const T d1 = (w < g.W - 1) ? fp(pa, c, ty, q + 1) - xc : T(0);
-              TV2Cout[i] = sqrt(d0 * d0 + nu2) - nu;
-              TV2Cout[g.N + i] = sqrt(d1 * d1 + nu2) - nu;
+          const T yc = fp(ty, q);
+          const T d0 = (h < H - 1) ? fp(ty + 1, q) - yc : T(0);
+          const T d1 = (w < W - 1) ? fp(ty, q + 1) - yc : T(0);
+          const T rt0 = sqrt(d0 * d0 + nu2), rt1 = sqrt(d1 * d1 + nu2);
+          q0[o] = d0 / rt0;
+          q1[o] = d1 / rt1;
+          if (h < H && w < W) {
+            if (fused) {
+              put_term(1, ty, q, (double)rt0);
+              put_term(2, ty, q, (double)rt1);
+            } else {
+              const int64_t i = gidx(h, w, ch);
+              TV2out[i] = rt0;
+              TV2out[N + i] = rt1;
             }
-            if (Xout) Xout[i] = xc;
-            if (sdot) part += (double)ldcg(Gin + i) * (double)(xc - ldcg(Xold + i));
+          }
+          q0u[o] = T(0);
+          if (ty == 0 && h0 >= 1) {     // edge (h0-1) -> (h0): h0 - 1 < H - 1 always
+            const T du = yc - fp(-1, q);
+            q0u[o] = du / sqrt(du * du + nu2);
+          }
+        }
+        if (tx == 0 && w0 >= 1) {
+          const T dl = fp(ty, 0) - fp(ty, -1);
+          q1l = dl / sqrt(dl * dl + nu2);
+        }
+        // publish neighbour values through the (now free) plane region
+        __syncthreads();
+        T* Q0 = pa();                                    // [C][TH+1][TW]  (row r at r+1)
+        T* Q1 = Q0 + (size_t)C * (TH + 1) * TW;          // [C][TH][TW+1]  (col q at q+1)
+#pragma unroll
+        for (int o = 0; o < RW; ++o) {
+          const int q = tx * RW + o;
+          Q0[((size_t)ch * (TH + 1) + ty + 1) * TW + q] = q0[o];
+          if (ty == 0) Q0[((size_t)ch * (TH + 1)) * TW + q] = q0u[o];
+          Q1[((size_t)ch * TH + ty) * (TW + 1) + q + 1] = q1[o];
+        }
+        if (tx == 0) Q1[((size_t)ch * TH + ty) * (TW + 1)] = q1l;
+        __syncthreads();
+#pragma unroll
+        for (int o = 0; o < RW; ++o) {
+          const int q = tx * RW + o;
+          const int w = w0 + q;
+          if (h < H && w < W) {
+            // image_forward_diff_adjoint (regularizers.py:61-67), per-pixel order
+            T t = T(0);
+            if (h >= 1) t = t + Q0[((size_t)ch * (TH + 1) + ty) * TW + q];
+            if (h <= H - 2) t = t - q0[o];
+            if (w >= 1) t = t + (o > 0 ? q1[o > 0 ? o - 1 : 0] : Q1[((size_t)ch * TH + ty) * (TW + 1) + q]);
+            if (w <= W - 2) t = t - q1[o];
+            TVGout[gidx(h, w, ch)] = t;
           }
         }
       }
-      if (sdot) store_tile_partial(*sdot, tile, part, red);
+      if (fused) tile_leaves(h0, w0, tv ? 3 : 1, sfit, stv, (int)(N / a.g.leafL));
+    }
+  }
+
+  // Stage B: g = 2 * B^T r (+ alpha * tvg); tile partial of g.g -> sgg.
+  // Optionally the first backtracking candidate xc = y - g / L for the own
+  // pixels (y = x + beta (x - x_prev)), written to Xc.
+  __device__ void stageB(const T* Rin, bool tv, const T* TVGin, T* Gout, const SumDev* sgg, const T* Xs = nullptr,
+                         const T* XPs = nullptr, T beta = T(0), T L = T(1), T* Xc = nullptr) {
+    const T two = T(2), alpha = T(a.alpha);
+    const int H = a.g.H, W = a.g.W;
+    for (int tile = blockIdx.x; tile < a.g.nTiles; tile += gridDim.x) {
+      int h0, w0;
+      tile_origin(tile, h0, w0);
+      __syncthreads();
+      load_full(h0, w0, SrcLin<T>{Rin});
+      __syncthreads();
+      const int h = h0 + ty;
+      double part = 0.0;
+      T acc[RW];
+      stencil_adj(acc);
+#pragma unroll
+      for (int o = 0; o < RW; ++o) {
+        const int w = w0 + tx * RW + o;
+        if (h < H && w < W) {
+          const int64_t i = gidx(h, w, ch);
+          T gv = two * acc[o];
+          if (tv) gv = gv + alpha * ldcg(TVGin + i);
+          Gout[i] = gv;
+          part += (double)gv * (double)gv;
+          if (Xc) {
+            const T xv = ldcg(Xs + i), xpv = ldcg(XPs + i);
+            const T y = xv + beta * (xv - xpv);
+            Xc[i] = y - gv / L;
+          }
+        }
+      }
+      if (sgg) store_tile_partial(*sgg, tile, part, red());
+    }
+  }
+
+  // Stage C (value at a candidate): xc = src; rc = B xc - y; TV terms
+  // sqrt(d^2+nu^2) - nu (tv_value, regularizers.py:70-72); optional tile
+  // partial of g.(xc - xold); xc written to Xout (if non-null).  Fused:
+  // leaves to sfitc / stvc; otherwise rc -> RCout and TV terms -> TV2Cout.
+  template <class Src>
+  __device__ void stageC(const Src& src, T* RCout, bool tv, T* TV2Cout, T* Xout, const T* Gin, const T* Xold,
+                         const SumDev* sdot, const SumDev* sfitc, const SumDev* stvc) {
+    const T nu = T(a.nu), nu2 = nu * nu;
+    const int H = a.g.H, W = a.g.W;
+    const bool fused = a.g.fused && sfitc;
+    const int64_t N = a.g.N;
+    for (int tile = blockIdx.x; tile < a.g.nTiles; tile += gridDim.x) {
+      int h0, w0;
+      tile_origin(tile, h0, w0);
+      __syncthreads();
+      load_full(h0, w0, src);
+      __syncthreads();
+      const int h = h0 + ty;
+      double part = 0.0;
+      T acc[RW];
+      stencil_fwd(acc);
+#pragma unroll
+      for (int o = 0; o < RW; ++o) {
+        const int q = tx * RW + o;
+        const int w = w0 + q;
+        if (h < H && w < W) {
+          const int64_t i = gidx(h, w, ch);
+          const T rc = acc[o] - a.ydat[i];
+          const T xc = fp(ty, q);
+          if (fused) put_term(0, ty, q, (double)(rc * rc));
+          else RCout[i] = rc;
+          if (tv) {
+            const T d0 = (h < H - 1) ? fp(ty + 1, q) - xc : T(0);
+            const T d1 = (w < W - 1) ? fp(ty, q + 1) - xc : T(0);
+            const T t0 = sqrt(d0 * d0 + nu2) - nu;
+            const T t1 = sqrt(d1 * d1 + nu2) - nu;
+            if (fused) {
+              put_term(1, ty, q, (double)t0);
+              put_term(2, ty, q, (double)t1);
+            } else {
+              TV2Cout[i] = t0;
+              TV2Cout[N + i] = t1;
+            }
+          }
+          if (Xout) Xout[i] = xc;
+          if (sdot) part += (double)ldcg(Gin + i) * (double)(xc - ldcg(Xold + i));
+        }
+      }
+      if (sdot) store_tile_partial(*sdot, tile, part, red());
+      if (fused) tile_leaves(h0, w0, tv ? 3 : 1, sfitc, stvc, (int)(N / a.g.leafL));
     }
   }
 
   // Light candidate (non-adaptive step): xc = src per own pixel, dot partial.
   template <class Src>
   __device__ void stageCLight(const Src& src, T* Xout, const T* Gin, const T* Xold, const SumDev* sdot) {
-    for (int tile = blockIdx.x; tile < g.nTiles; tile += gridDim.x) {
-      int h0, w0;
-      tile_origin(tile, h0, w0);
-      const int h = h0 + ty;
-      double part = 0.0;
-      for (int c = 0; c < g.C; ++c) {
-#pragma unroll
-        for (int o = 0; o < RW; ++o) {
-          const int w = w0 + tx * RW + o;
-          if (h < g.H && w < g.W) {
-            const int64_t i = gidx(h, w, c);
-            const T xc = src(i);
-            Xout[i] = xc;
-            part += (double)ldcg(Gin + i) * (double)(xc - ldcg(Xold + i));
-          }
-        }
-      }
-      store_tile_partial(*sdot, tile, part, red);
-    }
+    foreach_pixel_sum([&](int64_t i, int, int, int) {
+      const T xc = src(i);
+      Xout[i] = xc;
+      return (double)ldcg(Gin + i) * (double)(xc - ldcg(Xold + i));
+    }, *sdot);
   }
 
-  // Plain correlation pass: out = B src (or B^T src with flipped taps),
-  // optional ydat subtraction and tile partial of out.out.
+  // Plain correlation pass: out = scale * (B src - sub) (or B^T with flipped
+  // taps), optional tile partial of out.out.
   template <class Src>
   __device__ void stage_corr(const Src& src, bool flipped, T* Out, const T* sub, T scale, const SumDev* ssq) {
-    for (int tile = blockIdx.x; tile < g.nTiles; tile += gridDim.x) {
+    const int H = a.g.H, W = a.g.W;
+    for (int tile = blockIdx.x; tile < a.g.nTiles; tile += gridDim.x) {
       int h0, w0;
       tile_origin(tile, h0, w0);
       __syncthreads();
-      load_full(pa, h0, w0, src);
+      load_full(h0, w0, src);
       __syncthreads();
       const int h = h0 + ty;
       double part = 0.0;
-      for (int c = 0; c < g.C; ++c) {
-        T acc[RW];
-        stencil(plane(pa, c), (flipped ? wf : ws) + c * g.kh * g.kw, acc);
+      T acc[RW];
+      if (flipped) stencil_adj(acc);
+      else stencil_fwd(acc);
 #pragma unroll
-        for (int o = 0; o < RW; ++o) {
-          const int w = w0 + tx * RW + o;
-          if (h < g.H && w < g.W) {
-            const int64_t i = gidx(h, w, c);
-            T v = acc[o];
-            if (sub) v = v - sub[i];
-            v = scale * v;
-            Out[i] = v;
-            part += (double)v * (double)v;
-          }
+      for (int o = 0; o < RW; ++o) {
+        const int w = w0 + tx * RW + o;
+        if (h < H && w < W) {
+          const int64_t i = gidx(h, w, ch);
+          T v = acc[o];
+          if (sub) v = v - sub[i];
+          v = scale * v;
+          Out[i] = v;
+          part += (double)v * (double)v;
         }
       }
-      if (ssq) store_tile_partial(*ssq, tile, part, red);
+      if (ssq) store_tile_partial(*ssq, tile, part, red());
     }
   }
 
   // Elementwise over own pixels of every tile (grid-stride by tiles).
   template <class F>
   __device__ void foreach_pixel(const F& f) {
-    for (int tile = blockIdx.x; tile < g.nTiles; tile += gridDim.x) {
+    const int H = a.g.H, W = a.g.W;
+    for (int tile = blockIdx.x; tile < a.g.nTiles; tile += gridDim.x) {
       int h0, w0;
       tile_origin(tile, h0, w0);
       const int h = h0 + ty;
-      for (int c = 0; c < g.C; ++c)
 #pragma unroll
-        for (int o = 0; o < RW; ++o) {
-          const int w = w0 + tx * RW + o;
-          if (h < g.H && w < g.W) f(gidx(h, w, c), h, w, c);
-        }
+      for (int o = 0; o < RW; ++o) {
+        const int w = w0 + tx * RW + o;
+        if (h < H && w < W) f(gidx(h, w, ch), h, w, ch);
+      }
     }
   }
-  // Same, with a per-tile partial accumulated by f's return value.
+  // Same, with a per-tile partial accumulated from f's return value.
   template <class F>
   __device__ void foreach_pixel_sum(const F& f, const SumDev& s) {
-    for (int tile = blockIdx.x; tile < g.nTiles; tile += gridDim.x) {
+    const int H = a.g.H, W = a.g.W;
+    for (int tile = blockIdx.x; tile < a.g.nTiles; tile += gridDim.x) {
       int h0, w0;
       tile_origin(tile, h0, w0);
       const int h = h0 + ty;
       double part = 0.0;
-      for (int c = 0; c < g.C; ++c)
 #pragma unroll
-        for (int o = 0; o < RW; ++o) {
-          const int w = w0 + tx * RW + o;
-          if (h < g.H && w < g.W) part += f(gidx(h, w, c), h, w, c);
-        }
-      store_tile_partial(s, tile, part, red);
+      for (int o = 0; o < RW; ++o) {
+        const int w = w0 + tx * RW + o;
+        if (h < H && w < W) part += f(gidx(h, w, ch), h, w, ch);
+      }
+      store_tile_partial(s, tile, part, red());
     }
   }
-};
-
-template <typename T> struct SqOf {
-  const T* p;
-  __device__ double operator()(int64_t i) const {
-    const T v = ldcg(p + i);
-    return (double)(v * v);
-  }
-};
-template <typename T> struct Plain {
-  const T* p;
-  __device__ double operator()(int64_t i) const { return (double)ldcg(p + i); }
 };
 
 }  // namespace adp

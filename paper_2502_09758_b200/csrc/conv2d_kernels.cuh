@@ -5,42 +5,45 @@
 
 namespace adp {
 
-
 template <typename T, bool FAST, int RW>
 struct ConvOps : Conv<T, FAST, RW> {
   using Base = Conv<T, FAST, RW>;
-  using Base::a; using Base::g; using Base::sv; using Base::red;
+  using Base::a;
   GridBarrier gb;
 
-  __device__ ConvOps(const ConvArgs<T>& a_, unsigned char* smem) : Base(a_, smem) {
+  __device__ explicit ConvOps(const ConvArgs<T>& a_) : Base(a_) {
     gb.counter = a_.bar;
     gb.nblocks = gridDim.x;
     gb.target = 0;
   }
 
-  __device__ double reduce1(const SumDev& s) {
-    const SumDev* ss[1] = {&s};
-    double o[1];
-    reduce_list(ss, 1, o, sv, gb);
-    return o[0];
-  }
   __device__ void reduce(std::initializer_list<const SumDev*> l, double* out) {
     const SumDev* ss[8];
     int k = 0;
     for (const SumDev* p : l) ss[k++] = p;
-    reduce_list(ss, k, out, sv, gb);
+    reduce_list(ss, k, out, this->sv(), gb);
+  }
+  __device__ double reduce1(const SumDev& s) {
+    double o;
+    reduce({&s}, &o);
+    return o;
+  }
+  // element-sum leaves for the non-fused layout (after a barrier)
+  __device__ void leaves_if_unfused(const SumDev& s, const T* terms, bool square) {
+    if (a.g.fused) return;
+    if (square) np_leaves(s, SqOf<T>{terms});
+    else np_leaves(s, Plain<T>{terms});
   }
 
   // Power iteration on B^T B (op_norm_sq, operators.py:137-173).  Uses R
   // (B v) and G (w) as scratch.  Returns lambda; sets iters / converged.
   __device__ double power(int max_iters, double tol, int& iters, int& conv) {
-    // v /= ||v||  (operators.py:150)
     this->foreach_pixel_sum([&](int64_t i, int, int, int) {
       const double v = (double)a.v0[i];
       return v * v;
     }, a.s_t0);
     gb.sync();
-    const double nv = sqrt(reduce1(a.s_t0));
+    const double nv = sqrt(reduce1(a.s_t0));      // v /= ||v||  (operators.py:150)
     double lam = 0.0;
     conv = 0;
     iters = 0;
@@ -61,16 +64,37 @@ struct ConvOps : Conv<T, FAST, RW> {
     }
     return lam;
   }
+
+  // value + gradient at a source point: stage A, barrier, stage B (+ leaves
+  // when unfused).  Caller syncs afterwards.
+  template <class Src>
+  __device__ void value_grad(const Src& src, bool tv, T* Gout, const T* Xs = nullptr, const T* XPs = nullptr,
+                             T beta = T(0), T L = T(1), T* Xc = nullptr) {
+    this->stageA(src, a.R, a.ydat, tv, a.TV2, a.TVG, &a.s_fit, &a.s_tv);
+    gb.sync();
+    this->stageB(a.R, tv, a.TVG, Gout, &a.s_t0, Xs, XPs, beta, L, Xc);
+    leaves_if_unfused(a.s_fit, a.R, true);
+    if (tv) leaves_if_unfused(a.s_tv, a.TV2, false);
+  }
+  // value at a candidate (lower_value form) + restart-dot partial; caller syncs.
+  template <class Src>
+  __device__ void value_cand(const Src& src, bool tv, T* Xout, const T* Gin, const T* Xold, const SumDev* sdot) {
+    this->stageC(src, a.RC, tv, a.TV2C, Xout, Gin, Xold, sdot, &a.s_fitc, &a.s_tvc);
+    if (!a.g.fused) {
+      gb.sync();
+      np_leaves(a.s_fitc, SqOf<T>{a.RC});
+      if (tv) np_leaves(a.s_tvc, Plain<T>{a.TV2C});
+    }
+  }
 };
 
 // ---------------------------------------------------------------------------
 // solve_lower (lower_solvers.py:104-213) as one persistent kernel.
 template <typename T, bool FAST, int RW>
 __global__ void __launch_bounds__(512, 1) conv_solve_kernel(const __grid_constant__ ConvArgs<T> a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  ConvOps<T, FAST, RW> E(a, smem);
+  ConvOps<T, FAST, RW> E(a);
   const ConvGeom& g = a.g;
-  if (a.kern) E.load_weights(a.kern);
+  E.load_weights(a.kern);
   const bool tv = (a.alpha != 0.0);
   const double twoN = 2.0 * (double)g.N;
 
@@ -116,24 +140,20 @@ __global__ void __launch_bounds__(512, 1) conv_solve_kernel(const __grid_constan
       ixp = ix;
     }
     const T tb = T(beta);
-    // value and gradient at y
-    E.stageA(SrcExtrap<T>{a.X[ix], a.X[ixp], tb}, a.R, a.ydat, tv, a.TV2, a.TVG);
-    E.gb.sync();
-    E.stageB(a.R, tv, a.TVG, a.G, &a.s_t0);
-    np_leaves(a.s_fit, SqOf<T>{a.R});
-    if (tv) np_leaves(a.s_tv, Plain<T>{a.TV2});
-    ++vg;
     // first candidate, computed speculatively before the convergence test
-    const bool gd_fixed = (a.method == M_PROXGRAD && !a.adaptive);
     double L_try = (a.method == M_PROXGRAD) ? 1.0 / gd_step : lip_t;
+    // value and gradient at y (stages A, B); stage B also writes the own
+    // pixels of the first candidate y - g / L_try (adaptive path)
+    if (a.adaptive)
+      E.value_grad(SrcExtrap<T>{a.X[ix], a.X[ixp], tb}, tv, a.G, a.X[ix], a.X[ixp], tb, T(L_try), a.X[ic]);
+    else
+      E.value_grad(SrcExtrap<T>{a.X[ix], a.X[ixp], tb}, tv, a.G);
+    ++vg;
     E.gb.sync();
     if (a.adaptive) {
-      E.stageC(SrcCand<T>{a.X[ix], a.X[ixp], a.G, tb, T(L_try)}, a.RC, tv, a.TV2C, a.X[ic], a.G, a.X[ix], &a.s_t1);
-      E.gb.sync();
-      np_leaves(a.s_fitc, SqOf<T>{a.RC});
-      if (tv) np_leaves(a.s_tvc, Plain<T>{a.TV2C});
+      E.value_cand(SrcLin<T>{a.X[ic]}, tv, nullptr, a.G, a.X[ix], &a.s_t1);
       ++vals;
-    } else if (gd_fixed) {
+    } else if (a.method == M_PROXGRAD) {
       E.stageCLight(SrcStep<T>{a.X[ix], a.G, T(gd_step)}, a.X[ic], a.G, a.X[ix], &a.s_t1);
     } else {
       E.stageCLight(SrcCand<T>{a.X[ix], a.X[ixp], a.G, tb, T(lip_t)}, a.X[ic], a.G, a.X[ix], &a.s_t1);
@@ -150,7 +170,6 @@ __global__ void __launch_bounds__(512, 1) conv_solve_kernel(const __grid_constan
     if (tv) h_y = fit + a.alpha * (o[1] - a.nu * twoN);
     gn = sqrt(o[2]);
     double dot = o[3];
-    const double tvc0 = o[5];
     if (!isfinite(gn)) { status = ST_DIVERGED; fail_iter = t; done = true; break; }
     if (gn <= a.tol) {
       // converged: return y (lower_solvers.py:200-201)
@@ -165,18 +184,15 @@ __global__ void __launch_bounds__(512, 1) conv_solve_kernel(const __grid_constan
     }
     if (a.adaptive) {
       // _backtracked_step (lower_solvers.py:170-177)
-      double fitc = o[4], tvc = tvc0;
+      double fitc = o[4], tvc = o[5];
       int k = 0;
       while (true) {
         const double val = tv ? fitc + a.alpha * tvc : fitc + a.alpha * 0.0;
         if (val <= h_y - 0.5 * gn * gn / L_try + 1e-15 * fabs(h_y)) break;
         L_try *= 2.0;
         if (++k >= 60) { status = ST_BT_FAIL; fail_iter = t; break; }
-        E.gb.sync();
-        E.stageC(SrcCand<T>{a.X[ix], a.X[ixp], a.G, tb, T(L_try)}, a.RC, tv, a.TV2C, a.X[ic], a.G, a.X[ix], &a.s_t1);
-        E.gb.sync();
-        np_leaves(a.s_fitc, SqOf<T>{a.RC});
-        if (tv) np_leaves(a.s_tvc, Plain<T>{a.TV2C});
+        E.gb.sync();   // every CTA has finished reading the previous candidate sums
+        E.value_cand(SrcCand<T>{a.X[ix], a.X[ixp], a.G, tb, T(L_try)}, tv, a.X[ic], a.G, a.X[ix], &a.s_t1);
         ++vals;
         E.gb.sync();
         double o3[3] = {0, 0, 0};
@@ -190,25 +206,20 @@ __global__ void __launch_bounds__(512, 1) conv_solve_kernel(const __grid_constan
       else lip_t = fmax(1.0 / bstep * 0.9, lip * 1e-8);
     }
     // x_prev = x; x = candidate; restart (lower_solvers.py:202-211)
-    const int old_x = ix, old_xp = ixp;
-    ixp = old_x;
+    ixp = ix;
     ix = ic;
     if (a.method == M_AGD && dot > 0.0) {
       t_mom = 1.0;
       ixp = ix;
       ++restarts;
     }
-    // free buffer for the next candidate: not ix, not ixp
     for (int b = 0; b < 3; ++b)
       if (b != ix && b != ixp) { ic = b; break; }
-    (void)old_xp;
   }
 
   if (!done) {
     // max_iters reached: g = lower_grad(p, x) (lower_solvers.py:212-213)
-    E.stageA(SrcLin<T>{a.X[ix]}, a.R, a.ydat, tv, a.TV2, a.TVG);
-    E.gb.sync();
-    E.stageB(a.R, tv, a.TVG, a.G, &a.s_t0);
+    E.value_grad(SrcLin<T>{a.X[ix]}, tv, a.G);
     E.foreach_pixel([&](int64_t i, int, int, int) { a.out[i] = ldcg(a.X[ix] + i); });
     E.gb.sync();
     gn = sqrt(E.reduce1(a.s_t0));
@@ -236,21 +247,21 @@ __global__ void __launch_bounds__(512, 1) conv_solve_kernel(const __grid_constan
 // ---------------------------------------------------------------------------
 // Hessian of the lower problem (lower_hess_vec, lower_solvers.py:66-71):
 //   H v = 2 B^T (B v) + alpha * D^T (rho''(D x) . D v)
-// Two stages: (1) BP = B v   (2) out = 2 B^T BP + alpha * TV-Hessian term.
 template <typename T, bool FAST, int RW>
 struct HessOps : ConvOps<T, FAST, RW> {
   using Base = ConvOps<T, FAST, RW>;
-  using Base::a; using Base::g;
-  __device__ HessOps(const ConvArgs<T>& a_, unsigned char* smem) : Base(a_, smem) {}
+  using Base::a;
+  __device__ explicit HessOps(const ConvArgs<T>& a_) : Base(a_) {}
 
   // rho'' weights of x: WV (vertical edges), WH (horizontal); _rho_curv
   // (regularizers.py:34-36): nu^2 / (t^2 + nu^2)^1.5
   __device__ void hess_weights(const T* x) {
     const T nu = T(a.nu), nu2 = nu * nu;
-    this->foreach_pixel([&](int64_t i, int h, int w, int c) {
+    const int H = a.g.H, W = a.g.W, C = a.g.C;
+    this->foreach_pixel([&](int64_t i, int h, int w, int) {
       const T xc = ldcg(x + i);
-      const T d0 = (h < g.H - 1) ? ldcg(x + i + (int64_t)g.W * g.C) - xc : T(0);
-      const T d1 = (w < g.W - 1) ? ldcg(x + i + g.C) - xc : T(0);
+      const T d0 = (h < H - 1) ? ldcg(x + i + (int64_t)W * C) - xc : T(0);
+      const T d1 = (w < W - 1) ? ldcg(x + i + C) - xc : T(0);
       const T s0 = d0 * d0 + nu2, s1 = d1 * d1 + nu2;
       a.WV[i] = nu2 / (s0 * sqrt(s0));
       a.WH[i] = nu2 / (s1 * sqrt(s1));
@@ -262,39 +273,40 @@ struct HessOps : ConvOps<T, FAST, RW> {
   // (out - sub)^2 (true residual).
   __device__ void hess_stage2(const T* V, bool tv, T* Out, const T* pdot, const T* sub, const SumDev* s) {
     const T two = T(2), alpha = T(a.alpha);
-    const int C = g.C;
-    const int64_t rowS = (int64_t)g.W * C;
-    for (int tile = blockIdx.x; tile < g.nTiles; tile += gridDim.x) {
+    const int C = a.g.C, H = a.g.H, W = a.g.W;
+    const int64_t rowS = (int64_t)W * C;
+    for (int tile = blockIdx.x; tile < a.g.nTiles; tile += gridDim.x) {
       int h0, w0;
       this->tile_origin(tile, h0, w0);
       __syncthreads();
-      this->load_full(this->pa, h0, w0, SrcLin<T>{a.BP});
+      this->load_full(h0, w0, SrcLin<T>{a.BP});
       __syncthreads();
       const int h = h0 + this->ty;
       double part = 0.0;
-      for (int c = 0; c < C; ++c) {
+      {
         T acc[RW];
-        this->stencil(this->plane(this->pa, c), this->wf + c * g.kh * g.kw, acc);
+        this->stencil_adj(acc);
 #pragma unroll
         for (int o = 0; o < RW; ++o) {
           const int w = w0 + this->tx * RW + o;
-          if (h < g.H && w < g.W) {
-            const int64_t i = this->gidx(h, w, c);
+          if (h < H && w < W) {
+            const int64_t i = this->gidx(h, w, this->ch);
             T hv = two * acc[o];
             if (tv) {
               // D^T (W . D v) at pixel i, image_forward_diff_adjoint order
               const T vc = ldcg(V + i);
               T t = T(0);
               if (h >= 1) t = t + ldcg(a.WV + i - rowS) * (vc - ldcg(V + i - rowS));
-              if (h <= g.H - 2) t = t - ldcg(a.WV + i) * (ldcg(V + i + rowS) - vc);
+              if (h <= H - 2) t = t - ldcg(a.WV + i) * (ldcg(V + i + rowS) - vc);
               if (w >= 1) t = t + ldcg(a.WH + i - C) * (vc - ldcg(V + i - C));
-              if (w <= g.W - 2) t = t - ldcg(a.WH + i) * (ldcg(V + i + C) - vc);
+              if (w <= W - 2) t = t - ldcg(a.WH + i) * (ldcg(V + i + C) - vc);
               hv = hv + alpha * t;
             }
             Out[i] = hv;
             if (s) {
-              if (pdot) part += (double)ldcg(pdot + i) * (double)hv;
-              else {
+              if (pdot) {
+                part += (double)ldcg(pdot + i) * (double)hv;
+              } else {
                 const double d = (double)(hv - ldcg(sub + i));
                 part += d * d;
               }
@@ -302,33 +314,31 @@ struct HessOps : ConvOps<T, FAST, RW> {
           }
         }
       }
-      if (s) store_tile_partial(*s, tile, part, this->red);
+      if (s) store_tile_partial(*s, tile, part, this->red());
     }
   }
 
   // H v with v = src (materialised into Vbuf by stage 1).
   template <class Src>
   __device__ void hess_vec(const Src& src, T* Vbuf, bool tv, T* Out, const T* pdot, const T* sub, const SumDev* s) {
-    // stage 1: Vbuf = src (own pixels), BP = B src
-    for (int tile = blockIdx.x; tile < g.nTiles; tile += gridDim.x) {
+    const int H = a.g.H, W = a.g.W;
+    for (int tile = blockIdx.x; tile < a.g.nTiles; tile += gridDim.x) {
       int h0, w0;
       this->tile_origin(tile, h0, w0);
       __syncthreads();
-      this->load_full(this->pa, h0, w0, src);
+      this->load_full(h0, w0, src);
       __syncthreads();
       const int h = h0 + this->ty;
-      for (int c = 0; c < g.C; ++c) {
-        T acc[RW];
-        this->stencil(this->plane(this->pa, c), this->ws + c * g.kh * g.kw, acc);
+      T acc[RW];
+      this->stencil_fwd(acc);
 #pragma unroll
-        for (int o = 0; o < RW; ++o) {
-          const int q = this->tx * RW + o;
-          const int w = w0 + q;
-          if (h < g.H && w < g.W) {
-            const int64_t i = this->gidx(h, w, c);
-            a.BP[i] = acc[o];
-            if (Vbuf) Vbuf[i] = this->fp(this->pa, c, this->ty, q);
-          }
+      for (int o = 0; o < RW; ++o) {
+        const int q = this->tx * RW + o;
+        const int w = w0 + q;
+        if (h < H && w < W) {
+          const int64_t i = this->gidx(h, w, this->ch);
+          a.BP[i] = acc[o];
+          if (Vbuf) Vbuf[i] = this->fp(this->ty, q);
         }
       }
     }
@@ -336,37 +346,37 @@ struct HessOps : ConvOps<T, FAST, RW> {
     hess_stage2(Vbuf, tv, Out, pdot, sub, s);
   }
 
-  // lower_hess_diag (lower_solvers.py:74-80) into DIAG (before flooring when
-  // floor == false); TV part: SmoothedTV.hess_diag (regularizers.py:185-199).
+  // lower_hess_diag (lower_solvers.py:74-80) into Out; TV part:
+  // SmoothedTV.hess_diag (regularizers.py:185-199).
   __device__ void hess_diag(const T* x, bool tv, T* Out) {
     this->load_weights_sq(a.kern);
     const T nu = T(a.nu), nu2 = nu * nu, two = T(2), alpha = T(a.alpha);
-    const int C = g.C;
-    const int64_t rowS = (int64_t)g.W * C;
+    const int C = a.g.C, H = a.g.H, W = a.g.W;
+    const int64_t rowS = (int64_t)W * C;
     double mx = -INFINITY;
-    for (int tile = blockIdx.x; tile < g.nTiles; tile += gridDim.x) {
+    for (int tile = blockIdx.x; tile < a.g.nTiles; tile += gridDim.x) {
       int h0, w0;
       this->tile_origin(tile, h0, w0);
       __syncthreads();
-      this->load_full(this->pa, h0, w0, SrcOnes<T>{});
+      this->load_full(h0, w0, SrcOnes<T>{});
       __syncthreads();
       const int h = h0 + this->ty;
-      for (int c = 0; c < C; ++c) {
+      {
         T acc[RW];
-        this->stencil(this->plane(this->pa, c), this->wf + c * g.kh * g.kw, acc);
+        this->stencil_adj(acc);
 #pragma unroll
         for (int o = 0; o < RW; ++o) {
           const int w = w0 + this->tx * RW + o;
-          if (h < g.H && w < g.W) {
-            const int64_t i = this->gidx(h, w, c);
+          if (h < H && w < W) {
+            const int64_t i = this->gidx(h, w, this->ch);
             T d = two * acc[o];
             if (tv) {
               const T xc = ldcg(x + i);
               T t = T(0);
               // diag[:-1] += wv; diag[1:] += wv; diag[:, :-1] += wh; diag[:, 1:] += wh
-              if (h <= g.H - 2) { const T dd = ldcg(x + i + rowS) - xc, s = dd * dd + nu2; t = t + nu2 / (s * sqrt(s)); }
+              if (h <= H - 2) { const T dd = ldcg(x + i + rowS) - xc, s = dd * dd + nu2; t = t + nu2 / (s * sqrt(s)); }
               if (h >= 1) { const T dd = xc - ldcg(x + i - rowS), s = dd * dd + nu2; t = t + nu2 / (s * sqrt(s)); }
-              if (w <= g.W - 2) { const T dd = ldcg(x + i + C) - xc, s = dd * dd + nu2; t = t + nu2 / (s * sqrt(s)); }
+              if (w <= W - 2) { const T dd = ldcg(x + i + C) - xc, s = dd * dd + nu2; t = t + nu2 / (s * sqrt(s)); }
               if (w >= 1) { const T dd = xc - ldcg(x + i - C), s = dd * dd + nu2; t = t + nu2 / (s * sqrt(s)); }
               d = d + alpha * t;
             }
@@ -377,12 +387,12 @@ struct HessOps : ConvOps<T, FAST, RW> {
       }
     }
     // global max -> floor (np.maximum(d, 1e-12 * d.max() + 1e-300))
-    mx = block_max(mx, this->red);
+    mx = block_max(mx, this->red());
     if (threadIdx.x == 0) a.s_t2.leaf_vals[blockIdx.x] = mx;
     this->gb.sync();
     double gmx = -INFINITY;
     for (int b = threadIdx.x; b < gridDim.x; b += blockDim.x) gmx = fmax(gmx, ldcg(a.s_t2.leaf_vals + b));
-    gmx = block_max(gmx, this->red);
+    gmx = block_max(gmx, this->red());
     const T fl = T(1e-12 * gmx + 1e-300);
     if (!a.nofloor) this->foreach_pixel([&](int64_t i, int, int, int) {
       const T d = ldcg(Out + i);
@@ -398,9 +408,7 @@ struct HessOps : ConvOps<T, FAST, RW> {
 // 171-176).  Q in/out (warm start when a.warm), DIAG gets the preconditioner.
 template <typename T, bool FAST, int RW>
 __global__ void __launch_bounds__(512, 1) conv_cg_kernel(const __grid_constant__ ConvArgs<T> a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  HessOps<T, FAST, RW> E(a, smem);
-  const ConvGeom& g = a.g;
+  HessOps<T, FAST, RW> E(a);
   if (a.kern) E.load_weights(a.kern);
   const bool tv = (a.alpha != 0.0);
   const double tol = a.tol;
@@ -450,7 +458,6 @@ __global__ void __launch_bounds__(512, 1) conv_cg_kernel(const __grid_constant__
   double beta = 0.0;
   for (iters = 1; iters <= a.max_iters; ++iters) {
     if (sqrt(rr) <= tol) { iters -= 1; break; }
-    // p = s + beta * p_old (materialised by hess stage 1), Hp
     const int nxt = first ? cur : cur ^ 1;
     E.hess_vec(SrcCGDir<T>{a.CS, a.P[cur], T(beta), first}, a.P[nxt], tv, a.HP, a.P[nxt], nullptr, &a.s_t0);
     ++hv;
@@ -509,8 +516,7 @@ __global__ void __launch_bounds__(512, 1) conv_cg_kernel(const __grid_constant__
 // Per-call primitives (one cooperative launch each).
 template <typename T, bool FAST, int RW>
 __global__ void __launch_bounds__(512, 1) conv_misc_kernel(const __grid_constant__ ConvArgs<T> a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  HessOps<T, FAST, RW> E(a, smem);
+  HessOps<T, FAST, RW> E(a);
   const ConvGeom& g = a.g;
   if (a.kern) E.load_weights(a.kern);
   const bool tv = (a.alpha != 0.0);
@@ -527,10 +533,7 @@ __global__ void __launch_bounds__(512, 1) conv_misc_kernel(const __grid_constant
       break;
     case CM_VALUE: {
       // lower_value (lower_solvers.py:37-39): sum(r*r) + alpha * tv_value(x)
-      E.stageC(SrcLin<T>{a.in0}, a.RC, true, a.TV2C, nullptr, nullptr, nullptr, nullptr);
-      E.gb.sync();
-      np_leaves(a.s_fitc, SqOf<T>{a.RC});
-      np_leaves(a.s_tvc, Plain<T>{a.TV2C});
+      E.value_cand(SrcLin<T>{a.in0}, true, nullptr, nullptr, nullptr, nullptr);
       E.gb.sync();
       double o[2];
       E.reduce({&a.s_fitc, &a.s_tvc}, o);
@@ -539,11 +542,7 @@ __global__ void __launch_bounds__(512, 1) conv_misc_kernel(const __grid_constant
     }
     case CM_VALUE_GRAD:
     case CM_GRAD: {
-      E.stageA(SrcLin<T>{a.in0}, a.R, a.ydat, tv, a.TV2, a.TVG);
-      E.gb.sync();
-      E.stageB(a.R, tv, a.TVG, a.out0, &a.s_t0);
-      np_leaves(a.s_fit, SqOf<T>{a.R});
-      if (tv) np_leaves(a.s_tv, Plain<T>{a.TV2});
+      E.value_grad(SrcLin<T>{a.in0}, tv, a.out0);
       E.gb.sync();
       double o[3] = {0, 0, 0};
       if (tv) E.reduce({&a.s_fit, &a.s_tv, &a.s_t0}, o);
@@ -606,18 +605,15 @@ __global__ void __launch_bounds__(512, 1) conv_misc_kernel(const __grid_constant
 template <typename T>
 __global__ void __launch_bounds__(256) kgc_partial_kernel(const __grid_constant__ KgcArgs<T> a) {
   const ConvGeom& g = a.g;
-  extern __shared__ __align__(16) unsigned char smem[];
-  // tile of KT x KT outputs pixels + halo of x, plus v tile
   constexpr int KT = 16;
   const int SHx = KT + g.kh - 1, SWx = KT + g.kw - 1;
-  T* xs = reinterpret_cast<T*>(smem);
+  T* xs = reinterpret_cast<T*>(dsm());
   T* vs = xs + SHx * SWx;
   const int ntap = g.kh * g.kw;
   const int thH = (g.H + KT - 1) / KT, thW = (g.W + KT - 1) / KT;
   const int ntile = thH * thW;
   for (int grp = blockIdx.x; grp < a.ngroups; grp += gridDim.x) {
     for (int c = 0; c < g.C; ++c) {
-      // each thread owns taps t = threadIdx.x + k*blockDim
       double acc[12];
 #pragma unroll
       for (int k = 0; k < 12; ++k) acc[k] = 0.0;

@@ -632,7 +632,7 @@ int dense_plan_init(PlanImpl& P) {
   DenseState* S = new DenseState();
   P.ws[0] = S;
   ProgPool pool;
-  build_sum(S->sn, n, true, pool);
+  build_sum(S->sn, n, true, pool, false);   // in-CTA program evaluation (signal-length vectors)
   if (S->sn.nSub != 1) return dense_fail(ADP_ERR_UNSUPPORTED, "dense1d signal too long");
   const size_t es = (size_t)P.esize;
   size_t base = 64 * sizeof(double) + (size_t)(2 * S->sn.nLeaves + 2) * sizeof(double);

@@ -85,3 +85,56 @@ extern "C" int adp_vec(int32_t op, int64_t n, int32_t dtype, double a, const voi
   if (e != cudaSuccess) return dense_fail(ADP_ERR_CUDA, cudaGetErrorString(e));
   return ADP_OK;
 }
+
+// ---------------------------------------------------------------------------
+// FP64 roof microbenchmark: 8 independent DFMA chains per thread, 148 SMs x
+// full occupancy; reports sustained DFMA TFLOP/s (2 flop per DFMA) for the
+// roofline denominator (MEASURED_PEAKS.json carries no FP64 figure).
+__global__ void __launch_bounds__(256) dfma_peak_kernel(double* out, int iters, double a, double b) {
+  double r0 = threadIdx.x * 1e-9, r1 = r0 + 1e-9, r2 = r0 + 2e-9, r3 = r0 + 3e-9;
+  double r4 = r0 + 4e-9, r5 = r0 + 5e-9, r6 = r0 + 6e-9, r7 = r0 + 7e-9;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      r0 = fma(r0, a, b); r1 = fma(r1, a, b); r2 = fma(r2, a, b); r3 = fma(r3, a, b);
+      r4 = fma(r4, a, b); r5 = fma(r5, a, b); r6 = fma(r6, a, b); r7 = fma(r7, a, b);
+    }
+  }
+  const double s = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
+  if (s == 1234.5) out[0] = s;  // keep the chains alive
+}
+
+extern "C" int adp_fp64_peak(double* tflops, double* ms, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, dfma_peak_kernel, 256, 0);
+  const int grid = sms * nb, iters = 4096;
+  double* d_out = nullptr;
+  if (cudaMalloc(&d_out, sizeof(double)) != cudaSuccess) return dense_fail(ADP_ERR_CUDA, "alloc");
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  dfma_peak_kernel<<<grid, 256, 0, st>>>(d_out, 64, 0.999999, 1e-7);  // warm-up
+  float best = 1e30f;
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaEventRecord(e0, st);
+    dfma_peak_kernel<<<grid, 256, 0, st>>>(d_out, iters, 0.999999, 1e-7);
+    cudaEventRecord(e1, st);
+    cudaEventSynchronize(e1);
+    float t = 0;
+    cudaEventElapsedTime(&t, e0, e1);
+    best = t < best ? t : best;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d_out);
+  const double flops = 2.0 * 8.0 * 16.0 * (double)iters * 256.0 * (double)grid;
+  *ms = best;
+  *tflops = flops / (best * 1e-3) / 1e12;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return dense_fail(ADP_ERR_CUDA, cudaGetErrorString(e));
+  return ADP_OK;
+}

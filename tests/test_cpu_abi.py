@@ -70,6 +70,18 @@ def np_leaf(a):
     return res
 
 
+def perfect(vals):
+    """Perfect binary tree over vals zero-padded to a power of two."""
+    v = list(vals)
+    p = 1
+    while p < len(v):
+        p *= 2
+    v += [0.0] * (p - len(v))
+    while len(v) > 1:
+        v = [v[2 * i] + v[2 * i + 1] for i in range(len(v) // 2)]
+    return v[0]
+
+
 def eval_prog(words, off, vals):
     nL, nI, nLev = words[off], words[off + 1], words[off + 2]
     lev = words[off + 3: off + 4 + nLev]
@@ -89,7 +101,12 @@ def test_sum_layout_reproduces_np_sum(n):
     a = (rng.standard_normal(n) * np.exp(3 * rng.standard_normal(n))).astype(np.float64)
     nl, ns, top, leaf, sub_leaf, sub_prog, words = layout(n)
     leaves = [np_leaf(a[leaf[i]:leaf[i + 1]]) for i in range(nl)]
-    if ns == 1:
+    if top == -1:   # regular: perfect tree, device evaluates it in registers / shuffles
+        if ns == 1:
+            s = perfect(leaves)
+        else:
+            s = perfect([perfect(leaves[sub_leaf[t]:sub_leaf[t + 1]]) for t in range(ns)])
+    elif ns == 1:
         s = eval_prog(words, top, leaves)
     else:
         roots = [eval_prog(words, sub_prog[t], leaves[sub_leaf[t]:sub_leaf[t + 1]]) for t in range(ns)]
@@ -99,7 +116,6 @@ def test_sum_layout_reproduces_np_sum(n):
 
 def test_sum_layout_binary_tile_tree():
     nl, ns, top, leaf, sub_leaf, sub_prog, words = layout(5000, np_rule=False)
-    assert nl == 5000 and ns > 1
+    assert nl == 5000 and ns == 3 and top == -1
     vals = np.arange(5000, dtype=float)
-    roots = [eval_prog(words, sub_prog[t], vals[sub_leaf[t]:sub_leaf[t + 1]]) for t in range(ns)]
-    assert eval_prog(words, top, roots) == vals.sum()
+    assert perfect([perfect(vals[sub_leaf[t]:sub_leaf[t + 1]]) for t in range(ns)]) == vals.sum()
