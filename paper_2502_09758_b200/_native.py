@@ -90,6 +90,7 @@ SIGNATURES = {
     "adp_dot": (_I, [_P, _P, _P, ctypes.POINTER(_D), _P]),
     "adp_reg_op": (_I, [_P, ctypes.POINTER(Lower), _I, _P, _P, _P, ctypes.POINTER(_D), _P]),
     "adp_vec": (_I, [_I, ctypes.c_int64, _I, _D, _P, _P, _P, ctypes.POINTER(_D), _P]),
+    "adp_debug_trace": (_I, [_P, _I, _P]),
     "adp_fp64_peak": (_I, [ctypes.POINTER(_D), ctypes.POINTER(_D), _P]),
     "adp_sum_layout": (_I, [ctypes.c_int64, _I, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(_I),
                             ctypes.POINTER(_I), _P, ctypes.c_int64, _P, _P, ctypes.c_int64, _P, ctypes.c_int64,

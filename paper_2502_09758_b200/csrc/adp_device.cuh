@@ -198,6 +198,48 @@ __device__ __forceinline__ double eval_prog(const int* __restrict__ prog, double
   return r;
 }
 
+// 8-byte asynchronous global -> shared copy (LDGSTS); valid == false
+// zero-fills the destination.
+__device__ __forceinline__ void cp_async8(double* dst_smem, const double* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst_smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+// Perfect binary tree over c[0..chunk), chunk a power of two (registers for
+// chunk <= 16; 16-blocks combined by a binary counter beyond).
+__device__ __forceinline__ double fold8(const double* c) {
+  return ((c[0] + c[1]) + (c[2] + c[3])) + ((c[4] + c[5]) + (c[6] + c[7]));
+}
+__device__ __forceinline__ double fold_pow2(const double* c, int chunk) {
+  switch (chunk) {
+    case 1: return c[0];
+    case 2: return c[0] + c[1];
+    case 4: return (c[0] + c[1]) + (c[2] + c[3]);
+    case 8: return fold8(c);
+    case 16: return fold8(c) + fold8(c + 8);
+    default: break;
+  }
+  double st[12];
+  double root = 0.0;
+  for (int b = 0; b < chunk / 16; ++b) {
+    double v = fold8(c + 16 * b) + fold8(c + 16 * b + 8);
+#pragma unroll
+    for (int lv = 0; lv < 12; ++lv) {
+      if ((b >> lv) & 1) {
+        v = st[lv] + v;
+      } else {
+        st[lv] = v;
+        break;
+      }
+    }
+    root = v;
+  }
+  return root;
+}
+
 // Perfect binary tree over vals[0..n), zero-padded to the next power of two,
 // evaluated by one CTA (blockDim a power of two): values staged in shared
 // memory, each thread folds a contiguous power-of-two chunk with a binary
@@ -209,38 +251,11 @@ __device__ __forceinline__ double tree_reduce_cta(const double* __restrict__ val
   const int BD = blockDim.x;
   const int T = 1 << (31 - __clz(BD));          // folding threads: largest power of two <= blockDim
   const int chunk = P > T ? P / T : 1;
-  for (int k0 = threadIdx.x; k0 < P; k0 += 8 * BD) {
-    double v[8];
-#pragma unroll
-    for (int b = 0; b < 8; ++b) {
-      const int k = k0 + b * BD;
-      v[b] = k < n ? ldcg(vals + k) : 0.0;
-    }
-#pragma unroll
-    for (int b = 0; b < 8; ++b)
-      if (k0 + b * BD < P) sv[k0 + b * BD] = v[b];
-  }
+  for (int e = threadIdx.x; e < P; e += BD) cp_async8(sv + e, vals + (e < n ? e : 0), e < n);
+  cp_async_wait_all();
   __syncthreads();
   double root = 0.0;
-  if (threadIdx.x * chunk < P) {
-    const double* c = sv + threadIdx.x * chunk;
-    double st[14];
-#pragma unroll
-    for (int lv = 0; lv < 14; ++lv) st[lv] = 0.0;
-    for (int i = 0; i < chunk; ++i) {
-      double v = c[i];
-#pragma unroll
-      for (int lv = 0; lv < 14; ++lv) {
-        if ((i >> lv) & 1) {
-          v = st[lv] + v;
-        } else {
-          st[lv] = v;
-          break;
-        }
-      }
-      root = v;
-    }
-  }
+  if (threadIdx.x * chunk < P) root = fold_pow2(sv + threadIdx.x * chunk, chunk);
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) root = root + __shfl_xor_sync(kFull, root, o);
   __syncthreads();
@@ -330,23 +345,15 @@ __device__ __forceinline__ void reduce_list(const SumDev* const* ss, int k, doub
     for (int i = 0; i < k; ++i) out[i] = sum_phase2(*ss[i], sv);
     return;
   }
-  // stage all regular sums, 8 loads in flight per thread
+  // stage all regular sums with asynchronous copies: every element of every
+  // sum is in flight at once (zero-filled past n), one wait for all
   for (int i = 0; i < k; ++i) {
     if (!P[i]) continue;
     const SumDev& s = *ss[i];
     const double* src = s.nSub > 1 ? s.sub_vals : s.leaf_vals;
-    for (int k0 = threadIdx.x; k0 < P[i]; k0 += 8 * BD) {
-      double v[8];
-#pragma unroll
-      for (int b = 0; b < 8; ++b) {
-        const int e = k0 + b * BD;
-        v[b] = e < n[i] ? ldcg(src + e) : 0.0;
-      }
-#pragma unroll
-      for (int b = 0; b < 8; ++b)
-        if (k0 + b * BD < P[i]) sv[base[i] + k0 + b * BD] = v[b];
-    }
+    for (int e = threadIdx.x; e < P[i]; e += BD) cp_async8(sv + base[i] + e, src + (e < n[i] ? e : 0), e < n[i]);
   }
+  cp_async_wait_all();
   __syncthreads();
   double* red = sv + kTreeStage;   // 8 x 32 warp partials + 8 results
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = BD >> 5;
@@ -354,25 +361,7 @@ __device__ __forceinline__ void reduce_list(const SumDev* const* ss, int k, doub
     if (!P[i]) continue;
     const int chunk = P[i] > T ? P[i] / T : 1;
     double root = 0.0;
-    if (threadIdx.x * chunk < P[i]) {
-      const double* c = sv + base[i] + threadIdx.x * chunk;
-      double st[14];
-#pragma unroll
-      for (int lv = 0; lv < 14; ++lv) st[lv] = 0.0;
-      for (int e = 0; e < chunk; ++e) {
-        double v = c[e];
-#pragma unroll
-        for (int lv = 0; lv < 14; ++lv) {
-          if ((e >> lv) & 1) {
-            v = st[lv] + v;
-          } else {
-            st[lv] = v;
-            break;
-          }
-        }
-        root = v;
-      }
-    }
+    if (threadIdx.x * chunk < P[i]) root = fold_pow2(sv + base[i] + threadIdx.x * chunk, chunk);
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) root = root + __shfl_xor_sync(kFull, root, o);
     if (lane == 0) red[i * 32 + warp] = root;

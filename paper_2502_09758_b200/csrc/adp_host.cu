@@ -313,6 +313,10 @@ static int conv_plan_init(PlanImpl& P) {
   g.SH = g.TH + 2 * g.rh + 2;
   const int SWL = g.TW + 2 * g.rw + 2;
   g.SWP = SWL + SWL / kRW + 1;
+  {
+    const unsigned long long rowE = (unsigned long long)SWL * g.C;
+    g.magicRow = (unsigned)(((1ull << 32) + rowE - 1) / rowE);
+  }
   g.YSH = g.TH + 2;
   g.YSWP = (g.TW + 2) + (g.TW + 2) / kRW + 1;
   g.N = (int64_t)g.H * g.W * g.C;
@@ -716,6 +720,7 @@ int adp_lower_solve(adp_plan* p, const adp_lower* lp, const void* x0, void* x_ou
     a.v0 = (const T*)sa->v0;
     a.x0 = (const T*)x0;
     a.out = (T*)x_out;
+    a.trace = P.d_trace;
     if (int e = launch_coop(P, P.k_solve, a, STREAM(stream))) return e;
     CK(cudaMemcpyAsync(P.h_sres, P.d_sres, sizeof(SolveOut), cudaMemcpyDeviceToHost, STREAM(stream)));
     CK(cudaStreamSynchronize(STREAM(stream)));
@@ -882,5 +887,25 @@ extern "C" int adp_sum_layout(int64_t n, int32_t np_rule, int64_t* n_leaves, int
   for (size_t i = 0; i < s.sub_leaf.size(); ++i) sub_leaf[i] = s.sub_leaf[i];
   for (size_t i = 0; i < s.sub_prog.size(); ++i) sub_prog[i] = s.sub_prog[i];
   for (size_t i = 0; i < pool.words.size(); ++i) words[i] = pool.words[i];
+  return ADP_OK;
+}
+
+// Debug: enable (enable = 1) per-phase %globaltimer stamps of the next solves
+// (first 64 iterations, 16 slots each); enable = 0 copies them to host_out
+// (64 * 16 uint64) and disables.
+extern "C" int adp_debug_trace(adp_plan* p, int32_t enable, uint64_t* host_out) {
+  if (!p) return fail(ADP_ERR_ARG, "null plan");
+  PlanImpl& P = p->impl;
+  if (enable) {
+    if (!P.d_trace) CK(cudaMalloc(&P.d_trace, 64 * 16 * sizeof(unsigned long long)));
+    CK(cudaMemset(P.d_trace, 0, 64 * 16 * sizeof(unsigned long long)));
+    return ADP_OK;
+  }
+  if (P.d_trace) {
+    CK(cudaDeviceSynchronize());
+    if (host_out) CK(cudaMemcpy(host_out, P.d_trace, 64 * 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    cudaFree(P.d_trace);
+    P.d_trace = nullptr;
+  }
   return ADP_OK;
 }

@@ -64,6 +64,7 @@ struct PlanImpl {
   CGOut* h_cres = nullptr;
   double* h_scal = nullptr;
   KernelInfo k_solve, k_cg, k_misc;
+  unsigned long long* d_trace = nullptr;   // debug: per-phase timestamps of solve (adp_debug_trace)
   // dense 1-D engine data
   int dense_grid = 0;
   size_t dense_smem = 0;

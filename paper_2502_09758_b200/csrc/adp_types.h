@@ -67,6 +67,7 @@ struct ConvGeom {
   int QP;                  // pitch of the TV Q planes
   int tpc;                 // threads per channel (TH * TW / RW); CTA = tpc * C threads
   unsigned magicC;         // ceil(2^20 / C): px = (e * magicC) >> 20 for e < 2^15
+  unsigned magicRow;       // ceil(2^32 / rowE): row of a flattened tile-box index
   int o_ws, o_wf, o_pa, o_pq, o_tm, o_sv;   // byte offsets in dynamic smem
   int64_t N;               // H*W*C
 };

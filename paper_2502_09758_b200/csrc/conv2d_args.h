@@ -58,6 +58,7 @@ struct ConvArgs {
   double* scal;            // misc scalar outputs
   int mode;                // misc kernel mode
   int nofloor;             // hess_diag without the 1e-12*max floor (regularizer-only call)
+  unsigned long long* trace;  // optional phase timestamps (CTA 0): [iter][16] %globaltimer ns
   const T* in0; const T* in1; T* out0; T* out1;
 };
 

@@ -161,36 +161,63 @@ struct Conv {
   // ---- load tile + (r+1) halo of all channels into the planes.  One warp
   // per tile row (a contiguous run of global memory), lanes over elements,
   // kB loads per lane in flight before any store.
+  // element k of the flattened (row, interleaved column) tile box -> global
+  // index (or -1 when outside the image) and plane offset
+  __device__ __forceinline__ void box_elem(int k, int gh0, int gw0, int64_t& gi, int& off) const {
+    const int C = a.g.C, rowE = (a.g.TW + 2 * a.g.rw + 2) * C;
+    const int sr = (int)(((unsigned long long)k * a.g.magicRow) >> 32);
+    const int e = k - sr * rowE;
+    const int px = (int)(((unsigned long long)e * a.g.magicC) >> 20);
+    const int c = e - px * C;
+    const int gh = gh0 + sr, gw = gw0 + px;
+    off = c * a.g.SH * a.g.SWP + sr * a.g.SWP + sk(px);
+    gi = (gh >= 0 && gh < a.g.H && gw >= 0 && gw < a.g.W) ? ((int64_t)gh * a.g.W + gw) * C + c : -1;
+  }
+
+  // computed sources: kB2 loads per thread in flight, then the stores
+  static constexpr int kB2 = 16;
   template <class Src>
   __device__ void load_full(int h0, int w0, const Src& src) const {
-    const int C = a.g.C, SWL = a.g.TW + 2 * a.g.rw + 2, rowE = SWL * C, H = a.g.H, W = a.g.W;
-    const int SH = a.g.SH, SWP = a.g.SWP;
-    const unsigned magic = a.g.magicC;
+    const int total = a.g.SH * (a.g.TW + 2 * a.g.rw + 2) * a.g.C;
     const int gh0 = h0 - a.g.rh - 1, gw0 = w0 - a.g.rw - 1;
-    const int lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    const int BD = blockDim.x;
     T* dst = pa();
-    for (int sr = threadIdx.x >> 5; sr < SH; sr += nwarps) {
-      const int gh = gh0 + sr;
-      const bool rowok = gh >= 0 && gh < H;
-      const int64_t gbase = ((int64_t)gh * W + gw0) * C;
-      for (int e0 = lane; e0 < rowE; e0 += 32 * kB) {
-        T v[kB];
-        int off[kB];
+    for (int k0 = threadIdx.x; k0 < total; k0 += kB2 * BD) {
+      T v[kB2];
+      int off[kB2];
 #pragma unroll
-        for (int b = 0; b < kB; ++b) {
-          const int e = e0 + 32 * b;
-          const int px = (int)(((unsigned long long)e * magic) >> 20);
-          const int c = e - px * C;
-          const int gw = gw0 + px;
-          off[b] = e < rowE ? c * SH * SWP + sr * SWP + sk(px) : -1;
-          v[b] = (e < rowE && rowok && gw >= 0 && gw < W) ? src(gbase + e) : T(0);
-        }
-#pragma unroll
-        for (int b = 0; b < kB; ++b)
-          if (off[b] >= 0) dst[off[b]] = v[b];
+      for (int b = 0; b < kB2; ++b) {
+        const int k = k0 + b * BD;
+        int64_t gi = -1;
+        off[b] = -1;
+        if (k < total) box_elem(k, gh0, gw0, gi, off[b]);
+        v[b] = gi >= 0 ? src(gi) : T(0);
       }
+#pragma unroll
+      for (int b = 0; b < kB2; ++b)
+        if (off[b] >= 0) dst[off[b]] = v[b];
     }
   }
+  // plain copies: asynchronous global -> shared (LDGSTS), zero fill outside;
+  // the caller's __syncthreads() after cp_async_wait_all() publishes them
+  __device__ void load_copy(int h0, int w0, const T* x) const {
+    const int total = a.g.SH * (a.g.TW + 2 * a.g.rw + 2) * a.g.C;
+    const int gh0 = h0 - a.g.rh - 1, gw0 = w0 - a.g.rw - 1;
+    T* dst = pa();
+    for (int k = threadIdx.x; k < total; k += blockDim.x) {
+      int64_t gi;
+      int off;
+      box_elem(k, gh0, gw0, gi, off);
+      const unsigned d = (unsigned)__cvta_generic_to_shared(dst + off);
+      const T* s = x + (gi >= 0 ? gi : 0);
+      if (sizeof(T) == 8)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(s), "r"(gi >= 0 ? 8 : 0) : "memory");
+      else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(s), "r"(gi >= 0 ? 4 : 0) : "memory");
+    }
+    cp_async_wait_all();
+  }
+  __device__ __forceinline__ void load_full(int h0, int w0, const SrcLin<T>& src) const { load_copy(h0, w0, src.x); }
 
   // ---- register-blocked correlation: RW consecutive outputs (row ty, cols
   // tx*RW..) of the thread's channel plane with stencil w (kh x kw).  Per
@@ -304,8 +331,14 @@ struct Conv {
       tile_origin(tile, h0, w0);
       __syncthreads();
       load_full(h0, w0, src);
-      __syncthreads();
       const int h = h0 + ty;
+      T ypre[RW];   // epilogue operands prefetched so their latency overlaps the stencil
+#pragma unroll
+      for (int o = 0; o < RW; ++o) {
+        const int w = w0 + tx * RW + o;
+        ypre[o] = (h < H && w < W) ? ydat[gidx(h, w, ch)] : T(0);
+      }
+      __syncthreads();
       T acc[RW];
       stencil_fwd(acc);
 #pragma unroll
@@ -314,7 +347,7 @@ struct Conv {
         const int w = w0 + q;
         if (h < H && w < W) {
           const int64_t i = gidx(h, w, ch);
-          const T r = acc[o] - ydat[i];
+          const T r = acc[o] - ypre[o];
           Rout[i] = r;
           if (fused) put_term(0, ty, q, (double)(r * r));
         }
@@ -397,8 +430,23 @@ struct Conv {
       tile_origin(tile, h0, w0);
       __syncthreads();
       load_full(h0, w0, SrcLin<T>{Rin});
-      __syncthreads();
       const int h = h0 + ty;
+      T tpre[RW], ypre[RW];   // prefetched epilogue operands
+#pragma unroll
+      for (int o = 0; o < RW; ++o) {
+        const int w = w0 + tx * RW + o;
+        tpre[o] = T(0);
+        ypre[o] = T(0);
+        if (h < H && w < W) {
+          const int64_t i = gidx(h, w, ch);
+          if (tv) tpre[o] = ldcg(TVGin + i);
+          if (Xc) {
+            const T xv = ldcg(Xs + i), xpv = ldcg(XPs + i);
+            ypre[o] = xv + beta * (xv - xpv);
+          }
+        }
+      }
+      __syncthreads();
       double part = 0.0;
       T acc[RW];
       stencil_adj(acc);
@@ -408,14 +456,10 @@ struct Conv {
         if (h < H && w < W) {
           const int64_t i = gidx(h, w, ch);
           T gv = two * acc[o];
-          if (tv) gv = gv + alpha * ldcg(TVGin + i);
+          if (tv) gv = gv + alpha * tpre[o];
           Gout[i] = gv;
           part += (double)gv * (double)gv;
-          if (Xc) {
-            const T xv = ldcg(Xs + i), xpv = ldcg(XPs + i);
-            const T y = xv + beta * (xv - xpv);
-            Xc[i] = y - gv / L;
-          }
+          if (Xc) Xc[i] = ypre[o] - gv / L;
         }
       }
       if (sgg) store_tile_partial(*sgg, tile, part, red());
@@ -438,8 +482,22 @@ struct Conv {
       tile_origin(tile, h0, w0);
       __syncthreads();
       load_full(h0, w0, src);
-      __syncthreads();
       const int h = h0 + ty;
+      T ypre[RW], gpre[RW], xopre[RW];   // prefetched epilogue operands
+#pragma unroll
+      for (int o = 0; o < RW; ++o) {
+        const int w = w0 + tx * RW + o;
+        ypre[o] = gpre[o] = xopre[o] = T(0);
+        if (h < H && w < W) {
+          const int64_t i = gidx(h, w, ch);
+          ypre[o] = a.ydat[i];
+          if (sdot) {
+            gpre[o] = ldcg(Gin + i);
+            xopre[o] = ldcg(Xold + i);
+          }
+        }
+      }
+      __syncthreads();
       double part = 0.0;
       T acc[RW];
       stencil_fwd(acc);
@@ -449,7 +507,7 @@ struct Conv {
         const int w = w0 + q;
         if (h < H && w < W) {
           const int64_t i = gidx(h, w, ch);
-          const T rc = acc[o] - a.ydat[i];
+          const T rc = acc[o] - ypre[o];
           const T xc = fp(ty, q);
           if (fused) put_term(0, ty, q, (double)(rc * rc));
           else RCout[i] = rc;
@@ -467,7 +525,7 @@ struct Conv {
             }
           }
           if (Xout) Xout[i] = xc;
-          if (sdot) part += (double)ldcg(Gin + i) * (double)(xc - ldcg(Xold + i));
+          if (sdot) part += (double)gpre[o] * (double)(xc - xopre[o]);
         }
       }
       if (sdot) store_tile_partial(*sdot, tile, part, red());

@@ -88,6 +88,16 @@ struct ConvOps : Conv<T, FAST, RW> {
   }
 };
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define ADP_TRACE(it, k)                                                               \
+  do {                                                                                 \
+    if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && (it) < 64) a.trace[(it) * 16 + (k)] = gtimer(); \
+  } while (0)
+
 // ---------------------------------------------------------------------------
 // solve_lower (lower_solvers.py:104-213) as one persistent kernel.
 template <typename T, bool FAST, int RW>
@@ -144,12 +154,22 @@ __global__ void __launch_bounds__(512, 1) conv_solve_kernel(const __grid_constan
     double L_try = (a.method == M_PROXGRAD) ? 1.0 / gd_step : lip_t;
     // value and gradient at y (stages A, B); stage B also writes the own
     // pixels of the first candidate y - g / L_try (adaptive path)
-    if (a.adaptive)
-      E.value_grad(SrcExtrap<T>{a.X[ix], a.X[ixp], tb}, tv, a.G, a.X[ix], a.X[ixp], tb, T(L_try), a.X[ic]);
-    else
+    ADP_TRACE(t, 0);
+    if (a.adaptive) {
+      E.stageA(SrcExtrap<T>{a.X[ix], a.X[ixp], tb}, a.R, a.ydat, tv, a.TV2, a.TVG, &a.s_fit, &a.s_tv);
+      ADP_TRACE(t, 1);
+      E.gb.sync();
+      ADP_TRACE(t, 2);
+      E.stageB(a.R, tv, a.TVG, a.G, &a.s_t0, a.X[ix], a.X[ixp], tb, T(L_try), a.X[ic]);
+      E.leaves_if_unfused(a.s_fit, a.R, true);
+      if (tv) E.leaves_if_unfused(a.s_tv, a.TV2, false);
+    } else {
       E.value_grad(SrcExtrap<T>{a.X[ix], a.X[ixp], tb}, tv, a.G);
+    }
     ++vg;
+    ADP_TRACE(t, 3);
     E.gb.sync();
+    ADP_TRACE(t, 4);
     if (a.adaptive) {
       E.value_cand(SrcLin<T>{a.X[ic]}, tv, nullptr, a.G, a.X[ix], &a.s_t1);
       ++vals;
@@ -158,13 +178,16 @@ __global__ void __launch_bounds__(512, 1) conv_solve_kernel(const __grid_constan
     } else {
       E.stageCLight(SrcCand<T>{a.X[ix], a.X[ixp], a.G, tb, T(lip_t)}, a.X[ic], a.G, a.X[ix], &a.s_t1);
     }
+    ADP_TRACE(t, 5);
     E.gb.sync();
+    ADP_TRACE(t, 6);
     // fit(y), tv(y), g.g, dot, [fit(xc), tv(xc)]
     double o[6] = {0, 0, 0, 0, 0, 0};
     if (a.adaptive && tv) E.reduce({&a.s_fit, &a.s_tv, &a.s_t0, &a.s_t1, &a.s_fitc, &a.s_tvc}, o);
     else if (a.adaptive) { E.reduce({&a.s_fit, &a.s_t0, &a.s_t1, &a.s_fitc}, o + 2); o[0] = o[2]; o[2] = o[3]; o[3] = o[4]; o[4] = o[5]; o[5] = 0.0; }
     else if (tv) E.reduce({&a.s_fit, &a.s_tv, &a.s_t0, &a.s_t1}, o);
     else { E.reduce({&a.s_fit, &a.s_t0, &a.s_t1}, o + 1); o[0] = o[1]; o[1] = 0.0; }
+    ADP_TRACE(t, 7);
     const double fit = o[0];
     h_y = fit;
     if (tv) h_y = fit + a.alpha * (o[1] - a.nu * twoN);
@@ -199,6 +222,7 @@ __global__ void __launch_bounds__(512, 1) conv_solve_kernel(const __grid_constan
         if (tv) E.reduce({&a.s_fitc, &a.s_tvc, &a.s_t1}, o3);
         else { E.reduce({&a.s_fitc, &a.s_t1}, o3); o3[2] = o3[1]; o3[1] = 0.0; }
         fitc = o3[0]; tvc = o3[1]; dot = o3[2];
+        ADP_TRACE(t, 8 + min(k, 7));
       }
       if (status != ST_OK) { done = true; break; }
       const double bstep = 1.0 / L_try;
