@@ -67,6 +67,7 @@ typedef struct {
   int32_t H, W, C; /* depthwise2d image; dense1d: H = 1, W = n, C = 1 */
   int32_t kh, kw;  /* stencil size (odd); dense1d: kh = kw = n */
   int32_t tile_h, tile_w; /* 0 = auto */
+  int32_t rw;             /* register blocking: outputs per thread (1, 2, 4); 0 = auto */
 } adp_plan_desc;
 
 /* Lower problem h(x, b) = ||B_b x - y||^2 + alpha J(x) (lower_solvers.py:20-25) */

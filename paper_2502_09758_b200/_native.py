@@ -31,7 +31,7 @@ STATUS_OK, STATUS_DIVERGED, STATUS_BT_FAIL, STATUS_NEGCURV = 0, 1, 2, 3
 
 class PlanDesc(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in
-                ("layout", "dtype", "mode", "H", "W", "C", "kh", "kw", "tile_h", "tile_w")]
+                ("layout", "dtype", "mode", "H", "W", "C", "kh", "kw", "tile_h", "tile_w", "rw")]
 
 
 class Lower(ctypes.Structure):

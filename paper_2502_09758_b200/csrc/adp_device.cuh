@@ -27,7 +27,10 @@ __device__ __forceinline__ T madd(T acc, T a, T b) {
   }
 }
 
-template <typename T> __device__ __forceinline__ T ldcg(const T* p) { return __ldcg(p); }
+// Loads of data produced earlier in the same (persistent) kernel.  Every
+// grid barrier ends with a GPU-scope fence that invalidates the SM's L1
+// (CCTL.IVALL), so plain weak loads observe the other CTAs' writes.
+template <typename T> __device__ __forceinline__ T ldcg(const T* p) { return *p; }
 
 // ---------------------------------------------------------------------------
 // Grid barrier (all CTAs co-resident: cooperative launch).  `counter` is

@@ -276,7 +276,11 @@ static void fill_sum(SumDev& sd, const SumHost& sh, const int* d_progs, const in
 
 static int setup_kernel(PlanImpl& P, KernelInfo& k, const void* fn, int threads, size_t smem, int max_grid) {
   k.fn = fn;
-  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_optin));
+  cudaFuncAttributes fa;
+  CK(cudaFuncGetAttributes(&fa, fn));
+  const size_t dyn_max = P.smem_optin - fa.sharedSizeBytes;   // static smem (argument copy) counts too
+  if (smem > dyn_max) return fail(ADP_ERR_UNSUPPORTED, "tile + halo exceeds shared memory; use a smaller tile");
+  CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_max));
   int nb = 0;
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem));
   if (nb <= 0) return fail(ADP_ERR_UNSUPPORTED, "kernel does not fit on an SM (smem/registers)");
@@ -299,10 +303,26 @@ static int conv_plan_init(PlanImpl& P) {
     g.leafL = s.regular ? s.leaf_len : 0;
   }
   choose_tiles(d, g.leafL, g.TH, g.TW, g.fused);
-  if (g.TW % kRW) return fail(ADP_ERR_ARG, "tile width must be a multiple of 4");
+  // register blocking: small single-channel problems are latency-bound with
+  // one warp per SM sub-partition at RW = 4; RW = 2 gives 2x the warps on the
+  // same tile (c2 512x512x1: 41 us/iter vs 51 at RW = 4; RW = 1 measured 43,
+  // the extra warps do not pay for the lost window reuse).  ADP_RW overrides.
+  {
+    const int64_t px_per_sm = (int64_t)d.H * d.W / std::max(1, P.sm_count);
+    int rwb = (d.C == 1 && px_per_sm < 8192) ? 2 : 4;
+    if (d.rw == 1 || d.rw == 2 || d.rw == 4) rwb = d.rw;
+    if (const char* ev = getenv("ADP_RW")) {
+      const int v = atoi(ev);
+      if (v == 1 || v == 2 || v == 4) rwb = v;
+    }
+    if (P.d.dtype == ADP_DTYPE_F32) rwb = 4;
+    g.rwb = rwb;
+  }
+  const int kRWp = g.rwb;
+  if (g.TW % 4) return fail(ADP_ERR_ARG, "tile width must be a multiple of 4");
   if (d.tile_h <= 0)
-    while (g.TH > 1 && g.TH * (g.TW / kRW) * g.C > 512) g.TH /= 2;   // channel-parallel CTA <= 512 threads
-  g.tpc = g.TH * g.TW / kRW;
+    while (g.TH > 1 && g.TH * (g.TW / kRWp) * g.C > 512) g.TH /= 2;   // channel-parallel CTA <= 512 threads
+  g.tpc = g.TH * g.TW / kRWp;
   g.threads = g.tpc * g.C;
   g.magicC = (unsigned)((1u << 20) + g.C - 1) / (unsigned)g.C;
   if (g.tpc % 32 || g.threads > 512)
@@ -312,13 +332,13 @@ static int conv_plan_init(PlanImpl& P) {
   g.nTiles = g.tilesH * g.tilesW;
   g.SH = g.TH + 2 * g.rh + 2;
   const int SWL = g.TW + 2 * g.rw + 2;
-  g.SWP = SWL + SWL / kRW + 1;
+  g.SWP = kRWp == 1 ? SWL + 1 : SWL + SWL / kRWp + 1;
   {
     const unsigned long long rowE = (unsigned long long)SWL * g.C;
     g.magicRow = (unsigned)(((1ull << 32) + rowE - 1) / rowE);
   }
   g.YSH = g.TH + 2;
-  g.YSWP = (g.TW + 2) + (g.TW + 2) / kRW + 1;
+  g.YSWP = (g.TW + 2) + (g.TW + 2) / kRWp + 1;
   g.N = (int64_t)g.H * g.W * g.C;
   P.smem = conv_smem(g, P.esize);
   if (P.smem > smem_optin) return fail(ADP_ERR_UNSUPPORTED, "tile + halo exceeds shared memory; use a smaller tile");
@@ -407,9 +427,7 @@ static int conv_plan_init(PlanImpl& P) {
   CK(cudaMallocHost(&P.h_cres, sizeof(CGOut)));
   CK(cudaMallocHost(&P.h_scal, 64 * sizeof(double)));
 
-  ConvKernelSet ks = P.d.dtype == ADP_DTYPE_F32 ? conv_kernels_f32()
-                     : P.d.mode == ADP_MODE_FAST ? conv_kernels_f64f()
-                                                 : conv_kernels_f64s();
+  ConvKernelSet ks = conv_kernels(P.d.dtype, P.d.mode, P.g.rwb);
   const int maxg = g.nTiles;
   if (int e = setup_kernel(P, P.k_solve, ks.solve, g.threads, P.smem, maxg)) return e;
   if (int e = setup_kernel(P, P.k_cg, ks.cg, g.threads, P.smem, maxg)) return e;
@@ -483,9 +501,7 @@ static int conv_misc(PlanImpl& P, int mode, const adp_lower* lp, const void* ker
 template <typename T>
 static int conv_kgc(PlanImpl& P, const void* xa, const void* va, const void* xb, const void* vb, void* out,
                     double scale, cudaStream_t st) {
-  ConvKernelSet ks = P.d.dtype == ADP_DTYPE_F32 ? conv_kernels_f32()
-                     : P.d.mode == ADP_MODE_FAST ? conv_kernels_f64f()
-                                                 : conv_kernels_f64s();
+  ConvKernelSet ks = conv_kernels(P.d.dtype, P.d.mode, P.g.rwb);
   KgcArgs<T> a;
   std::memset(&a, 0, sizeof(a));
   a.g = P.g;
@@ -896,14 +912,15 @@ extern "C" int adp_sum_layout(int64_t n, int32_t np_rule, int64_t* n_leaves, int
 extern "C" int adp_debug_trace(adp_plan* p, int32_t enable, uint64_t* host_out) {
   if (!p) return fail(ADP_ERR_ARG, "null plan");
   PlanImpl& P = p->impl;
+  const size_t bytes = (64 * 16 + 64) * sizeof(unsigned long long);   // + sub-phase stamps
   if (enable) {
-    if (!P.d_trace) CK(cudaMalloc(&P.d_trace, 64 * 16 * sizeof(unsigned long long)));
-    CK(cudaMemset(P.d_trace, 0, 64 * 16 * sizeof(unsigned long long)));
+    if (!P.d_trace) CK(cudaMalloc(&P.d_trace, bytes));
+    CK(cudaMemset(P.d_trace, 0, bytes));
     return ADP_OK;
   }
   if (P.d_trace) {
     CK(cudaDeviceSynchronize());
-    if (host_out) CK(cudaMemcpy(host_out, P.d_trace, 64 * 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    if (host_out) CK(cudaMemcpy(host_out, P.d_trace, bytes, cudaMemcpyDeviceToHost));
     cudaFree(P.d_trace);
     P.d_trace = nullptr;
   }

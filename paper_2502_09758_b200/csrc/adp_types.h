@@ -66,6 +66,7 @@ struct ConvGeom {
   int leafL;               // common leaf length (elements) when fused
   int QP;                  // pitch of the TV Q planes
   int tpc;                 // threads per channel (TH * TW / RW); CTA = tpc * C threads
+  int rwb;                 // register blocking RW of the instantiated kernels (1, 2, 4)
   unsigned magicC;         // ceil(2^20 / C): px = (e * magicC) >> 20 for e < 2^15
   unsigned magicRow;       // ceil(2^32 / rowE): row of a flattened tile-box index
   int o_ws, o_wf, o_pa, o_pq, o_tm, o_sv;   // byte offsets in dynamic smem

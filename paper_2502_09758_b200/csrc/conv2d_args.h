@@ -82,5 +82,16 @@ struct ConvKernelSet {
 ConvKernelSet conv_kernels_f64s();
 ConvKernelSet conv_kernels_f64f();
 ConvKernelSet conv_kernels_f32();
+ConvKernelSet conv_kernels_f64s_rw2();
+ConvKernelSet conv_kernels_f64f_rw2();
+ConvKernelSet conv_kernels_f64s_rw1();
+ConvKernelSet conv_kernels_f64f_rw1();
+inline ConvKernelSet conv_kernels(int dtype, int mode, int rw) {
+  if (dtype == 1) return conv_kernels_f32();
+  const bool fast = mode == 1;
+  if (rw == 1) return fast ? conv_kernels_f64f_rw1() : conv_kernels_f64s_rw1();
+  if (rw == 2) return fast ? conv_kernels_f64f_rw2() : conv_kernels_f64s_rw2();
+  return fast ? conv_kernels_f64f() : conv_kernels_f64s();
+}
 
 }  // namespace adp

@@ -36,6 +36,26 @@ __device__ __forceinline__ unsigned char* dsm() {
   return adp_dyn_smem;
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// sub-phase SM-cycle stamps (CTA 0, thread 0), accumulated over calls:
+// trace[1024 + k] += t_{k+1} - t_k, trace[1023 + 64] counts calls
+#define ADP_SUB(k)                                                                  \
+  do {                                                                              \
+    if (a.trace && blockIdx.x == 0 && (threadIdx.x & 31) == 0) sub_t[k] = clock64(); \
+  } while (0)
+#define ADP_SUB_FLUSH(n)                                                            \
+  do {                                                                              \
+    if (a.trace && blockIdx.x == 0 && (threadIdx.x & 31) == 0 && threadIdx.x < 7 * 32) { \
+      for (int k_ = 0; k_ + 1 < (n); ++k_)                                          \
+        a.trace[1024 + (threadIdx.x >> 5) * 8 + k_] += (unsigned long long)(sub_t[k_ + 1] - sub_t[k_]); \
+      if (threadIdx.x == 0) a.trace[1024 + 63] += 1;                                \
+    }                                                                               \
+  } while (0)
+
 // ---------------------------------------------------------------------------
 // value sources used by the tile loaders (each computes exactly the
 // reference expression for one element)
@@ -102,7 +122,8 @@ struct Conv {
   const ConvArgs<T>& a;
   int ch, ty, tx;                // this thread's channel, tile row, column group
 
-  __device__ static __forceinline__ int sk(int col) { return col + (col >> kShift); }
+  __device__ static __forceinline__ int sk(int col) { return RW == 1 ? col : col + (col >> kShift); }
+  __device__ static __forceinline__ int skr(int m) { return RW == 1 ? m : m + (m >> kShift); }
 
   __device__ explicit Conv(const ConvArgs<T>& a_) : a(a_) {
     const int tpr = a.g.TW / RW;
@@ -174,28 +195,45 @@ struct Conv {
     gi = (gh >= 0 && gh < a.g.H && gw >= 0 && gw < a.g.W) ? ((int64_t)gh * a.g.W + gw) * C + c : -1;
   }
 
-  // computed sources: kB2 loads per thread in flight, then the stores
-  static constexpr int kB2 = 16;
+  // Tile-box loader: warps own rows (each a contiguous run of global
+  // memory), lanes walk the row's interleaved elements; two rows per warp
+  // in flight, predicated (branch-free) loads, geometry in registers.
+  static constexpr int kJ = 8;   // lane steps per row handled per pass (rows longer than 256 loop)
   template <class Src>
   __device__ void load_full(int h0, int w0, const Src& src) const {
-    const int total = a.g.SH * (a.g.TW + 2 * a.g.rw + 2) * a.g.C;
+    const int C = a.g.C, H = a.g.H, W = a.g.W, SH = a.g.SH, SWP = a.g.SWP;
+    const unsigned mC = a.g.magicC;
+    const int rowE = (a.g.TW + 2 * a.g.rw + 2) * C, planeSz = SH * SWP;
     const int gh0 = h0 - a.g.rh - 1, gw0 = w0 - a.g.rw - 1;
-    const int BD = blockDim.x;
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     T* dst = pa();
-    for (int k0 = threadIdx.x; k0 < total; k0 += kB2 * BD) {
-      T v[kB2];
-      int off[kB2];
+    for (int e0 = 0; e0 < rowE; e0 += 32 * kJ) {
+      for (int sr0 = threadIdx.x >> 5; sr0 < SH; sr0 += 2 * nw) {
+        T v[2][kJ];
+        int off[2][kJ];
 #pragma unroll
-      for (int b = 0; b < kB2; ++b) {
-        const int k = k0 + b * BD;
-        int64_t gi = -1;
-        off[b] = -1;
-        if (k < total) box_elem(k, gh0, gw0, gi, off[b]);
-        v[b] = gi >= 0 ? src(gi) : T(0);
+        for (int rr = 0; rr < 2; ++rr) {
+          const int sr = sr0 + rr * nw;
+          const int gh = gh0 + sr;
+          const bool rowok = sr < SH && gh >= 0 && gh < H;
+          const int64_t rowbase = ((int64_t)gh * W + gw0) * C;
+#pragma unroll
+          for (int j = 0; j < kJ; ++j) {
+            const int e = e0 + lane + 32 * j;
+            const int px = (int)(((unsigned long long)(unsigned)e * mC) >> 20);
+            const int c = e - px * C;
+            const int gw = gw0 + px;
+            const bool ok = rowok && e < rowE && (unsigned)gw < (unsigned)W;
+            off[rr][j] = (sr < SH && e < rowE) ? c * planeSz + sr * SWP + sk(px) : -1;
+            v[rr][j] = ok ? src(rowbase + e) : T(0);
+          }
+        }
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr)
+#pragma unroll
+          for (int j = 0; j < kJ; ++j)
+            if (off[rr][j] >= 0) dst[off[rr][j]] = v[rr][j];
       }
-#pragma unroll
-      for (int b = 0; b < kB2; ++b)
-        if (off[b] >= 0) dst[off[b]] = v[b];
     }
   }
   // plain copies: asynchronous global -> shared (LDGSTS), zero fill outside;
@@ -217,7 +255,6 @@ struct Conv {
     }
     cp_async_wait_all();
   }
-  __device__ __forceinline__ void load_full(int h0, int w0, const SrcLin<T>& src) const { load_copy(h0, w0, src.x); }
 
   // ---- register-blocked correlation: RW consecutive outputs (row ty, cols
   // tx*RW..) of the thread's channel plane with stencil w (kh x kw).  Per
@@ -226,32 +263,34 @@ struct Conv {
 #pragma unroll
     for (int o = 0; o < RW; ++o) acc[o] = T(0);
     const int kh = a.g.kh, kw = a.g.kw, SWP = a.g.SWP;
-    const T* base = pl + (ty + 1) * SWP + tx * (RW + 1);
+    // phys(tx*RW + m) = sk(tx*RW) + skr(m); separable because tx*RW and the
+    // j-block starts are multiples of RW
+    const T* base = pl + (ty + 1) * SWP + sk(tx * RW);
     for (int i = 0; i < kh; ++i) {
       const T* row = base + i * SWP;
       const T* wr = w + i * kw;
       T win[RW];
 #pragma unroll
-      for (int q = 0; q < RW - 1; ++q) win[q] = row[(1 + q) + ((1 + q) >> kShift)];
+      for (int q = 0; q < RW - 1; ++q) win[q] = row[skr(1 + q)];
       int j = 0;
       for (; j + RW <= kw; j += RW) {
-        const T* rj = row + j + (j >> kShift);
+        const T* rj = row + skr(j);
 #pragma unroll
         for (int jj = 0; jj < RW; ++jj) {
           const int q = jj + RW - 1;
-          win[(jj + RW - 1) % RW] = rj[(1 + q) + ((1 + q) >> kShift)];
+          win[(jj + RW - 1) % RW] = rj[skr(1 + q)];
           const T wt = wr[j + jj];
 #pragma unroll
           for (int o = 0; o < RW; ++o) acc[o] = madd<FAST>(acc[o], win[(o + jj) % RW], wt);
         }
       }
       if (j < kw) {
-        const T* rj = row + j + (j >> kShift);
+        const T* rj = row + skr(j);
 #pragma unroll
         for (int jj = 0; jj < RW - 1; ++jj) {
           if (j + jj < kw) {
             const int q = jj + RW - 1;
-            win[(jj + RW - 1) % RW] = rj[(1 + q) + ((1 + q) >> kShift)];
+            win[(jj + RW - 1) % RW] = rj[skr(1 + q)];
             const T wt = wr[j + jj];
 #pragma unroll
             for (int o = 0; o < RW; ++o) acc[o] = madd<FAST>(acc[o], win[(o + jj) % RW], wt);
@@ -330,14 +369,14 @@ struct Conv {
       int h0, w0;
       tile_origin(tile, h0, w0);
       __syncthreads();
-      load_full(h0, w0, src);
       const int h = h0 + ty;
-      T ypre[RW];   // epilogue operands prefetched so their latency overlaps the stencil
+      T ypre[RW];   // epilogue operands: issued before the tile box so both share one round trip
 #pragma unroll
       for (int o = 0; o < RW; ++o) {
         const int w = w0 + tx * RW + o;
         ypre[o] = (h < H && w < W) ? ydat[gidx(h, w, ch)] : T(0);
       }
+      load_full(h0, w0, src);
       __syncthreads();
       T acc[RW];
       stencil_fwd(acc);
@@ -425,31 +464,48 @@ struct Conv {
                          const T* XPs = nullptr, T beta = T(0), T L = T(1), T* Xc = nullptr) {
     const T two = T(2), alpha = T(a.alpha);
     const int H = a.g.H, W = a.g.W;
+    long long sub_t[8];
     for (int tile = blockIdx.x; tile < a.g.nTiles; tile += gridDim.x) {
       int h0, w0;
       tile_origin(tile, h0, w0);
+      ADP_SUB(0);
+      if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+        // latency probe: 16 dependent loads from the just-written R array
+        const long long p0 = clock64();
+        double s = 0.0;
+        int idx = 0;
+        for (int k = 0; k < 16; ++k) {
+          s += *(volatile const T*)(Rin + idx);
+          idx = (int)(s * 0.0) + (k + 1) * 2048;
+        }
+        const long long p1 = clock64();
+        a.trace[1024 + 56] += (unsigned long long)(p1 - p0);
+        a.trace[1024 + 57] += (unsigned long long)(s != s);
+      }
       __syncthreads();
-      load_full(h0, w0, SrcLin<T>{Rin});
       const int h = h0 + ty;
-      T tpre[RW], ypre[RW];   // prefetched epilogue operands
+      T tpre[RW], xpre[RW], xppre[RW];   // epilogue operands, in flight with the tile box
 #pragma unroll
       for (int o = 0; o < RW; ++o) {
         const int w = w0 + tx * RW + o;
-        tpre[o] = T(0);
-        ypre[o] = T(0);
+        tpre[o] = xpre[o] = xppre[o] = T(0);
         if (h < H && w < W) {
           const int64_t i = gidx(h, w, ch);
           if (tv) tpre[o] = ldcg(TVGin + i);
           if (Xc) {
-            const T xv = ldcg(Xs + i), xpv = ldcg(XPs + i);
-            ypre[o] = xv + beta * (xv - xpv);
+            xpre[o] = ldcg(Xs + i);
+            xppre[o] = ldcg(XPs + i);
           }
         }
       }
+      load_full(h0, w0, SrcLin<T>{Rin});
+      ADP_SUB(1);
       __syncthreads();
+      ADP_SUB(2);
       double part = 0.0;
       T acc[RW];
       stencil_adj(acc);
+      ADP_SUB(3);
 #pragma unroll
       for (int o = 0; o < RW; ++o) {
         const int w = w0 + tx * RW + o;
@@ -459,10 +515,13 @@ struct Conv {
           if (tv) gv = gv + alpha * tpre[o];
           Gout[i] = gv;
           part += (double)gv * (double)gv;
-          if (Xc) Xc[i] = ypre[o] - gv / L;
+          if (Xc) Xc[i] = (xpre[o] + beta * (xpre[o] - xppre[o])) - gv / L;
         }
       }
+      ADP_SUB(4);
       if (sgg) store_tile_partial(*sgg, tile, part, red());
+      ADP_SUB(5);
+      ADP_SUB_FLUSH(6);
     }
   }
 
@@ -481,9 +540,8 @@ struct Conv {
       int h0, w0;
       tile_origin(tile, h0, w0);
       __syncthreads();
-      load_full(h0, w0, src);
       const int h = h0 + ty;
-      T ypre[RW], gpre[RW], xopre[RW];   // prefetched epilogue operands
+      T ypre[RW], gpre[RW], xopre[RW];   // epilogue operands, in flight with the tile box
 #pragma unroll
       for (int o = 0; o < RW; ++o) {
         const int w = w0 + tx * RW + o;
@@ -497,6 +555,7 @@ struct Conv {
           }
         }
       }
+      load_full(h0, w0, src);
       __syncthreads();
       double part = 0.0;
       T acc[RW];

@@ -1,0 +1,15 @@
+// Instantiation: double, strict (reference order, no FMA) stencils, RW = 1
+// (small single-channel problems: more warps per SM).
+#include "conv2d_kernels.cuh"
+
+namespace adp {
+ConvKernelSet conv_kernels_f64s_rw1() {
+  ConvKernelSet k;
+  k.solve = (const void*)conv_solve_kernel<double, false, 1>;
+  k.cg = (const void*)conv_cg_kernel<double, false, 1>;
+  k.misc = (const void*)conv_misc_kernel<double, false, 1>;
+  k.kgc_part = (const void*)kgc_partial_kernel<double>;
+  k.kgc_final = (const void*)kgc_final_kernel<double>;
+  return k;
+}
+}  // namespace adp

@@ -88,11 +88,6 @@ struct ConvOps : Conv<T, FAST, RW> {
   }
 };
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 #define ADP_TRACE(it, k)                                                               \
   do {                                                                                 \
     if (a.trace && blockIdx.x == 0 && threadIdx.x == 0 && (it) < 64) a.trace[(it) * 16 + (k)] = gtimer(); \

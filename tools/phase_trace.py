@@ -26,9 +26,11 @@ plan = p.op.plan()
 nat.check(nat.lib().adp_debug_trace(plan.handle, 1, None))
 p = up.lower_problem(up.b0)
 adp.solve_lower(p, x0, 1e-14, 10.0, max_iters=64, method="agd", adaptive=True)
-buf = np.zeros(64 * 16, dtype=np.uint64)
+buf = np.zeros(64 * 16 + 64, dtype=np.uint64)
 nat.check(nat.lib().adp_debug_trace(plan.handle, 0, buf.ctypes.data))
-tr = buf.reshape(64, 16).astype(np.int64)
+cnt = max(int(buf[1024 + 63]), 1)
+subs = [buf[1024 + 8 * w:1024 + 8 * w + 5].astype(np.float64) / cnt for w in range(4)]
+tr = buf[:1024].reshape(64, 16).astype(np.int64)
 names = ["A", "bar1", "B", "bar2", "C", "bar3", "reduce"]
 d = np.diff(tr[:, :8], axis=1)[4:60]
 print("phase means (us):", {n: round(float(v) / 1e3, 2) for n, v in zip(names, d.mean(axis=0))})
@@ -37,3 +39,6 @@ print(f"iteration mean {it.mean():.2f} us, median {np.median(it):.2f}")
 rt = tr[:, 8:]
 extra = [(rt[i][rt[i] > 0].max() - tr[i, 7]) / 1e3 for i in range(4, 60) if (rt[i] > 0).any()]
 print(f"retries: {len(extra)} iterations, mean extra {np.mean(extra) if extra else 0:.2f} us")
+for w, sub in enumerate(subs):
+    print(f"stage B warp {w}, mean SM cycles over {cnt} calls:", {n: round(float(v)) for n, v in zip(["sync+issue+box", "->", "sync", "stencil", "epilogue"], sub)})
+print(f"dependent-load probe: {float(buf[1024 + 56]) / cnt / 16:.0f} SM cycles per load (16-chain, {cnt} calls)")
