@@ -177,7 +177,7 @@ int adp_vec(int32_t op, int64_t n, int32_t dtype, double a, const void* x, const
 int adp_fp64_peak(double* tflops, double* ms, void* stream);
 
 /* ---- debug: per-phase %globaltimer stamps of conv solves (enable=1 arms; enable=0 copies
- * 64 iterations x 16 slots of uint64 nanoseconds to host_out and disarms) ---- */
+ * 64 x 16 uint64 nanosecond stamps + 128 sub-phase cycle counters to host_out and disarms) ---- */
 int adp_debug_trace(adp_plan* p, int32_t enable, uint64_t* host_out);
 
 /* ---- host-only introspection (no device): the deterministic-sum layout for n

@@ -207,6 +207,11 @@ __device__ __forceinline__ void cp_async8(double* dst_smem, const double* src, b
   const unsigned d = (unsigned)__cvta_generic_to_shared(dst_smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(valid ? 8 : 0) : "memory");
 }
+// 16-byte variant: `bytes` (0, 8 or 16) valid source bytes, the rest zero-filled
+__device__ __forceinline__ void cp_async16(double* dst_smem, const double* src, int bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst_smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
@@ -216,15 +221,17 @@ __device__ __forceinline__ void cp_async_wait_all() {
 __device__ __forceinline__ double fold8(const double* c) {
   return ((c[0] + c[1]) + (c[2] + c[3])) + ((c[4] + c[5]) + (c[6] + c[7]));
 }
-__device__ __forceinline__ double fold_pow2(const double* c, int chunk) {
+__device__ __forceinline__ double fold_small(const double* c, int chunk) {   // chunk <= 16
   switch (chunk) {
     case 1: return c[0];
     case 2: return c[0] + c[1];
     case 4: return (c[0] + c[1]) + (c[2] + c[3]);
     case 8: return fold8(c);
-    case 16: return fold8(c) + fold8(c + 8);
-    default: break;
+    default: return fold8(c) + fold8(c + 8);
   }
+}
+__device__ __forceinline__ double fold_pow2(const double* c, int chunk) {
+  if (chunk <= 16) return fold_small(c, chunk);
   double st[12];
   double root = 0.0;
   for (int b = 0; b < chunk / 16; ++b) {
@@ -277,22 +284,25 @@ __device__ __forceinline__ double tree_reduce_cta(const double* __restrict__ val
   return r;
 }
 
-// Evaluate a single-level sum (nSub == 1) redundantly in this CTA.
-__device__ __forceinline__ double sum_single(const SumDev& s, double* sv) {
+// Evaluate a single-level sum (nSub == 1) redundantly in this CTA.  The
+// slow paths below (program trees, two-level sums, oversized batches) are
+// kept out of line: one copy of their code per kernel instead of one per
+// call site keeps the hot loop's instruction footprint small.
+static __device__ __noinline__ double sum_single(const SumDev& s, double* sv) {
   if (s.nLeaves == 0) return 0.0;
-  if (s.regular) return tree_reduce_cta(s.leaf_vals, s.nLeaves, sv, sv + 4096);
+  if (s.regular) return tree_reduce_cta(s.leaf_vals, s.nLeaves, sv, sv + kTreeStage);
   for (int k = threadIdx.x; k < s.nLeaves; k += blockDim.x) sv[k] = ldcg(s.leaf_vals + k);
   __syncthreads();
   return eval_prog(s.progs + s.top_prog, sv);
 }
 
 // Two-level sums: phase 1 (subtrees, distributed), grid barrier, phase 2 (top).
-__device__ __forceinline__ void sum_phase1(const SumDev& s, double* sv) {
+static __device__ __noinline__ void sum_phase1(const SumDev& s, double* sv) {
   if (s.nSub <= 1) return;
   if (s.regular) {
     for (int t = blockIdx.x; t < s.nSub; t += gridDim.x) {
       const int a = t * s.sub_size;
-      const double r = tree_reduce_cta(s.leaf_vals + a, min(s.sub_size, s.nLeaves - a), sv, sv + 4096);
+      const double r = tree_reduce_cta(s.leaf_vals + a, min(s.sub_size, s.nLeaves - a), sv, sv + kTreeStage);
       if (threadIdx.x == 0) s.sub_vals[t] = r;
     }
     return;
@@ -306,84 +316,211 @@ __device__ __forceinline__ void sum_phase1(const SumDev& s, double* sv) {
   }
 }
 
-__device__ __forceinline__ double sum_phase2(const SumDev& s, double* sv) {
+static __device__ __noinline__ double sum_phase2(const SumDev& s, double* sv) {
   if (s.nSub <= 1) return sum_single(s, sv);
-  if (s.regular) return tree_reduce_cta(s.sub_vals, s.nSub, sv, sv + 4096);
+  if (s.regular) return tree_reduce_cta(s.sub_vals, s.nSub, sv, sv + kTreeStage);
   for (int k = threadIdx.x; k < s.nSub; k += blockDim.x) sv[k] = ldcg(s.sub_vals + k);
   __syncthreads();
   return eval_prog(s.progs + s.top_prog, sv);
 }
 
+static __device__ __noinline__ double fold_pow2_big(const double* c, int chunk) { return fold_pow2(c, chunk); }
 
 // Reduce k (<= 8) sums: phase 1 (distributed subtrees) for two-level sums and
 // one grid barrier if there are any; then every regular sum (its leaves, or
 // its subtree roots) is folded in ONE batched CTA pass — all loads in
-// flight together, one shuffle/smem exchange for all sums; irregular
-// (program) sums fall back to the level-by-level evaluator.  out[i] valid in
-// every thread of every CTA.
-__device__ __forceinline__ void reduce_list(const SumDev* const* ss, int k, double* out, double* sv,
-                                            GridBarrier& gb) {
-  bool two = false;
+// flight together (16-byte async copies), per-thread perfect-tree chunks,
+// xor-shuffles across lanes, then every warp folds the warp partials itself
+// (no broadcast round).  Irregular (program) sums fall back to the
+// level-by-level evaluator.  out[i] valid in every thread of every CTA.
+// Out of line and loop-based on purpose: it is called from every decision
+// point of the persistent kernels, and a straight-line copy per call site
+// (~5k instructions each) made instruction fetch its dominant cost.
+static __device__ __noinline__ void reduce_list(const SumDev* const* ss, int k, double* out, double* sv,
+                                         GridBarrier& gb, unsigned long long* tr) {
+  const bool stamp = tr && blockIdx.x == 0 && threadIdx.x == 0;
+  long long c0 = stamp ? clock64() : 0;
+  auto lap = [&](int slot) {
+    if (stamp) {
+      const long long c = clock64();
+      tr[slot] += (unsigned long long)(c - c0);
+      c0 = c;
+    }
+  };
+  bool two = false, irregular = false;
+  int total = 0;
+#pragma unroll 1
   for (int i = 0; i < k; ++i) {
-    if (ss[i]->nSub > 1) {
+    const SumDev& s = *ss[i];
+    if (s.nSub > 1) {
       two = true;
-      sum_phase1(*ss[i], sv);
+      sum_phase1(s, sv);
+    }
+    if (s.regular) {
+      const int n = s.nSub > 1 ? s.nSub : s.nLeaves;
+      const int P = n <= 1 ? 1 : 1 << (32 - __clz(n - 1));
+      total += (P + 1) & ~1;   // keep every base 16-byte aligned
+    } else {
+      irregular = true;
     }
   }
   if (two) gb.sync();
-  const int BD = blockDim.x;
-  const int T = 1 << (31 - __clz(BD));          // folding threads (power of two)
-  int P[8], base[8], n[8];
-  int total = 0;
-  for (int i = 0; i < k; ++i) {
-    const SumDev& s = *ss[i];
-    n[i] = s.regular ? (s.nSub > 1 ? s.nSub : s.nLeaves) : 0;
-    int p = 1;
-    while (p < n[i]) p <<= 1;
-    P[i] = s.regular ? p : 0;
-    base[i] = total;
-    total += P[i];
-  }
+  lap(0);
   if (total > kTreeStage) {
+#pragma unroll 1
     for (int i = 0; i < k; ++i) out[i] = sum_phase2(*ss[i], sv);
     return;
   }
+  const int BD = blockDim.x;
+  const int T = 1 << (31 - __clz(BD));          // folding threads (power of two)
   // stage all regular sums with asynchronous copies: every element of every
   // sum is in flight at once (zero-filled past n), one wait for all
+  int base = 0;
+#pragma unroll 1
   for (int i = 0; i < k; ++i) {
-    if (!P[i]) continue;
     const SumDev& s = *ss[i];
+    if (!s.regular) continue;
+    const int n = s.nSub > 1 ? s.nSub : s.nLeaves;
+    const int P = n <= 1 ? 1 : 1 << (32 - __clz(n - 1));
     const double* src = s.nSub > 1 ? s.sub_vals : s.leaf_vals;
-    for (int e = threadIdx.x; e < P[i]; e += BD) cp_async8(sv + base[i] + e, src + (e < n[i] ? e : 0), e < n[i]);
+    if (P == 1) {
+      if (threadIdx.x == 0) cp_async8(sv + base, src, n > 0);
+    } else {
+      // pairs: base and P are even, sources 256-byte aligned
+#pragma unroll 1
+      for (int e = 2 * threadIdx.x; e < P; e += 2 * BD)
+        cp_async16(sv + base + e, src + (e < n ? e : 0), min(max(n - e, 0), 2) * 8);
+    }
+    base += (P + 1) & ~1;
   }
+  lap(1);
   cp_async_wait_all();
   __syncthreads();
-  double* red = sv + kTreeStage;   // 8 x 32 warp partials + 8 results
+  lap(2);
+  double* red = sv + kTreeStage;   // 8 x 32 warp partials
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = BD >> 5;
+  base = 0;
+#pragma unroll 1
   for (int i = 0; i < k; ++i) {
-    if (!P[i]) continue;
-    const int chunk = P[i] > T ? P[i] / T : 1;
+    const SumDev& s = *ss[i];
+    if (!s.regular) continue;
+    const int n = s.nSub > 1 ? s.nSub : s.nLeaves;
+    const int P = n <= 1 ? 1 : 1 << (32 - __clz(n - 1));
+    const int chunk = P > T ? P / T : 1;
+    const double* c = sv + base + threadIdx.x * chunk;
     double root = 0.0;
-    if (threadIdx.x * chunk < P[i]) root = fold_pow2(sv + base[i] + threadIdx.x * chunk, chunk);
+    if (threadIdx.x * chunk < P) root = chunk <= 16 ? fold_small(c, chunk) : fold_pow2_big(c, chunk);
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) root = root + __shfl_xor_sync(kFull, root, o);
     if (lane == 0) red[i * 32 + warp] = root;
+    base += (P + 1) & ~1;
   }
   __syncthreads();
-  if (warp == 0) {
-    for (int i = 0; i < k; ++i) {
-      if (!P[i]) continue;
-      double t = lane < nw ? red[i * 32 + lane] : 0.0;
+  lap(3);
+  // every warp folds the warp partials (identical order in all warps)
+#pragma unroll 1
+  for (int i = 0; i < k; ++i) {
+    if (!ss[i]->regular) continue;
+    double t = lane < nw ? red[i * 32 + lane] : 0.0;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) t = t + __shfl_xor_sync(kFull, t, o);
-      if (lane == 0) red[256 + i] = t;
+    for (int o = 1; o < 32; o <<= 1) t = t + __shfl_xor_sync(kFull, t, o);
+    out[i] = t;
+  }
+  __syncthreads();   // red / staging are reused by the caller's next shared-memory phase
+  if (irregular) {
+#pragma unroll 1
+    for (int i = 0; i < k; ++i)
+      if (!ss[i]->regular) out[i] = sum_phase2(*ss[i], sv);
+  }
+  lap(4);
+  if (stamp) tr[7] += 1;
+}
+
+// Hot-path form of reduce_list for K sums known at the call site: when every
+// sum is a regular single-level tree and the batch fits the staging area,
+// all descriptor reads, copies, folds and shuffles of the K sums are
+// independent (unrolled) so their latencies overlap; otherwise the generic
+// out-of-line routine runs.  Same tree order, same results.
+template <int K>
+__device__ __forceinline__ void reduce_k(const SumDev* const (&ss)[K], double* out, double* sv, GridBarrier& gb,
+                                         unsigned long long* tr) {
+  const bool stamp = tr && blockIdx.x == 0 && threadIdx.x == 0;
+  long long c0 = stamp ? clock64() : 0;
+  auto lap = [&](int slot) {
+    if (stamp) {
+      const long long c = clock64();
+      tr[slot] += (unsigned long long)(c - c0);
+      c0 = c;
     }
+  };
+  int n[K], P[K];
+  const double* src[K];
+  bool fast = true;
+  int total = 0;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    const SumDev& s = *ss[i];
+    fast = fast && s.regular && s.nSub <= 1;
+    n[i] = s.nLeaves;
+    P[i] = n[i] <= 1 ? 1 : 1 << (32 - __clz(n[i] - 1));
+    src[i] = s.leaf_vals;
+    total += (P[i] + 1) & ~1;
+  }
+  if (!fast || total > kTreeStage) {
+    reduce_list(ss, K, out, sv, gb, tr);
+    return;
+  }
+  const int BD = blockDim.x;
+  const int T = 1 << (31 - __clz(BD));
+  int base = 0;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    if (P[i] == 1) {
+      if (threadIdx.x == 0) cp_async8(sv + base, src[i], n[i] > 0);
+    } else {
+      for (int e = 2 * threadIdx.x; e < P[i]; e += 2 * BD)
+        cp_async16(sv + base + e, src[i] + (e < n[i] ? e : 0), min(max(n[i] - e, 0), 2) * 8);
+    }
+    base += (P[i] + 1) & ~1;
+  }
+  lap(1);
+  cp_async_wait_all();
+  __syncthreads();
+  lap(2);
+  double root[K];
+  base = 0;
+#pragma unroll
+  for (int i = 0; i < K; ++i) {
+    const int chunk = P[i] > T ? P[i] / T : 1;
+    root[i] = 0.0;
+    if (threadIdx.x * chunk < P[i])
+      root[i] = chunk <= 16 ? fold_small(sv + base + threadIdx.x * chunk, chunk)
+                            : fold_pow2_big(sv + base + threadIdx.x * chunk, chunk);
+    base += (P[i] + 1) & ~1;
+  }
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+    for (int i = 0; i < K; ++i) root[i] = root[i] + __shfl_xor_sync(kFull, root[i], o);
+  double* red = sv + kTreeStage;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = BD >> 5;
+  if (lane == 0) {
+#pragma unroll
+    for (int i = 0; i < K; ++i) red[i * 32 + warp] = root[i];
   }
   __syncthreads();
-  for (int i = 0; i < k; ++i) out[i] = P[i] ? red[256 + i] : 0.0;
+  lap(3);
+#pragma unroll
+  for (int i = 0; i < K; ++i) root[i] = lane < nw ? red[i * 32 + lane] : 0.0;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+    for (int i = 0; i < K; ++i) root[i] = root[i] + __shfl_xor_sync(kFull, root[i], o);
+#pragma unroll
+  for (int i = 0; i < K; ++i) out[i] = root[i];
   __syncthreads();
-  for (int i = 0; i < k; ++i)
-    if (!ss[i]->regular) out[i] = sum_phase2(*ss[i], sv);
+  lap(4);
+  if (stamp) tr[7] += 1;
 }
 
 // Tile partial (ddot-type): per-thread accumulation in a fixed order then

@@ -908,11 +908,11 @@ extern "C" int adp_sum_layout(int64_t n, int32_t np_rule, int64_t* n_leaves, int
 
 // Debug: enable (enable = 1) per-phase %globaltimer stamps of the next solves
 // (first 64 iterations, 16 slots each); enable = 0 copies them to host_out
-// (64 * 16 uint64) and disables.
+// (64 * 16 + 128 uint64: phases, stage-B and reduce sub-phase cycles) and disables.
 extern "C" int adp_debug_trace(adp_plan* p, int32_t enable, uint64_t* host_out) {
   if (!p) return fail(ADP_ERR_ARG, "null plan");
   PlanImpl& P = p->impl;
-  const size_t bytes = (64 * 16 + 64) * sizeof(unsigned long long);   // + sub-phase stamps
+  const size_t bytes = (64 * 16 + 128) * sizeof(unsigned long long);   // + sub-phase stamps
   if (enable) {
     if (!P.d_trace) CK(cudaMalloc(&P.d_trace, bytes));
     CK(cudaMemset(P.d_trace, 0, bytes));

@@ -35,7 +35,8 @@ struct SumDev {
 };
 
 constexpr int kMaxProgLeaves = 2048;   // smem tree evaluation capacity (nL + nI <= 4095)
-constexpr int kTreeStage = 4096;       // doubles of CTA tree staging; then 512 doubles of scratch
+constexpr int kTreeStage = 16384;      // doubles of CTA tree staging (one batched pass over all
+                                       // the sums of a decision point); then 512 doubles of scratch
 
 // regularizer kinds (regularizers.py:75-199)
 enum RegKind : int { REG_TV = 0, REG_ELASTIC = 1 };

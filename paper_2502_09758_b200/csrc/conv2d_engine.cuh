@@ -469,19 +469,6 @@ struct Conv {
       int h0, w0;
       tile_origin(tile, h0, w0);
       ADP_SUB(0);
-      if (a.trace && blockIdx.x == 0 && threadIdx.x == 0) {
-        // latency probe: 16 dependent loads from the just-written R array
-        const long long p0 = clock64();
-        double s = 0.0;
-        int idx = 0;
-        for (int k = 0; k < 16; ++k) {
-          s += *(volatile const T*)(Rin + idx);
-          idx = (int)(s * 0.0) + (k + 1) * 2048;
-        }
-        const long long p1 = clock64();
-        a.trace[1024 + 56] += (unsigned long long)(p1 - p0);
-        a.trace[1024 + 57] += (unsigned long long)(s != s);
-      }
       __syncthreads();
       const int h = h0 + ty;
       T tpre[RW], xpre[RW], xppre[RW];   // epilogue operands, in flight with the tile box

@@ -1,6 +1,5 @@
 // Cooperative persistent kernels of the depthwise 2-D engine.
 #pragma once
-#include <initializer_list>
 #include "conv2d_engine.cuh"
 
 namespace adp {
@@ -10,18 +9,30 @@ struct ConvOps : Conv<T, FAST, RW> {
   using Base = Conv<T, FAST, RW>;
   using Base::a;
   GridBarrier gb;
+  SumDev* ssm;   // shared-memory copies of a.s_fit .. a.s_t2 (read at every decision point)
 
   __device__ explicit ConvOps(const ConvArgs<T>& a_) : Base(a_) {
     gb.counter = a_.bar;
     gb.nblocks = gridDim.x;
     gb.target = 0;
+    __shared__ SumDev sh_sums[kNumSums];
+    static_assert(offsetof(ConvArgs<T>, s_t2) - offsetof(ConvArgs<T>, s_fit) == (kNumSums - 1) * sizeof(SumDev),
+                  "sum descriptors must be contiguous");
+    if (threadIdx.x < kNumSums) sh_sums[threadIdx.x] = (&a_.s_fit)[threadIdx.x];
+    ssm = sh_sums;
+    __syncthreads();
   }
+  static constexpr int kNumSums = 7;
 
-  __device__ void reduce(std::initializer_list<const SumDev*> l, double* out) {
-    const SumDev* ss[8];
-    int k = 0;
-    for (const SumDev* p : l) ss[k++] = p;
-    reduce_list(ss, k, out, this->sv(), gb);
+  template <int K>
+  __device__ void reduce(const SumDev* const (&l)[K], double* out) {
+    const SumDev* ss[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const ptrdiff_t j = l[i] - &a.s_fit;
+      ss[i] = (j >= 0 && j < kNumSums) ? ssm + j : l[i];
+    }
+    reduce_k<K>(ss, out, this->sv(), gb, a.trace ? a.trace + 1088 : nullptr);
   }
   __device__ double reduce1(const SumDev& s) {
     double o;

@@ -26,7 +26,7 @@ plan = p.op.plan()
 nat.check(nat.lib().adp_debug_trace(plan.handle, 1, None))
 p = up.lower_problem(up.b0)
 adp.solve_lower(p, x0, 1e-14, 10.0, max_iters=64, method="agd", adaptive=True)
-buf = np.zeros(64 * 16 + 64, dtype=np.uint64)
+buf = np.zeros(64 * 16 + 128, dtype=np.uint64)
 nat.check(nat.lib().adp_debug_trace(plan.handle, 0, buf.ctypes.data))
 cnt = max(int(buf[1024 + 63]), 1)
 subs = [buf[1024 + 8 * w:1024 + 8 * w + 5].astype(np.float64) / cnt for w in range(4)]
@@ -41,4 +41,6 @@ extra = [(rt[i][rt[i] > 0].max() - tr[i, 7]) / 1e3 for i in range(4, 60) if (rt[
 print(f"retries: {len(extra)} iterations, mean extra {np.mean(extra) if extra else 0:.2f} us")
 for w, sub in enumerate(subs):
     print(f"stage B warp {w}, mean SM cycles over {cnt} calls:", {n: round(float(v)) for n, v in zip(["sync+issue+box", "->", "sync", "stencil", "epilogue"], sub)})
-print(f"dependent-load probe: {float(buf[1024 + 56]) / cnt / 16:.0f} SM cycles per load (16-chain, {cnt} calls)")
+rc = max(int(buf[1088 + 7]), 1)
+print(f"reduce sub-phases, CTA 0 mean SM cycles over {rc} calls:",
+      {n: round(float(buf[1088 + k]) / rc) for k, n in enumerate(["phase1+bar", "issue", "wait+sync", "fold", "final"])})
