@@ -68,6 +68,14 @@ typedef struct {
   int32_t kh, kw;  /* stencil size (odd); dense1d: kh = kw = n */
   int32_t tile_h, tile_w; /* 0 = auto */
   int32_t rw;             /* register blocking: outputs per thread (1, 2, 4); 0 = auto */
+  /* row slab of a larger image (multi-GPU c5); Hg = 0: not a slab.
+   * The plan covers local rows [0, H) = global rows [row0, row0 + H) (owned rows
+   * plus ghost rows); only local rows [own0, own1) enter its sums, which keep the
+   * GLOBAL image's trees (leaf and tile indices are global).  Tile geometry is
+   * chosen from the global shape, so it equals the unsplit plan's; row0, own0 and
+   * own1 must be multiples of the tile height (own1 may also be H at the global
+   * bottom) and owned ranges of two-level sums must be subtree-aligned. */
+  int32_t row0, Hg, own0, own1;
 } adp_plan_desc;
 
 /* Lower problem h(x, b) = ||B_b x - y||^2 + alpha J(x) (lower_solvers.py:20-25) */
@@ -177,8 +185,34 @@ int adp_vec(int32_t op, int64_t n, int32_t dtype, double a, const void* x, const
 int adp_fp64_peak(double* tflops, double* ms, void* stream);
 
 /* ---- debug: per-phase %globaltimer stamps of conv solves (enable=1 arms; enable=0 copies
- * 64 x 16 uint64 nanosecond stamps + 128 sub-phase cycle counters to host_out and disarms) ---- */
+ * 64 x 16 uint64 nanosecond stamps + 256 sub-phase cycle counters to host_out and disarms) ---- */
 int adp_debug_trace(adp_plan* p, int32_t enable, uint64_t* host_out);
+
+/* ---- plan geometry: out[0..9] = TH, TW, tilesH, tilesW, fused, leafL, rw, grid, threads, smem bytes;
+ * adp_plan_probe computes the same for a descriptor without allocating (grid = 0) */
+int adp_plan_geometry(const adp_plan* p, int32_t* out);
+int adp_plan_probe(const adp_plan_desc* desc, int32_t* out);
+
+/* ---- row slabs (multi-GPU c5).  One lower-level AGD iteration is split at its reductions:
+ * op 0 (ABC): value+grad at y = x + beta (x - xp), first candidate out = y - g / L and its value,
+ *             restart dot g.(out - x)                               (lower_solvers.py:196-207)
+ * op 1 (C):   backtracking retry: out = y - g / L (g from the last op 0) and its value (:170-177)
+ * op 2 (POWER): out = B^T B (x / L) and ||out||^2                   (operators.py:150-165)
+ * op 3 (NORM0): ||x||^2                                              (operators.py:150)
+ * op 4 (GRAD):  g = lower_grad(x), ||g||^2, fit and tv terms         (lower_solvers.py:212)
+ * Each step leaves phase 1 of its sums in the plan; adp_slab_units exposes them. */
+int adp_slab_step(adp_plan* p, const adp_lower* lp, int32_t op, const void* x, const void* xp, void* out,
+                  double beta, double L, void* stream);
+/* Sum units of a slab plan for sum `which` (0 fit, 1 tv, 2 fitc, 3 tvc, 4 ||g||^2 / norm, 5 restart dot):
+ * the global tree has n_units units (leaf values, or subtree roots when the sum is two-level), of
+ * which this plan produces [own[0], own[1]) and [own[2], own[3]).  If dst (device, n_units doubles)
+ * is non-NULL those ranges are copied into it at their global offsets (stream-ordered).  Once every
+ * rank's ranges are in place (the other entries zero: an all-reduce SUM assembles them exactly),
+ * adp_fold_units gives the sum in the single-GPU tree order. */
+int adp_slab_units(adp_plan* p, int32_t which, int64_t* n_units, int64_t* own, double* dst, void* stream);
+/* k (<= 8) perfect-tree folds (zero-padded to a power of two, <= 16384 units each) of device unit
+ * vectors units[i] (n[i] doubles); results to HOST out[i]; synchronises the stream. */
+int adp_fold_units(int32_t k, const double* const* units, const int64_t* n, double* out, void* stream);
 
 /* ---- host-only introspection (no device): the deterministic-sum layout for n
  * elements (np_rule = 1: NumPy pairwise leaves of <= 128; 0: binary over n items):

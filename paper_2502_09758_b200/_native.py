@@ -31,7 +31,8 @@ STATUS_OK, STATUS_DIVERGED, STATUS_BT_FAIL, STATUS_NEGCURV = 0, 1, 2, 3
 
 class PlanDesc(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in
-                ("layout", "dtype", "mode", "H", "W", "C", "kh", "kw", "tile_h", "tile_w", "rw")]
+                ("layout", "dtype", "mode", "H", "W", "C", "kh", "kw", "tile_h", "tile_w", "rw",
+                 "row0", "Hg", "own0", "own1")]
 
 
 class Lower(ctypes.Structure):
@@ -92,6 +93,11 @@ SIGNATURES = {
     "adp_vec": (_I, [_I, ctypes.c_int64, _I, _D, _P, _P, _P, ctypes.POINTER(_D), _P]),
     "adp_debug_trace": (_I, [_P, _I, _P]),
     "adp_fp64_peak": (_I, [ctypes.POINTER(_D), ctypes.POINTER(_D), _P]),
+    "adp_plan_geometry": (_I, [_P, _P]),
+    "adp_plan_probe": (_I, [ctypes.POINTER(PlanDesc), _P]),
+    "adp_slab_step": (_I, [_P, ctypes.POINTER(Lower), _I, _P, _P, _P, _D, _D, _P]),
+    "adp_slab_units": (_I, [_P, _I, ctypes.POINTER(ctypes.c_int64), _P, _P, _P]),
+    "adp_fold_units": (_I, [_I, _P, _P, _P, _P]),
     "adp_sum_layout": (_I, [ctypes.c_int64, _I, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(_I),
                             ctypes.POINTER(_I), _P, ctypes.c_int64, _P, _P, ctypes.c_int64, _P, ctypes.c_int64,
                             ctypes.POINTER(ctypes.c_int64)]),
@@ -185,7 +191,7 @@ def torch_dtype():
 class Plan:
     """Owns one ``adp_plan`` (device workspace for one problem shape)."""
 
-    def __init__(self, layout, shape, ksize, dtype, mode, tile=(0, 0)):
+    def __init__(self, layout, shape, ksize, dtype, mode, tile=(0, 0), slab=None):
         d = PlanDesc()
         d.layout = layout
         d.dtype = DTYPE_F64 if dtype == "float64" else DTYPE_F32
@@ -197,6 +203,8 @@ class Plan:
             d.H, d.W, d.C = (int(s) for s in shape)
             d.kh, d.kw = int(ksize[0]), int(ksize[1])
         d.tile_h, d.tile_w = int(tile[0]), int(tile[1])
+        if slab is not None:        # (row0, Hg, own0, own1): a row slab of a larger image
+            d.row0, d.Hg, d.own0, d.own1 = (int(v) for v in slab)
         self.desc = d
         self.handle = ctypes.c_void_p()
         check(lib().adp_plan_create(ctypes.byref(self.handle), ctypes.byref(d)), "adp_plan_create")
@@ -213,6 +221,12 @@ class Plan:
     @property
     def workspace_bytes(self) -> int:
         return int(lib().adp_plan_workspace_bytes(self.handle))
+
+    def geometry(self) -> dict:
+        """Tile geometry chosen by the plan (depthwise 2-D)."""
+        out = (ctypes.c_int32 * 10)()
+        check(lib().adp_plan_geometry(self.handle, out), "adp_plan_geometry")
+        return dict(zip(GEOMETRY_KEYS, (int(v) for v in out)))
 
 
 _plans: dict = {}
@@ -233,6 +247,23 @@ def plan_for(layout, shape, ksize=(0, 0), slot=None) -> Plan:
         p = Plan(layout, shape, ksize, _settings["dtype"], _settings["mode"], tile)
         _plans[key] = p
     return p
+
+
+GEOMETRY_KEYS = ("TH", "TW", "tilesH", "tilesW", "fused", "leafL", "rw", "grid", "threads", "smem")
+
+
+def probe_geometry(shape, ksize, tile=(0, 0)) -> dict:
+    """Tile geometry a depthwise 2-D plan of this shape would use (no allocation)."""
+    d = PlanDesc()
+    d.layout = LAYOUT_DEPTHWISE2D
+    d.dtype = DTYPE_F64 if _settings["dtype"] == "float64" else DTYPE_F32
+    d.mode = MODE_STRICT if _settings["mode"] == "strict" else MODE_FAST
+    d.H, d.W, d.C = (int(s) for s in shape)
+    d.kh, d.kw = int(ksize[0]), int(ksize[1])
+    d.tile_h, d.tile_w = int(tile[0]), int(tile[1])
+    out = (ctypes.c_int32 * 10)()
+    check(lib().adp_plan_probe(ctypes.byref(d), out), "adp_plan_probe")
+    return dict(zip(GEOMETRY_KEYS, (int(v) for v in out)))
 
 
 def clear_plans():

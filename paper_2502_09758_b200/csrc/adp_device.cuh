@@ -297,17 +297,25 @@ static __device__ __noinline__ double sum_single(const SumDev& s, double* sv) {
 }
 
 // Two-level sums: phase 1 (subtrees, distributed), grid barrier, phase 2 (top).
-static __device__ __noinline__ void sum_phase1(const SumDev& s, double* sv) {
+// Subtree t of this sum goes to CTA (off + t) mod grid, so the subtrees of
+// the several sums reduced together spread over different CTAs.
+// Only subtrees [sub_own0, sub_own1) are evaluated (a row slab's own ones).
+static __device__ __noinline__ void sum_phase1(const SumDev& s, double* sv, int off) {
   if (s.nSub <= 1) return;
+  const int G = gridDim.x;
+  const int u0 = ((int)blockIdx.x - off % G + G) % G;
+  const int n0 = s.sub_own1 - s.sub_own0, n = n0 + (s.sub_own3 - s.sub_own2);
   if (s.regular) {
-    for (int t = blockIdx.x; t < s.nSub; t += gridDim.x) {
+    for (int u = u0; u < n; u += G) {
+      const int t = u < n0 ? s.sub_own0 + u : s.sub_own2 + (u - n0);
       const int a = t * s.sub_size;
       const double r = tree_reduce_cta(s.leaf_vals + a, min(s.sub_size, s.nLeaves - a), sv, sv + kTreeStage);
       if (threadIdx.x == 0) s.sub_vals[t] = r;
     }
     return;
   }
-  for (int t = blockIdx.x; t < s.nSub; t += gridDim.x) {
+  for (int u = u0; u < n; u += G) {
+    const int t = u < n0 ? s.sub_own0 + u : s.sub_own2 + (u - n0);
     const int l0 = s.sub_leaf[t], l1 = s.sub_leaf[t + 1];
     for (int k = threadIdx.x; k < l1 - l0; k += blockDim.x) sv[k] = ldcg(s.leaf_vals + l0 + k);
     __syncthreads();
@@ -348,13 +356,14 @@ static __device__ __noinline__ void reduce_list(const SumDev* const* ss, int k, 
     }
   };
   bool two = false, irregular = false;
-  int total = 0;
+  int total = 0, off = 0;
 #pragma unroll 1
   for (int i = 0; i < k; ++i) {
     const SumDev& s = *ss[i];
     if (s.nSub > 1) {
       two = true;
-      sum_phase1(s, sv);
+      sum_phase1(s, sv, off);
+      off += s.nSub;
     }
     if (s.regular) {
       const int n = s.nSub > 1 ? s.nSub : s.nLeaves;
@@ -455,20 +464,34 @@ __device__ __forceinline__ void reduce_k(const SumDev* const (&ss)[K], double* o
   };
   int n[K], P[K];
   const double* src[K];
-  bool fast = true;
+  bool fast = true, two = false;
   int total = 0;
 #pragma unroll
   for (int i = 0; i < K; ++i) {
     const SumDev& s = *ss[i];
-    fast = fast && s.regular && s.nSub <= 1;
-    n[i] = s.nLeaves;
+    fast = fast && s.regular;
+    two = two || s.nSub > 1;
+    n[i] = s.nSub > 1 ? s.nSub : s.nLeaves;
     P[i] = n[i] <= 1 ? 1 : 1 << (32 - __clz(n[i] - 1));
-    src[i] = s.leaf_vals;
+    src[i] = s.nSub > 1 ? s.sub_vals : s.leaf_vals;
     total += (P[i] + 1) & ~1;
   }
   if (!fast || total > kTreeStage) {
     reduce_list(ss, K, out, sv, gb, tr);
     return;
+  }
+  if (two) {
+    // phase 1: subtrees of the two-level sums, spread over the CTAs
+    int off = 0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      if (ss[i]->nSub > 1) {
+        sum_phase1(*ss[i], sv, off);
+        off += ss[i]->nSub;
+      }
+    }
+    gb.sync();
+    lap(0);
   }
   const int BD = blockDim.x;
   const int T = 1 << (31 - __clz(BD));

@@ -262,6 +262,9 @@ static void fill_sum(SumDev& sd, const SumHost& sh, const int* d_progs, const in
                      int* d_subprog, double* leaf_vals, double* sub_vals) {
   sd.nLeaves = sh.nLeaves;
   sd.nSub = sh.nSub;
+  sd.sub_own0 = 0;
+  sd.sub_own1 = sh.nSub;
+  sd.sub_own2 = sd.sub_own3 = 0;
   sd.regular = sh.regular;
   sd.sub_size = sh.sub_size;
   sd.leaf_len = sh.leaf_len;
@@ -296,19 +299,30 @@ static int conv_plan_init(PlanImpl& P) {
   ConvGeom& g = P.g;
   g.H = d.H; g.W = d.W; g.C = d.C; g.kh = d.kh; g.kw = d.kw;
   g.rh = d.kh / 2; g.rw = d.kw / 2;
+  // row slab: sums, tiles and heuristics follow the GLOBAL image
+  const bool slab = d.Hg > 0;
+  if (slab && (d.row0 < 0 || d.row0 + d.H > d.Hg || d.own0 < 0 || d.own0 >= d.own1 || d.own1 > d.H))
+    return fail(ADP_ERR_ARG, "bad row-slab geometry");
+  g.row0 = slab ? d.row0 : 0;
+  g.Hg = slab ? d.Hg : d.H;
+  g.own0 = slab ? d.own0 : 0;
+  g.own1 = slab ? d.own1 : d.H;
+  g.Ng = (int64_t)g.Hg * d.W * d.C;
+  adp_plan_desc dg = d;
+  dg.H = g.Hg;
   {
     ProgPool tmp;
     SumHost s;
-    build_sum(s, (int64_t)d.H * d.W * d.C, true, tmp);
+    build_sum(s, g.Ng, true, tmp);
     g.leafL = s.regular ? s.leaf_len : 0;
   }
-  choose_tiles(d, g.leafL, g.TH, g.TW, g.fused);
+  choose_tiles(dg, g.leafL, g.TH, g.TW, g.fused);
   // register blocking: small single-channel problems are latency-bound with
   // one warp per SM sub-partition at RW = 4; RW = 2 gives 2x the warps on the
   // same tile (c2 512x512x1: 41 us/iter vs 51 at RW = 4; RW = 1 measured 43,
   // the extra warps do not pay for the lost window reuse).  ADP_RW overrides.
   {
-    const int64_t px_per_sm = (int64_t)d.H * d.W / std::max(1, P.sm_count);
+    const int64_t px_per_sm = (int64_t)g.Hg * d.W / std::max(1, P.sm_count);
     int rwb = (d.C == 1 && px_per_sm < 8192) ? 2 : 4;
     if (d.rw == 1 || d.rw == 2 || d.rw == 4) rwb = d.rw;
     if (const char* ev = getenv("ADP_RW")) {
@@ -340,8 +354,16 @@ static int conv_plan_init(PlanImpl& P) {
   g.YSH = g.TH + 2;
   g.YSWP = (g.TW + 2) + (g.TW + 2) / kRWp + 1;
   g.N = (int64_t)g.H * g.W * g.C;
+  g.tileOff = (g.row0 / g.TH) * g.tilesW;
+  if (slab) {
+    if (!g.fused) return fail(ADP_ERR_UNSUPPORTED, "row slabs need the fused (tile-aligned pairwise) sum layout");
+    const bool bottom = g.row0 + g.H == g.Hg && g.own1 == g.H;
+    if (g.row0 % g.TH || g.own0 % g.TH || (g.own1 % g.TH && !bottom))
+      return fail(ADP_ERR_ARG, "row slab bounds must be multiples of the tile height");
+  }
   P.smem = conv_smem(g, P.esize);
   if (P.smem > smem_optin) return fail(ADP_ERR_UNSUPPORTED, "tile + halo exceeds shared memory; use a smaller tile");
+  if (P.probe_only) return ADP_OK;   // adp_plan_probe: geometry only, no device memory
 
   // workspace: 18 N-arrays + 2 arrays of 2N
   const int64_t N = g.N;
@@ -353,9 +375,10 @@ static int conv_plan_init(PlanImpl& P) {
   // sums
   ProgPool pool;
   SumHost sN, s2N, sT;
-  build_sum(sN, N, true, pool);
-  build_sum(s2N, 2 * N, true, pool);
-  build_sum(sT, g.nTiles, false, pool);
+  const int nTilesG = ((g.Hg + g.TH - 1) / g.TH) * g.tilesW;
+  build_sum(sN, g.Ng, true, pool);
+  build_sum(s2N, 2 * g.Ng, true, pool);
+  build_sum(sT, nTilesG, false, pool);
   // kgc partial groups
   P.kgc_groups = std::min(4 * P.sm_count, std::max(1, ((g.H + 15) / 16) * ((g.W + 15) / 16)));
   const size_t nk = (size_t)g.kh * g.kw * g.C;
@@ -418,6 +441,34 @@ static int conv_plan_init(PlanImpl& P) {
     fill_sum<double>(*sds[k], sh, P.d_progs, dl, P.d_sub[2 * which[k]], P.d_sub[2 * which[k] + 1],
                      (double*)(base + o_lv[k]), (double*)(base + o_sv[k]));
   }
+  // units each sum contributes: leaves, or subtree roots when two-level; a
+  // slab fills only the ranges of its owned rows / tiles
+  {
+    const int64_t rowL = g.fused ? (int64_t)g.W * g.C / g.leafL : 0;
+    const int64_t NL = g.fused ? g.Ng / g.leafL : 0;
+    const int64_t l0 = (g.row0 + g.own0) * rowL, l1 = (g.row0 + g.own1) * rowL;
+    const int64_t t0 = g.tileOff + (int64_t)(g.own0 / g.TH) * g.tilesW;
+    const int64_t t1 = g.tileOff + (int64_t)((g.own1 + g.TH - 1) / g.TH) * g.tilesW;
+    const int64_t rng[7][4] = {{l0, l1, 0, 0}, {l0, l1, l0 + NL, l1 + NL}, {l0, l1, 0, 0}, {l0, l1, l0 + NL, l1 + NL},
+                               {t0, t1, 0, 0}, {t0, t1, 0, 0}, {t0, t1, 0, 0}};
+    for (int k = 0; k < 7; ++k) {
+      SumDev& sd = *sds[k];
+      P.units_n[k] = sd.nSub > 1 ? sd.nSub : sd.nLeaves;
+      for (int j = 0; j < 4; ++j) P.units_own[k][j] = slab ? rng[k][j] : (j == 1 ? P.units_n[k] : 0);
+      if (slab && sd.nSub > 1) {
+        for (int j = 0; j < 4; ++j) {
+          const int64_t v = rng[k][j];
+          const bool end = (j & 1) && v == (int64_t)sd.nLeaves;
+          if (v % sd.sub_size && !end) return fail(ADP_ERR_UNSUPPORTED, "row slab is not aligned to the sum's subtrees");
+          P.units_own[k][j] = (v + sd.sub_size - 1) / sd.sub_size;
+        }
+        sd.sub_own0 = (int)P.units_own[k][0];
+        sd.sub_own1 = (int)P.units_own[k][1];
+        sd.sub_own2 = (int)P.units_own[k][2];
+        sd.sub_own3 = (int)P.units_own[k][3];
+      }
+    }
+  }
   P.d_bar = (unsigned int*)(base + o_bar);
   P.d_sres = (SolveOut*)(base + o_sres);
   P.d_cres = (CGOut*)(base + o_cres);
@@ -470,6 +521,8 @@ static void set_lower(ConvArgs<T>& a, const adp_lower* lp) {
 
 template <typename T>
 static int launch_coop(PlanImpl& P, KernelInfo& k, ConvArgs<T>& a, cudaStream_t st) {
+  if ((P.g.Hg != P.g.H || P.g.row0) && !(k.fn == P.k_misc.fn && a.mode >= CM_SLAB_ABC))
+    return fail(ADP_ERR_UNSUPPORTED, "row-slab plans run adp_slab_step only");
   a.g.grid = k.grid;
   CK(cudaMemsetAsync(P.d_bar, 0, sizeof(unsigned int), st));
   void* args[] = {&a};
@@ -499,8 +552,24 @@ static int conv_misc(PlanImpl& P, int mode, const adp_lower* lp, const void* ker
 }
 
 template <typename T>
+static int conv_slab_step(PlanImpl& P, const adp_lower* lp, int op, const void* x, const void* xp, void* out,
+                          double beta, double L, cudaStream_t st) {
+  static const int modes[5] = {CM_SLAB_ABC, CM_SLAB_C, CM_SLAB_POWER, CM_SLAB_NORM0, CM_SLAB_GRAD};
+  ConvArgs<T> a = conv_base<T>(P);
+  if (lp) set_lower(a, lp);
+  a.mode = modes[op];
+  a.in0 = (const T*)x;
+  a.in1 = (const T*)xp;
+  a.out0 = (T*)out;
+  a.sbeta = beta;
+  a.sL = L;
+  return launch_coop(P, P.k_misc, a, st);
+}
+
+template <typename T>
 static int conv_kgc(PlanImpl& P, const void* xa, const void* va, const void* xb, const void* vb, void* out,
                     double scale, cudaStream_t st) {
+  if (P.g.Hg != P.g.H || P.g.row0) return fail(ADP_ERR_UNSUPPORTED, "row-slab plans run adp_slab_step only");
   ConvKernelSet ks = conv_kernels(P.d.dtype, P.d.mode, P.g.rwb);
   KgcArgs<T> a;
   std::memset(&a, 0, sizeof(a));
@@ -906,13 +975,81 @@ extern "C" int adp_sum_layout(int64_t n, int32_t np_rule, int64_t* n_leaves, int
   return ADP_OK;
 }
 
+extern "C" int adp_plan_geometry(const adp_plan* p, int32_t* out) {
+  if (!p || !out) return fail(ADP_ERR_ARG, "null argument");
+  const PlanImpl& P = p->impl;
+  const ConvGeom& g = P.g;
+  if (P.d.layout != ADP_LAYOUT_DEPTHWISE2D) return fail(ADP_ERR_UNSUPPORTED, "geometry: depthwise2d plans only");
+  const int32_t v[10] = {g.TH, g.TW, g.tilesH, g.tilesW, g.fused, g.leafL, g.rwb, P.k_solve.grid, g.threads,
+                         (int32_t)P.smem};
+  for (int i = 0; i < 10; ++i) out[i] = v[i];
+  return ADP_OK;
+}
+
+extern "C" int adp_plan_probe(const adp_plan_desc* desc, int32_t* out) {
+  if (!desc || !out) return fail(ADP_ERR_ARG, "null argument");
+  if (desc->layout != ADP_LAYOUT_DEPTHWISE2D) return fail(ADP_ERR_UNSUPPORTED, "probe: depthwise2d plans only");
+  if (desc->H < 1 || desc->W < 1 || desc->C < 1 || desc->kh < 1 || desc->kw < 1 || desc->kh % 2 == 0 ||
+      desc->kw % 2 == 0)
+    return fail(ADP_ERR_ARG, "bad shape");
+  adp_plan tmp;
+  tmp.impl.d = *desc;
+  tmp.impl.esize = desc->dtype == ADP_DTYPE_F32 ? 4 : 8;
+  tmp.impl.probe_only = true;
+  if (int e = conv_plan_init(tmp.impl)) return e;
+  const ConvGeom& g = tmp.impl.g;
+  const int32_t v[10] = {g.TH, g.TW, g.tilesH, g.tilesW, g.fused, g.leafL, g.rwb, 0, g.threads, (int32_t)tmp.impl.smem};
+  for (int i = 0; i < 10; ++i) out[i] = v[i];
+  return ADP_OK;
+}
+
+extern "C" int adp_slab_step(adp_plan* p, const adp_lower* lp, int32_t op, const void* x, const void* xp, void* out,
+                  double beta, double L, void* stream) {
+  if (!p || !x) return fail(ADP_ERR_ARG, "null argument");
+  PlanImpl& P = p->impl;
+  if (P.d.layout != ADP_LAYOUT_DEPTHWISE2D) return fail(ADP_ERR_UNSUPPORTED, "slab steps: depthwise2d plans only");
+  if (op < 0 || op > 4) return fail(ADP_ERR_ARG, "slab step: unknown op");
+  const bool needs_lower = op != 3;
+  if (needs_lower && (!lp || !lp->kernel)) return fail(ADP_ERR_ARG, "slab step: lower problem / kernel missing");
+  if ((op == 0 || op == 1 || op == 4) && (!lp->y || lp->reg != ADP_REG_TV))
+    return fail(ADP_ERR_UNSUPPORTED, "slab steps: TV lower problems with data y");
+  if ((op == 0 || op == 1) && !xp) return fail(ADP_ERR_ARG, "slab step: x_prev missing");
+  if ((op <= 2) && !out) return fail(ADP_ERR_ARG, "slab step: output missing");
+  if (op == 2 && !(L != 0.0)) return fail(ADP_ERR_ARG, "slab power step: zero scale");
+  return DISPATCH_T(P, conv_slab_step)(P, needs_lower ? lp : nullptr, op, x, xp, out, beta, L,
+                                      (cudaStream_t)stream);
+}
+
+extern "C" int adp_slab_units(adp_plan* p, int32_t which, int64_t* n_units, int64_t* own, double* dst,
+                              void* stream) {
+  if (!p || !n_units || !own) return fail(ADP_ERR_ARG, "null argument");
+  PlanImpl& P = p->impl;
+  if (P.d.layout != ADP_LAYOUT_DEPTHWISE2D) return fail(ADP_ERR_UNSUPPORTED, "slab units: depthwise2d plans only");
+  if (which < 0 || which > 5) return fail(ADP_ERR_ARG, "slab units: unknown sum");
+  const SumDev* sds[6] = {&P.s_fit, &P.s_tv, &P.s_fitc, &P.s_tvc, &P.s_t0, &P.s_t1};
+  const SumDev& sd = *sds[which];
+  if (!sd.regular) return fail(ADP_ERR_UNSUPPORTED, "slab units: irregular (program) sum");
+  *n_units = P.units_n[which];
+  for (int j = 0; j < 4; ++j) own[j] = P.units_own[which][j];
+  if (dst) {
+    const double* src = sd.nSub > 1 ? sd.sub_vals : sd.leaf_vals;
+    for (int j = 0; j < 4; j += 2) {
+      const int64_t a = own[j], b = own[j + 1];
+      if (b > a)
+        CK(cudaMemcpyAsync(dst + a, src + a, (size_t)(b - a) * sizeof(double), cudaMemcpyDeviceToDevice,
+                           (cudaStream_t)stream));
+    }
+  }
+  return ADP_OK;
+}
+
 // Debug: enable (enable = 1) per-phase %globaltimer stamps of the next solves
 // (first 64 iterations, 16 slots each); enable = 0 copies them to host_out
-// (64 * 16 + 128 uint64: phases, stage-B and reduce sub-phase cycles) and disables.
+// (64 * 16 + 256 uint64: phases, reduce and per-warp stage-B sub-phase cycles) and disables.
 extern "C" int adp_debug_trace(adp_plan* p, int32_t enable, uint64_t* host_out) {
   if (!p) return fail(ADP_ERR_ARG, "null plan");
   PlanImpl& P = p->impl;
-  const size_t bytes = (64 * 16 + 128) * sizeof(unsigned long long);   // + sub-phase stamps
+  const size_t bytes = (64 * 16 + 256) * sizeof(unsigned long long);   // + sub-phase stamps
   if (enable) {
     if (!P.d_trace) CK(cudaMalloc(&P.d_trace, bytes));
     CK(cudaMemset(P.d_trace, 0, bytes));

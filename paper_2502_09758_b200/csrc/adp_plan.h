@@ -41,6 +41,7 @@ struct PlanImpl {
   int esize = 8;
   size_t smem = 0;
   size_t smem_optin = 0;        // device max dynamic smem per block (function attribute set to this)
+  bool probe_only = false;      // adp_plan_probe: stop after the geometry
   int sm_count = 0;
   // device memory
   void* dmem = nullptr;
@@ -53,6 +54,8 @@ struct PlanImpl {
   int64_t* d_leaf_2N = nullptr;
   int* d_sub[8] = {};           // sub_leaf / sub_prog per layout
   SumDev s_fit{}, s_tv{}, s_fitc{}, s_tvc{}, s_t0{}, s_t1{}, s_t2{};
+  int64_t units_n[7] = {};       // sum units (leaves, or subtree roots when two-level)
+  int64_t units_own[7][4] = {};  // unit ranges this plan fills (row slabs: its owned rows)
   unsigned int* d_bar = nullptr;
   SolveOut* d_sres = nullptr;
   CGOut* d_cres = nullptr;

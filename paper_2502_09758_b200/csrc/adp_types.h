@@ -26,6 +26,8 @@ struct SumDev {
                            //    in registers / shuffles, subtrees of sub_size leaves
   int sub_size;            // regular two-level: leaves per subtree (pow2)
   int leaf_len;            // regular element sums: common leaf length (elements)
+  int sub_own0, sub_own1;  // phase-1 subtrees evaluated by this plan ([0, nSub) unless a row slab)
+  int sub_own2, sub_own3;  // second owned range (the 2N TV sums of a slab); empty otherwise
   const int64_t* leaf_start;  // nLeaves+1 element offsets (element sums only)
   const int* sub_leaf;     // nSub+1 leaf boundaries
   const int* sub_prog;     // nSub program offsets
@@ -68,10 +70,14 @@ struct ConvGeom {
   int QP;                  // pitch of the TV Q planes
   int tpc;                 // threads per channel (TH * TW / RW); CTA = tpc * C threads
   int rwb;                 // register blocking RW of the instantiated kernels (1, 2, 4)
+  int row0, Hg;            // row slab: global row of local row 0, global image rows (0, H otherwise)
+  int own0, own1;          // row slab: owned local rows (multiples of TH); [0, H) otherwise
+  int tileOff;             // global index of local tile 0 (row0 / TH * tilesW)
   unsigned magicC;         // ceil(2^20 / C): px = (e * magicC) >> 20 for e < 2^15
   unsigned magicRow;       // ceil(2^32 / rowE): row of a flattened tile-box index
   int o_ws, o_wf, o_pa, o_pq, o_tm, o_sv;   // byte offsets in dynamic smem
   int64_t N;               // H*W*C
+  int64_t Ng;              // global element count (Hg*W*C; = N unless a row slab)
 };
 
 // Device scalar results (one block, written by CTA 0, copied to the host).

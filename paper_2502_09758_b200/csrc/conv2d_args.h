@@ -17,6 +17,11 @@ enum ConvMode : int {
   CM_POWER = 9,          // scal[0] = op_norm_sq, scal[1] = converged, scal[2] = iters
   CM_MIXED_PREP = 10,    // out0 = B in0 - y (residual), out1 = B in1 (B q)
   CM_DOT = 11,           // scal[0] = <in0, in1> (ddot-type, fixed tree)
+  CM_SLAB_ABC = 12,      // row slab: A, B (+ candidate out0), C at out0; phase-1 sums
+  CM_SLAB_C = 13,        // row slab: candidate retry at L -> out0; phase-1 sums
+  CM_SLAB_POWER = 14,    // row slab: out0 = B^T B (in0 / sL); phase-1 of ||out0||^2
+  CM_SLAB_NORM0 = 15,    // row slab: phase-1 of ||in0||^2
+  CM_SLAB_GRAD = 16,     // row slab: lower_grad(in0) -> G; phase-1 of fit, tv, ||g||^2
 };
 
 
@@ -58,6 +63,7 @@ struct ConvArgs {
   double* scal;            // misc scalar outputs
   int mode;                // misc kernel mode
   int nofloor;             // hess_diag without the 1e-12*max floor (regularizer-only call)
+  double sbeta, sL;        // row-slab steps: momentum beta, trial Lipschitz L (or power scale)
   unsigned long long* trace;  // optional phase timestamps (CTA 0): [iter][16] %globaltimer ns
   const T* in0; const T* in1; T* out0; T* out1;
 };

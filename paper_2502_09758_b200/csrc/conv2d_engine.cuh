@@ -49,9 +49,9 @@ __device__ __forceinline__ unsigned long long gtimer() {
   } while (0)
 #define ADP_SUB_FLUSH(n)                                                            \
   do {                                                                              \
-    if (a.trace && blockIdx.x == 0 && (threadIdx.x & 31) == 0 && threadIdx.x < 7 * 32) { \
+    if (a.trace && blockIdx.x == 0 && (threadIdx.x & 31) == 0) {                      \
       for (int k_ = 0; k_ + 1 < (n); ++k_)                                          \
-        a.trace[1024 + (threadIdx.x >> 5) * 8 + k_] += (unsigned long long)(sub_t[k_ + 1] - sub_t[k_]); \
+        a.trace[1152 + (threadIdx.x >> 5) * 8 + k_] += (unsigned long long)(sub_t[k_ + 1] - sub_t[k_]); \
       if (threadIdx.x == 0) a.trace[1024 + 63] += 1;                                \
     }                                                                               \
   } while (0)
@@ -259,10 +259,41 @@ struct Conv {
   // ---- register-blocked correlation: RW consecutive outputs (row ty, cols
   // tx*RW..) of the thread's channel plane with stencil w (kh x kw).  Per
   // output the taps are accumulated in row-major order starting from 0.
+  // Compile-time K x K form (the benchmark stencils): fully unrolled, so the
+  // window and tap loads of a row are issued together with immediate
+  // offsets and their latency overlaps the multiply-add chains.  Same tap
+  // order as the generic loop.
+  template <int K>
+  __device__ __forceinline__ void stencil_k(const T* __restrict__ pl, const T* __restrict__ w, T (&acc)[RW]) const {
+    const int SWP = a.g.SWP;
+    const T* base = pl + (ty + 1) * SWP + sk(tx * RW);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const T* row = base + i * SWP;
+      T win[K + RW - 1];
+#pragma unroll
+      for (int m = 0; m < K + RW - 1; ++m) win[m] = row[skr(1 + m)];
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const T wt = w[i * K + j];
+#pragma unroll
+        for (int o = 0; o < RW; ++o) acc[o] = madd<FAST>(acc[o], win[o + j], wt);
+      }
+    }
+  }
+
   __device__ __forceinline__ void stencil(const T* __restrict__ pl, const T* __restrict__ w, T (&acc)[RW]) const {
 #pragma unroll
     for (int o = 0; o < RW; ++o) acc[o] = T(0);
     const int kh = a.g.kh, kw = a.g.kw, SWP = a.g.SWP;
+    if (kh == 9 && kw == 9) {
+      stencil_k<9>(pl, w, acc);
+      return;
+    }
+    if (kh == 15 && kw == 15) {
+      stencil_k<15>(pl, w, acc);
+      return;
+    }
     // phys(tx*RW + m) = sk(tx*RW) + skr(m); separable because tx*RW and the
     // j-block starts are multiples of RW
     const T* base = pl + (ty + 1) * SWP + sk(tx * RW);
@@ -311,11 +342,24 @@ struct Conv {
     return plane(ch)[(r + a.g.rh + 1) * a.g.SWP + sk(q + a.g.rw + 1)];
   }
 
+  // TV edges are those of the GLOBAL image (a row slab sees its global row
+  // index h + row0); the zero padding of the stencils is that of the local
+  // array, whose outer rows are either global edges or ghost rows.
+  __device__ __forceinline__ bool has_below(int h) const { return h + a.g.row0 < a.g.Hg - 1; }
+  __device__ __forceinline__ bool has_above(int h) const { return h + a.g.row0 >= 1; }
+  // sums cover owned rows only, indexed globally (tiles are TH-aligned, so a
+  // tile is wholly owned or not)
+  __device__ __forceinline__ bool tile_owned(int h0) const { return h0 >= a.g.own0 && h0 < a.g.own1; }
+  __device__ __forceinline__ void tile_partial(const SumDev& s, int tile, double part) const {
+    if (tile_owned((tile / a.g.tilesW) * a.g.TH)) store_tile_partial(s, tile + a.g.tileOff, part, red());
+  }
+
   // ---- fused NumPy-pairwise leaves of up to 3 term buffers (tm[k], each
   // TH x (TW*C) doubles, interleaved like the image) -> leaf_vals.  Leaf
   // index of (tile row r, segment s): (h*W*C + w0*C)/L + s; buffer k goes to
   // sums[k] with a leaf offset koff[k].
   __device__ void tile_leaves(int h0, int w0, int nbuf, const SumDev* s0, const SumDev* s1, int koff2) {
+    if (!tile_owned(h0)) return;   // CTA-uniform
     __syncthreads();
     const int C = a.g.C, L = a.g.leafL, W = a.g.W;
     const int rows = min(a.g.TH, a.g.H - h0);
@@ -344,7 +388,7 @@ struct Conv {
       acc = acc + __shfl_xor_sync(kFull, acc, 2);
       acc = acc + __shfl_xor_sync(kFull, acc, 4);
       if (act && k == 0) {
-        const int64_t li = (((int64_t)(h0 + r) * W + w0) * C) / L + s + (buf == 2 ? koff2 : 0);
+        const int64_t li = (((int64_t)(h0 + r + a.g.row0) * W + w0) * C) / L + s + (buf == 2 ? koff2 : 0);
         (buf == 0 ? s0 : s1)->leaf_vals[li] = acc;
       }
     }
@@ -400,7 +444,7 @@ struct Conv {
           const int q = tx * RW + o;
           const int w = w0 + q;
           const T yc = fp(ty, q);
-          const T d0 = (h < H - 1) ? fp(ty + 1, q) - yc : T(0);
+          const T d0 = has_below(h) ? fp(ty + 1, q) - yc : T(0);
           const T d1 = (w < W - 1) ? fp(ty, q + 1) - yc : T(0);
           const T rt0 = sqrt(d0 * d0 + nu2), rt1 = sqrt(d1 * d1 + nu2);
           q0[o] = d0 / rt0;
@@ -416,7 +460,7 @@ struct Conv {
             }
           }
           q0u[o] = T(0);
-          if (ty == 0 && h0 >= 1) {     // edge (h0-1) -> (h0): h0 - 1 < H - 1 always
+          if (ty == 0 && has_above(h0)) {     // edge (h0-1) -> (h0): h0 - 1 < H - 1 always
             const T du = yc - fp(-1, q);
             q0u[o] = du / sqrt(du * du + nu2);
           }
@@ -445,15 +489,15 @@ struct Conv {
           if (h < H && w < W) {
             // image_forward_diff_adjoint (regularizers.py:61-67), per-pixel order
             T t = T(0);
-            if (h >= 1) t = t + Q0[((size_t)ch * (TH + 1) + ty) * TW + q];
-            if (h <= H - 2) t = t - q0[o];
+            if (has_above(h)) t = t + Q0[((size_t)ch * (TH + 1) + ty) * TW + q];
+            if (has_below(h)) t = t - q0[o];
             if (w >= 1) t = t + (o > 0 ? q1[o > 0 ? o - 1 : 0] : Q1[((size_t)ch * TH + ty) * (TW + 1) + q]);
             if (w <= W - 2) t = t - q1[o];
             TVGout[gidx(h, w, ch)] = t;
           }
         }
       }
-      if (fused) tile_leaves(h0, w0, tv ? 3 : 1, sfit, stv, (int)(N / a.g.leafL));
+      if (fused) tile_leaves(h0, w0, tv ? 3 : 1, sfit, stv, (int)(a.g.Ng / a.g.leafL));
     }
   }
 
@@ -506,7 +550,7 @@ struct Conv {
         }
       }
       ADP_SUB(4);
-      if (sgg) store_tile_partial(*sgg, tile, part, red());
+      if (sgg) tile_partial(*sgg, tile, part);
       ADP_SUB(5);
       ADP_SUB_FLUSH(6);
     }
@@ -558,7 +602,7 @@ struct Conv {
           if (fused) put_term(0, ty, q, (double)(rc * rc));
           else RCout[i] = rc;
           if (tv) {
-            const T d0 = (h < H - 1) ? fp(ty + 1, q) - xc : T(0);
+            const T d0 = has_below(h) ? fp(ty + 1, q) - xc : T(0);
             const T d1 = (w < W - 1) ? fp(ty, q + 1) - xc : T(0);
             const T t0 = sqrt(d0 * d0 + nu2) - nu;
             const T t1 = sqrt(d1 * d1 + nu2) - nu;
@@ -574,8 +618,8 @@ struct Conv {
           if (sdot) part += (double)gpre[o] * (double)(xc - xopre[o]);
         }
       }
-      if (sdot) store_tile_partial(*sdot, tile, part, red());
-      if (fused) tile_leaves(h0, w0, tv ? 3 : 1, sfitc, stvc, (int)(N / a.g.leafL));
+      if (sdot) tile_partial(*sdot, tile, part);
+      if (fused) tile_leaves(h0, w0, tv ? 3 : 1, sfitc, stvc, (int)(a.g.Ng / a.g.leafL));
     }
   }
 
@@ -617,7 +661,7 @@ struct Conv {
           part += (double)v * (double)v;
         }
       }
-      if (ssq) store_tile_partial(*ssq, tile, part, red());
+      if (ssq) tile_partial(*ssq, tile, part);
     }
   }
 
@@ -650,7 +694,7 @@ struct Conv {
         const int w = w0 + tx * RW + o;
         if (h < H && w < W) part += f(gidx(h, w, ch), h, w, ch);
       }
-      store_tile_partial(s, tile, part, red());
+      tile_partial(s, tile, part);
     }
   }
 };

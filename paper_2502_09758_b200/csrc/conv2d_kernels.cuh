@@ -34,6 +34,20 @@ struct ConvOps : Conv<T, FAST, RW> {
     }
     reduce_k<K>(ss, out, this->sv(), gb, a.trace ? a.trace + 1088 : nullptr);
   }
+  // phase 1 only (subtrees of two-level sums), for the row-slab steps
+  template <int K>
+  __device__ void phase1(const SumDev* const (&l)[K]) {
+    int off = 0;
+#pragma unroll 1
+    for (int i = 0; i < K; ++i) {
+      const ptrdiff_t j = l[i] - &a.s_fit;
+      const SumDev& s = (j >= 0 && j < kNumSums) ? ssm[j] : *l[i];
+      if (s.nSub > 1) {
+        sum_phase1(s, this->sv(), off);
+        off += s.nSub;
+      }
+    }
+  }
   __device__ double reduce1(const SumDev& s) {
     double o;
     reduce({&s}, &o);
@@ -290,7 +304,7 @@ struct HessOps : ConvOps<T, FAST, RW> {
     const int H = a.g.H, W = a.g.W, C = a.g.C;
     this->foreach_pixel([&](int64_t i, int h, int w, int) {
       const T xc = ldcg(x + i);
-      const T d0 = (h < H - 1) ? ldcg(x + i + (int64_t)W * C) - xc : T(0);
+      const T d0 = this->has_below(h) ? ldcg(x + i + (int64_t)W * C) - xc : T(0);
       const T d1 = (w < W - 1) ? ldcg(x + i + C) - xc : T(0);
       const T s0 = d0 * d0 + nu2, s1 = d1 * d1 + nu2;
       a.WV[i] = nu2 / (s0 * sqrt(s0));
@@ -326,8 +340,8 @@ struct HessOps : ConvOps<T, FAST, RW> {
               // D^T (W . D v) at pixel i, image_forward_diff_adjoint order
               const T vc = ldcg(V + i);
               T t = T(0);
-              if (h >= 1) t = t + ldcg(a.WV + i - rowS) * (vc - ldcg(V + i - rowS));
-              if (h <= H - 2) t = t - ldcg(a.WV + i) * (ldcg(V + i + rowS) - vc);
+              if (this->has_above(h)) t = t + ldcg(a.WV + i - rowS) * (vc - ldcg(V + i - rowS));
+              if (this->has_below(h)) t = t - ldcg(a.WV + i) * (ldcg(V + i + rowS) - vc);
               if (w >= 1) t = t + ldcg(a.WH + i - C) * (vc - ldcg(V + i - C));
               if (w <= W - 2) t = t - ldcg(a.WH + i) * (ldcg(V + i + C) - vc);
               hv = hv + alpha * t;
@@ -344,7 +358,7 @@ struct HessOps : ConvOps<T, FAST, RW> {
           }
         }
       }
-      if (s) store_tile_partial(*s, tile, part, this->red());
+      if (s) this->tile_partial(*s, tile, part);
     }
   }
 
@@ -404,8 +418,8 @@ struct HessOps : ConvOps<T, FAST, RW> {
               const T xc = ldcg(x + i);
               T t = T(0);
               // diag[:-1] += wv; diag[1:] += wv; diag[:, :-1] += wh; diag[:, 1:] += wh
-              if (h <= H - 2) { const T dd = ldcg(x + i + rowS) - xc, s = dd * dd + nu2; t = t + nu2 / (s * sqrt(s)); }
-              if (h >= 1) { const T dd = xc - ldcg(x + i - rowS), s = dd * dd + nu2; t = t + nu2 / (s * sqrt(s)); }
+              if (this->has_below(h)) { const T dd = ldcg(x + i + rowS) - xc, s = dd * dd + nu2; t = t + nu2 / (s * sqrt(s)); }
+              if (this->has_above(h)) { const T dd = xc - ldcg(x + i - rowS), s = dd * dd + nu2; t = t + nu2 / (s * sqrt(s)); }
               if (w <= W - 2) { const T dd = ldcg(x + i + C) - xc, s = dd * dd + nu2; t = t + nu2 / (s * sqrt(s)); }
               if (w >= 1) { const T dd = xc - ldcg(x + i - C), s = dd * dd + nu2; t = t + nu2 / (s * sqrt(s)); }
               d = d + alpha * t;
@@ -622,6 +636,51 @@ __global__ void __launch_bounds__(512, 1) conv_misc_kernel(const __grid_constant
       if (blockIdx.x == 0 && threadIdx.x == 0) a.scal[0] = d;
       break;
     }
+    // ---- row-slab steps (multi-GPU c5, multigpu.SlabSolver): each stops
+    // after phase 1 of its sums; the ranks all-gather the sum units and fold
+    // the tops on the host, in the single-GPU tree order.
+    case CM_SLAB_ABC: {
+      // value + grad at y = x + beta (x - xp), first candidate xc = y - g / L
+      // and its value, restart dot g.(xc - x)   (lower_solvers.py:196-207)
+      E.stageA(SrcExtrap<T>{a.in0, a.in1, T(a.sbeta)}, a.R, a.ydat, tv, a.TV2, a.TVG, &a.s_fit, &a.s_tv);
+      E.gb.sync();
+      E.stageB(a.R, tv, a.TVG, a.G, &a.s_t0, a.in0, a.in1, T(a.sbeta), T(a.sL), a.out0);
+      E.gb.sync();
+      E.value_cand(SrcLin<T>{a.out0}, tv, nullptr, a.G, a.in0, &a.s_t1);
+      E.gb.sync();
+      E.phase1({&a.s_fit, &a.s_tv, &a.s_t0, &a.s_t1, &a.s_fitc, &a.s_tvc});
+      break;
+    }
+    case CM_SLAB_C:
+      // backtracking retry: xc = y - g / L and its value   (lower_solvers.py:170-177)
+      E.value_cand(SrcCand<T>{a.in0, a.in1, a.G, T(a.sbeta), T(a.sL)}, tv, a.out0, a.G, a.in0, &a.s_t1);
+      E.gb.sync();
+      E.phase1({&a.s_fitc, &a.s_tvc, &a.s_t1});
+      break;
+    case CM_SLAB_POWER:
+      // power step: out = B^T B (src / scale), partials of ||out||^2   (operators.py:150-165)
+      E.stage_corr(SrcScaled<T>{a.in0, T(a.sL)}, false, a.R, nullptr, T(1), nullptr);
+      E.gb.sync();
+      E.stage_corr(SrcLin<T>{a.R}, true, a.out0, nullptr, T(1), &a.s_t0);
+      E.gb.sync();
+      E.phase1({&a.s_t0});
+      break;
+    case CM_SLAB_NORM0:
+      E.foreach_pixel_sum([&](int64_t i, int, int, int) {
+        const double v = (double)a.in0[i];
+        return v * v;
+      }, a.s_t0);
+      E.gb.sync();
+      E.phase1({&a.s_t0});
+      break;
+    case CM_SLAB_GRAD:
+      // g = lower_grad(x) partials (final gradient norm, lower_solvers.py:212)
+      E.stageA(SrcLin<T>{a.in0}, a.R, a.ydat, tv, a.TV2, a.TVG, &a.s_fit, &a.s_tv);
+      E.gb.sync();
+      E.stageB(a.R, tv, a.TVG, a.G, &a.s_t0);
+      E.gb.sync();
+      E.phase1({&a.s_fit, &a.s_tv, &a.s_t0});
+      break;
     default:
       break;
   }

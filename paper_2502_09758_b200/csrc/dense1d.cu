@@ -704,6 +704,9 @@ static DenseArgs<T> dense_base(PlanImpl& P) {
   a.part = S->d_part;
   a.s_n.nLeaves = S->sn.nLeaves;
   a.s_n.nSub = 1;
+  a.s_n.sub_own0 = 0;
+  a.s_n.sub_own1 = 1;
+  a.s_n.sub_own2 = a.s_n.sub_own3 = 0;
   a.s_n.top_prog = S->sn.top_prog;
   a.s_n.leaf_start = S->d_leaf;
   a.s_n.progs = S->d_progs;

@@ -138,3 +138,46 @@ extern "C" int adp_fp64_peak(double* tflops, double* ms, void* stream) {
   if (e != cudaSuccess) return dense_fail(ADP_ERR_CUDA, cudaGetErrorString(e));
   return ADP_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Perfect-tree folds of assembled sum units (row-slab reductions): one CTA
+// per sum, the same zero-padded perfect tree the persistent kernels use.
+namespace adp {
+struct FoldArgs {
+  const double* u[8];
+  int n[8];
+  double* out;
+};
+constexpr int kFoldMax = 16384;
+
+__global__ void __launch_bounds__(1024) fold_units_kernel(FoldArgs f) {
+  extern __shared__ __align__(16) double fsm[];
+  const double r = tree_reduce_cta(f.u[blockIdx.x], f.n[blockIdx.x], fsm, fsm + kFoldMax);
+  if (threadIdx.x == 0) f.out[blockIdx.x] = r;
+}
+}  // namespace adp
+
+extern "C" int adp_fold_units(int32_t k, const double* const* units, const int64_t* n, double* out, void* stream) {
+  using namespace adp;
+  if (k < 1 || k > 8 || !units || !n || !out) return dense_fail(ADP_ERR_ARG, "fold: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  FoldArgs f{};
+  for (int i = 0; i < k; ++i) {
+    if (n[i] < 0 || n[i] > kFoldMax) return dense_fail(ADP_ERR_UNSUPPORTED, "fold: more than 16384 units");
+    if (n[i] > 0 && !units[i]) return dense_fail(ADP_ERR_ARG, "fold: null unit vector");
+    f.u[i] = units[i];
+    f.n[i] = (int)n[i];
+  }
+  const size_t smem = (size_t)(kFoldMax + 64) * sizeof(double);
+  if (cudaFuncSetAttribute(fold_units_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return dense_fail(ADP_ERR_CUDA, "fold: smem attribute");
+  double* d_out = nullptr;
+  if (cudaMallocAsync((void**)&d_out, 8 * sizeof(double), st) != cudaSuccess) return dense_fail(ADP_ERR_CUDA, "fold: alloc");
+  f.out = d_out;
+  fold_units_kernel<<<k, 1024, smem, st>>>(f);
+  cudaMemcpyAsync(out, d_out, k * sizeof(double), cudaMemcpyDeviceToHost, st);
+  cudaFreeAsync(d_out, st);
+  const cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return dense_fail(ADP_ERR_CUDA, cudaGetErrorString(e));
+  return ADP_OK;
+}

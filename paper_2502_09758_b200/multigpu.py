@@ -21,6 +21,7 @@ The per-rank device work reuses the single-GPU kernels on the local array
 """
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass
 
 import numpy as np
@@ -87,12 +88,13 @@ def ghost_width(kh: int) -> int:
     return 3 * (kh // 2) + 1
 
 
-def plan_slabs(H: int, world: int, kh: int, row_align: int = 1) -> list:
+def plan_slabs(H: int, world: int, kh: int, row_align: int = 1, ghost: int | None = None) -> list:
     """Split H rows into `world` contiguous slabs (sizes differ by at most
-    `row_align`), each padded with ghost rows toward its neighbours."""
+    `row_align`), each padded with ghost rows toward its neighbours
+    (`ghost` rows, default 3r + 1)."""
     if world < 1 or H < world:
         raise ValueError("need 1 <= world <= H")
-    gw = ghost_width(kh)
+    gw = ghost_width(kh) if ghost is None else int(ghost)
     units = H // row_align
     base, extra = divmod(units, world)
     bounds = [0]
@@ -176,3 +178,293 @@ def perfect_tree_sum(vals) -> float:
     while v.size > 1:
         v = v[0::2] + v[1::2]
     return float(v[0])
+
+
+# ---------------------------------------------------------------------------
+# c5: the lower-level solve on row slabs, host-stepped at its reductions.
+#
+# Per AGD iteration each rank runs ONE device step (adp_slab_step op 0:
+# value+grad at y, first candidate, its value, restart dot) over its slab +
+# ghosts, then the ranks assemble the sum units (all-reduce SUM of vectors
+# that are zero outside each rank's own ranges: exact) and fold them on the
+# device in the single-GPU tree order (adp_fold_units).  The decisions
+# (acceptance, backtracking retries = op 1, restart) are the scalar logic of
+# conv_solve_kernel / _accelerated (lower_solvers.py:180-213) evaluated
+# identically on every rank; then one ghost exchange of the new iterate.
+# Leaves, tile partials and trees are those of the unsplit plan, so the
+# iterates are bitwise identical to the single-GPU solve.
+
+class LocalComm:
+    """Every slab in this process (one device): ghost refresh by device
+    copies between the slabs' arrays; unit vectors are shared, so assembly
+    needs no collective."""
+
+    def exchange(self, states, arrays):
+        for i, st in enumerate(states):
+            s = st.slab
+            if s.ghost_top:
+                nb = states[i - 1]
+                src = arrays[i - 1][nb.slab.owned]
+                arrays[i][: s.ghost_top].copy_(src[src.shape[0] - s.ghost_top:])
+            if s.ghost_bot:
+                nb = states[i + 1]
+                src = arrays[i + 1][nb.slab.owned]
+                arrays[i][arrays[i].shape[0] - s.ghost_bot:].copy_(src[: s.ghost_bot])
+
+    def assemble(self, bufs):
+        return bufs
+
+
+class DistComm:
+    """One slab per rank over torch.distributed (NCCL over NVLink on the GPU
+    box): ghost rows by send/recv, unit vectors by one all-reduce SUM."""
+
+    def __init__(self, group=None):
+        self.group = group
+
+    def exchange(self, states, arrays):
+        for st, arr in zip(states, arrays):
+            halo_exchange(arr, st.slab, self.group)
+
+    def assemble(self, bufs):
+        import torch
+        import torch.distributed as dist
+        flat = torch.cat([b.reshape(-1) for b in bufs])
+        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=self.group)
+        out, o = [], 0
+        for b in bufs:
+            out.append(flat[o:o + b.numel()].view_as(b))
+            o += b.numel()
+        return out
+
+
+@dataclass
+class _SlabState:
+    slab: Slab
+    plan: object
+    lower: object
+    keep: tuple
+    X: list
+
+
+SUM_FIT, SUM_TV, SUM_FITC, SUM_TVC, SUM_GG, SUM_DOT = range(6)
+
+
+class SlabSolver:
+    """solve_lower (agd, adaptive: the c2-c5 settings) of one image split into
+    row slabs.  `ranks` are the slab indices held by this process: all of
+    them with LocalComm (one device), [rank] with DistComm."""
+
+    def __init__(self, p, world: int, ranks=None, comm=None):
+        import ctypes
+        from . import _native as nat
+        from .lower_solvers import _check_reg_smooth
+        from .operators import ConvOperator
+        from .regularizers import SmoothedTV
+        if not isinstance(p.op, ConvOperator) or not isinstance(p.reg, SmoothedTV):
+            raise ValueError("row slabs: depthwise 2-D operator with SmoothedTV")
+        _check_reg_smooth(p)
+        self.p = p
+        self.nat = nat
+        self.ctypes = ctypes
+        H, W, C = p.op.signal_shape
+        K = p.op.kernel.data.shape[0]
+        if p.op.kernel.data.shape[1] != K:
+            raise ValueError("row slabs: square stencils")
+        self.shape = (H, W, C)
+        self.K = K
+        geo = nat.probe_geometry((H, W, C), (K, K))
+        if not geo["fused"]:
+            raise ValueError("row slabs need a leaf-aligned (fused) sum layout")
+        TH, TW, tilesW, L = geo["TH"], geo["TW"], geo["tilesW"], geo["leafL"]
+        self.geo = geo
+        align = TH
+        n_leaves = H * W * C // L
+        if n_leaves > 4096:                      # two-level element sums: subtree-aligned rows
+            align = _lcm(align, max(1, 2048 * L // (W * C)))
+        tiles_h = (H + TH - 1) // TH
+        if tiles_h * tilesW > 4096:              # two-level tile sums
+            align = _lcm(align, max(1, 2048 // tilesW) * TH)
+        r = K // 2
+        gw = -(-(3 * r + 1) // TH) * TH          # ghost rows: 3r + 1, tile aligned
+        self.slabs = plan_slabs(H, world, K, row_align=align, ghost=gw)
+        for s in self.slabs:
+            if (s.row1 - s.row0) < gw and world > 1:
+                raise ValueError(f"slab of {s.row1 - s.row0} rows is thinner than its ghost width {gw}")
+        self.ranks = list(range(world)) if ranks is None else list(ranks)
+        self.comm = comm if comm is not None else LocalComm()
+        if isinstance(self.comm, LocalComm) and len(self.ranks) != world:
+            raise ValueError("LocalComm holds every slab")
+        kd = p.op.kernel.device()
+        self.states = []
+        for rk in self.ranks:
+            s = self.slabs[rk]
+            g0 = s.row0 - s.ghost_top
+            rows = s.local_rows
+            own = (s.ghost_top, s.ghost_top + s.row1 - s.row0)
+            plan = nat.Plan(nat.LAYOUT_DEPTHWISE2D, (rows, W, C), (K, K), nat.get_precision()["dtype"],
+                            nat.get_precision()["mode"], tile=(TH, TW), slab=(g0, H, own[0], own[1]))
+            yd = nat.to_dev(np.ascontiguousarray(np.asarray(p.y)[g0:g0 + rows]) if not nat.is_torch(p.y)
+                            else p.y[g0:g0 + rows].contiguous())
+            low = p.reg.native()
+            low.kernel = kd.data_ptr()
+            low.y = yd.data_ptr()
+            low.alpha = float(p.alpha)
+            X = [nat.empty_like_dev((rows, W, C)) for _ in range(3)]
+            self.states.append(_SlabState(s, plan, low, (kd, yd), X))
+        self.units_meta = []
+        for which in range(6):
+            n = ctypes.c_int64()
+            own = (ctypes.c_int64 * 4)()
+            nat.check(nat.lib().adp_slab_units(self.states[0].plan.handle, which, ctypes.byref(n), own, None, None),
+                      "adp_slab_units")
+            self.units_meta.append(int(n.value))
+        self.stats = {}
+
+    # -- device steps and reductions
+    def _step(self, op, xs, xps, outs, beta=0.0, L=1.0):
+        nat, ct = self.nat, self.ctypes
+        for st, x, xp, o in zip(self.states, xs, xps, outs):
+            nat.check(nat.lib().adp_slab_step(st.plan.handle, ct.byref(st.lower), op, nat.ptr(x), nat.ptr(xp),
+                                              nat.ptr(o), float(beta), float(L), nat.stream_ptr()),
+                      "adp_slab_step")
+
+    def _sums(self, which):
+        import torch
+        nat, ct = self.nat, self.ctypes
+        bufs = [torch.zeros(self.units_meta[w], dtype=torch.float64, device="cuda") for w in which]
+        for st in self.states:
+            for w, b in zip(which, bufs):
+                n = ct.c_int64()
+                own = (ct.c_int64 * 4)()
+                nat.check(nat.lib().adp_slab_units(st.plan.handle, w, ct.byref(n), own, nat.ptr(b),
+                                                   nat.stream_ptr()), "adp_slab_units")
+        bufs = self.comm.assemble(bufs)
+        k = len(which)
+        ptrs = (ct.c_void_p * k)(*[b.data_ptr() for b in bufs])
+        ns = (ct.c_int64 * k)(*[b.numel() for b in bufs])
+        out = (ct.c_double * k)()
+        nat.check(nat.lib().adp_fold_units(k, ptrs, ns, out, nat.stream_ptr()), "adp_fold_units")
+        return [float(v) for v in out]
+
+    def _local(self, full):
+        """Per-state local arrays (slab + ghosts) of a full image (host or device)."""
+        nat = self.nat
+        out = []
+        for st in self.states:
+            s = st.slab
+            g0 = s.row0 - s.ghost_top
+            out.append(nat.to_dev(full[g0:g0 + s.local_rows]))
+        return out
+
+    def op_norm_sq(self, max_iters: int = 300, tol: float = 1e-4):
+        """Power iteration on B^T B (operators.py:137-173) over the slabs."""
+        nat = self.nat
+        src = self._local(nat.power_start(self.shape))
+        bufs = ([nat.empty_like_dev(x.shape) for x in src], [nat.empty_like_dev(x.shape) for x in src])
+        self._step(3, src, src, src)
+        scale = math.sqrt(self._sums([SUM_GG])[0])    # v /= ||v||
+        lam, conv, iters = 0.0, False, 0
+        for it in range(max_iters):
+            iters = it + 1
+            out = bufs[it % 2]
+            self._step(2, src, src, out, L=scale)     # w = B^T B v
+            lam_new = math.sqrt(self._sums([SUM_GG])[0])
+            if lam_new == 0.0:
+                lam, conv = 0.0, True
+                break
+            src, scale = out, lam_new                 # v = w / ||w||
+            if abs(lam_new - lam) <= tol * max(lam_new, 1e-300):
+                lam, conv = lam_new, True
+                break
+            lam = lam_new
+            self.comm.exchange(self.states, src)
+        self.stats.update(power_iters=iters, power_converged=conv)
+        return lam
+
+    def solve(self, x0, eps: float, mu: float, max_iters: int = 1200, norm_sq: float | None = None):
+        """Adaptive AGD (lower_solvers.py:180-213).  Returns (x_owned list per
+        held slab, grad_norm, iters, converged)."""
+        from .lower_solvers import SolveDiverged
+        nat = self.nat
+        p = self.p
+        H, W, C = self.shape
+        if eps <= 0 or mu <= 0:
+            raise ValueError("eps and mu must be > 0")
+        tol = eps * mu
+        lam = self.op_norm_sq() if norm_sq is None else float(norm_sq)
+        alpha, nu = float(p.alpha), float(p.reg.nu)
+        lip = 2.0 * lam + alpha * p.reg.curvature
+        twoN = 2.0 * float(H * W * C)
+        tv = alpha != 0.0
+        xs = self._local(x0)
+        for st, x in zip(self.states, xs):
+            st.X[0].copy_(x)
+        ix = ixp = 0
+        ic = 1
+        t_mom, lip_t = 1.0, lip
+        vg = vals = restarts = 0
+        for t in range(max_iters):
+            t_next = 0.5 * (1.0 + math.sqrt(1.0 + 4.0 * t_mom * t_mom))
+            beta = (t_mom - 1.0) / t_next
+            t_mom = t_next
+            L_try = lip_t
+            X = [st.X for st in self.states]
+            self._step(0, [x[ix] for x in X], [x[ixp] for x in X], [x[ic] for x in X], beta, L_try)
+            vg += 1
+            vals += 1
+            fit, tvs, gg, dot, fitc, tvc = self._sums([SUM_FIT, SUM_TV, SUM_GG, SUM_DOT, SUM_FITC, SUM_TVC])
+            h_y = fit + alpha * (tvs - nu * twoN) if tv else fit
+            gn = math.sqrt(gg)
+            if not math.isfinite(gn):
+                raise SolveDiverged(f"objective became non-finite at lower iteration {t}")
+            if gn <= tol:
+                # converged: return y = x + beta (x - x_prev)   (lower_solvers.py:200-201)
+                from .hypergradient import _vec
+                out = []
+                for x in X:
+                    d = nat.empty_like_dev(x[ix].shape)
+                    y = nat.empty_like_dev(x[ix].shape)
+                    _vec(4, d.numel(), 0.0, x[ix], x[ixp], d)      # x - x_prev
+                    _vec(0, d.numel(), beta, x[ix], d, y)          # x + beta (x - x_prev)
+                    out.append(y)
+                self.stats.update(vg_evals=vg, value_evals=vals, restarts=restarts, lip=lip)
+                return self._owned(out), gn, t, True
+            k = 0
+            while True:
+                val = fitc + alpha * tvc if tv else fitc + alpha * 0.0
+                if val <= h_y - 0.5 * gn * gn / L_try + 1e-15 * abs(h_y):
+                    break
+                L_try *= 2.0
+                k += 1
+                if k >= 60:
+                    raise SolveDiverged("backtracking line search failed to find a decreasing step")
+                self._step(1, [x[ix] for x in X], [x[ixp] for x in X], [x[ic] for x in X], beta, L_try)
+                vals += 1
+                fitc, tvc, dot = self._sums([SUM_FITC, SUM_TVC, SUM_DOT])
+            bstep = 1.0 / L_try
+            lip_t = max(1.0 / bstep * 0.9, lip * 1e-8)
+            ixp, ix = ix, ic
+            if dot > 0.0:
+                t_mom = 1.0
+                ixp = ix
+                restarts += 1
+            for b in range(3):
+                if b != ix and b != ixp:
+                    ic = b
+                    break
+            self.comm.exchange(self.states, [x[ix] for x in X])
+        # max_iters reached: gradient norm at x   (lower_solvers.py:212-213)
+        X = [st.X for st in self.states]
+        self._step(4, [x[ix] for x in X], [x[ix] for x in X], [None] * len(X))
+        gn = math.sqrt(self._sums([SUM_GG])[0])
+        self.stats.update(vg_evals=vg, value_evals=vals, restarts=restarts, lip=lip)
+        return self._owned([x[ix] for x in X]), gn, max_iters, gn <= tol
+
+    def _owned(self, arrs):
+        return [a[st.slab.owned] for st, a in zip(self.states, arrs)]
+
+
+def _lcm(a: int, b: int) -> int:
+    import math as _m
+    return a * b // _m.gcd(a, b)

@@ -125,3 +125,36 @@ def _stencil_case(rank, world):
 
 def test_slab_ghost_width_reproduces_global_iteration():
     assert run_ranks(_stencil_case) == {0: True, 1: True}
+
+
+def _assemble_case(rank, world):
+    # units of two sums, each rank owning disjoint ranges (the TV-like sum has
+    # two ranges per rank); DistComm.assemble = all-reduce SUM of zero-padded
+    # vectors must reproduce the full vectors exactly (incl. tiny / huge values)
+    rng = np.random.default_rng(11)
+    full_a = rng.standard_normal(40) * np.exp(8 * rng.standard_normal(40))
+    full_b = rng.standard_normal(64) * 1e-300
+    ranges_a = [(0, 25), (25, 40)]
+    ranges_b = [[(0, 16), (32, 48)], [(16, 32), (48, 64)]]
+    a = torch.zeros(40, dtype=torch.float64)
+    b = torch.zeros(64, dtype=torch.float64)
+    lo, hi = ranges_a[rank]
+    a[lo:hi] = torch.from_numpy(full_a[lo:hi])
+    for lo, hi in ranges_b[rank]:
+        b[lo:hi] = torch.from_numpy(full_b[lo:hi])
+    ra, rb = mg.DistComm().assemble([a, b])
+    return bool(np.array_equal(ra.numpy(), full_a) and np.array_equal(rb.numpy(), full_b))
+
+
+def test_dist_unit_assembly_is_exact():
+    assert run_ranks(_assemble_case) == {0: True, 1: True}
+
+
+def test_slab_alignment_rules():
+    # ghost rows are 3r + 1 rounded up to the tile height, slabs align to it
+    slabs = mg.plan_slabs(4096, 8, 31, row_align=64, ghost=48)
+    assert [s.row1 - s.row0 for s in slabs] == [512] * 8
+    assert slabs[0].ghost_top == 0 and slabs[-1].ghost_bot == 0
+    assert all(s.ghost_top == 48 for s in slabs[1:]) and all(s.ghost_bot == 48 for s in slabs[:-1])
+    assert all((s.row0 - s.ghost_top) % 8 == 0 for s in slabs)
+    assert mg._lcm(8, 64) == 64 and mg._lcm(8, 12) == 24

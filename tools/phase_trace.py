@@ -26,10 +26,10 @@ plan = p.op.plan()
 nat.check(nat.lib().adp_debug_trace(plan.handle, 1, None))
 p = up.lower_problem(up.b0)
 adp.solve_lower(p, x0, 1e-14, 10.0, max_iters=64, method="agd", adaptive=True)
-buf = np.zeros(64 * 16 + 128, dtype=np.uint64)
+buf = np.zeros(64 * 16 + 256, dtype=np.uint64)
 nat.check(nat.lib().adp_debug_trace(plan.handle, 0, buf.ctypes.data))
 cnt = max(int(buf[1024 + 63]), 1)
-subs = [buf[1024 + 8 * w:1024 + 8 * w + 5].astype(np.float64) / cnt for w in range(4)]
+subs = [buf[1152 + 8 * w:1152 + 8 * w + 5].astype(np.float64) / cnt for w in range(16)]
 tr = buf[:1024].reshape(64, 16).astype(np.int64)
 names = ["A", "bar1", "B", "bar2", "C", "bar3", "reduce"]
 d = np.diff(tr[:, :8], axis=1)[4:60]
@@ -39,8 +39,10 @@ print(f"iteration mean {it.mean():.2f} us, median {np.median(it):.2f}")
 rt = tr[:, 8:]
 extra = [(rt[i][rt[i] > 0].max() - tr[i, 7]) / 1e3 for i in range(4, 60) if (rt[i] > 0).any()]
 print(f"retries: {len(extra)} iterations, mean extra {np.mean(extra) if extra else 0:.2f} us")
+print(f"stage B per warp, mean SM cycles over {cnt} calls: sync+issue+box / -> / sync / stencil / epilogue")
 for w, sub in enumerate(subs):
-    print(f"stage B warp {w}, mean SM cycles over {cnt} calls:", {n: round(float(v)) for n, v in zip(["sync+issue+box", "->", "sync", "stencil", "epilogue"], sub)})
+    if sub.any():
+        print(f"  warp {w:2d}:", " ".join(f"{float(v):6.0f}" for v in sub))
 rc = max(int(buf[1088 + 7]), 1)
 print(f"reduce sub-phases, CTA 0 mean SM cycles over {rc} calls:",
       {n: round(float(buf[1088 + k]) / rc) for k, n in enumerate(["phase1+bar", "issue", "wait+sync", "fold", "final"])})

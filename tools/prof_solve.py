@@ -1,6 +1,6 @@
 """Profiling driver: one warm-up and one profiled c2 solve_lower (strict f64).
 
-    python tools/prof_solve.py [--iters 100] [--size 256] [--mode strict|fast] [--config c2|c3]
+    python tools/prof_solve.py [--iters 100] [--size 256] [--mode strict|fast] [--config c2|c3|c5]
 
 Used as the ncu target (the profiled launch is the 2nd conv_solve_kernel).
 """
@@ -27,7 +27,7 @@ from paper_2502_09758_b200 import _native as nat  # noqa: E402
 from paper_2502_09758_b200 import configs  # noqa: E402
 
 adp.set_precision("float64", a.mode)
-up = configs.config2(0, size=a.size) if a.config == "c2" else configs.config3(0, size=a.size)
+up = configs.CONFIGS[a.config](0, size=a.size)
 x0 = nat.to_dev(up.x0)
 out = nat.empty_like_dev(up.x0.shape)
 for rep in range(a.reps):
