@@ -48,7 +48,11 @@ def parse():
     ap.add_argument("--size", type=int, default=256)
     ap.add_argument("--maid-steps", type=int, default=2, help="accepted MAID steps for upper iters/s (0: skip)")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--no-extra", action="store_true", help="skip the fast-mode / fp32 side measurements")
+    ap.add_argument("--no-extra", action="store_true", help="skip the fast-mode / fp32 / other-config side measurements")
+    ap.add_argument("--workload", default="c2", choices=["c2", "c5"],
+                    help="main-line workload (default c2 = BASELINE configs[1]); c5 under torchrun = row slabs")
+    ap.add_argument("--c5-size", type=int, default=4096)
+    ap.add_argument("--c5-iters", type=int, default=10)
     return ap.parse_args()
 
 
@@ -329,6 +333,11 @@ def run_native(args):
         adp.set_precision(dtype, mode)
         line["other_modes"] = side
 
+    # ---- the other BASELINE configs, one timed call each (rank 0, N = 1)
+    if not args.no_extra and rank == 0 and ws == 1:
+        adp.set_precision(dtype, mode)
+        line["configs"] = other_configs(args, flush)
+
     # ---- CPU baseline (rank 0, N = 1 only): bounded oracle sample
     if not args.no_cpu and rank == 0 and ws == 1:
         iters = 40
@@ -342,9 +351,126 @@ def run_native(args):
         dist.destroy_process_group()
 
 
+def _timed(fn):
+    import torch
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    r = fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return r, e0.elapsed_time(e1) / 1e3
+
+
+def other_configs(args, flush):
+    """c3 (one 512x512x3 image), c4 (8 c3 instances = one GPU's share of 64)
+    and c5 (one 4096x4096x3 image, K = 31) through solve_lower, device time,
+    power iteration included (fresh operator per solve, as MAID calls it)."""
+    import paper_2502_09758_b200 as adp
+    from paper_2502_09758_b200 import _native as nat
+    from paper_2502_09758_b200 import configs
+    out = {}
+    eps, mu = 1e-14, 10.0
+
+    def solve(up, iters):
+        x0 = nat.to_dev(up.x0)
+        xo = nat.empty_like_dev(up.x0.shape)
+        p = up.lower_problem(up.b0)
+        return adp.solve_lower(p, x0, eps, mu, max_iters=iters, method="agd", adaptive=True, x_out=xo)
+
+    up3 = configs.config3(0)
+    solve(up3, 50)
+    flush.zero_()
+    r, t = _timed(lambda: solve(up3, 1200))
+    out["c3"] = {"value": up3.y_delta.size * r.iters / t / 1e9, "unit": UNIT, "iters": r.iters,
+                 "ms_per_solve": 1e3 * t, "workload": "512x512x3, 15x15 line-Gaussian, 1200 AGD iterations"}
+    ups = [configs.config3(seed) for seed in range(8)]
+    flush.zero_()
+
+    def c4():
+        return [solve(u, 300) for u in ups]
+    rs, t = _timed(c4)
+    out["c4"] = {"value": sum(u.y_delta.size * q.iters for u, q in zip(ups, rs)) / t / 1e9, "unit": UNIT,
+                 "instances": len(ups), "ms": 1e3 * t,
+                 "workload": "8 c3 instances (seeds 0-7) = one GPU's share of 64, 300 AGD iterations each, "
+                             "no collectives (weak scaling over GPUs)"}
+    del ups
+    up5 = configs.config5(0, size=args.c5_size)
+    solve(up5, 2)
+    flush.zero_()
+    r, t = _timed(lambda: solve(up5, args.c5_iters))
+    out["c5"] = {"value": up5.y_delta.size * r.iters / t / 1e9, "unit": UNIT, "iters": r.iters,
+                 "ms_per_solve": 1e3 * t,
+                 "workload": f"{args.c5_size}x{args.c5_size}x3, 31x31 Gaussian, {args.c5_iters} AGD iterations "
+                             "(+ power iteration), one GPU"}
+    return out
+
+
+def run_c5(args):
+    """c5 main line: one 4096x4096x3 image; N > 1 ranks hold one row slab each
+    (3r+1 ghost rows, one exchange per iteration, NCCL over NVLink), strong
+    scaling; the iterates are bitwise those of the unsplit solve."""
+    import torch
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    import paper_2502_09758_b200 as adp
+    from paper_2502_09758_b200 import configs
+    from paper_2502_09758_b200 import multigpu
+    dtype, mode = ("float32", "fast") if args.mode == "fp32" else ("float64", args.mode)
+    adp.set_precision(dtype, mode)
+    up = configs.config5(0, size=args.c5_size)
+    N = up.y_delta.size
+    x0 = np.ascontiguousarray(up.x0)
+    comm = multigpu.DistComm() if ws > 1 else multigpu.LocalComm()
+    sv = multigpu.SlabSolver(up.lower_problem(up.b0), ws, ranks=[rank] if ws > 1 else None, comm=comm)
+
+    def step():
+        sv.p = up.lower_problem(up.b0)      # fresh operator: power iteration included
+        return sv.solve(x0, 1e-14, 10.0, max_iters=args.c5_iters)
+
+    for _ in range(args.warmup):
+        step()
+    times, units, launches = [], 0, 0
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            if ws > 1:
+                torch.distributed.barrier()
+            (xs, gn, it, conv), dt = _timed(step)
+            times.append(dt)
+            units += N * it
+            st = sv.stats
+            n_steps = 1 + st["power_iters"] + st["value_evals"] + (0 if conv or it < args.c5_iters else 1)
+            launches += 2 * n_steps          # one slab step + one unit fold per reduction point
+    t_dev = float(np.sum(times))
+    if ws > 1:
+        tt = torch.tensor([t_dev], device="cuda", dtype=torch.float64)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        t_dev = float(tt.item())
+    line = {"metric": METRIC, "value": units / t_dev / 1e9, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t_dev / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64" if dtype == "float64" else "f32",
+            "data": "synthetic",
+            "config": {"workload": f"c5: {args.c5_size}x{args.c5_size}x3 image, 31x31 stencil, smoothed TV, "
+                                   f"adaptive AGD, {args.c5_iters} lower iterations per solve (+ power iteration)",
+                       "mode": mode, "l2": "inputs larger than L2",
+                       "parallelism": f"row slabs x{ws} (ghost {sv.slabs[0].ghost_bot if ws > 1 else 0} rows)"},
+            "gpu_launches": launches, "clocks": clk.summary()}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+
+
+
 if __name__ == "__main__":
     a = parse()
     if a.impl == "reference":
         run_reference(a)
+    elif a.workload == "c5":
+        run_c5(a)
     else:
         run_native(a)

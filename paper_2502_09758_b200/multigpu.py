@@ -124,6 +124,15 @@ def halo_exchange(local, slab: Slab, group=None):
     rows up and its last ghost_bot owned rows down.  Works for CUDA tensors
     (NCCL) and CPU tensors (gloo)."""
     import torch.distributed as dist
+    if local.is_cuda and dist.get_backend(group) != "nccl":
+        # host-staged exchange (gloo with device arrays: functional tests on one GPU)
+        host = local.cpu()
+        halo_exchange(host, slab, group)
+        if slab.ghost_top:
+            local[: slab.ghost_top].copy_(host[: slab.ghost_top])
+        if slab.ghost_bot:
+            local[local.shape[0] - slab.ghost_bot:].copy_(host[host.shape[0] - slab.ghost_bot:])
+        return local
     ops = []
     own = local[slab.owned]
     if slab.rank > 0 and slab.ghost_top:
@@ -230,7 +239,12 @@ class DistComm:
         import torch
         import torch.distributed as dist
         flat = torch.cat([b.reshape(-1) for b in bufs])
-        dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=self.group)
+        if flat.is_cuda and dist.get_backend(self.group) != "nccl":
+            host = flat.cpu()
+            dist.all_reduce(host, op=dist.ReduceOp.SUM, group=self.group)
+            flat = host.to(flat.device)
+        else:
+            dist.all_reduce(flat, op=dist.ReduceOp.SUM, group=self.group)
         out, o = [], 0
         for b in bufs:
             out.append(flat[o:o + b.numel()].view_as(b))

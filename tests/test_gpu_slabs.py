@@ -58,3 +58,51 @@ def test_slab_plan_only_runs_slab_steps(adp):
     out = nat.zeros_dev((152, 256, 3))
     rc = nat.lib().adp_apply(plan.handle, nat.ptr(k), nat.ptr(x), nat.ptr(out), nat.stream_ptr())
     assert rc != 0 and b"slab" in nat.lib().adp_last_error()
+
+
+def _two_proc_worker(rank, world, port, q):
+    import os
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2502_09758_b200 as adp
+        from paper_2502_09758_b200 import multigpu
+        p, y = _problem(adp, (512, 512, 3), 15, 3.5)
+        sv = multigpu.SlabSolver(p, world, ranks=[rank], comm=multigpu.DistComm())
+        xs, gn, it, conv = sv.solve(np.ascontiguousarray(y), 1e-14, 10.0, max_iters=20)
+        q.put((rank, (xs[0].cpu().numpy(), gn, it, dict(sv.stats))))
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_slab_solve_two_processes_match_single_gpu(adp):
+    """The distributed orchestration (DistComm: ghost send/recv, all-reduce
+    of the sum units) with two processes, one slab each, on the one device
+    (gloo, host-staged): identical to the unsplit solve."""
+    import socket
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_two_proc_worker, args=(r, 2, port, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    out = dict(q.get(timeout=300) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=60)
+    assert all(not isinstance(v, str) for v in out.values()), out
+    p, y = _problem(adp, (512, 512, 3), 15, 3.5)
+    st = {}
+    ref = adp.solve_lower(p, np.ascontiguousarray(y), 1e-14, 10.0, max_iters=20, method="agd", adaptive=True,
+                          stats=st)
+    x = np.concatenate([out[0][0], out[1][0]], axis=0)
+    assert out[0][1] == out[1][1] == ref.grad_norm and out[0][2] == ref.iters
+    assert out[0][3]["restarts"] == st["restarts"] and out[0][3]["value_evals"] == st["value_evals"]
+    assert np.array_equal(x, ref.x_tilde)
