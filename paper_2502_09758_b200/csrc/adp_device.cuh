@@ -494,7 +494,8 @@ __device__ __forceinline__ void reduce_k(const SumDev* const (&ss)[K], double* o
     lap(0);
   }
   const int BD = blockDim.x;
-  const int T = 1 << (31 - __clz(BD));
+  const int lgT = 31 - __clz(BD);
+  const int T = 1 << lgT;
   int base = 0;
 #pragma unroll
   for (int i = 0; i < K; ++i) {
@@ -514,7 +515,7 @@ __device__ __forceinline__ void reduce_k(const SumDev* const (&ss)[K], double* o
   base = 0;
 #pragma unroll
   for (int i = 0; i < K; ++i) {
-    const int chunk = P[i] > T ? P[i] / T : 1;
+    const int chunk = P[i] > T ? P[i] >> lgT : 1;
     root[i] = 0.0;
     if (threadIdx.x * chunk < P[i])
       root[i] = chunk <= 16 ? fold_small(sv + base + threadIdx.x * chunk, chunk)

@@ -355,6 +355,15 @@ static int conv_plan_init(PlanImpl& P) {
   g.YSWP = (g.TW + 2) + (g.TW + 2) / kRWp + 1;
   g.N = (int64_t)g.H * g.W * g.C;
   g.tileOff = (g.row0 / g.TH) * g.tilesW;
+  // division-free device indexing (exact for numerators < 2^16)
+  auto magic = [](int d) { return d <= 1 ? 0u : (unsigned)(((1ull << 32) + d - 1) / d); };   // 0: d == 1
+  g.magicTW = magic(g.tilesW);
+  g.magicTWpx = magic(g.TW);
+  g.segs = g.fused ? g.TW * g.C / g.leafL : 1;
+  g.magicSegs = magic(g.segs);
+  g.rowL = g.fused ? (int64_t)g.W * g.C / g.leafL : 0;
+  if ((int64_t)g.tilesH * g.tilesW >= 65536 || g.W >= 65536)
+    return fail(ADP_ERR_UNSUPPORTED, "more than 65535 tiles or columns per plan");
   if (slab) {
     if (!g.fused) return fail(ADP_ERR_UNSUPPORTED, "row slabs need the fused (tile-aligned pairwise) sum layout");
     const bool bottom = g.row0 + g.H == g.Hg && g.own1 == g.H;

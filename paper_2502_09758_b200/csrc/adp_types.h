@@ -73,6 +73,11 @@ struct ConvGeom {
   int row0, Hg;            // row slab: global row of local row 0, global image rows (0, H otherwise)
   int own0, own1;          // row slab: owned local rows (multiples of TH); [0, H) otherwise
   int tileOff;             // global index of local tile 0 (row0 / TH * tilesW)
+  unsigned magicTW;        // ceil(2^32 / tilesW): tile / tilesW = umulhi(tile, magicTW) (tile < 2^16)
+  unsigned magicTWpx;      // ceil(2^32 / TW): w0 / TW = umulhi(w0, magicTWpx) (w0 < 2^16)
+  int segs;                // fused: leaves per tile row (TW * C / leafL)
+  unsigned magicSegs;      // ceil(2^32 / segs)
+  int64_t rowL;            // fused: leaves per image row (W * C / leafL)
   unsigned magicC;         // ceil(2^20 / C): px = (e * magicC) >> 20 for e < 2^15
   unsigned magicRow;       // ceil(2^32 / rowE): row of a flattened tile-box index
   int o_ws, o_wf, o_pa, o_pq, o_tm, o_sv;   // byte offsets in dynamic smem

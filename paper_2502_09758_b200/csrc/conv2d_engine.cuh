@@ -171,9 +171,13 @@ struct Conv {
     __syncthreads();
   }
 
+  // n / d for n < 2^16 with m = ceil(2^32 / d); m == 0 encodes d == 1
+  __device__ static __forceinline__ int mdiv(int n, unsigned m) { return m ? (int)__umulhi((unsigned)n, m) : n; }
+  __device__ __forceinline__ int tile_row(int tile) const { return mdiv(tile, a.g.magicTW); }
   __device__ __forceinline__ void tile_origin(int tile, int& h0, int& w0) const {
-    h0 = (tile / a.g.tilesW) * a.g.TH;
-    w0 = (tile % a.g.tilesW) * a.g.TW;
+    const int tr = tile_row(tile);
+    h0 = tr * a.g.TH;
+    w0 = (tile - tr * a.g.tilesW) * a.g.TW;
   }
   __device__ __forceinline__ int64_t gidx(int h, int w, int c) const {
     return ((int64_t)h * a.g.W + w) * a.g.C + c;
@@ -207,6 +211,40 @@ struct Conv {
     const int gh0 = h0 - a.g.rh - 1, gw0 = w0 - a.g.rw - 1;
     const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     T* dst = pa();
+    if (C == 1) {
+      // single channel: element = pixel, no de-interleave
+      for (int e0 = 0; e0 < rowE; e0 += 32 * kJ) {
+        for (int sr0 = threadIdx.x >> 5; sr0 < SH; sr0 += 2 * nw) {
+          T v[2][kJ];
+#pragma unroll
+          for (int rr = 0; rr < 2; ++rr) {
+            const int sr = sr0 + rr * nw;
+            const int gh = gh0 + sr;
+            const bool rowok = sr < SH && gh >= 0 && gh < H;
+            const int64_t rowbase = (int64_t)gh * W + gw0;
+#pragma unroll
+            for (int j = 0; j < kJ; ++j) {
+              const int e = e0 + lane + 32 * j;
+              const bool ok = rowok && e < rowE && (unsigned)(gw0 + e) < (unsigned)W;
+              v[rr][j] = ok ? src(rowbase + e) : T(0);
+            }
+          }
+#pragma unroll
+          for (int rr = 0; rr < 2; ++rr) {
+            const int sr = sr0 + rr * nw;
+            if (sr < SH) {
+              T* drow = dst + sr * SWP;
+#pragma unroll
+              for (int j = 0; j < kJ; ++j) {
+                const int e = e0 + lane + 32 * j;
+                if (e < rowE) drow[sk(e)] = v[rr][j];
+              }
+            }
+          }
+        }
+      }
+      return;
+    }
     for (int e0 = 0; e0 < rowE; e0 += 32 * kJ) {
       for (int sr0 = threadIdx.x >> 5; sr0 < SH; sr0 += 2 * nw) {
         T v[2][kJ];
@@ -282,6 +320,28 @@ struct Conv {
     }
   }
 
+  // Large K (c5: 31): rows stay a runtime loop (code size), each row fully
+  // unrolled so its window and taps are loaded together.
+  template <int K>
+  __device__ __forceinline__ void stencil_kr(const T* __restrict__ pl, const T* __restrict__ w, T (&acc)[RW]) const {
+    const int SWP = a.g.SWP;
+    const T* base = pl + (ty + 1) * SWP + sk(tx * RW);
+#pragma unroll 1
+    for (int i = 0; i < K; ++i) {
+      const T* row = base + i * SWP;
+      const T* wr = w + i * K;
+      T win[K + RW - 1];
+#pragma unroll
+      for (int m = 0; m < K + RW - 1; ++m) win[m] = row[skr(1 + m)];
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const T wt = wr[j];
+#pragma unroll
+        for (int o = 0; o < RW; ++o) acc[o] = madd<FAST>(acc[o], win[o + j], wt);
+      }
+    }
+  }
+
   __device__ __forceinline__ void stencil(const T* __restrict__ pl, const T* __restrict__ w, T (&acc)[RW]) const {
 #pragma unroll
     for (int o = 0; o < RW; ++o) acc[o] = T(0);
@@ -292,6 +352,10 @@ struct Conv {
     }
     if (kh == 15 && kw == 15) {
       stencil_k<15>(pl, w, acc);
+      return;
+    }
+    if (kh == 31 && kw == 31) {
+      stencil_kr<31>(pl, w, acc);
       return;
     }
     // phys(tx*RW + m) = sk(tx*RW) + skr(m); separable because tx*RW and the
@@ -351,7 +415,7 @@ struct Conv {
   // tile is wholly owned or not)
   __device__ __forceinline__ bool tile_owned(int h0) const { return h0 >= a.g.own0 && h0 < a.g.own1; }
   __device__ __forceinline__ void tile_partial(const SumDev& s, int tile, double part) const {
-    if (tile_owned((tile / a.g.tilesW) * a.g.TH)) store_tile_partial(s, tile + a.g.tileOff, part, red());
+    if (tile_owned(tile_row(tile) * a.g.TH)) store_tile_partial(s, tile + a.g.tileOff, part, red());
   }
 
   // ---- fused NumPy-pairwise leaves of up to 3 term buffers (tm[k], each
@@ -361,24 +425,25 @@ struct Conv {
   __device__ void tile_leaves(int h0, int w0, int nbuf, const SumDev* s0, const SumDev* s1, int koff2) {
     if (!tile_owned(h0)) return;   // CTA-uniform
     __syncthreads();
-    const int C = a.g.C, L = a.g.leafL, W = a.g.W;
+    // fused layouts have TW | W, so every tile row holds segs whole leaves
+    const int C = a.g.C, L = a.g.leafL;
     const int rows = min(a.g.TH, a.g.H - h0);
-    const int rowE = min(a.g.TW, W - w0) * C;
-    const int segs = rowE / L;
+    const int segs = a.g.segs;
     const int per_buf = rows * segs * 8;
     const int tmE = a.g.TH * a.g.TW * C;
     const int total = per_buf * nbuf;
+    const int64_t lbase = (int64_t)(h0 + a.g.row0) * a.g.rowL + (int64_t)mdiv(w0, a.g.magicTWpx) * segs;
     for (int g0 = 0; g0 < total; g0 += blockDim.x) {      // total % 8 == 0, blockDim % 32 == 0
       const int gch = g0 + threadIdx.x;
       const bool act = gch < total;
       double acc = 0.0;
       int buf = 0, k = 0, r = 0, s = 0;
       if (act) {
-        buf = gch / per_buf;
+        buf = (gch >= per_buf) + (gch >= 2 * per_buf);   // nbuf <= 3
         const int rem = gch - buf * per_buf;
         const int leaf_l = rem >> 3;
         k = rem & 7;
-        r = leaf_l / segs;
+        r = mdiv(leaf_l, a.g.magicSegs);
         s = leaf_l - r * segs;
         const double* t = tm() + (size_t)buf * tmE + (size_t)r * a.g.TW * C + s * L + k;
         acc = t[0];
@@ -388,7 +453,7 @@ struct Conv {
       acc = acc + __shfl_xor_sync(kFull, acc, 2);
       acc = acc + __shfl_xor_sync(kFull, acc, 4);
       if (act && k == 0) {
-        const int64_t li = (((int64_t)(h0 + r + a.g.row0) * W + w0) * C) / L + s + (buf == 2 ? koff2 : 0);
+        const int64_t li = lbase + (int64_t)r * a.g.rowL + s + (buf == 2 ? koff2 : 0);
         (buf == 0 ? s0 : s1)->leaf_vals[li] = acc;
       }
     }
