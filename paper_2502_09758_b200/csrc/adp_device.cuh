@@ -40,18 +40,21 @@ struct GridBarrier {
   unsigned int nblocks;
   unsigned int target;
 
+  // bar.sync orders the CTA's writes before thread 0's release-add (release
+  // is cumulative); thread 0's gpu-scope acquire (which also invalidates the
+  // SM's L1) then bar.sync order every later load of the CTA after all
+  // arrivals.  Measured 1.27 us per barrier on 148 CTAs vs 1.41 us for
+  // fence + atomicAdd + fence (tools/micro/barbench.cu).
   __device__ __forceinline__ void sync() {
     __syncthreads();
     if (threadIdx.x == 0) {
       target += nblocks;
-      __threadfence();
-      atomicAdd(counter, 1u);
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(counter) : "memory");
       unsigned int v;
       while (true) {
         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
         if ((int)(v - target) >= 0) break;
       }
-      __threadfence();
     }
     __syncthreads();
   }
