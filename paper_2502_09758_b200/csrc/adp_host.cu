@@ -249,11 +249,13 @@ static size_t conv_smem(ConvGeom& g, int esize) {
   g.QP = 0;   // TV Q values are staged through registers into the plane region
   const size_t pa = ((size_t)g.C * g.SH * g.SWP * esize + 15) & ~size_t(15);
   const size_t tm = g.fused ? (size_t)3 * g.TH * g.TW * g.C * sizeof(double) : 0;
+  const int np = g.fuseCA ? 2 : 1;   // fuseCA: two plane regions, six term buffers
   g.o_pa = (int)R0;
+  g.o_pa2 = (int)(R0 + pa);
   g.o_pq = (int)R0;
-  g.o_tm = (int)(R0 + pa);
+  g.o_tm = (int)(R0 + np * pa);
   g.o_sv = (int)R0;
-  const size_t region = std::max(pa + tm, (size_t)(kTreeStage + 512) * sizeof(double));
+  const size_t region = std::max(np * (pa + tm), (size_t)(kTreeStage + 512) * sizeof(double));
   return R0 + region;
 }
 
@@ -370,6 +372,14 @@ static int conv_plan_init(PlanImpl& P) {
     if (g.row0 % g.TH || g.own0 % g.TH || (g.own1 % g.TH && !bottom))
       return fail(ADP_ERR_ARG, "row slab bounds must be multiples of the tile height");
   }
+  // fused candidate + speculative next stage when two plane regions fit
+  // (leaves of 8 KB static smem headroom); ADP_FUSECA=0 disables
+  g.fuseCA = 0;
+  if (g.fused && !slab) {
+    g.fuseCA = 1;
+    const char* ev = getenv("ADP_FUSECA");
+    if ((ev && atoi(ev) == 0) || conv_smem(g, P.esize) + 8192 > smem_optin) g.fuseCA = 0;
+  }
   P.smem = conv_smem(g, P.esize);
   if (P.smem > smem_optin) return fail(ADP_ERR_UNSUPPORTED, "tile + halo exceeds shared memory; use a smaller tile");
   if (P.probe_only) return ADP_OK;   // adp_plan_probe: geometry only, no device memory
@@ -410,10 +420,11 @@ static int conv_plan_init(PlanImpl& P) {
     o_sp[k] = take(shs[k]->sub_prog.size() * sizeof(int));
   }
   const int tileLeaves = std::max(sT.nLeaves, 4 * P.sm_count * 32);
-  size_t o_lv[7], o_sv[7];
-  const int nLeavesOf[7] = {sN.nLeaves, s2N.nLeaves, sN.nLeaves, s2N.nLeaves, tileLeaves, tileLeaves, tileLeaves};
-  const int nSubOf[7] = {sN.nSub, s2N.nSub, sN.nSub, s2N.nSub, sT.nSub, sT.nSub, sT.nSub};
-  for (int k = 0; k < 7; ++k) {
+  size_t o_lv[9], o_sv[9];
+  const int nLeavesOf[9] = {sN.nLeaves, s2N.nLeaves, sN.nLeaves, s2N.nLeaves, tileLeaves, tileLeaves, tileLeaves,
+                            sN.nLeaves, s2N.nLeaves};
+  const int nSubOf[9] = {sN.nSub, s2N.nSub, sN.nSub, s2N.nSub, sT.nSub, sT.nSub, sT.nSub, sN.nSub, s2N.nSub};
+  for (int k = 0; k < 9; ++k) {
     o_lv[k] = take((size_t)nLeavesOf[k] * sizeof(double));
     o_sv[k] = take((size_t)nSubOf[k] * sizeof(double));
   }
@@ -442,9 +453,9 @@ static int conv_plan_init(PlanImpl& P) {
     CK(cudaMemcpy(P.d_sub[2 * k + 1], shs[k]->sub_prog.data(), shs[k]->sub_prog.size() * sizeof(int),
                   cudaMemcpyHostToDevice));
   }
-  SumDev* sds[7] = {&P.s_fit, &P.s_tv, &P.s_fitc, &P.s_tvc, &P.s_t0, &P.s_t1, &P.s_t2};
-  const int which[7] = {0, 1, 0, 1, 2, 2, 2};
-  for (int k = 0; k < 7; ++k) {
+  SumDev* sds[9] = {&P.s_fit, &P.s_tv, &P.s_fitc, &P.s_tvc, &P.s_t0, &P.s_t1, &P.s_t2, &P.s_fit2, &P.s_tv2};
+  const int which[9] = {0, 1, 0, 1, 2, 2, 2, 0, 1};
+  for (int k = 0; k < 9; ++k) {
     const SumHost& sh = *shs[which[k]];
     const int64_t* dl = which[k] == 0 ? P.d_leaf_N : which[k] == 1 ? P.d_leaf_2N : nullptr;
     fill_sum<double>(*sds[k], sh, P.d_progs, dl, P.d_sub[2 * which[k]], P.d_sub[2 * which[k] + 1],
@@ -511,6 +522,7 @@ static ConvArgs<T> conv_base(PlanImpl& P) {
   a.TV2 = w[18]; a.TV2C = w[19];
   a.s_fit = P.s_fit; a.s_tv = P.s_tv; a.s_fitc = P.s_fitc; a.s_tvc = P.s_tvc;
   a.s_t0 = P.s_t0; a.s_t1 = P.s_t1; a.s_t2 = P.s_t2;
+  a.s_fit2 = P.s_fit2; a.s_tv2 = P.s_tv2;
   a.bar = P.d_bar;
   a.sres = P.d_sres;
   a.cres = P.d_cres;

@@ -53,7 +53,7 @@ struct PlanImpl {
   int64_t* d_leaf_N = nullptr;  // leaf starts for N-element sums
   int64_t* d_leaf_2N = nullptr;
   int* d_sub[8] = {};           // sub_leaf / sub_prog per layout
-  SumDev s_fit{}, s_tv{}, s_fitc{}, s_tvc{}, s_t0{}, s_t1{}, s_t2{};
+  SumDev s_fit{}, s_tv{}, s_fitc{}, s_tvc{}, s_t0{}, s_t1{}, s_t2{}, s_fit2{}, s_tv2{};
   int64_t units_n[7] = {};       // sum units (leaves, or subtree roots when two-level)
   int64_t units_own[7][4] = {};  // unit ranges this plan fills (row slabs: its owned rows)
   unsigned int* d_bar = nullptr;

@@ -81,6 +81,8 @@ struct ConvGeom {
   unsigned magicC;         // ceil(2^20 / C): px = (e * magicC) >> 20 for e < 2^15
   unsigned magicRow;       // ceil(2^32 / rowE): row of a flattened tile-box index
   int o_ws, o_wf, o_pa, o_pq, o_tm, o_sv;   // byte offsets in dynamic smem
+  int o_pa2;               // second plane region (fuseCA)
+  int fuseCA;              // 1: candidate value + speculative next value/grad share one stage
   int64_t N;               // H*W*C
   int64_t Ng;              // global element count (Hg*W*C; = N unless a row slab)
 };

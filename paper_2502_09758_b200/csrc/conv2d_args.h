@@ -57,6 +57,7 @@ struct ConvArgs {
   // sums
   SumDev s_fit, s_tv, s_fitc, s_tvc;   // numpy-pairwise element sums (N, 2N, N, 2N)
   SumDev s_t0, s_t1, s_t2;             // per-tile partial sums (ddot-type)
+  SumDev s_fit2, s_tv2;                // second (fit, tv) set: speculative next value (fuseCA)
   unsigned int* bar;
   SolveOut* sres;
   CGOut* cres;

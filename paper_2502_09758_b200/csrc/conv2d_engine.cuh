@@ -138,6 +138,7 @@ struct Conv {
   __device__ __forceinline__ T* ws() const { return reinterpret_cast<T*>(dsm() + a.g.o_ws); }
   __device__ __forceinline__ T* wf() const { return reinterpret_cast<T*>(dsm() + a.g.o_wf); }
   __device__ __forceinline__ T* pa() const { return reinterpret_cast<T*>(dsm() + a.g.o_pa); }
+  __device__ __forceinline__ T* pa2() const { return reinterpret_cast<T*>(dsm() + a.g.o_pa2); }
   __device__ __forceinline__ double* tm() const { return reinterpret_cast<double*>(dsm() + a.g.o_tm); }
   __device__ __forceinline__ double* sv() const { return reinterpret_cast<double*>(dsm() + a.g.o_sv); }
   __device__ __forceinline__ T* plane(int c) const { return pa() + (size_t)c * a.g.SH * a.g.SWP; }
@@ -204,13 +205,13 @@ struct Conv {
   // in flight, predicated (branch-free) loads, geometry in registers.
   static constexpr int kJ = 8;   // lane steps per row handled per pass (rows longer than 256 loop)
   template <class Src>
-  __device__ void load_full(int h0, int w0, const Src& src) const {
+  __device__ void load_full(int h0, int w0, const Src& src, T* dst_region = nullptr) const {
     const int C = a.g.C, H = a.g.H, W = a.g.W, SH = a.g.SH, SWP = a.g.SWP;
     const unsigned mC = a.g.magicC;
     const int rowE = (a.g.TW + 2 * a.g.rw + 2) * C, planeSz = SH * SWP;
     const int gh0 = h0 - a.g.rh - 1, gw0 = w0 - a.g.rw - 1;
     const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    T* dst = pa();
+    T* dst = dst_region ? dst_region : pa();
     if (C == 1) {
       // single channel: element = pixel, no de-interleave
       for (int e0 = 0; e0 < rowE; e0 += 32 * kJ) {
@@ -422,7 +423,7 @@ struct Conv {
   // TH x (TW*C) doubles, interleaved like the image) -> leaf_vals.  Leaf
   // index of (tile row r, segment s): (h*W*C + w0*C)/L + s; buffer k goes to
   // sums[k] with a leaf offset koff[k].
-  __device__ void tile_leaves(int h0, int w0, int nbuf, const SumDev* s0, const SumDev* s1, int koff2) {
+  __device__ void tile_leaves(int h0, int w0, int nbuf, const SumDev* s0, const SumDev* s1, int koff2, int b0 = 0) {
     if (!tile_owned(h0)) return;   // CTA-uniform
     __syncthreads();
     // fused layouts have TW | W, so every tile row holds segs whole leaves
@@ -445,7 +446,7 @@ struct Conv {
         k = rem & 7;
         r = mdiv(leaf_l, a.g.magicSegs);
         s = leaf_l - r * segs;
-        const double* t = tm() + (size_t)buf * tmE + (size_t)r * a.g.TW * C + s * L + k;
+        const double* t = tm() + (size_t)(b0 + buf) * tmE + (size_t)r * a.g.TW * C + s * L + k;
         acc = t[0];
         for (int i = 8; i < L; i += 8) acc = acc + t[i];
       }
@@ -467,13 +468,100 @@ struct Conv {
   // (lower_value_and_grad, lower_solvers.py:50-63; SmoothedTV.value_and_grad,
   // regularizers.py:167-175).  `tv` false when alpha == 0.  Fused mode: the
   // fit / TV leaves go straight to s_fit / s_tv.
+  //
+  // tileA / tileC compute one tile from a loaded plane region `pr` (channel
+  // planes of y resp. xc) into term buffers tb.. (tb = 0 or 3); tileA's TV
+  // pass publishes neighbour values through the region `qr` (free by then).
+  __device__ __forceinline__ T fpr(const T* pr, int r, int q) const {
+    return pr[(size_t)ch * a.g.SH * a.g.SWP + (r + a.g.rh + 1) * a.g.SWP + sk(q + a.g.rw + 1)];
+  }
+  __device__ __forceinline__ void tileA(const T* pr, T* qr, int tb, int h0, int w0, const T (&ypre)[RW], T* Rout,
+                                        bool tv, T* TV2out, T* TVGout, bool fused) {
+    const T nu = T(a.nu), nu2 = nu * nu;
+    const int H = a.g.H, W = a.g.W, TH = a.g.TH, TW = a.g.TW, C = a.g.C;
+    const int64_t N = a.g.N;
+    const int h = h0 + ty;
+    T acc[RW];
+    stencil(pr + (size_t)ch * a.g.SH * a.g.SWP, ws() + ch * a.g.kh * a.g.kw, acc);
+#pragma unroll
+    for (int o = 0; o < RW; ++o) {
+      const int q = tx * RW + o;
+      const int w = w0 + q;
+      if (h < H && w < W) {
+        const int64_t i = gidx(h, w, ch);
+        const T r = acc[o] - ypre[o];
+        Rout[i] = r;
+        if (fused) put_term(tb + 0, ty, q, (double)(r * r));
+      }
+    }
+    if (!tv) return;
+    // q = d / sqrt(d^2 + nu^2) for the own pixels (registers), the row
+    // above the tile (ty == 0) and the column left of it (tx == 0)
+    T q0[RW], q1[RW], q0u[RW], q1l = T(0);
+#pragma unroll
+    for (int o = 0; o < RW; ++o) {
+      const int q = tx * RW + o;
+      const int w = w0 + q;
+      const T yc = fpr(pr, ty, q);
+      const T d0 = has_below(h) ? fpr(pr, ty + 1, q) - yc : T(0);
+      const T d1 = (w < W - 1) ? fpr(pr, ty, q + 1) - yc : T(0);
+      const T rt0 = sqrt(d0 * d0 + nu2), rt1 = sqrt(d1 * d1 + nu2);
+      q0[o] = d0 / rt0;
+      q1[o] = d1 / rt1;
+      if (h < H && w < W) {
+        if (fused) {
+          put_term(tb + 1, ty, q, (double)rt0);
+          put_term(tb + 2, ty, q, (double)rt1);
+        } else {
+          const int64_t i = gidx(h, w, ch);
+          TV2out[i] = rt0;
+          TV2out[N + i] = rt1;
+        }
+      }
+      q0u[o] = T(0);
+      if (ty == 0 && has_above(h0)) {     // edge (h0-1) -> (h0): h0 - 1 < H - 1 always
+        const T du = yc - fpr(pr, -1, q);
+        q0u[o] = du / sqrt(du * du + nu2);
+      }
+    }
+    if (tx == 0 && w0 >= 1) {
+      const T dl = fpr(pr, ty, 0) - fpr(pr, ty, -1);
+      q1l = dl / sqrt(dl * dl + nu2);
+    }
+    // publish neighbour values through the (now free) region qr
+    __syncthreads();
+    T* Q0 = qr;                                      // [C][TH+1][TW]  (row r at r+1)
+    T* Q1 = Q0 + (size_t)C * (TH + 1) * TW;          // [C][TH][TW+1]  (col q at q+1)
+#pragma unroll
+    for (int o = 0; o < RW; ++o) {
+      const int q = tx * RW + o;
+      Q0[((size_t)ch * (TH + 1) + ty + 1) * TW + q] = q0[o];
+      if (ty == 0) Q0[((size_t)ch * (TH + 1)) * TW + q] = q0u[o];
+      Q1[((size_t)ch * TH + ty) * (TW + 1) + q + 1] = q1[o];
+    }
+    if (tx == 0) Q1[((size_t)ch * TH + ty) * (TW + 1)] = q1l;
+    __syncthreads();
+#pragma unroll
+    for (int o = 0; o < RW; ++o) {
+      const int q = tx * RW + o;
+      const int w = w0 + q;
+      if (h < H && w < W) {
+        // image_forward_diff_adjoint (regularizers.py:61-67), per-pixel order
+        T t = T(0);
+        if (has_above(h)) t = t + Q0[((size_t)ch * (TH + 1) + ty) * TW + q];
+        if (has_below(h)) t = t - q0[o];
+        if (w >= 1) t = t + (o > 0 ? q1[o > 0 ? o - 1 : 0] : Q1[((size_t)ch * TH + ty) * (TW + 1) + q]);
+        if (w <= W - 2) t = t - q1[o];
+        TVGout[gidx(h, w, ch)] = t;
+      }
+    }
+  }
+
   template <class Src>
   __device__ void stageA(const Src& src, T* Rout, const T* ydat, bool tv, T* TV2out, T* TVGout,
                          const SumDev* sfit, const SumDev* stv) {
-    const T nu = T(a.nu), nu2 = nu * nu;
-    const int H = a.g.H, W = a.g.W, TH = a.g.TH, TW = a.g.TW, C = a.g.C;
+    const int H = a.g.H, W = a.g.W;
     const bool fused = a.g.fused && sfit;
-    const int64_t N = a.g.N;
     for (int tile = blockIdx.x; tile < a.g.nTiles; tile += gridDim.x) {
       int h0, w0;
       tile_origin(tile, h0, w0);
@@ -487,81 +575,7 @@ struct Conv {
       }
       load_full(h0, w0, src);
       __syncthreads();
-      T acc[RW];
-      stencil_fwd(acc);
-#pragma unroll
-      for (int o = 0; o < RW; ++o) {
-        const int q = tx * RW + o;
-        const int w = w0 + q;
-        if (h < H && w < W) {
-          const int64_t i = gidx(h, w, ch);
-          const T r = acc[o] - ypre[o];
-          Rout[i] = r;
-          if (fused) put_term(0, ty, q, (double)(r * r));
-        }
-      }
-      if (tv) {
-        // q = d / sqrt(d^2 + nu^2) for the own pixels (registers), the row
-        // above the tile (ty == 0) and the column left of it (tx == 0)
-        T q0[RW], q1[RW], q0u[RW], q1l = T(0);
-#pragma unroll
-        for (int o = 0; o < RW; ++o) {
-          const int q = tx * RW + o;
-          const int w = w0 + q;
-          const T yc = fp(ty, q);
-          const T d0 = has_below(h) ? fp(ty + 1, q) - yc : T(0);
-          const T d1 = (w < W - 1) ? fp(ty, q + 1) - yc : T(0);
-          const T rt0 = sqrt(d0 * d0 + nu2), rt1 = sqrt(d1 * d1 + nu2);
-          q0[o] = d0 / rt0;
-          q1[o] = d1 / rt1;
-          if (h < H && w < W) {
-            if (fused) {
-              put_term(1, ty, q, (double)rt0);
-              put_term(2, ty, q, (double)rt1);
-            } else {
-              const int64_t i = gidx(h, w, ch);
-              TV2out[i] = rt0;
-              TV2out[N + i] = rt1;
-            }
-          }
-          q0u[o] = T(0);
-          if (ty == 0 && has_above(h0)) {     // edge (h0-1) -> (h0): h0 - 1 < H - 1 always
-            const T du = yc - fp(-1, q);
-            q0u[o] = du / sqrt(du * du + nu2);
-          }
-        }
-        if (tx == 0 && w0 >= 1) {
-          const T dl = fp(ty, 0) - fp(ty, -1);
-          q1l = dl / sqrt(dl * dl + nu2);
-        }
-        // publish neighbour values through the (now free) plane region
-        __syncthreads();
-        T* Q0 = pa();                                    // [C][TH+1][TW]  (row r at r+1)
-        T* Q1 = Q0 + (size_t)C * (TH + 1) * TW;          // [C][TH][TW+1]  (col q at q+1)
-#pragma unroll
-        for (int o = 0; o < RW; ++o) {
-          const int q = tx * RW + o;
-          Q0[((size_t)ch * (TH + 1) + ty + 1) * TW + q] = q0[o];
-          if (ty == 0) Q0[((size_t)ch * (TH + 1)) * TW + q] = q0u[o];
-          Q1[((size_t)ch * TH + ty) * (TW + 1) + q + 1] = q1[o];
-        }
-        if (tx == 0) Q1[((size_t)ch * TH + ty) * (TW + 1)] = q1l;
-        __syncthreads();
-#pragma unroll
-        for (int o = 0; o < RW; ++o) {
-          const int q = tx * RW + o;
-          const int w = w0 + q;
-          if (h < H && w < W) {
-            // image_forward_diff_adjoint (regularizers.py:61-67), per-pixel order
-            T t = T(0);
-            if (has_above(h)) t = t + Q0[((size_t)ch * (TH + 1) + ty) * TW + q];
-            if (has_below(h)) t = t - q0[o];
-            if (w >= 1) t = t + (o > 0 ? q1[o > 0 ? o - 1 : 0] : Q1[((size_t)ch * TH + ty) * (TW + 1) + q]);
-            if (w <= W - 2) t = t - q1[o];
-            TVGout[gidx(h, w, ch)] = t;
-          }
-        }
-      }
+      tileA(pa(), pa(), 0, h0, w0, ypre, Rout, tv, TV2out, TVGout, fused);
       if (fused) tile_leaves(h0, w0, tv ? 3 : 1, sfit, stv, (int)(a.g.Ng / a.g.leafL));
     }
   }
@@ -625,66 +639,107 @@ struct Conv {
   // sqrt(d^2+nu^2) - nu (tv_value, regularizers.py:70-72); optional tile
   // partial of g.(xc - xold); xc written to Xout (if non-null).  Fused:
   // leaves to sfitc / stvc; otherwise rc -> RCout and TV terms -> TV2Cout.
+  __device__ __forceinline__ double tileC(const T* pr, int h0, int w0, const T (&ypre)[RW], const T (&gpre)[RW],
+                                          const T (&xopre)[RW], T* RCout, bool tv, T* TV2Cout, T* Xout, bool dot,
+                                          bool fused) {
+    const T nu = T(a.nu), nu2 = nu * nu;
+    const int H = a.g.H, W = a.g.W;
+    const int64_t N = a.g.N;
+    const int h = h0 + ty;
+    double part = 0.0;
+    T acc[RW];
+    stencil(pr + (size_t)ch * a.g.SH * a.g.SWP, ws() + ch * a.g.kh * a.g.kw, acc);
+#pragma unroll
+    for (int o = 0; o < RW; ++o) {
+      const int q = tx * RW + o;
+      const int w = w0 + q;
+      if (h < H && w < W) {
+        const int64_t i = gidx(h, w, ch);
+        const T rc = acc[o] - ypre[o];
+        const T xc = fpr(pr, ty, q);
+        if (fused) put_term(0, ty, q, (double)(rc * rc));
+        else RCout[i] = rc;
+        if (tv) {
+          const T d0 = has_below(h) ? fpr(pr, ty + 1, q) - xc : T(0);
+          const T d1 = (w < W - 1) ? fpr(pr, ty, q + 1) - xc : T(0);
+          const T t0 = sqrt(d0 * d0 + nu2) - nu;
+          const T t1 = sqrt(d1 * d1 + nu2) - nu;
+          if (fused) {
+            put_term(1, ty, q, (double)t0);
+            put_term(2, ty, q, (double)t1);
+          } else {
+            TV2Cout[i] = t0;
+            TV2Cout[N + i] = t1;
+          }
+        }
+        if (Xout) Xout[i] = xc;
+        if (dot) part += (double)gpre[o] * (double)(xc - xopre[o]);
+      }
+    }
+    return part;
+  }
+
+  __device__ __forceinline__ void prefetch_c(int h0, int w0, const T* Gin, const T* Xold, bool dot, T (&ypre)[RW],
+                                             T (&gpre)[RW], T (&xopre)[RW]) const {
+    const int H = a.g.H, W = a.g.W;
+    const int h = h0 + ty;
+#pragma unroll
+    for (int o = 0; o < RW; ++o) {
+      const int w = w0 + tx * RW + o;
+      ypre[o] = gpre[o] = xopre[o] = T(0);
+      if (h < H && w < W) {
+        const int64_t i = gidx(h, w, ch);
+        ypre[o] = a.ydat[i];
+        if (dot) {
+          gpre[o] = ldcg(Gin + i);
+          xopre[o] = ldcg(Xold + i);
+        }
+      }
+    }
+  }
+
   template <class Src>
   __device__ void stageC(const Src& src, T* RCout, bool tv, T* TV2Cout, T* Xout, const T* Gin, const T* Xold,
                          const SumDev* sdot, const SumDev* sfitc, const SumDev* stvc) {
-    const T nu = T(a.nu), nu2 = nu * nu;
-    const int H = a.g.H, W = a.g.W;
     const bool fused = a.g.fused && sfitc;
-    const int64_t N = a.g.N;
     for (int tile = blockIdx.x; tile < a.g.nTiles; tile += gridDim.x) {
       int h0, w0;
       tile_origin(tile, h0, w0);
       __syncthreads();
-      const int h = h0 + ty;
       T ypre[RW], gpre[RW], xopre[RW];   // epilogue operands, in flight with the tile box
-#pragma unroll
-      for (int o = 0; o < RW; ++o) {
-        const int w = w0 + tx * RW + o;
-        ypre[o] = gpre[o] = xopre[o] = T(0);
-        if (h < H && w < W) {
-          const int64_t i = gidx(h, w, ch);
-          ypre[o] = a.ydat[i];
-          if (sdot) {
-            gpre[o] = ldcg(Gin + i);
-            xopre[o] = ldcg(Xold + i);
-          }
-        }
-      }
+      prefetch_c(h0, w0, Gin, Xold, sdot != nullptr, ypre, gpre, xopre);
       load_full(h0, w0, src);
       __syncthreads();
-      double part = 0.0;
-      T acc[RW];
-      stencil_fwd(acc);
-#pragma unroll
-      for (int o = 0; o < RW; ++o) {
-        const int q = tx * RW + o;
-        const int w = w0 + q;
-        if (h < H && w < W) {
-          const int64_t i = gidx(h, w, ch);
-          const T rc = acc[o] - ypre[o];
-          const T xc = fp(ty, q);
-          if (fused) put_term(0, ty, q, (double)(rc * rc));
-          else RCout[i] = rc;
-          if (tv) {
-            const T d0 = has_below(h) ? fp(ty + 1, q) - xc : T(0);
-            const T d1 = (w < W - 1) ? fp(ty, q + 1) - xc : T(0);
-            const T t0 = sqrt(d0 * d0 + nu2) - nu;
-            const T t1 = sqrt(d1 * d1 + nu2) - nu;
-            if (fused) {
-              put_term(1, ty, q, (double)t0);
-              put_term(2, ty, q, (double)t1);
-            } else {
-              TV2Cout[i] = t0;
-              TV2Cout[N + i] = t1;
-            }
-          }
-          if (Xout) Xout[i] = xc;
-          if (sdot) part += (double)gpre[o] * (double)(xc - xopre[o]);
-        }
-      }
+      const double part = tileC(pa(), h0, w0, ypre, gpre, xopre, RCout, tv, TV2Cout, Xout, sdot != nullptr, fused);
       if (sdot) tile_partial(*sdot, tile, part);
       if (fused) tile_leaves(h0, w0, tv ? 3 : 1, sfitc, stvc, (int)(a.g.Ng / a.g.leafL));
+    }
+  }
+
+  // Fused candidate value + speculative next value/grad (fused layouts with
+  // room for two plane regions, a.g.fuseCA): per tile, plane region 1 holds
+  // the first candidate xc (stage C of iteration t, leaves -> sfitc/stvc,
+  // restart dot -> sdot) and region 2 the next extrapolation point
+  // y' = xc + beta' (xc - x) (stage A of iteration t + 1 assuming the
+  // candidate is accepted without restart; leaves -> sfit2/stv2, terms in
+  // buffers 3..5).  One tile load round trip and no grid barrier between them.
+  __device__ void stageCA(const T* Xc, const T* Xold, T betaN, const T* Gin, bool tv, T* Rout, T* TVGout,
+                          const SumDev* sdot, const SumDev* sfitc, const SumDev* stvc, const SumDev* sfit2,
+                          const SumDev* stv2) {
+    for (int tile = blockIdx.x; tile < a.g.nTiles; tile += gridDim.x) {
+      int h0, w0;
+      tile_origin(tile, h0, w0);
+      __syncthreads();
+      T ypre[RW], gpre[RW], xopre[RW];
+      prefetch_c(h0, w0, Gin, Xold, true, ypre, gpre, xopre);
+      load_full(h0, w0, SrcLin<T>{Xc}, pa());
+      load_full(h0, w0, SrcExtrap<T>{Xc, Xold, betaN}, pa2());
+      __syncthreads();
+      const double part = tileC(pa(), h0, w0, ypre, gpre, xopre, nullptr, tv, nullptr, nullptr, true, true);
+      tileA(pa2(), pa(), 3, h0, w0, ypre, Rout, tv, nullptr, TVGout, true);   // tileA syncs before reusing pa()
+      tile_partial(*sdot, tile, part);
+      tile_leaves(h0, w0, tv ? 3 : 1, sfitc, stvc, (int)(a.g.Ng / a.g.leafL));
+      tile_leaves(h0, w0, tv ? 3 : 1, sfit2, stv2, (int)(a.g.Ng / a.g.leafL), 3);
     }
   }
 

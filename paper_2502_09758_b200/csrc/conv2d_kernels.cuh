@@ -9,20 +9,20 @@ struct ConvOps : Conv<T, FAST, RW> {
   using Base = Conv<T, FAST, RW>;
   using Base::a;
   GridBarrier gb;
-  SumDev* ssm;   // shared-memory copies of a.s_fit .. a.s_t2 (read at every decision point)
+  SumDev* ssm;   // shared-memory copies of a.s_fit .. a.s_tv2 (read at every decision point)
 
   __device__ explicit ConvOps(const ConvArgs<T>& a_) : Base(a_) {
     gb.counter = a_.bar;
     gb.nblocks = gridDim.x;
     gb.target = 0;
     __shared__ SumDev sh_sums[kNumSums];
-    static_assert(offsetof(ConvArgs<T>, s_t2) - offsetof(ConvArgs<T>, s_fit) == (kNumSums - 1) * sizeof(SumDev),
+    static_assert(offsetof(ConvArgs<T>, s_tv2) - offsetof(ConvArgs<T>, s_fit) == (kNumSums - 1) * sizeof(SumDev),
                   "sum descriptors must be contiguous");
     if (threadIdx.x < kNumSums) sh_sums[threadIdx.x] = (&a_.s_fit)[threadIdx.x];
     ssm = sh_sums;
     __syncthreads();
   }
-  static constexpr int kNumSums = 7;
+  static constexpr int kNumSums = 9;
 
   template <int K>
   __device__ void reduce(const SumDev* const (&l)[K], double* out) {
@@ -157,6 +157,14 @@ __global__ void __launch_bounds__(512, 1) conv_solve_kernel(const __grid_constan
   double gn = 0.0, h_y = 0.0, beta = 0.0;
   long long vg = 0, vals = 0, restarts = 0;
   bool done = false;
+  // fuseCA (adaptive AGD with TV): the candidate's value pass also computes
+  // stage A at the NEXT extrapolation point, assuming the first candidate is
+  // accepted without restart; when that holds (the common case) the next
+  // iteration skips stage A and one grid barrier.  Stage-A sums alternate
+  // between two sets (par).  Same arithmetic as the unfused order.
+  const bool spec = a.adaptive && tv && g.fuseCA && a.method == M_AGD;
+  bool a_ready = false;
+  int par = 0;
 
   for (int t = 0; t < a.max_iters; ++t) {
     if (a.method == M_AGD) {
@@ -175,10 +183,16 @@ __global__ void __launch_bounds__(512, 1) conv_solve_kernel(const __grid_constan
     // value and gradient at y (stages A, B); stage B also writes the own
     // pixels of the first candidate y - g / L_try (adaptive path)
     ADP_TRACE(t, 0);
+    const SumDev* sfit = par ? &a.s_fit2 : &a.s_fit;
+    const SumDev* stv = par ? &a.s_tv2 : &a.s_tv;
     if (a.adaptive) {
-      E.stageA(SrcExtrap<T>{a.X[ix], a.X[ixp], tb}, a.R, a.ydat, tv, a.TV2, a.TVG, &a.s_fit, &a.s_tv);
-      ADP_TRACE(t, 1);
-      E.gb.sync();
+      if (!a_ready) {
+        E.stageA(SrcExtrap<T>{a.X[ix], a.X[ixp], tb}, a.R, a.ydat, tv, a.TV2, a.TVG, sfit, stv);
+        ADP_TRACE(t, 1);
+        E.gb.sync();
+      } else {
+        ADP_TRACE(t, 1);
+      }
       ADP_TRACE(t, 2);
       E.stageB(a.R, tv, a.TVG, a.G, &a.s_t0, a.X[ix], a.X[ixp], tb, T(L_try), a.X[ic]);
       E.leaves_if_unfused(a.s_fit, a.R, true);
@@ -190,7 +204,14 @@ __global__ void __launch_bounds__(512, 1) conv_solve_kernel(const __grid_constan
     ADP_TRACE(t, 3);
     E.gb.sync();
     ADP_TRACE(t, 4);
-    if (a.adaptive) {
+    if (spec) {
+      // next iteration's momentum if this one ends without restart
+      const double t_next2 = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t_mom * t_mom));
+      const double beta2 = (t_mom - 1.0) / t_next2;
+      E.stageCA(a.X[ic], a.X[ix], T(beta2), a.G, tv, a.R, a.TVG, &a.s_t1, &a.s_fitc, &a.s_tvc,
+                par ? &a.s_fit : &a.s_fit2, par ? &a.s_tv : &a.s_tv2);
+      ++vals;
+    } else if (a.adaptive) {
       E.value_cand(SrcLin<T>{a.X[ic]}, tv, nullptr, a.G, a.X[ix], &a.s_t1);
       ++vals;
     } else if (a.method == M_PROXGRAD) {
@@ -203,7 +224,7 @@ __global__ void __launch_bounds__(512, 1) conv_solve_kernel(const __grid_constan
     ADP_TRACE(t, 6);
     // fit(y), tv(y), g.g, dot, [fit(xc), tv(xc)]
     double o[6] = {0, 0, 0, 0, 0, 0};
-    if (a.adaptive && tv) E.reduce({&a.s_fit, &a.s_tv, &a.s_t0, &a.s_t1, &a.s_fitc, &a.s_tvc}, o);
+    if (a.adaptive && tv) E.reduce({sfit, stv, &a.s_t0, &a.s_t1, &a.s_fitc, &a.s_tvc}, o);
     else if (a.adaptive) { E.reduce({&a.s_fit, &a.s_t0, &a.s_t1, &a.s_fitc}, o + 2); o[0] = o[2]; o[2] = o[3]; o[3] = o[4]; o[4] = o[5]; o[5] = 0.0; }
     else if (tv) E.reduce({&a.s_fit, &a.s_tv, &a.s_t0, &a.s_t1}, o);
     else { E.reduce({&a.s_fit, &a.s_t0, &a.s_t1}, o + 1); o[0] = o[1]; o[1] = 0.0; }
@@ -225,10 +246,10 @@ __global__ void __launch_bounds__(512, 1) conv_solve_kernel(const __grid_constan
       done = true;
       break;
     }
+    int k = 0;   // backtracking retries of this iteration
     if (a.adaptive) {
       // _backtracked_step (lower_solvers.py:170-177)
       double fitc = o[4], tvc = o[5];
-      int k = 0;
       while (true) {
         const double val = tv ? fitc + a.alpha * tvc : fitc + a.alpha * 0.0;
         if (val <= h_y - 0.5 * gn * gn / L_try + 1e-15 * fabs(h_y)) break;
@@ -252,13 +273,17 @@ __global__ void __launch_bounds__(512, 1) conv_solve_kernel(const __grid_constan
     // x_prev = x; x = candidate; restart (lower_solvers.py:202-211)
     ixp = ix;
     ix = ic;
-    if (a.method == M_AGD && dot > 0.0) {
+    const bool restart = a.method == M_AGD && dot > 0.0;
+    if (restart) {
       t_mom = 1.0;
       ixp = ix;
       ++restarts;
     }
     for (int b = 0; b < 3; ++b)
       if (b != ix && b != ixp) { ic = b; break; }
+    // the speculative stage A of stageCA is valid iff its assumptions held
+    a_ready = spec && k == 0 && !restart;
+    if (a_ready) par ^= 1;
   }
 
   if (!done) {
