@@ -273,8 +273,14 @@ def run_native(args):
     bytes_px_it = 48.0 if dtype == "float64" else 24.0
     hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath) and args.size == 256 and args.iters == 1200 and mode == "strict":
+        traffic = json.load(open(tpath))["conv_solve_kernel"]["dram_bytes_per_launch"]
     roof = {"bound": "fp64", "achieved": achieved_tf, "peak": peak, "unit": "TFLOP/s",
-            "frac": achieved_tf / peak, "traffic": None,
+            "frac": achieved_tf / peak, "traffic": traffic,
+            "traffic_note": "DRAM bytes per conv_solve_kernel launch (one step) from the committed ncu capture; "
+                            "the algorithmic bytes are 48 B/px-it = 3.77 GB per step, L2-resident",
             "peak_source": "measured live: DFMA microbenchmark (adp_fp64_peak), 2 flop/DFMA",
             "flop_per_px_it": flop_px_it, "kernel": "conv_solve_kernel",
             "note": ("strict mode issues DMUL+DADD per tap (reference rounding), so its attainable fraction "
