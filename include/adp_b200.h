@@ -175,8 +175,15 @@ int adp_reg_op(adp_plan* p, const adp_lower* reg, int32_t op, const void* x, con
 /* ddot-type inner product with the plan's fixed reduction tree (np.vdot sites) */
 int adp_dot(adp_plan* p, const void* a, const void* b, double* out, void* stream);
 
+/* ---- IFT baseline lower iteration (baselines.py:46-55, prox_grad_iterations) ----
+ * n_iters steps of x = prox_l1(x - step (2 B^T (B x - y) + 2 alpha l2 x), step alpha l1) on a dense1d plan
+ * with an elastic-net lower problem, one persistent launch; x0 -> x_out (device). */
+int adp_prox_grad(adp_plan* p, const adp_lower* lp, const void* x0, void* x_out, int32_t n_iters, double step,
+                  void* stream);
+
 /* ---- plan-free vector primitives (generic cg_solve with a caller-supplied hess_vec) ----
  * op 0: out = x + a*y   1: out = x - a*y   2: out = x*y   3: out = 1/x   4: out = x - y   5: out = x
+ * op 6: out = prox_l1(x, a) = sign(x) * max(|x| - a, 0)   (regularizers.py:22-27)
  * op 10: *red_out = <x, y> (fixed-order tree)   11: *red_out = count(x <= 0) */
 int adp_vec(int32_t op, int64_t n, int32_t dtype, double a, const void* x, const void* y, void* out,
             double* red_out, void* stream);

@@ -13,6 +13,7 @@ reference's own rounding order, bitwise on stencils and np.sum sites),
 """
 
 from ._native import NativeError, get_precision, precision, set_precision
+from .baselines import BaselineConfig, prox_grad_iterations, run_ift
 from .hypergradient import (
     CGResult,
     HypergradResult,
@@ -63,6 +64,7 @@ from .regularizers import (
     SmoothedTV,
     image_forward_diff,
     image_forward_diff_adjoint,
+    prox_l1,
     smoothed_abs_norm,
     tv_value,
 )
@@ -70,14 +72,14 @@ from .regularizers import (
 __version__ = "0.1.0"
 
 __all__ = [
-    "BacktrackingStalled", "CGResult", "ConvOperator", "DENSE1D", "DEPTHWISE2D", "DenseOperator",
+    "BacktrackingStalled", "BaselineConfig", "CGResult", "ConvOperator", "DENSE1D", "DEPTHWISE2D", "DenseOperator",
     "HypergradResult", "Kernel", "L_of_b", "LowerProblem", "LowerSolveResult", "MAIDConfig",
     "NativeError", "NegativeCurvatureError", "RunTrace", "SmoothedElasticNet", "SmoothedTV", "SolveDiverged",
     "UpperProblem", "WarmState", "build_deconv1d", "build_motion2d", "build_semiblind2d", "cg_solve",
     "gaussian_conv_matrix", "get_precision", "image_forward_diff", "image_forward_diff_adjoint",
     "inexact_hypergradient", "kernel_gram_correlation", "lip_upper_x", "lower_grad", "lower_hess_diag",
     "lower_hess_vec", "lower_value", "lower_value_and_grad", "maid_run", "mixed_second_transpose", "mu_of_b",
-    "op_norm_sq", "operator_from_kernel", "piecewise_signal", "precision", "psi", "psi_value",
+    "op_norm_sq", "operator_from_kernel", "piecewise_signal", "precision", "prox_grad_iterations", "prox_l1", "psi", "psi_value", "run_ift",
     "set_precision", "smoothed_abs_norm", "sobolev_grad", "sobolev_value", "solve_lower", "solve_lower_at",
     "tv_value", "upper_fit_grad",
 ]

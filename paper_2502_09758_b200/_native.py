@@ -93,6 +93,7 @@ SIGNATURES = {
     "adp_vec": (_I, [_I, ctypes.c_int64, _I, _D, _P, _P, _P, ctypes.POINTER(_D), _P]),
     "adp_debug_trace": (_I, [_P, _I, _P]),
     "adp_fp64_peak": (_I, [ctypes.POINTER(_D), ctypes.POINTER(_D), _P]),
+    "adp_prox_grad": (_I, [_P, ctypes.POINTER(Lower), _P, _P, _I, _D, _P]),
     "adp_plan_geometry": (_I, [_P, _P]),
     "adp_plan_probe": (_I, [ctypes.POINTER(PlanDesc), _P]),
     "adp_slab_step": (_I, [_P, ctypes.POINTER(Lower), _I, _P, _P, _P, _D, _D, _P]),
@@ -239,11 +240,11 @@ def set_tile(shape_key, tile):
 
 def plan_for(layout, shape, ksize=(0, 0), slot=None) -> Plan:
     """Cached plan per (layout, shape, kernel size, precision, thread/slot)."""
+    tile = _tile_override.get((layout, tuple(int(s) for s in shape), tuple(int(k) for k in ksize)), (0, 0))
     key = (layout, tuple(int(s) for s in shape), tuple(int(k) for k in ksize), _settings["dtype"],
-           _settings["mode"], threading.get_ident() if slot is None else slot)
+           _settings["mode"], threading.get_ident() if slot is None else slot, tuple(tile))
     p = _plans.get(key)
     if p is None:
-        tile = _tile_override.get((layout, tuple(int(s) for s in shape), tuple(int(k) for k in ksize)), (0, 0))
         p = Plan(layout, shape, ksize, _settings["dtype"], _settings["mode"], tile)
         _plans[key] = p
     return p

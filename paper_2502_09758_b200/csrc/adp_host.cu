@@ -624,6 +624,8 @@ int dense_solve(PlanImpl& P, const adp_lower* lp, const void* x0, void* x_out, c
                 adp_solve_result* res, cudaStream_t st);
 int dense_cg(PlanImpl& P, const adp_lower* lp, const void* xt, const void* rhs, void* q, int warm,
              const void* precond, double tol, int max_iters, adp_cg_result* res, cudaStream_t st);
+int dense_prox(PlanImpl& P, const adp_lower* lp, const void* x0, void* x_out, int n_iters, double step,
+               cudaStream_t st);
 void dense_plan_free(PlanImpl& P);
 }  // namespace adp
 
@@ -994,6 +996,16 @@ extern "C" int adp_sum_layout(int64_t n, int32_t np_rule, int64_t* n_leaves, int
   for (size_t i = 0; i < s.sub_prog.size(); ++i) sub_prog[i] = s.sub_prog[i];
   for (size_t i = 0; i < pool.words.size(); ++i) words[i] = pool.words[i];
   return ADP_OK;
+}
+
+extern "C" int adp_prox_grad(adp_plan* p, const adp_lower* lp, const void* x0, void* x_out, int32_t n_iters,
+                             double step, void* stream) {
+  if (!p || !lp || !x0 || !x_out || !lp->kernel || !lp->y) return fail(ADP_ERR_ARG, "null argument");
+  if (n_iters < 0) return fail(ADP_ERR_ARG, "n_iters must be >= 0");
+  PlanImpl& P = p->impl;
+  if (P.d.layout != ADP_LAYOUT_DENSE1D)
+    return fail(ADP_ERR_UNSUPPORTED, "fused prox-gradient: dense1d plans (compose apply/adjoint/adp_vec otherwise)");
+  return dense_prox(P, lp, x0, x_out, n_iters, step, (cudaStream_t)stream);
 }
 
 extern "C" int adp_plan_geometry(const adp_plan* p, int32_t* out) {

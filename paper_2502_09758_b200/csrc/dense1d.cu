@@ -20,7 +20,7 @@ namespace adp {
 
 enum DenseMode : int {
   DM_APPLY = 0, DM_ADJOINT, DM_GRAM, DM_VALUE, DM_VG, DM_GRAD, DM_HV, DM_HDIAG, DM_UPPER, DM_POWER, DM_MIXED,
-  DM_DOT, DM_KGC
+  DM_DOT, DM_KGC, DM_PROX
 };
 
 constexpr int kDenseVecs = 12;
@@ -579,6 +579,35 @@ __global__ void __launch_bounds__(256) dense_misc_kernel(const __grid_constant__
       if (lead && threadIdx.x == 0) a.scal[0] = d;
       break;
     }
+    case DM_PROX: {
+      // prox_grad_iterations (baselines.py:46-55): piters steps of
+      //   x = prox_l1(x - step * (2 B^T (B x - y) + 2 alpha l2 x), step alpha l1)
+      // with the reference's expression order; prox_l1 = sign(u) * max(|u| - thr, 0)
+      // (regularizers.py:22-27, np.sign / np.maximum semantics incl. NaN)
+      T* x = U;
+      load(x, a.in0);
+      const T step = T(a.pstep), thr = T(a.pthr), c2al2 = T((2.0 * a.alpha) * a.l2);
+      for (int it = 0; it < a.piters; ++it) {
+        E.gemv_rows(x, a.ydat);
+        E.gb.sync();
+        T* r = E.v[4];
+        E.gather_rows(r);
+        E.gemvT_partial(r);
+        E.gb.sync();
+        E.gemvT_finish(V, T(2));
+        for (int k = threadIdx.x; k < n; k += blockDim.x) {
+          const T g = V[k] + c2al2 * x[k];
+          const T u = x[k] - step * g;
+          const T m = fabs(u) - thr;
+          const T mx = (m > T(0) || m != m) ? m : T(0);
+          const T sg = u > T(0) ? T(1) : (u < T(0) ? T(-1) : (u == T(0) ? T(0) : u));
+          x[k] = sg * mx;
+        }
+        __syncthreads();
+      }
+      store(a.out0, x);
+      break;
+    }
     case DM_KGC: {
       // np.outer(v, x)  (operators.py:208-209)
       load(U, a.in0);
@@ -856,6 +885,28 @@ static int dense_cg_t(PlanImpl& P, const adp_lower* lp, const void* xt, const vo
   res->residual = o.residual; res->curv = o.curv; res->iters = o.iters; res->converged = o.converged;
   res->status = o.status; res->hv = o.hv;
   return ADP_OK;
+}
+
+template <typename T>
+static int dense_prox_t(PlanImpl& P, const adp_lower* lp, const void* x0, void* x_out, int n_iters, double step,
+                        cudaStream_t st) {
+  DenseState* S = (DenseState*)P.ws[0];
+  DenseArgs<T> a = dense_base<T>(P);
+  dense_set_lower(a, lp);
+  a.mode = DM_PROX;
+  a.in0 = (const T*)x0;
+  a.out0 = (T*)x_out;
+  a.piters = n_iters;
+  a.pstep = step;
+  a.pthr = (step * lp->alpha) * lp->l1;    // threshold = step * alpha * l1
+  return dense_launch(P, S->km, a, st);
+}
+
+int dense_prox(PlanImpl& P, const adp_lower* lp, const void* x0, void* x_out, int n_iters, double step,
+               cudaStream_t st) {
+  if (lp->reg != ADP_REG_ELASTIC) return dense_fail(ADP_ERR_UNSUPPORTED, "prox-gradient: SmoothedElasticNet");
+  return P.d.dtype == ADP_DTYPE_F32 ? dense_prox_t<float>(P, lp, x0, x_out, n_iters, step, st)
+                                    : dense_prox_t<double>(P, lp, x0, x_out, n_iters, step, st);
 }
 
 int dense_cg(PlanImpl& P, const adp_lower* lp, const void* xt, const void* rhs, void* q, int warm, const void* precond,

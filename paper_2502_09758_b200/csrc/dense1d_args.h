@@ -28,6 +28,7 @@ struct DenseArgs {
   int reg_only;                  // regularizer alone (operator term dropped)
   int nofloor;
   const T* in0; const T* in1; T* out0; T* out1;
+  double pstep, pthr; int piters;   // prox_grad_iterations (DM_PROX)
 };
 
 struct DenseKernelSet {

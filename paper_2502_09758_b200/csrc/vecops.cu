@@ -24,6 +24,13 @@ __global__ void vec_elementwise(int op, int64_t n, double a, const T* x, const T
       case 3: out[i] = T(1) / x[i]; break;        // 1.0 / precond_diag
       case 4: out[i] = x[i] - y[i]; break;        // rhs - H q
       case 5: out[i] = x[i]; break;               // copy
+      case 6: {                                   // prox_l1(x, a) = sign(x) * max(|x| - a, 0) (np semantics)
+        const T u = x[i], m = fabs(u) - ta;
+        const T mx = (m > T(0) || m != m) ? m : T(0);
+        const T sg = u > T(0) ? T(1) : (u < T(0) ? T(-1) : (u == T(0) ? T(0) : u));
+        out[i] = sg * mx;
+        break;
+      }
       default: break;
     }
   }

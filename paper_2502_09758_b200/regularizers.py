@@ -23,6 +23,19 @@ import numpy as np
 from . import _native as nat
 
 
+def prox_l1(x, threshold: float):
+    """Component-wise soft threshold sign(x) * max(|x| - threshold, 0)
+    (regularizers.py:22-27), on the device (adp_vec op 6, NumPy's sign /
+    maximum semantics).  Returns the kind of ``x``."""
+    if threshold < 0:
+        raise ValueError("threshold must be >= 0")
+    from .hypergradient import _vec
+    xd = nat.to_dev(x, tuple(np.shape(x)))
+    out = nat.empty_like_dev(xd.shape)
+    _vec(6, xd.numel(), float(threshold), xd, xd, out)
+    return nat.like(out, x)
+
+
 def image_forward_diff(x) -> np.ndarray:
     """Forward differences along the first two axes, zero last row/column,
     stacked as (2,) + x.shape (regularizers.py:46-58).  Kernel-space helper."""

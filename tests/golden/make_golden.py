@@ -185,7 +185,36 @@ def config_cases():
          solve_gn=r.grad_norm, solve_iters=r.iters, solve_conv=r.converged)
 
 
+def baseline_cases():
+    """IFT baseline (baselines.py:46-90) on the BASELINE c1 problem: the
+    reference's prox_l1, prox_grad_iterations and 5 outer steps of run_ift."""
+    from adp import baselines as BL
+    from paper_2502_09758_b200 import configs as C
+    up = C.config1(0)
+    refup = P.UpperProblem(name="c1", A=O.DenseOperator(up.A.matrix), a=O.Kernel(up.a.data, O.DENSE1D),
+                           y_delta=up.y_delta, beta=0.0, alpha=1.0, reg=R.SmoothedElasticNet(1.2e-3, 4e-3, 1e-4),
+                           b0=O.Kernel(up.b0.data, O.DENSE1D), x0=up.x0, mu_floor=1e-3, lower_method="agd",
+                           lower_max_iters=300)
+    rng = np.random.default_rng(31)
+    v = rng.standard_normal(64) * 0.01
+    v[:4] = [0.0, -0.0, 0.004, -0.004]
+    pl = R.prox_l1(v, 0.004)
+    p = refup.lower_problem(refup.b0)
+    x50, traj = BL.prox_grad_iterations(p.op, p.y, p.alpha, 1.2e-3, 4e-3, np.zeros(256), 50, 0.1,
+                                        keep_trajectory=True)
+    cfg = BL.BaselineConfig(method="ift", upper_iters=5, upper_step=0.002)   # defaults.cfg [ift]
+    b, x, tr = BL.run_ift(refup, cfg)
+    save("ift_c1.npz", prox_in=v, prox_out=pl, prox_thr=0.004, pg_x50=x50, pg_traj3=np.array(traj[:4]),
+         ift_b=b.data, ift_x=x, ift_loss=np.array(tr.loss), ift_grad=np.array(tr.grad_norm),
+         ift_lower_cum=np.array(tr.lower_iters_cum), ift_cg_cum=np.array(tr.cg_iters_cum),
+         ift_final=tr.final_loss)
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 1:
+        for name in sys.argv[1:]:
+            globals()[name]()
+        sys.exit(0)
     reductions()
     conv_case("conv_small.npz", (24, 20, 3), 5, 11)
     conv_case("conv_k9.npz", (33, 40, 1), 9, 12)
@@ -193,3 +222,4 @@ if __name__ == "__main__":
     dense_case("dense_small.npz", 40, 21)
     solver_cases()
     config_cases()
+    baseline_cases()

@@ -88,3 +88,25 @@ def test_dense_maid_short_run(orc, golden):
     assert tr["cg_iters_cum"] == [int(v) for v in d["maid_cg_cum"]]
     assert rel(tr["loss"], d["maid_loss"]) <= 1e-12
     assert rel(b, d["maid_b"]) <= 1e-12
+
+
+def test_ift_baseline_oracle(orc, golden):
+    """prox_l1, prox_grad_iterations and 5 outer steps of run_ift on c1
+    (baselines.py:46-90, regularizers.py:22-27) against the reference."""
+    d = golden("ift_c1.npz")
+    out = orc.prox_l1(d["prox_in"], float(d["prox_thr"]))
+    assert np.array_equal(out, d["prox_out"]) and np.array_equal(np.signbit(out), np.signbit(d["prox_out"]))
+    d1 = golden("c1_maid.npz")
+    up = orc.Upper(A_kernel=d1["A"], a=d1["A"], y_delta=d1["y_delta"], beta=0.0, alpha=1.0,
+                   reg=orc.ElasticNet(1.2e-3, 4e-3, 1e-4), b0=d1["A"], x0=np.zeros(256), dense=True)
+    p = up.lower_problem(up.b0)
+    x50, traj = orc.prox_grad_iterations(p.op, p.y, p.alpha, 1.2e-3, 4e-3, np.zeros(256), 50, 0.1,
+                                         keep_trajectory=True)
+    assert rel(x50, d["pg_x50"]) <= 1e-13
+    assert rel(np.array(traj[:4]), d["pg_traj3"]) <= 1e-13
+    b, x, tr = orc.run_ift(up, dict(upper_iters=5, lower_iters=500, step_x=0.1, cg_tol=1e-10, cg_max_iters=400,
+                                    upper_step=0.002))
+    assert tr["lower_cum"] == [int(v) for v in d["ift_lower_cum"]]
+    assert tr["cg_cum"] == [int(v) for v in d["ift_cg_cum"]]
+    assert rel(tr["loss"], d["ift_loss"]) <= 1e-10
+    assert rel(b, d["ift_b"]) <= 1e-10 and rel(x, d["ift_x"]) <= 1e-10

@@ -1,0 +1,74 @@
+"""IFT baseline: the soft-threshold prox, the fused dense
+prox-gradient lower loop and run_ift on c1 against the REAL reference's
+outputs (tests/golden/ift_c1.npz); the composed 2-D prox-gradient path
+against the CPU oracle."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a, b = np.asarray(a, dtype=float), np.asarray(b, dtype=float)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def test_prox_l1_bitwise(adp, golden):
+    d = golden("ift_c1.npz")
+    out = adp.prox_l1(d["prox_in"], float(d["prox_thr"]))
+    assert np.array_equal(out, d["prox_out"]) and np.array_equal(np.signbit(out), np.signbit(d["prox_out"]))
+    with pytest.raises(ValueError):
+        adp.prox_l1(d["prox_in"], -1.0)
+
+
+def test_dense_prox_grad_iterations(adp, golden):
+    from paper_2502_09758_b200 import configs
+    d = golden("ift_c1.npz")
+    up = configs.config1(0)
+    p = up.lower_problem(up.b0)
+    x50 = adp.prox_grad_iterations(p.op, p.y, p.alpha, up.reg.l1, up.reg.l2, np.zeros(256), 50, 0.1)
+    # dgemv sites: the reference's OpenBLAS order vs the device's fixed order
+    assert rel(x50, d["pg_x50"]) <= 1e-12
+    x3, traj = adp.prox_grad_iterations(p.op, p.y, p.alpha, up.reg.l1, up.reg.l2, np.zeros(256), 3, 0.1,
+                                        keep_trajectory=True)
+    assert len(traj) == 4 and rel(np.array(traj), d["pg_traj3"]) <= 1e-12
+    assert np.array_equal(x3, traj[-1])
+    # l1 large: everything thresholded to zero (reference test_soft_threshold_active)
+    xz = adp.prox_grad_iterations(p.op, p.y, p.alpha, 1e3, 1.0, np.zeros(256), 20, 0.1)
+    assert np.all(xz == 0.0)
+
+
+def test_run_ift_c1(adp, golden):
+    from paper_2502_09758_b200 import configs
+    d = golden("ift_c1.npz")
+    up = configs.config1(0)
+    b, x, tr = adp.run_ift(up, adp.BaselineConfig(method="ift", upper_iters=5, upper_step=0.002))
+    assert tr.lower_iters_cum == [int(v) for v in d["ift_lower_cum"]]
+    # cg_tol = 1e-10 puts CG's stopping test at the rounding-noise floor: the
+    # reference's OpenBLAS ddot/dgemv order vs the device's fixed order may
+    # stop one iteration apart (a tolerance site, DESIGN.md Parity)
+    per_step = np.diff([0] + tr.cg_iters_cum)
+    ref_step = np.diff([0] + [int(v) for v in d["ift_cg_cum"]])
+    assert np.all(np.abs(per_step - ref_step) <= 1), (per_step, ref_step)
+    print("ift rel errors: loss", rel(tr.loss, d["ift_loss"]), "b", rel(b.data, d["ift_b"]), "x", rel(x, d["ift_x"]))
+    assert rel(tr.loss, d["ift_loss"]) <= 1e-9
+    assert rel(b.data, d["ift_b"]) <= 1e-9 and rel(x, d["ift_x"]) <= 1e-9
+    assert abs(tr.final_loss - float(d["ift_final"])) <= 1e-9 * abs(float(d["ift_final"]))
+    with pytest.raises(ValueError):
+        adp.run_ift(up, adp.BaselineConfig(method="unrolled"))
+    b0, _, tr0 = adp.run_ift(up, adp.BaselineConfig(method="ift", lower_iters=10, upper_iters=0))
+    assert np.array_equal(b0.data, up.b0.data) and len(tr0) == 0
+
+
+def test_composed_prox_grad_2d_bitwise(adp, orc):
+    """Non-dense operators compose device apply/adjoint + vector kernels; in
+    strict mode every step is the reference's arithmetic, bit for bit."""
+    rng = np.random.default_rng(3)
+    shape = (20, 24, 2)
+    k = rng.uniform(0.0, 1.0, (5, 5, 2))
+    k /= k.sum(axis=(0, 1), keepdims=True)
+    y = rng.uniform(0.0, 1.0, shape)
+    op = adp.ConvOperator(adp.Kernel(k, adp.DEPTHWISE2D), shape)
+    x = adp.prox_grad_iterations(op, y, 0.7, 2e-2, 3e-3, np.zeros(shape), 6, 0.1)
+    xo = orc.prox_grad_iterations(orc.Conv(k, shape), y, 0.7, 2e-2, 3e-3, np.zeros(shape), 6, 0.1)
+    assert np.array_equal(x, xo)

@@ -11,6 +11,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2")
 ap.add_argument("--size", type=int, default=256)
 ap.add_argument("--mode", default="strict")
+ap.add_argument("--tile", type=int, nargs=2, default=None, help="TH TW override")
 a = ap.parse_args()
 import torch  # noqa: E402
 import paper_2502_09758_b200 as adp  # noqa: E402
@@ -18,11 +19,15 @@ from paper_2502_09758_b200 import _native as nat  # noqa: E402
 from paper_2502_09758_b200 import configs  # noqa: E402
 
 adp.set_precision("float64", a.mode)
-up = configs.config2(0, size=a.size) if a.config == "c2" else configs.config3(0, size=a.size)
+up = configs.CONFIGS[a.config](0, size=a.size)
+if a.tile:
+    ks = tuple(up.b0.data.shape[:2])
+    nat.set_tile((nat.LAYOUT_DEPTHWISE2D, tuple(up.x0.shape), ks), tuple(a.tile))
 x0 = nat.to_dev(up.x0)
 p = up.lower_problem(up.b0)
 adp.solve_lower(p, x0, 1e-14, 10.0, max_iters=64, method="agd", adaptive=True)
 plan = p.op.plan()
+print("geometry", plan.geometry())
 nat.check(nat.lib().adp_debug_trace(plan.handle, 1, None))
 p = up.lower_problem(up.b0)
 adp.solve_lower(p, x0, 1e-14, 10.0, max_iters=64, method="agd", adaptive=True)
