@@ -148,7 +148,7 @@ def run_reference(args):
     import multiprocessing as mp
     cores = len(os.sched_getaffinity(0))
     iters = 12
-    rates = []
+    rates, dts = [], []
     ctx = mp.get_context("spawn")
     with ctx.Pool(cores) as pool:
         for s in range(args.warmup + args.steps):
@@ -157,9 +157,11 @@ def run_reference(args):
             dt = time.perf_counter() - t0
             if s >= args.warmup:
                 rates.append(sum(r[0] for r in res) / dt / 1e9)
+                dts.append(dt)
     v = float(np.mean(rates))
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(dts)), "higher_is_better": True,
+            "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"c2: {args.size}x{args.size}x1 f64, 9x9 stencil, TV, adaptive AGD",
                        "sample": f"{iters} lower iterations per process per step"},
@@ -402,6 +404,16 @@ def other_configs(args, flush):
                  "workload": "8 c3 instances (seeds 0-7) = one GPU's share of 64, 300 AGD iterations each, "
                              "no collectives (weak scaling over GPUs)"}
     del ups
+    # IFT baseline on c1 (baselines.py:58-90 with defaults.cfg [ift]): upper iters/s
+    up1 = configs.config1(0)
+    adp.run_ift(up1, adp.BaselineConfig(method="ift", upper_iters=1, upper_step=0.002))
+    t0 = time.perf_counter()
+    _, _, tr = adp.run_ift(up1, adp.BaselineConfig(method="ift", upper_iters=10, upper_step=0.002))
+    dt = time.perf_counter() - t0
+    out["ift_c1"] = {"metric": "IFT upper iters/s", "value": len(tr) / dt, "upper_iters": len(tr),
+                     "lower_iters_per_upper": 500, "cg_iters_cum": tr.cg_iters_cum[-1],
+                     "workload": "c1 (n=256 dense, elastic net): run_ift, 500 prox-gradient steps + CG(1e-10) "
+                                 "per upper iteration, wall clock"}
     up5 = configs.config5(0, size=args.c5_size)
     solve(up5, 2)
     flush.zero_()
