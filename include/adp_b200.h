@@ -184,6 +184,7 @@ int adp_prox_grad(adp_plan* p, const adp_lower* lp, const void* x0, void* x_out,
 /* ---- plan-free vector primitives (generic cg_solve with a caller-supplied hess_vec) ----
  * op 0: out = x + a*y   1: out = x - a*y   2: out = x*y   3: out = 1/x   4: out = x - y   5: out = x
  * op 6: out = prox_l1(x, a) = sign(x) * max(|x| - a, 0)   (regularizers.py:22-27)
+ * op 7: out = |y| > a ? x : 0   (soft-threshold activity mask, baselines.py:135)
  * op 10: *red_out = <x, y> (fixed-order tree)   11: *red_out = count(x <= 0) */
 int adp_vec(int32_t op, int64_t n, int32_t dtype, double a, const void* x, const void* y, void* out,
             double* red_out, void* stream);

@@ -13,7 +13,7 @@ reference's own rounding order, bitwise on stencils and np.sum sites),
 """
 
 from ._native import NativeError, get_precision, precision, set_precision
-from .baselines import BaselineConfig, prox_grad_iterations, run_ift
+from .baselines import BaselineConfig, prox_grad_iterations, run_ift, run_unrolled, unrolled_gradient
 from .hypergradient import (
     CGResult,
     HypergradResult,
@@ -79,7 +79,7 @@ __all__ = [
     "gaussian_conv_matrix", "get_precision", "image_forward_diff", "image_forward_diff_adjoint",
     "inexact_hypergradient", "kernel_gram_correlation", "lip_upper_x", "lower_grad", "lower_hess_diag",
     "lower_hess_vec", "lower_value", "lower_value_and_grad", "maid_run", "mixed_second_transpose", "mu_of_b",
-    "op_norm_sq", "operator_from_kernel", "piecewise_signal", "precision", "prox_grad_iterations", "prox_l1", "psi", "psi_value", "run_ift",
+    "op_norm_sq", "operator_from_kernel", "piecewise_signal", "precision", "prox_grad_iterations", "prox_l1", "psi", "psi_value", "run_ift", "run_unrolled",
     "set_precision", "smoothed_abs_norm", "sobolev_grad", "sobolev_value", "solve_lower", "solve_lower_at",
-    "tv_value", "upper_fit_grad",
+    "tv_value", "unrolled_gradient", "upper_fit_grad",
 ]

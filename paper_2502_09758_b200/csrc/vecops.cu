@@ -31,6 +31,7 @@ __global__ void vec_elementwise(int op, int64_t n, double a, const T* x, const T
         out[i] = sg * mx;
         break;
       }
+      case 7: out[i] = fabs(y[i]) > ta ? x[i] : T(0); break;   // np.where(|u| > thr, w, 0.0)
       default: break;
     }
   }

@@ -204,10 +204,14 @@ def baseline_cases():
                                         keep_trajectory=True)
     cfg = BL.BaselineConfig(method="ift", upper_iters=5, upper_step=0.002)   # defaults.cfg [ift]
     b, x, tr = BL.run_ift(refup, cfg)
+    ug, ux = BL.unrolled_gradient(refup, refup.b0, np.zeros(256), 50, 0.1)
+    ucfg = BL.BaselineConfig(method="unrolled", lower_iters=50, upper_iters=3, upper_step=0.005)  # defaults.cfg
+    ub, uxr, utr = BL.run_unrolled(refup, ucfg)
     save("ift_c1.npz", prox_in=v, prox_out=pl, prox_thr=0.004, pg_x50=x50, pg_traj3=np.array(traj[:4]),
          ift_b=b.data, ift_x=x, ift_loss=np.array(tr.loss), ift_grad=np.array(tr.grad_norm),
          ift_lower_cum=np.array(tr.lower_iters_cum), ift_cg_cum=np.array(tr.cg_iters_cum),
-         ift_final=tr.final_loss)
+         ift_final=tr.final_loss, unr_grad=ug, unr_x=ux, unr_b=ub.data, unr_xr=uxr, unr_loss=np.array(utr.loss),
+         unr_gnorm=np.array(utr.grad_norm), unr_final=utr.final_loss)
 
 
 if __name__ == "__main__":

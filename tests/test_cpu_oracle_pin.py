@@ -110,3 +110,14 @@ def test_ift_baseline_oracle(orc, golden):
     assert tr["cg_cum"] == [int(v) for v in d["ift_cg_cum"]]
     assert rel(tr["loss"], d["ift_loss"]) <= 1e-10
     assert rel(b, d["ift_b"]) <= 1e-10 and rel(x, d["ift_x"]) <= 1e-10
+
+
+def test_unrolled_gradient_oracle(orc, golden):
+    """unrolled_gradient (baselines.py:93-139) on c1 against the reference."""
+    d = golden("ift_c1.npz")
+    d1 = golden("c1_maid.npz")
+    up = orc.Upper(A_kernel=d1["A"], a=d1["A"], y_delta=d1["y_delta"], beta=0.0, alpha=1.0,
+                   reg=orc.ElasticNet(1.2e-3, 4e-3, 1e-4), b0=d1["A"], x0=np.zeros(256), dense=True)
+    g, x = orc.unrolled_gradient(up, d1["A"], np.zeros(256), 50, 0.1)
+    assert rel(x, d["unr_x"]) <= 1e-13
+    assert rel(g, d["unr_grad"]) <= 1e-12

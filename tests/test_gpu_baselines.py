@@ -72,3 +72,23 @@ def test_composed_prox_grad_2d_bitwise(adp, orc):
     x = adp.prox_grad_iterations(op, y, 0.7, 2e-2, 3e-3, np.zeros(shape), 6, 0.1)
     xo = orc.prox_grad_iterations(orc.Conv(k, shape), y, 0.7, 2e-2, 3e-3, np.zeros(shape), 6, 0.1)
     assert np.array_equal(x, xo)
+
+
+def test_unrolled_baseline_c1(adp, golden):
+    """Unrolled differentiation (baselines.py:93-162): the reverse-mode
+    gradient through 50 prox-gradient steps and 3 outer steps of
+    run_unrolled, against the reference (dgemv tolerance sites)."""
+    from paper_2502_09758_b200 import configs
+    d = golden("ift_c1.npz")
+    up = configs.config1(0)
+    g, x = adp.unrolled_gradient(up, up.b0, np.zeros(256), 50, 0.1)
+    assert rel(x, d["unr_x"]) <= 1e-12 and rel(g, d["unr_grad"]) <= 1e-10
+    b, xr, tr = adp.run_unrolled(up, adp.BaselineConfig(method="unrolled", lower_iters=50, upper_iters=3,
+                                                        upper_step=0.005))
+    assert tr.lower_iters_cum == [50, 100, 150] and tr.cg_iters_cum == [0, 0, 0]
+    assert rel(tr.loss, d["unr_loss"]) <= 1e-10 and rel(tr.grad_norm, d["unr_gnorm"]) <= 1e-10
+    assert rel(b.data, d["unr_b"]) <= 1e-10 and rel(xr, d["unr_xr"]) <= 1e-10
+    with pytest.raises(MemoryError):
+        adp.unrolled_gradient(up, up.b0, np.zeros(256), 1000, 0.1, memory_cap_bytes=1 << 20)
+    with pytest.raises(ValueError):
+        adp.run_unrolled(up, adp.BaselineConfig(method="ift"))
