@@ -113,7 +113,10 @@ template <typename T> struct Plain {
 };
 
 // ---------------------------------------------------------------------------
-template <typename T, bool FAST, int RW>
+// KS > 0: the stencil size is a compile-time constant (the latency-bound c2
+// solve kernel is instantiated with KS = 9 so it carries no other stencil
+// variant); KS = 0: runtime dispatch over the unrolled sizes + generic loop.
+template <typename T, bool FAST, int RW, int KS = 0>
 struct Conv {
   static_assert((RW & (RW - 1)) == 0, "RW must be a power of two");
   static constexpr int kShift = RW == 1 ? 0 : RW == 2 ? 1 : RW == 4 ? 2 : 3;
@@ -346,6 +349,10 @@ struct Conv {
   __device__ __forceinline__ void stencil(const T* __restrict__ pl, const T* __restrict__ w, T (&acc)[RW]) const {
 #pragma unroll
     for (int o = 0; o < RW; ++o) acc[o] = T(0);
+    if constexpr (KS > 0) {
+      stencil_k<KS>(pl, w, acc);
+      return;
+    }
     const int kh = a.g.kh, kw = a.g.kw, SWP = a.g.SWP;
     if (kh == 9 && kw == 9) {
       stencil_k<9>(pl, w, acc);

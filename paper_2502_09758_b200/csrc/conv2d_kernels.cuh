@@ -4,9 +4,9 @@
 
 namespace adp {
 
-template <typename T, bool FAST, int RW>
-struct ConvOps : Conv<T, FAST, RW> {
-  using Base = Conv<T, FAST, RW>;
+template <typename T, bool FAST, int RW, int KS = 0>
+struct ConvOps : Conv<T, FAST, RW, KS> {
+  using Base = Conv<T, FAST, RW, KS>;
   using Base::a;
   GridBarrier gb;
   SumDev* ssm;   // shared-memory copies of a.s_fit .. a.s_tv2 (read at every decision point)
@@ -120,9 +120,9 @@ struct ConvOps : Conv<T, FAST, RW> {
 
 // ---------------------------------------------------------------------------
 // solve_lower (lower_solvers.py:104-213) as one persistent kernel.
-template <typename T, bool FAST, int RW>
+template <typename T, bool FAST, int RW, int KS = 0>
 __global__ void __launch_bounds__(512, 1) conv_solve_kernel(const __grid_constant__ ConvArgs<T> a) {
-  ConvOps<T, FAST, RW> E(a);
+  ConvOps<T, FAST, RW, KS> E(a);
   const ConvGeom& g = a.g;
   E.load_weights(a.kern);
   const bool tv = (a.alpha != 0.0);
