@@ -14,7 +14,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libadpb200.so")
+LIB_PATH = os.environ.get("ADP_LIB") or os.path.join(_HERE, "lib", "libadpb200.so")   # ADP_LIB: A/B builds
 
 ADP_OK = 0
 LAYOUT_DEPTHWISE2D = 0

@@ -499,31 +499,58 @@ __device__ __forceinline__ void reduce_k(const SumDev* const (&ss)[K], double* o
   const int BD = blockDim.x;
   const int lgT = 31 - __clz(BD);
   const int T = 1 << lgT;
-  int base = 0;
+  bool small = true;
 #pragma unroll
-  for (int i = 0; i < K; ++i) {
-    if (P[i] == 1) {
-      if (threadIdx.x == 0) cp_async8(sv + base, src[i], n[i] > 0);
-    } else {
-      for (int e = 2 * threadIdx.x; e < P[i]; e += 2 * BD)
-        cp_async16(sv + base + e, src[i] + (e < n[i] ? e : 0), min(max(n[i] - e, 0), 2) * 8);
-    }
-    base += (P[i] + 1) & ~1;
-  }
-  lap(1);
-  cp_async_wait_all();
-  __syncthreads();
-  lap(2);
+  for (int i = 0; i < K; ++i) small = small && P[i] <= 4 * T;
   double root[K];
-  base = 0;
+  if (small) {
+    // every folding thread's chunk (<= 4 contiguous units) goes straight
+    // from L2 into registers: the loads of all K sums are in flight at once,
+    // no shared-memory staging; zero padding past n, perfect-tree fold
+    double v[K][4];
 #pragma unroll
-  for (int i = 0; i < K; ++i) {
-    const int chunk = P[i] > T ? P[i] >> lgT : 1;
-    root[i] = 0.0;
-    if (threadIdx.x * chunk < P[i])
-      root[i] = chunk <= 16 ? fold_small(sv + base + threadIdx.x * chunk, chunk)
-                            : fold_pow2_big(sv + base + threadIdx.x * chunk, chunk);
-    base += (P[i] + 1) & ~1;
+    for (int i = 0; i < K; ++i) {
+      const int chunk = P[i] > T ? P[i] >> lgT : 1;
+      const int e0 = threadIdx.x * chunk;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int e = e0 + m;
+        v[i][m] = (m < chunk && e < n[i] && (int)threadIdx.x < T) ? ldcg(src[i] + e) : 0.0;
+      }
+    }
+    lap(1);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const int chunk = P[i] > T ? P[i] >> lgT : 1;
+      root[i] = chunk == 1 ? v[i][0] : chunk == 2 ? v[i][0] + v[i][1] : (v[i][0] + v[i][1]) + (v[i][2] + v[i][3]);
+    }
+    lap(2);
+  } else {
+    int base = 0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      if (P[i] == 1) {
+        if (threadIdx.x == 0) cp_async8(sv + base, src[i], n[i] > 0);
+      } else {
+        for (int e = 2 * threadIdx.x; e < P[i]; e += 2 * BD)
+          cp_async16(sv + base + e, src[i] + (e < n[i] ? e : 0), min(max(n[i] - e, 0), 2) * 8);
+      }
+      base += (P[i] + 1) & ~1;
+    }
+    lap(1);
+    cp_async_wait_all();
+    __syncthreads();
+    lap(2);
+    base = 0;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const int chunk = P[i] > T ? P[i] >> lgT : 1;
+      root[i] = 0.0;
+      if (threadIdx.x * chunk < P[i])
+        root[i] = chunk <= 16 ? fold_small(sv + base + threadIdx.x * chunk, chunk)
+                              : fold_pow2_big(sv + base + threadIdx.x * chunk, chunk);
+      base += (P[i] + 1) & ~1;
+    }
   }
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1)

@@ -1013,6 +1013,30 @@ extern "C" int adp_prox_grad(adp_plan* p, const adp_lower* lp, const void* x0, v
   return dense_prox(P, lp, x0, x_out, n_iters, step, (cudaStream_t)stream);
 }
 
+// micro-benchmark of the solve's decision-point reduction (tools/bench_reduce.py)
+extern "C" int adp_debug_bench_reduce(adp_plan* p, int32_t reps, double* ms, void* stream) {
+  if (!p || !ms || reps < 1) return fail(ADP_ERR_ARG, "bad argument");
+  PlanImpl& P = p->impl;
+  if (P.d.layout != ADP_LAYOUT_DEPTHWISE2D || P.d.dtype != ADP_DTYPE_F64) return fail(ADP_ERR_UNSUPPORTED, "f64 conv");
+  cudaStream_t st = (cudaStream_t)stream;
+  ConvArgs<double> a = conv_base<double>(P);
+  a.mode = CM_BENCH_REDUCE;
+  a.max_iters = reps;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, st);
+  if (int e = launch_coop(P, P.k_misc, a, st)) return e;
+  cudaEventRecord(e1, st);
+  CK(cudaEventSynchronize(e1));
+  float t = 0;
+  cudaEventElapsedTime(&t, e0, e1);
+  *ms = t;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return ADP_OK;
+}
+
 extern "C" int adp_plan_geometry(const adp_plan* p, int32_t* out) {
   if (!p || !out) return fail(ADP_ERR_ARG, "null argument");
   const PlanImpl& P = p->impl;

@@ -22,6 +22,7 @@ enum ConvMode : int {
   CM_SLAB_POWER = 14,    // row slab: out0 = B^T B (in0 / sL); phase-1 of ||out0||^2
   CM_SLAB_NORM0 = 15,    // row slab: phase-1 of ||in0||^2
   CM_SLAB_GRAD = 16,     // row slab: lower_grad(in0) -> G; phase-1 of fit, tv, ||g||^2
+  CM_BENCH_REDUCE = 17,  // micro-benchmark: the solve's 6-sum reduction, mode-param times back to back
 };
 
 

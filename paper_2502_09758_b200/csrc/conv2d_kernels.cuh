@@ -698,6 +698,15 @@ __global__ void __launch_bounds__(512, 1) conv_misc_kernel(const __grid_constant
       E.gb.sync();
       E.phase1({&a.s_t0});
       break;
+    case CM_BENCH_REDUCE: {
+      double o[6], acc = 0.0;
+      for (int r = 0; r < a.max_iters; ++r) {
+        E.reduce({&a.s_fit, &a.s_tv, &a.s_t0, &a.s_t1, &a.s_fitc, &a.s_tvc}, o);
+        acc += o[0] + o[5];
+      }
+      if (blockIdx.x == 0 && threadIdx.x == 0) a.scal[0] = acc;
+      break;
+    }
     case CM_SLAB_GRAD:
       // g = lower_grad(x) partials (final gradient norm, lower_solvers.py:212)
       E.stageA(SrcLin<T>{a.in0}, a.R, a.ydat, tv, a.TV2, a.TVG, &a.s_fit, &a.s_tv);
