@@ -324,6 +324,49 @@ struct Conv {
     }
   }
 
+  // Two planes through the same compile-time K x K taps (the fused candidate
+  // stage): each tap is loaded once for both accumulations; per output the
+  // order is exactly stencil_k's.
+  template <int K>
+  __device__ __forceinline__ void stencil_k2(const T* __restrict__ pl1, const T* __restrict__ pl2,
+                                             const T* __restrict__ w, T (&acc1)[RW], T (&acc2)[RW]) const {
+    const int SWP = a.g.SWP;
+    const int b = (ty + 1) * SWP + sk(tx * RW);
+#pragma unroll
+    for (int o = 0; o < RW; ++o) acc1[o] = acc2[o] = T(0);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const T* row1 = pl1 + b + i * SWP;
+      const T* row2 = pl2 + b + i * SWP;
+      T win1[K + RW - 1], win2[K + RW - 1];
+#pragma unroll
+      for (int m = 0; m < K + RW - 1; ++m) {
+        win1[m] = row1[skr(1 + m)];
+        win2[m] = row2[skr(1 + m)];
+      }
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const T wt = w[i * K + j];
+#pragma unroll
+        for (int o = 0; o < RW; ++o) {
+          acc1[o] = madd<FAST>(acc1[o], win1[o + j], wt);
+          acc2[o] = madd<FAST>(acc2[o], win2[o + j], wt);
+        }
+      }
+    }
+  }
+  // forward taps over two regions; the compile-time-K kernels share the tap loads
+  __device__ __forceinline__ void stencil_fwd_pair(const T* pr1, const T* pr2, T (&acc1)[RW], T (&acc2)[RW]) const {
+    const size_t co = (size_t)ch * a.g.SH * a.g.SWP;
+    const T* w = ws() + ch * a.g.kh * a.g.kw;
+    if constexpr (KS > 0) {
+      stencil_k2<KS>(pr1 + co, pr2 + co, w, acc1, acc2);
+    } else {
+      stencil(pr1 + co, w, acc1);
+      stencil(pr2 + co, w, acc2);
+    }
+  }
+
   // Large K (c5: 31): rows stay a runtime loop (code size), each row fully
   // unrolled so its window and taps are loaded together.
   template <int K>
@@ -430,7 +473,10 @@ struct Conv {
   // TH x (TW*C) doubles, interleaved like the image) -> leaf_vals.  Leaf
   // index of (tile row r, segment s): (h*W*C + w0*C)/L + s; buffer k goes to
   // sums[k] with a leaf offset koff[k].
-  __device__ void tile_leaves(int h0, int w0, int nbuf, const SumDev* s0, const SumDev* s1, int koff2, int b0 = 0) {
+  // Optional second sum set (s0b, s1b) from term buffers 3.. (the fused
+  // candidate stage): both sets folded in one pass.
+  __device__ void tile_leaves(int h0, int w0, int nbuf, const SumDev* s0, const SumDev* s1, int koff2, int b0 = 0,
+                              const SumDev* s0b = nullptr, const SumDev* s1b = nullptr) {
     if (!tile_owned(h0)) return;   // CTA-uniform
     __syncthreads();
     // fused layouts have TW | W, so every tile row holds segs whole leaves
@@ -439,7 +485,8 @@ struct Conv {
     const int segs = a.g.segs;
     const int per_buf = rows * segs * 8;
     const int tmE = a.g.TH * a.g.TW * C;
-    const int total = per_buf * nbuf;
+    const int nb = s0b ? 2 * nbuf : nbuf;    // <= 6 buffers
+    const int total = per_buf * nb;
     const int64_t lbase = (int64_t)(h0 + a.g.row0) * a.g.rowL + (int64_t)mdiv(w0, a.g.magicTWpx) * segs;
     for (int g0 = 0; g0 < total; g0 += blockDim.x) {      // total % 8 == 0, blockDim % 32 == 0
       const int gch = g0 + threadIdx.x;
@@ -447,13 +494,15 @@ struct Conv {
       double acc = 0.0;
       int buf = 0, k = 0, r = 0, s = 0;
       if (act) {
-        buf = (gch >= per_buf) + (gch >= 2 * per_buf);   // nbuf <= 3
+        buf = (gch >= per_buf) + (gch >= 2 * per_buf) + (gch >= 3 * per_buf) + (gch >= 4 * per_buf) +
+              (gch >= 5 * per_buf);
         const int rem = gch - buf * per_buf;
         const int leaf_l = rem >> 3;
         k = rem & 7;
         r = mdiv(leaf_l, a.g.magicSegs);
         s = leaf_l - r * segs;
-        const double* t = tm() + (size_t)(b0 + buf) * tmE + (size_t)r * a.g.TW * C + s * L + k;
+        const int setb = buf >= nbuf, lb = buf - setb * nbuf;
+        const double* t = tm() + (size_t)(setb ? 3 + lb : b0 + lb) * tmE + (size_t)r * a.g.TW * C + s * L + k;
         acc = t[0];
         for (int i = 8; i < L; i += 8) acc = acc + t[i];
       }
@@ -461,8 +510,10 @@ struct Conv {
       acc = acc + __shfl_xor_sync(kFull, acc, 2);
       acc = acc + __shfl_xor_sync(kFull, acc, 4);
       if (act && k == 0) {
-        const int64_t li = lbase + (int64_t)r * a.g.rowL + s + (buf == 2 ? koff2 : 0);
-        (buf == 0 ? s0 : s1)->leaf_vals[li] = acc;
+        const int setb = buf >= nbuf, lb = buf - setb * nbuf;
+        const int64_t li = lbase + (int64_t)r * a.g.rowL + s + (lb == 2 ? koff2 : 0);
+        const SumDev* sd = setb ? (lb == 0 ? s0b : s1b) : (lb == 0 ? s0 : s1);
+        sd->leaf_vals[li] = acc;
       }
     }
   }
@@ -483,13 +534,18 @@ struct Conv {
     return pr[(size_t)ch * a.g.SH * a.g.SWP + (r + a.g.rh + 1) * a.g.SWP + sk(q + a.g.rw + 1)];
   }
   __device__ __forceinline__ void tileA(const T* pr, T* qr, int tb, int h0, int w0, const T (&ypre)[RW], T* Rout,
-                                        bool tv, T* TV2out, T* TVGout, bool fused) {
+                                        bool tv, T* TV2out, T* TVGout, bool fused, const T* pre_acc = nullptr) {
     const T nu = T(a.nu), nu2 = nu * nu;
     const int H = a.g.H, W = a.g.W, TH = a.g.TH, TW = a.g.TW, C = a.g.C;
     const int64_t N = a.g.N;
     const int h = h0 + ty;
     T acc[RW];
-    stencil(pr + (size_t)ch * a.g.SH * a.g.SWP, ws() + ch * a.g.kh * a.g.kw, acc);
+    if (pre_acc) {
+#pragma unroll
+      for (int o = 0; o < RW; ++o) acc[o] = pre_acc[o];
+    } else {
+      stencil(pr + (size_t)ch * a.g.SH * a.g.SWP, ws() + ch * a.g.kh * a.g.kw, acc);
+    }
 #pragma unroll
     for (int o = 0; o < RW; ++o) {
       const int q = tx * RW + o;
@@ -648,14 +704,19 @@ struct Conv {
   // leaves to sfitc / stvc; otherwise rc -> RCout and TV terms -> TV2Cout.
   __device__ __forceinline__ double tileC(const T* pr, int h0, int w0, const T (&ypre)[RW], const T (&gpre)[RW],
                                           const T (&xopre)[RW], T* RCout, bool tv, T* TV2Cout, T* Xout, bool dot,
-                                          bool fused) {
+                                          bool fused, const T* pre_acc = nullptr) {
     const T nu = T(a.nu), nu2 = nu * nu;
     const int H = a.g.H, W = a.g.W;
     const int64_t N = a.g.N;
     const int h = h0 + ty;
     double part = 0.0;
     T acc[RW];
-    stencil(pr + (size_t)ch * a.g.SH * a.g.SWP, ws() + ch * a.g.kh * a.g.kw, acc);
+    if (pre_acc) {
+#pragma unroll
+      for (int o = 0; o < RW; ++o) acc[o] = pre_acc[o];
+    } else {
+      stencil(pr + (size_t)ch * a.g.SH * a.g.SWP, ws() + ch * a.g.kh * a.g.kw, acc);
+    }
 #pragma unroll
     for (int o = 0; o < RW; ++o) {
       const int q = tx * RW + o;
@@ -742,11 +803,22 @@ struct Conv {
       load_full(h0, w0, SrcLin<T>{Xc}, pa());
       load_full(h0, w0, SrcExtrap<T>{Xc, Xold, betaN}, pa2());
       __syncthreads();
-      const double part = tileC(pa(), h0, w0, ypre, gpre, xopre, nullptr, tv, nullptr, nullptr, true, true);
-      tileA(pa2(), pa(), 3, h0, w0, ypre, Rout, tv, nullptr, TVGout, true);   // tileA syncs before reusing pa()
-      tile_partial(*sdot, tile, part);
-      tile_leaves(h0, w0, tv ? 3 : 1, sfitc, stvc, (int)(a.g.Ng / a.g.leafL));
-      tile_leaves(h0, w0, tv ? 3 : 1, sfit2, stv2, (int)(a.g.Ng / a.g.leafL), 3);
+      if constexpr (KS > 0) {
+        // compile-time K (c2): shared tap loads, both leaf sets in one pass
+        T acc1[RW], acc2[RW];
+        stencil_fwd_pair(pa(), pa2(), acc1, acc2);
+        const double part = tileC(pa(), h0, w0, ypre, gpre, xopre, nullptr, tv, nullptr, nullptr, true, true, acc1);
+        tileA(pa2(), pa(), 3, h0, w0, ypre, Rout, tv, nullptr, TVGout, true, acc2);   // syncs before reusing pa()
+        tile_partial(*sdot, tile, part);
+        tile_leaves(h0, w0, tv ? 3 : 1, sfitc, stvc, (int)(a.g.Ng / a.g.leafL), 0, sfit2, stv2);
+      } else {
+        // generic sizes: one stencil at a time (register pressure at RW = 4)
+        const double part = tileC(pa(), h0, w0, ypre, gpre, xopre, nullptr, tv, nullptr, nullptr, true, true);
+        tileA(pa2(), pa(), 3, h0, w0, ypre, Rout, tv, nullptr, TVGout, true);
+        tile_partial(*sdot, tile, part);
+        tile_leaves(h0, w0, tv ? 3 : 1, sfitc, stvc, (int)(a.g.Ng / a.g.leafL));
+        tile_leaves(h0, w0, tv ? 3 : 1, sfit2, stv2, (int)(a.g.Ng / a.g.leafL), 3);
+      }
     }
   }
 
