@@ -189,6 +189,19 @@ int adp_prox_grad(adp_plan* p, const adp_lower* lp, const void* x0, void* x_out,
 int adp_vec(int32_t op, int64_t n, int32_t dtype, double a, const void* x, const void* y, void* out,
             double* red_out, void* stream);
 
+/* ---- quality metrics (metrics_io.py:26-85), float64 device arrays ----
+ * adp_np_sum: np.sum of k contiguous segments of n elements each, in NumPy's pairwise order
+ * (bitwise); op 0: the elements of x, op 1: (x - y) ** 2 (psnr's squared error, metrics_io.py:34).
+ * Results to HOST out[k]; synchronises the stream. */
+int adp_np_sum(int32_t op, int32_t k, int64_t n, const void* x, const void* y, double* out, void* stream);
+/* ssim (metrics_io.py:47-76): for every channel c the map num/den over the interior windows
+ * (H-10) x (W-10) of x, ref (H, W, C) with the ksize x ksize window `win` (HOST, row-major, the
+ * reference's _ssim_window(): ksize must be 11) and constants c1, c2; chan_sum[c] (HOST) = np.sum of
+ * channel c's map (pairwise order; the caller divides by its size as np.mean does).  map_out
+ * (device, C x (H-10) x (W-10)) may be NULL.  Synchronises the stream. */
+int adp_ssim(int32_t H, int32_t W, int32_t C, const double* win, int32_t ksize, double c1, double c2,
+             const void* x, const void* ref, void* map_out, double* chan_sum, void* stream);
+
 /* ---- FP64 roof: sustained DFMA throughput (TFLOP/s, 2 flop per DFMA) of this device ---- */
 int adp_fp64_peak(double* tflops, double* ms, void* stream);
 

@@ -39,6 +39,7 @@ from .lower_solvers import (
     mu_of_b,
     solve_lower,
 )
+from .metrics_io import MetricReport, metric_report, psnr, ssim
 from .maid import BacktrackingStalled, MAIDConfig, RunTrace, lip_upper_x, maid_run, psi, psi_value
 from .operators import (
     DENSE1D,
@@ -73,7 +74,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "BacktrackingStalled", "BaselineConfig", "CGResult", "ConvOperator", "DENSE1D", "DEPTHWISE2D", "DenseOperator",
-    "HypergradResult", "Kernel", "L_of_b", "LowerProblem", "LowerSolveResult", "MAIDConfig",
+    "HypergradResult", "Kernel", "L_of_b", "LowerProblem", "LowerSolveResult", "MAIDConfig", "MetricReport", "metric_report", "psnr", "ssim",
     "NativeError", "NegativeCurvatureError", "RunTrace", "SmoothedElasticNet", "SmoothedTV", "SolveDiverged",
     "UpperProblem", "WarmState", "build_deconv1d", "build_motion2d", "build_semiblind2d", "cg_solve",
     "gaussian_conv_matrix", "get_precision", "image_forward_diff", "image_forward_diff_adjoint",

@@ -91,6 +91,8 @@ SIGNATURES = {
     "adp_dot": (_I, [_P, _P, _P, ctypes.POINTER(_D), _P]),
     "adp_reg_op": (_I, [_P, ctypes.POINTER(Lower), _I, _P, _P, _P, ctypes.POINTER(_D), _P]),
     "adp_vec": (_I, [_I, ctypes.c_int64, _I, _D, _P, _P, _P, ctypes.POINTER(_D), _P]),
+    "adp_np_sum": (_I, [_I, _I, ctypes.c_int64, _P, _P, ctypes.POINTER(_D), _P]),
+    "adp_ssim": (_I, [_I, _I, _I, ctypes.POINTER(_D), _I, _D, _D, _P, _P, _P, ctypes.POINTER(_D), _P]),
     "adp_debug_trace": (_I, [_P, _I, _P]),
     "adp_fp64_peak": (_I, [ctypes.POINTER(_D), ctypes.POINTER(_D), _P]),
     "adp_prox_grad": (_I, [_P, ctypes.POINTER(Lower), _P, _P, _I, _D, _P]),

@@ -96,6 +96,27 @@ def dense_case(name, n, seed):
          mixed=H.mixed_second_transpose(x, op.kernel, v, p))
 
 
+def metric_cases():
+    """metrics_io.psnr / ssim / rel_l2_error of seeded image pairs (f3)."""
+    from adp import metrics_io as MI
+    out = {}
+    cases = {"g": (37, 45), "rgb": (40, 48, 3), "big": (128, 96, 3), "thin": (11, 30, 2), "tiny": (9, 20, 1)}
+    for i, (name, shape) in enumerate(cases.items()):
+        rng = np.random.default_rng(100 + i)
+        ref = rng.uniform(0.0, 1.0, shape)
+        x = np.clip(ref + 0.05 * rng.standard_normal(shape), 0.0, 1.0)
+        out[f"{name}_x"], out[f"{name}_ref"] = x, ref
+        out[f"{name}_psnr"] = MI.psnr(x, ref)
+        out[f"{name}_psnr_peak"] = MI.psnr(x, ref, peak=2.5)
+        with np.errstate(all="ignore"):
+            import warnings
+            with warnings.catch_warnings():
+                warnings.simplefilter("ignore")
+                out[f"{name}_ssim"] = MI.ssim(x, ref)
+        out[f"{name}_rel"] = MI.rel_l2_error(x, ref)
+    save("metrics.npz", **out)
+
+
 def solver_cases():
     # 2-D adaptive AGD on a small semi-blind instance (motion2d semantics)
     up = P.build_semiblind2d(size=(40, 48), seed=3)
@@ -227,3 +248,4 @@ if __name__ == "__main__":
     solver_cases()
     config_cases()
     baseline_cases()
+    metric_cases()

@@ -121,3 +121,47 @@ def test_unrolled_gradient_oracle(orc, golden):
     g, x = orc.unrolled_gradient(up, d1["A"], np.zeros(256), 50, 0.1)
     assert rel(x, d["unr_x"]) <= 1e-13
     assert rel(g, d["unr_grad"]) <= 1e-12
+
+
+METRIC_CASES = ("g", "rgb", "big", "thin", "tiny")
+
+
+@pytest.mark.parametrize("name", METRIC_CASES)
+def test_metrics_oracle_bitwise(orc, golden, name):
+    """PSNR / SSIM / rel-L2 restatements (metrics_io.py:26-80) vs the real reference."""
+    import warnings
+    d = golden("metrics.npz")
+    x, r = d[f"{name}_x"], d[f"{name}_ref"]
+    assert orc.psnr(x, r) == float(d[f"{name}_psnr"])
+    assert orc.psnr(x, r, 2.5) == float(d[f"{name}_psnr_peak"])
+    assert orc.rel_l2_error(x, r) == float(d[f"{name}_rel"])
+    if name == "tiny":      # no interior window: the reference returns nan
+        assert np.isnan(float(d[f"{name}_ssim"]))
+    else:
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore")
+            assert orc.ssim(x, r) == float(d[f"{name}_ssim"])
+
+
+def test_trace_csv_roundtrip(tmp_path):
+    """write_trace_csv / read_trace_csv (metrics_io.py:88-116): host-only, same format."""
+    from paper_2502_09758_b200 import RunTrace
+    from paper_2502_09758_b200 import metrics_io as mi
+    t = RunTrace()
+    for k in range(4):
+        t.append(k, 1.0 / (k + 3), 0.1 * k, 0.25 / (k + 1), 0.2, 2e-5 * 1.5**k, 100 * k, 7 * k, 0.123456789 * k)
+    p = tmp_path / "trace.csv"
+    mi.write_trace_csv(t, p)
+    lines = p.read_text().splitlines()
+    assert lines[0] == ",".join(mi.TRACE_HEADER)
+    assert lines[2].split(",")[1] == repr(1.0 / 4)
+    back = mi.read_trace_csv(p)
+    for f in ("k", "loss", "grad_norm", "eps", "delta", "alpha", "lower_iters_cum", "cg_iters_cum", "wall_s"):
+        assert getattr(back, f) == getattr(t, f)
+    p.write_text("a,b\n1,2\n")
+    with pytest.raises(ValueError, match="unexpected trace header"):
+        mi.read_trace_csv(p)
+    with pytest.raises(OSError, match="cannot read trace"):
+        mi.read_trace_csv(tmp_path / "missing.csv")
+    assert mi.loss_axis_scale([[1.0, 2e3], [5.0]]) == "log"
+    assert mi.loss_axis_scale([[1.0, 2.0], [-1.0]]) == "linear"
