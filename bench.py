@@ -422,7 +422,50 @@ def other_configs(args, flush):
                  "ms_per_solve": 1e3 * t,
                  "workload": f"{args.c5_size}x{args.c5_size}x3, 31x31 Gaussian, {args.c5_iters} AGD iterations "
                              "(+ power iteration), one GPU"}
+    out["c5_fft"] = c5_fft(args, up5, solve, flush)
     return out
+
+
+def c5_fft(args, up5, solve, flush):
+    """the c5 solve with the tile-FFT stencils (tolerance
+    mode), and one stencil (ConvOperator.apply on a device image) direct
+    strict vs FFT, with the FFT stencil's HBM roofline."""
+    import paper_2502_09758_b200 as adp
+    from paper_2502_09758_b200 import _native as nat
+    hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    p = up5.lower_problem(up5.b0)
+    xd = nat.to_dev(up5.x0)
+
+    def stencil_ms(reps=3):
+        p.op.apply(xd)
+        flush.zero_()
+        _, t = _timed(lambda: [p.op.apply(xd) for _ in range(reps)])
+        return 1e3 * t / reps
+    direct_ms = stencil_ms()
+    with adp.precision("float64", "fft"):
+        fft_ms = stencil_ms()
+        solve(up5, 2)
+        flush.zero_()
+        r, t = _timed(lambda: solve(up5, args.c5_iters))
+        plan = p.op.fft_plan()
+    H, W, C = up5.x0.shape
+    kh = up5.b0.data.shape[0]
+    V = 512 - kh + 1
+    npairs = (-(-H // V) * -(-W // V) + 1) // 2
+    sbytes = 16 * C * npairs * 512 * 512
+    traffic = 5 * sbytes + 16 * H * W * C      # K1 write, K2 read+write+spectrum, K3 read; image in + out
+    return {"value": up5.y_delta.size * r.iters / t / 1e9, "unit": UNIT, "iters": r.iters, "ms_per_solve": 1e3 * t,
+            "stencil_ms": {"direct_strict": direct_ms, "fft": fft_ms, "speedup": direct_ms / fft_ms},
+            "fft_stencil_roofline": {"bound": "hbm", "achieved": traffic / (fft_ms * 1e-3) / 1e9, "peak": hbm,
+                                     "unit": "GB/s", "frac": traffic / (fft_ms * 1e-3) / 1e9 / hbm,
+                                     "bytes_per_stencil": traffic,
+                                     "note": "algorithmic bytes of the three tile-FFT passes (complex scratch "
+                                             "written once, read+written by the column pass, read by the "
+                                             "inverse row pass, spectrum read once) + image in/out"},
+            "workspace_bytes": plan.workspace_bytes,
+            "workload": f"c5 in FFT stencil mode (SURVEY.md §8 f2; tolerance parity): {H}x{W}x{C}, {kh}x{kh} "
+                        f"Gaussian, {args.c5_iters} AGD iterations (+ power iteration), 512x512 overlap-save tiles"}
 
 
 def run_c5(args):

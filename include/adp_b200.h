@@ -202,6 +202,29 @@ int adp_np_sum(int32_t op, int32_t k, int64_t n, const void* x, const void* y, d
 int adp_ssim(int32_t H, int32_t W, int32_t C, const double* win, int32_t ksize, double c1, double c2,
              const void* x, const void* ref, void* map_out, double* chan_sum, void* stream);
 
+/* ---- FFT stencil path (float64, smoothed TV, depthwise 2-D) ----
+ * The zero-padded depthwise correlation of operators.py:101-118 by overlap-save tile FFTs
+ * (512 x 512 tiles, two tiles per complex transform) instead of K^2 direct taps: the cheaper
+ * choice for large kernels (K = 31 at c5).  Tolerance mode (FFT rounding, ~1e-15 of the output
+ * scale); reductions fixed-order (bitwise reproducible run to run).  The plan owns the complex
+ * scratch, the kernel spectra (rebuilt from `kernel` at every call) and six image buffers. */
+typedef struct adp_fft_plan adp_fft_plan;
+int adp_fft_plan_create(adp_fft_plan** out, int32_t H, int32_t W, int32_t C, int32_t kh, int32_t kw);
+void adp_fft_plan_destroy(adp_fft_plan* plan);
+size_t adp_fft_plan_workspace_bytes(const adp_fft_plan* plan);
+/* ConvOperator.apply (adjoint = 0) / .adjoint (adjoint = 1)     (operators.py:108-118) */
+int adp_fft_apply(adp_fft_plan* p, const void* kernel, int32_t adjoint, const void* x, void* out, void* stream);
+/* lower_value / lower_value_and_grad (lower_solvers.py:37-63); value may be NULL */
+int adp_fft_lower_value(adp_fft_plan* p, const adp_lower* lp, const void* x, double* value, void* stream);
+int adp_fft_lower_value_and_grad(adp_fft_plan* p, const adp_lower* lp, const void* x, double* value, void* g,
+                                 void* stream);
+/* op_norm_sq power iteration (operators.py:137-173) */
+int adp_fft_op_norm_sq(adp_fft_plan* p, const void* kernel, const void* v0, int32_t max_iters, double tol,
+                       double* lam, int32_t* converged, int32_t* iters, void* stream);
+/* solve_lower (lower_solvers.py:104-213): same arguments and result fields as adp_lower_solve */
+int adp_fft_lower_solve(adp_fft_plan* p, const adp_lower* lp, const void* x0, void* x_out, const adp_solve_args* args,
+                        adp_solve_result* res, void* stream);
+
 /* ---- FP64 roof: sustained DFMA throughput (TFLOP/s, 2 flop per DFMA) of this device ---- */
 int adp_fp64_peak(double* tflops, double* ms, void* stream);
 

@@ -93,6 +93,15 @@ SIGNATURES = {
     "adp_vec": (_I, [_I, ctypes.c_int64, _I, _D, _P, _P, _P, ctypes.POINTER(_D), _P]),
     "adp_np_sum": (_I, [_I, _I, ctypes.c_int64, _P, _P, ctypes.POINTER(_D), _P]),
     "adp_ssim": (_I, [_I, _I, _I, ctypes.POINTER(_D), _I, _D, _D, _P, _P, _P, ctypes.POINTER(_D), _P]),
+    "adp_fft_plan_create": (_I, [ctypes.POINTER(_P), _I, _I, _I, _I, _I]),
+    "adp_fft_plan_destroy": (None, [_P]),
+    "adp_fft_plan_workspace_bytes": (ctypes.c_size_t, [_P]),
+    "adp_fft_apply": (_I, [_P, _P, _I, _P, _P, _P]),
+    "adp_fft_lower_value": (_I, [_P, ctypes.POINTER(Lower), _P, ctypes.POINTER(_D), _P]),
+    "adp_fft_lower_value_and_grad": (_I, [_P, ctypes.POINTER(Lower), _P, ctypes.POINTER(_D), _P, _P]),
+    "adp_fft_op_norm_sq": (_I, [_P, _P, _P, _I, _D, ctypes.POINTER(_D), ctypes.POINTER(_I), ctypes.POINTER(_I), _P]),
+    "adp_fft_lower_solve": (_I, [_P, ctypes.POINTER(Lower), _P, _P, ctypes.POINTER(SolveArgs),
+                                 ctypes.POINTER(SolveResult), _P]),
     "adp_debug_trace": (_I, [_P, _I, _P]),
     "adp_fp64_peak": (_I, [ctypes.POINTER(_D), ctypes.POINTER(_D), _P]),
     "adp_prox_grad": (_I, [_P, ctypes.POINTER(Lower), _P, _P, _I, _D, _P]),
@@ -158,9 +167,13 @@ _settings = {"dtype": "float64", "mode": "strict"}
 
 def set_precision(dtype: str = "float64", mode: str = "strict"):
     """Select the device arithmetic: float64 strict (bitwise reference order),
-    float64 fast (FMA stencils) or float32."""
-    if dtype not in ("float64", "float32") or mode not in ("strict", "fast"):
-        raise ValueError("dtype in {float64, float32}, mode in {strict, fast}")
+    float64 fast (FMA stencils), float64 fft (depthwise stencils of the
+    lower-level objective and solver by overlap-save tile FFTs, SURVEY.md
+    §8 f2; the other operations run as in fast mode) or float32."""
+    if dtype not in ("float64", "float32") or mode not in ("strict", "fast", "fft"):
+        raise ValueError("dtype in {float64, float32}, mode in {strict, fast, fft}")
+    if mode == "fft" and dtype != "float64":
+        raise ValueError("the FFT stencil mode is float64 only")
     _settings["dtype"] = dtype
     _settings["mode"] = mode
 
@@ -198,7 +211,7 @@ class Plan:
         d = PlanDesc()
         d.layout = layout
         d.dtype = DTYPE_F64 if dtype == "float64" else DTYPE_F32
-        d.mode = MODE_STRICT if mode == "strict" else MODE_FAST
+        d.mode = MODE_STRICT if mode == "strict" else MODE_FAST   # fft: direct kernels in fast mode
         if layout == LAYOUT_DENSE1D:
             n = int(shape[0])
             d.H, d.W, d.C, d.kh, d.kw = 1, n, 1, n, n
@@ -271,6 +284,47 @@ def probe_geometry(shape, ksize, tile=(0, 0)) -> dict:
 
 def clear_plans():
     _plans.clear()
+    _fft_plans.clear()
+
+
+def is_fft() -> bool:
+    return _settings["mode"] == "fft"
+
+
+class FFTPlan:
+    """Owns one ``adp_fft_plan`` (tile-FFT stencils for one image shape and kernel size)."""
+
+    def __init__(self, shape, ksize):
+        H, W, C = (int(s) for s in shape)
+        self.handle = ctypes.c_void_p()
+        check(lib().adp_fft_plan_create(ctypes.byref(self.handle), H, W, C, int(ksize[0]), int(ksize[1])),
+              "adp_fft_plan_create")
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h and _lib is not None:
+            try:
+                _lib.adp_fft_plan_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+    @property
+    def workspace_bytes(self) -> int:
+        return int(lib().adp_fft_plan_workspace_bytes(self.handle))
+
+
+_fft_plans: dict = {}
+
+
+def fft_plan_for(shape, ksize, slot=None) -> FFTPlan:
+    key = (tuple(int(s) for s in shape), tuple(int(k) for k in ksize),
+           threading.get_ident() if slot is None else slot)
+    p = _fft_plans.get(key)
+    if p is None:
+        p = FFTPlan(shape, ksize)
+        _fft_plans[key] = p
+    return p
 
 
 def stream_ptr():

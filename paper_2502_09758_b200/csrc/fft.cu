@@ -1,0 +1,834 @@
+// FFT stencil path for large kernels: the depthwise
+// zero-padded correlation of operators.py:101-118 computed by overlap-save
+// tile FFTs instead of K^2 direct taps, and the lower-level AGD solve
+// (lower_solvers.py:104-213) driven on top of it.
+//
+// Tiles.  The image (H, W, C) is cut into output tiles of Vh x Vw = (T-kh+1) x
+// (T-kw+1) pixels, T = 512.  Tile input u[a][b] = x[h0-rh+a, w0-rw+b] (zero
+// outside the image); the circular cross-correlation of u with the kernel
+// zero-padded to T x T equals the linear one on the first Vh x Vw outputs.
+// Two tiles of the same channel share one complex transform (tile a in the
+// real part, tile b in the imaginary part): the kernel is real, so the
+// correlation acts on both parts independently.
+//
+// Passes (one stencil = three launches, all in HBM-resident complex scratch):
+//   K1 row pass     : load the two tiles' rows (zero padded), FFT-512 per row
+//   K2 column pass  : FFT-512 per column, multiply by conj(FFT2(kernel)),
+//                     inverse FFT-512 per column (one shared-memory round trip)
+//   K3 inverse rows : inverse FFT-512 per row, crop the valid outputs, fused
+//                     epilogue (residual, gradient with the TV term, value
+//                     terms, power-iteration norm) with per-CTA partial sums
+// The FFT is a radix-8 Stockham autosort transform in shared memory
+// (3 stages for 512 points) with an accurately rounded twiddle table.
+//
+// Arithmetic: float64 with FMA contraction off (library-wide --fmad=false);
+// results differ from the direct strict stencil by FFT rounding (~1e-15
+// relative to the output scale): a tolerance-only mode, like "fast".
+// Reductions are fixed-order (per-CTA trees, then a fixed fold), so every run
+// is bitwise reproducible.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+#include "adp_device.cuh"
+#include "../../include/adp_b200.h"
+
+namespace adp {
+int dense_fail(int code, const char* m);
+
+namespace fft {
+
+constexpr int T = 512;          // transform length (both axes)
+constexpr int RROWS = 4;        // rows per CTA in the row passes (64 threads per row)
+constexpr int CCOLS = 8;        // columns per CTA in the column pass (64 threads per column)
+constexpr double kInvT2 = 1.0 / (512.0 * 512.0);   // exact power of two
+
+struct Geo {
+  int H, W, C, kh, kw, rh, rw, Vh, Vw, ntY, ntX, ntiles, npairs;
+};
+
+// ---------------------------------------------------------------------------
+// radix-8 butterflies
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+template <bool INV>
+__device__ __forceinline__ double2 mul_mi(double2 a) {   // forward: * (-i); inverse: * (+i)
+  return INV ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+}
+
+// In-register 8-point DFT, natural order in and out (decimation in frequency).
+template <bool INV>
+__device__ __forceinline__ void dft8(double2* v) {
+  constexpr double s = 0.70710678118654752440;
+  double2 b0 = cadd(v[0], v[4]), b4 = csub(v[0], v[4]);
+  double2 b1 = cadd(v[1], v[5]), b5 = csub(v[1], v[5]);
+  double2 b2 = cadd(v[2], v[6]), b6 = csub(v[2], v[6]);
+  double2 b3 = cadd(v[3], v[7]), b7 = csub(v[3], v[7]);
+  // b5 *= w8^1, b6 *= w8^2, b7 *= w8^3  (w8 = exp(-+2 pi i / 8))
+  b5 = INV ? make_double2(s * (b5.x - b5.y), s * (b5.x + b5.y)) : make_double2(s * (b5.x + b5.y), s * (b5.y - b5.x));
+  b6 = mul_mi<INV>(b6);
+  b7 = INV ? make_double2(-s * (b7.x + b7.y), s * (b7.x - b7.y)) : make_double2(s * (b7.y - b7.x), -s * (b7.x + b7.y));
+  double2 c0 = cadd(b0, b2), c2 = csub(b0, b2);
+  double2 c1 = cadd(b1, b3), c3 = mul_mi<INV>(csub(b1, b3));
+  double2 c4 = cadd(b4, b6), c6 = csub(b4, b6);
+  double2 c5 = cadd(b5, b7), c7 = mul_mi<INV>(csub(b5, b7));
+  v[0] = cadd(c0, c1);
+  v[4] = csub(c0, c1);
+  v[2] = cadd(c2, c3);
+  v[6] = csub(c2, c3);
+  v[1] = cadd(c4, c5);
+  v[5] = csub(c4, c5);
+  v[3] = cadd(c6, c7);
+  v[7] = csub(c6, c7);
+}
+
+// 512-point Stockham FFTs of nb batches in shared memory.  Element e of batch
+// bi lives at buf[bi * bstride + e * estride].  Ping-pongs a -> b -> a -> b;
+// returns the buffer holding the result (b).  All threads of the CTA take
+// part; ends with a barrier.  BFAST: consecutive threads walk batches
+// (column passes, batches adjacent in memory).
+template <bool INV, bool BFAST>
+__device__ double2* fft512(double2* a, double2* b, int nb, int bstride, int estride, const double2* __restrict__ tw) {
+  double2* src = a;
+  double2* dst = b;
+  const int nwork = nb * 64;
+#pragma unroll 1
+  for (int st = 0, Ns = 1; st < 3; ++st, Ns *= 8) {
+    for (int t = threadIdx.x; t < nwork; t += blockDim.x) {
+      const int bi = BFAST ? (t % nb) : (t >> 6);
+      const int j = BFAST ? (t / nb) : (t & 63);
+      const int k = j & (Ns - 1);
+      double2* s = src + bi * bstride;
+      double2 v[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) v[r] = s[(j + r * 64) * estride];
+      if (st > 0) {
+        const int step = 64 / Ns;            // angle index m = r * k * 512 / (8 Ns)
+#pragma unroll
+        for (int r = 1; r < 8; ++r) {
+          double2 w = tw[(r * k * step) & 511];
+          if (INV) w.y = -w.y;
+          v[r] = cmul(v[r], w);
+        }
+      }
+      dft8<INV>(v);
+      double2* d = dst + bi * bstride;
+      const int base = (j - k) * 8 + k;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) d[(base + r * Ns) * estride] = v[r];
+    }
+    __syncthreads();
+    double2* tmp = src;
+    src = dst;
+    dst = tmp;
+  }
+  return src;
+}
+
+__device__ __forceinline__ void load_twiddles(double2* tw_s, const double2* __restrict__ tw) {
+  for (int i = threadIdx.x; i < T; i += blockDim.x) tw_s[i] = tw[i];
+}
+
+// ---------------------------------------------------------------------------
+// K1: row pass.  grid (npairs * T / RROWS, C), 256 threads.
+// mode 0: image tiles of x; mode 1: kernel embedding (spectrum setup; pair p:
+// p = 0 the kernel, p = 1 the flipped kernel, channel = grid.y).
+struct RowArgs {
+  Geo g;
+  const double* x;
+  double2* S;       // scratch (C, npairs, T, T)
+  const double2* tw;
+  int mode;
+  const double* kern;   // (kh, kw, C)
+};
+
+__device__ __forceinline__ void tile_origin(const Geo& g, int t, int& h0, int& w0) {
+  const int ty = t / g.ntX, tx = t - ty * g.ntX;
+  h0 = ty * g.Vh;
+  w0 = tx * g.Vw;
+}
+
+__global__ void __launch_bounds__(256) row_fwd_kernel(const __grid_constant__ RowArgs A) {
+  extern __shared__ __align__(16) double2 sm[];
+  double2* tw_s = sm;
+  double2* bufA = sm + T;
+  double2* bufB = bufA + RROWS * T;
+  const Geo& g = A.g;
+  const int c = blockIdx.y;
+  const int rowgroups = T / RROWS;
+  const int p = blockIdx.x / rowgroups, row0 = (blockIdx.x - p * rowgroups) * RROWS;
+  load_twiddles(tw_s, A.tw);
+  if (A.mode == 0) {
+    int h0a, w0a, h0b = 0, w0b = 0;
+    tile_origin(g, 2 * p, h0a, w0a);
+    const bool hasb = 2 * p + 1 < g.ntiles;
+    if (hasb) tile_origin(g, 2 * p + 1, h0b, w0b);
+    for (int e = threadIdx.x; e < RROWS * T; e += blockDim.x) {
+      const int rr = e / T, col = e - rr * T;
+      const int ha = h0a - g.rh + row0 + rr, wa = w0a - g.rw + col;
+      double re = 0.0, im = 0.0;
+      if (ha >= 0 && ha < g.H && wa >= 0 && wa < g.W) re = A.x[((int64_t)ha * g.W + wa) * g.C + c];
+      if (hasb) {
+        const int hb = h0b - g.rh + row0 + rr, wb = w0b - g.rw + col;
+        if (hb >= 0 && hb < g.H && wb >= 0 && wb < g.W) im = A.x[((int64_t)hb * g.W + wb) * g.C + c];
+      }
+      bufA[e] = make_double2(re, im);
+    }
+  } else {
+    for (int e = threadIdx.x; e < RROWS * T; e += blockDim.x) {
+      const int rr = e / T, col = e - rr * T, i = row0 + rr;
+      double v = 0.0;
+      if (i < g.kh && col < g.kw) {
+        const int ii = p ? g.kh - 1 - i : i, jj = p ? g.kw - 1 - col : col;
+        v = A.kern[(ii * g.kw + jj) * g.C + c];
+      }
+      bufA[e] = make_double2(v, 0.0);
+    }
+  }
+  __syncthreads();
+  double2* res = fft512<false, false>(bufA, bufB, RROWS, T, 1, tw_s);
+  double2* S = A.S + (((int64_t)c * g.npairs + p) * T + row0) * T;
+  for (int e = threadIdx.x; e < RROWS * T; e += blockDim.x) S[e] = res[e];
+}
+
+// ---------------------------------------------------------------------------
+// K2: column pass.  grid (npairs * T / CCOLS, C), 512 threads.
+// mode 0: forward, multiply by the spectrum, inverse (a stencil);
+// mode 1: forward only, store conj (spectrum setup: S -> spec).
+struct ColArgs {
+  Geo g;
+  double2* S;
+  const double2* spec;   // (C, T, T): conj(FFT2(kernel pad)), this direction
+  double2* spec_out;     // mode 1: (2, C, T, T)
+  const double2* tw;
+  int mode;
+  int npairs;            // pairs held in S for this pass
+};
+
+__global__ void __launch_bounds__(512) col_kernel(const __grid_constant__ ColArgs A) {
+  extern __shared__ __align__(16) double2 sm[];
+  double2* tw_s = sm;
+  double2* bufA = sm + T;
+  double2* bufB = bufA + CCOLS * T;
+  const int c = blockIdx.y;
+  const int strips = T / CCOLS;
+  const int p = blockIdx.x / strips, col0 = (blockIdx.x - p * strips) * CCOLS;
+  load_twiddles(tw_s, A.tw);
+  double2* S = A.S + ((int64_t)c * A.npairs + p) * T * T + col0;
+  for (int e = threadIdx.x; e < CCOLS * T; e += blockDim.x) {
+    const int r = e / CCOLS, q = e - r * CCOLS;
+    bufA[e] = S[(int64_t)r * T + q];
+  }
+  __syncthreads();
+  double2* f = fft512<false, true>(bufA, bufB, CCOLS, 1, CCOLS, tw_s);
+  if (A.mode == 1) {
+    double2* o = A.spec_out + (((int64_t)p * A.g.C + c) * T) * T + col0;
+    for (int e = threadIdx.x; e < CCOLS * T; e += blockDim.x) {
+      const int r = e / CCOLS, q = e - r * CCOLS;
+      const double2 v = f[e];
+      o[(int64_t)r * T + q] = make_double2(v.x, -v.y);
+    }
+    return;
+  }
+  const double2* K = A.spec + (int64_t)c * T * T + col0;
+  for (int e = threadIdx.x; e < CCOLS * T; e += blockDim.x) {
+    const int r = e / CCOLS, q = e - r * CCOLS;
+    f[e] = cmul(f[e], K[(int64_t)r * T + q]);
+  }
+  __syncthreads();
+  double2* other = (f == bufA) ? bufB : bufA;
+  double2* res = fft512<true, true>(f, other, CCOLS, 1, CCOLS, tw_s);
+  for (int e = threadIdx.x; e < CCOLS * T; e += blockDim.x) {
+    const int r = e / CCOLS, q = e - r * CCOLS;
+    S[(int64_t)r * T + q] = res[e];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: inverse row pass + crop + epilogue.  grid (npairs * T / RROWS, C), 256 threads.
+enum Epi { E_STORE = 0, E_RESID = 1, E_GRAD = 2, E_VALUE = 3, E_POWER = 4 };
+
+struct InvArgs {
+  Geo g;
+  const double2* S;
+  const double2* tw;
+  double* out;          // E_STORE / E_RESID / E_GRAD / E_POWER
+  const double* y;      // data (E_RESID, E_VALUE)
+  const double* xp;     // point of the TV term (E_GRAD, E_VALUE)
+  double alpha, nu;
+  int epi;
+  double* part;         // 2 partial sums per CTA: part[2 * cta + {0, 1}]
+};
+
+struct TvTerms {
+  double root0, root1, grad;
+};
+
+// Smoothed anisotropic TV at pixel (h, w, c) of xp (regularizers.py:46-67, 158-175).
+__device__ __forceinline__ TvTerms tv_at(const Geo& g, const double* __restrict__ X, int h, int w, int c, double nu,
+                                         bool want_grad) {
+  const int64_t o = ((int64_t)h * g.W + w) * g.C + c;
+  const int64_t rs = (int64_t)g.W * g.C;
+  const double nu2 = nu * nu;
+  const double x0 = X[o];
+  const double d0 = (h + 1 < g.H) ? X[o + rs] - x0 : 0.0;
+  const double d1 = (w + 1 < g.W) ? X[o + g.C] - x0 : 0.0;
+  TvTerms t;
+  t.root0 = sqrt(d0 * d0 + nu2);
+  t.root1 = sqrt(d1 * d1 + nu2);
+  t.grad = 0.0;
+  if (want_grad) {
+    double acc = 0.0;
+    if (h > 0) {
+      const double du = x0 - X[o - rs];
+      acc = acc + du / sqrt(du * du + nu2);
+    }
+    acc = acc - d0 / t.root0;
+    if (w > 0) {
+      const double dl = x0 - X[o - g.C];
+      acc = acc + dl / sqrt(dl * dl + nu2);
+    }
+    acc = acc - d1 / t.root1;
+    t.grad = acc;
+  }
+  return t;
+}
+
+__global__ void __launch_bounds__(256) row_inv_kernel(const __grid_constant__ InvArgs A) {
+  extern __shared__ __align__(16) double2 sm[];
+  __shared__ double red[40];
+  double2* tw_s = sm;
+  double2* bufA = sm + T;
+  double2* bufB = bufA + RROWS * T;
+  const Geo& g = A.g;
+  const int c = blockIdx.y;
+  const int rowgroups = T / RROWS;
+  const int p = blockIdx.x / rowgroups, row0 = (blockIdx.x - p * rowgroups) * RROWS;
+  load_twiddles(tw_s, A.tw);
+  const double2* S = A.S + (((int64_t)c * g.npairs + p) * T + row0) * T;
+  for (int e = threadIdx.x; e < RROWS * T; e += blockDim.x) bufA[e] = S[e];
+  __syncthreads();
+  const double2* res = fft512<true, false>(bufA, bufB, RROWS, T, 1, tw_s);
+  double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll 1
+  for (int half = 0; half < 2; ++half) {
+    const int t = 2 * p + half;
+    if (t >= g.ntiles) break;
+    int h0, w0;
+    tile_origin(g, t, h0, w0);
+    for (int e = threadIdx.x; e < RROWS * T; e += blockDim.x) {
+      const int rr = e / T, q = e - rr * T;
+      const int h = h0 + row0 + rr, w = w0 + q;
+      if (row0 + rr >= g.Vh || q >= g.Vw || h >= g.H || w >= g.W) continue;
+      const double v = (half ? res[e].y : res[e].x) * kInvT2;
+      const int64_t o = ((int64_t)h * g.W + w) * g.C + c;
+      switch (A.epi) {
+        case E_STORE: A.out[o] = v; break;
+        case E_POWER: A.out[o] = v; acc0 = acc0 + v * v; break;
+        case E_RESID: {
+          const double r = v - A.y[o];
+          A.out[o] = r;
+          acc0 = acc0 + r * r;
+          break;
+        }
+        case E_GRAD: {   // g = 2 adj + alpha grad J (lower_solvers.py:54-62); vg TV form (regularizers.py:173-174)
+          const TvTerms tv = tv_at(g, A.xp, h, w, c, A.nu, true);
+          const double gv = 2.0 * v + A.alpha * tv.grad;
+          A.out[o] = gv;
+          acc0 = acc0 + gv * gv;
+          acc1 = acc1 + (tv.root0 + tv.root1);
+          break;
+        }
+        case E_VALUE: {  // sum (Bx - y)^2 and tv_value = sum(sqrt(d^2 + nu^2) - nu) (regularizers.py:70-72)
+          const double r = v - A.y[o];
+          acc0 = acc0 + r * r;
+          const TvTerms tv = tv_at(g, A.xp, h, w, c, A.nu, false);
+          acc1 = acc1 + ((tv.root0 - A.nu) + (tv.root1 - A.nu));
+          break;
+        }
+        default: break;
+      }
+    }
+  }
+  if (A.part) {
+    const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+    const double s0 = block_sum(acc0, red);
+    const double s1 = block_sum(acc1, red);
+    if (threadIdx.x == 0) {
+      A.part[2 * cta] = s0;
+      A.part[2 * cta + 1] = s1;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// elementwise steps of the solvers + fixed-order partials
+enum VecOp {
+  V_EXTRAP = 0,   // out = x + beta * (x - xp)                 (lower_solvers.py:197)
+  V_STEPDIV = 1,  // out = y - g / L                           (:173, :207)
+  V_STEPMUL = 2,  // out = x - step * g                        (:165)
+  V_DIVNORM = 3,  // out = x / a                               (operators.py:150, 162)
+  V_DOTDIFF = 4,  // partial: sum g * (x - xp)                 (:209)
+  V_NORM2 = 5,    // partial: sum x * x
+  V_COPY = 6
+};
+constexpr int kVecGrid = 1184;   // 8 x 148
+
+__global__ void __launch_bounds__(256) vec_kernel(int op, int64_t n, double a, const double* __restrict__ x,
+                                                  const double* __restrict__ xp, const double* __restrict__ gg,
+                                                  double* __restrict__ out, double* part) {
+  __shared__ double red[40];
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    switch (op) {
+      case V_EXTRAP: out[i] = x[i] + a * (x[i] - xp[i]); break;
+      case V_STEPDIV: out[i] = x[i] - gg[i] / a; break;
+      case V_STEPMUL: out[i] = x[i] - a * gg[i]; break;
+      case V_DIVNORM: out[i] = x[i] / a; break;
+      case V_DOTDIFF: acc = acc + gg[i] * (x[i] - xp[i]); break;
+      case V_NORM2: acc = acc + x[i] * x[i]; break;
+      case V_COPY: out[i] = x[i]; break;
+      default: break;
+    }
+  }
+  if (part) {
+    const double s = block_sum(acc, red);
+    if (threadIdx.x == 0) part[2 * blockIdx.x] = s;
+  }
+}
+
+// Fixed-order fold of k interleaved partial streams (part[k * i + j], i < n):
+// one CTA, contiguous per-thread chunks, then block_sum.
+__global__ void __launch_bounds__(1024) fold_kernel(const double* __restrict__ part, int n, int k, double* out) {
+  __shared__ double red[40];
+  const int per = (n + blockDim.x - 1) / blockDim.x;
+  for (int j = 0; j < k; ++j) {
+    double acc = 0.0;
+    const int i0 = threadIdx.x * per, i1 = min(n, i0 + per);
+    for (int i = i0; i < i1; ++i) acc = acc + part[(int64_t)k * i + j];
+    const double s = block_sum(acc, red);
+    if (threadIdx.x == 0) out[j] = s;
+  }
+}
+
+}  // namespace fft
+}  // namespace adp
+
+// ===========================================================================
+// host side
+using namespace adp;
+using namespace adp::fft;
+
+struct adp_fft_plan {
+  Geo g;
+  int64_t N = 0;
+  double2* S = nullptr;        // (C, npairs, T, T)
+  double2* spec = nullptr;     // (2, C, T, T): [0] apply, [1] adjoint
+  double2* tw = nullptr;       // T twiddles exp(-2 pi i m / T)
+  double* part = nullptr;      // partials (2 per CTA)
+  double* red = nullptr;       // fold results (device)
+  double* hred = nullptr;      // pinned host copy
+  double* buf[6] = {};         // solver images
+  int nrow_ctas = 0;
+  const void* spec_kernel = nullptr;   // kernel pointer the spectra were built from (this call)
+  size_t bytes = 0;
+};
+
+namespace {
+
+constexpr size_t kRowSmem = (size_t)(T + 2 * RROWS * T) * sizeof(double2);
+constexpr size_t kColSmem = (size_t)(T + 2 * CCOLS * T) * sizeof(double2);
+
+int setup_attrs() {
+  static int done = 0;
+  if (done) return ADP_OK;
+  if (cudaFuncSetAttribute(row_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmem) != cudaSuccess ||
+      cudaFuncSetAttribute(row_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmem) != cudaSuccess ||
+      cudaFuncSetAttribute(col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kColSmem) != cudaSuccess)
+    return dense_fail(ADP_ERR_CUDA, "fft: shared-memory attributes");
+  done = 1;
+  return ADP_OK;
+}
+
+int check_launch(const char* what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return dense_fail(ADP_ERR_CUDA, (std::string(what) + ": " + cudaGetErrorString(e)).c_str());
+  return ADP_OK;
+}
+
+// Spectra of the kernel and of the flipped kernel (conj(FFT2(pad))), into P->spec.
+int build_spectra(adp_fft_plan* P, const double* kern, cudaStream_t st) {
+  const Geo& g = P->g;
+  Geo kg = g;
+  kg.npairs = 2;   // S slots: pair 0 = kernel, pair 1 = flipped kernel
+  RowArgs ra{kg, nullptr, P->S, P->tw, 1, kern};
+  row_fwd_kernel<<<dim3(2 * T / RROWS, g.C), 256, kRowSmem, st>>>(ra);
+  ColArgs ca{kg, P->S, nullptr, P->spec, P->tw, 1, 2};
+  col_kernel<<<dim3(2 * T / CCOLS, g.C), 512, kColSmem, st>>>(ca);
+  return check_launch("fft spectra");
+}
+
+// One stencil: out/epilogue from x with the apply (adj = 0) or adjoint (adj = 1) spectrum.
+int stencil(adp_fft_plan* P, int adj, const double* x, int epi, double* out, const double* y, const double* xp,
+            double alpha, double nu, bool partials, cudaStream_t st) {
+  const Geo& g = P->g;
+  const dim3 rgrid(g.npairs * T / RROWS, g.C);
+  RowArgs ra{g, x, P->S, P->tw, 0, nullptr};
+  row_fwd_kernel<<<rgrid, 256, kRowSmem, st>>>(ra);
+  ColArgs ca{g, P->S, P->spec + (size_t)adj * g.C * T * T, nullptr, P->tw, 0, g.npairs};
+  col_kernel<<<dim3(g.npairs * T / CCOLS, g.C), 512, kColSmem, st>>>(ca);
+  InvArgs ia{g, P->S, P->tw, out, y, xp, alpha, nu, epi, partials ? P->part : nullptr};
+  row_inv_kernel<<<rgrid, 256, kRowSmem, st>>>(ia);
+  return check_launch("fft stencil");
+}
+
+int fold(adp_fft_plan* P, int n, int k, double* host, cudaStream_t st) {
+  fold_kernel<<<1, 1024, 0, st>>>(P->part, n, k, P->red);
+  cudaMemcpyAsync(P->hred, P->red, k * sizeof(double), cudaMemcpyDeviceToHost, st);
+  const cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) return dense_fail(ADP_ERR_CUDA, cudaGetErrorString(e));
+  for (int j = 0; j < k; ++j) host[j] = P->hred[j];
+  return ADP_OK;
+}
+
+int vec(adp_fft_plan* P, int op, double a, const double* x, const double* xp, const double* g, double* out,
+        double* host_red, cudaStream_t st) {
+  const bool red = (op == V_DOTDIFF || op == V_NORM2);
+  vec_kernel<<<kVecGrid, 256, 0, st>>>(op, P->N, a, x, xp, g, out, red ? P->part : nullptr);
+  int rc = check_launch("fft vec");
+  if (rc != ADP_OK || !red) return rc;
+  double r[2];
+  rc = fold(P, kVecGrid, 2, r, st);
+  *host_red = r[0];
+  return rc;
+}
+
+int rowctas(const adp_fft_plan* P) { return P->g.npairs * (T / RROWS) * P->g.C; }
+
+// value and gradient of the lower objective at x (lower_solvers.py:50-63):
+// r = Bx - y (stored in buf R), g = 2 B^T r + alpha grad TV(x); value = sum r^2 + alpha (sum root - nu * 2N)
+int vg(adp_fft_plan* P, const adp_lower* lp, const double* x, double* g, double* value, double* gn2,
+       cudaStream_t st) {
+  double* R = P->buf[5];
+  int rc = stencil(P, 0, x, E_RESID, R, (const double*)lp->y, nullptr, 0.0, 0.0, true, st);
+  if (rc) return rc;
+  double fit[2];
+  if ((rc = fold(P, rowctas(P), 2, fit, st))) return rc;
+  rc = stencil(P, 1, R, E_GRAD, g, nullptr, x, lp->alpha, lp->nu, true, st);
+  if (rc) return rc;
+  double gt[2];
+  if ((rc = fold(P, rowctas(P), 2, gt, st))) return rc;
+  const double tv = gt[1] - lp->nu * (double)(2 * P->N);
+  if (value) *value = fit[0] + lp->alpha * tv;
+  if (gn2) *gn2 = gt[0];
+  return ADP_OK;
+}
+
+// lower_value (lower_solvers.py:37-39): sum (Bx - y)^2 + alpha tv_value(x)
+int value(adp_fft_plan* P, const adp_lower* lp, const double* x, double* val, cudaStream_t st) {
+  int rc = stencil(P, 0, x, E_VALUE, nullptr, (const double*)lp->y, x, 0.0, lp->nu, true, st);
+  if (rc) return rc;
+  double t[2];
+  if ((rc = fold(P, rowctas(P), 2, t, st))) return rc;
+  *val = t[0] + lp->alpha * t[1];
+  return ADP_OK;
+}
+
+// op_norm_sq (operators.py:137-173)
+int power(adp_fft_plan* P, const double* v0, int max_iters, double tol, double* lam_out, int* conv_out,
+          int* iters_out, cudaStream_t st) {
+  double* V = P->buf[3];
+  double* Wb = P->buf[4];
+  double* Bv = P->buf[5];
+  double n2 = 0.0;
+  int rc = vec(P, V_NORM2, 0.0, v0, nullptr, nullptr, nullptr, &n2, st);
+  if (rc) return rc;
+  if ((rc = vec(P, V_DIVNORM, std::sqrt(n2), v0, nullptr, nullptr, V, nullptr, st))) return rc;
+  double lam = 0.0;
+  int converged = 0, it = 0;
+  for (; it < max_iters; ++it) {
+    if ((rc = stencil(P, 0, V, E_STORE, Bv, nullptr, nullptr, 0.0, 0.0, false, st))) return rc;
+    if ((rc = stencil(P, 1, Bv, E_POWER, Wb, nullptr, nullptr, 0.0, 0.0, true, st))) return rc;
+    double w2[2];
+    if ((rc = fold(P, rowctas(P), 2, w2, st))) return rc;
+    const double lam_new = std::sqrt(w2[0]);
+    if (lam_new == 0.0) {
+      lam = 0.0;
+      converged = 1;
+      ++it;
+      break;
+    }
+    if ((rc = vec(P, V_DIVNORM, lam_new, Wb, nullptr, nullptr, V, nullptr, st))) return rc;
+    if (std::fabs(lam_new - lam) <= tol * std::max(lam_new, 1e-300)) {
+      lam = lam_new;
+      converged = 1;
+      ++it;
+      break;
+    }
+    lam = lam_new;
+  }
+  *lam_out = lam;
+  if (conv_out) *conv_out = converged;
+  if (iters_out) *iters_out = it;
+  return ADP_OK;
+}
+
+int prepare(adp_fft_plan* P, const void* kernel, cudaStream_t st) {
+  int rc = setup_attrs();
+  if (rc) return rc;
+  return build_spectra(P, (const double*)kernel, st);
+}
+
+}  // namespace
+
+extern "C" int adp_fft_plan_create(adp_fft_plan** out, int32_t H, int32_t W, int32_t C, int32_t kh, int32_t kw) {
+  if (!out || H < 1 || W < 1 || C < 1 || kh < 1 || kw < 1 || kh % 2 == 0 || kw % 2 == 0)
+    return dense_fail(ADP_ERR_ARG, "fft plan: bad shape");
+  if (kh > T / 2 || kw > T / 2) return dense_fail(ADP_ERR_UNSUPPORTED, "fft plan: kernel larger than 256 taps");
+  adp_fft_plan* P = new adp_fft_plan();
+  Geo& g = P->g;
+  g.H = H; g.W = W; g.C = C; g.kh = kh; g.kw = kw; g.rh = kh / 2; g.rw = kw / 2;
+  g.Vh = T - kh + 1; g.Vw = T - kw + 1;
+  g.ntY = (H + g.Vh - 1) / g.Vh; g.ntX = (W + g.Vw - 1) / g.Vw;
+  g.ntiles = g.ntY * g.ntX;
+  g.npairs = (g.ntiles + 1) / 2;
+  P->N = (int64_t)H * W * C;
+  // >= 2 pair slots: the spectrum setup transforms the kernel and its flip together
+  const size_t sbytes = (size_t)C * std::max(2, g.npairs) * T * T * sizeof(double2);
+  const size_t specb = (size_t)2 * C * T * T * sizeof(double2);
+  const int nparts = std::max(rowctas(P), kVecGrid);
+  bool ok = cudaMalloc(&P->S, sbytes) == cudaSuccess && cudaMalloc(&P->spec, specb) == cudaSuccess &&
+            cudaMalloc(&P->tw, T * sizeof(double2)) == cudaSuccess &&
+            cudaMalloc(&P->part, (size_t)2 * nparts * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&P->red, 8 * sizeof(double)) == cudaSuccess &&
+            cudaMallocHost(&P->hred, 8 * sizeof(double)) == cudaSuccess;
+  for (int i = 0; ok && i < 6; ++i) ok = cudaMalloc(&P->buf[i], (size_t)P->N * sizeof(double)) == cudaSuccess;
+  if (!ok) {
+    adp_fft_plan_destroy(P);
+    return dense_fail(ADP_ERR_CUDA, "fft plan: device allocation failed");
+  }
+  P->bytes = sbytes + specb + (size_t)6 * P->N * sizeof(double) + 2 * nparts * sizeof(double);
+  // accurately rounded twiddles exp(-2 pi i m / T)
+  std::vector<double2> tw(T);
+  for (int m = 0; m < T; ++m) {
+    const long double a = -2.0L * 3.141592653589793238462643383279502884L * (long double)m / (long double)T;
+    tw[m] = make_double2((double)cosl(a), (double)sinl(a));
+  }
+  cudaMemcpy(P->tw, tw.data(), T * sizeof(double2), cudaMemcpyHostToDevice);
+  *out = P;
+  return ADP_OK;
+}
+
+extern "C" void adp_fft_plan_destroy(adp_fft_plan* P) {
+  if (!P) return;
+  cudaFree(P->S);
+  cudaFree(P->spec);
+  cudaFree(P->tw);
+  cudaFree(P->part);
+  cudaFree(P->red);
+  if (P->hred) cudaFreeHost(P->hred);
+  for (double* b : P->buf) cudaFree(b);
+  delete P;
+}
+
+extern "C" size_t adp_fft_plan_workspace_bytes(const adp_fft_plan* P) { return P ? P->bytes : 0; }
+
+extern "C" int adp_fft_apply(adp_fft_plan* P, const void* kernel, int32_t adjoint, const void* x, void* out,
+                             void* stream) {
+  if (!P || !kernel || !x || !out) return dense_fail(ADP_ERR_ARG, "fft apply: null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = prepare(P, kernel, st);
+  if (rc) return rc;
+  return stencil(P, adjoint ? 1 : 0, (const double*)x, E_STORE, (double*)out, nullptr, nullptr, 0.0, 0.0, false, st);
+}
+
+extern "C" int adp_fft_lower_value(adp_fft_plan* P, const adp_lower* lp, const void* x, double* val, void* stream) {
+  if (!P || !lp || !x || !val) return dense_fail(ADP_ERR_ARG, "fft lower_value: null argument");
+  if (lp->reg != ADP_REG_TV) return dense_fail(ADP_ERR_UNSUPPORTED, "fft path: smoothed TV only");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = prepare(P, lp->kernel, st);
+  if (rc) return rc;
+  return value(P, lp, (const double*)x, val, st);
+}
+
+extern "C" int adp_fft_lower_value_and_grad(adp_fft_plan* P, const adp_lower* lp, const void* x, double* val,
+                                            void* g, void* stream) {
+  if (!P || !lp || !x || !g) return dense_fail(ADP_ERR_ARG, "fft lower_value_and_grad: null argument");
+  if (lp->reg != ADP_REG_TV) return dense_fail(ADP_ERR_UNSUPPORTED, "fft path: smoothed TV only");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = prepare(P, lp->kernel, st);
+  if (rc) return rc;
+  double v = 0.0, gn2 = 0.0;
+  rc = vg(P, lp, (const double*)x, (double*)g, &v, &gn2, st);
+  if (val) *val = v;
+  return rc;
+}
+
+extern "C" int adp_fft_op_norm_sq(adp_fft_plan* P, const void* kernel, const void* v0, int32_t max_iters, double tol,
+                                  double* lam, int32_t* converged, int32_t* iters, void* stream) {
+  if (!P || !kernel || !v0 || !lam) return dense_fail(ADP_ERR_ARG, "fft op_norm_sq: null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = prepare(P, kernel, st);
+  if (rc) return rc;
+  int c = 0, it = 0;
+  rc = power(P, (const double*)v0, max_iters, tol, lam, &c, &it, st);
+  if (converged) *converged = c;
+  if (iters) *iters = it;
+  return rc;
+}
+
+// solve_lower (lower_solvers.py:104-213) on the FFT stencils; the scalar
+// control flow runs here on the host in the reference's order, one small
+// device->host read per reduction (negligible next to three 2-D FFT
+// stencils per iteration at the sizes this path is for).
+extern "C" int adp_fft_lower_solve(adp_fft_plan* P, const adp_lower* lp, const void* x0, void* x_out,
+                                   const adp_solve_args* a, adp_solve_result* res, void* stream) {
+  if (!P || !lp || !x0 || !x_out || !a || !res) return dense_fail(ADP_ERR_ARG, "fft solve: null argument");
+  if (lp->reg != ADP_REG_TV) return dense_fail(ADP_ERR_UNSUPPORTED, "fft path: smoothed TV only");
+  if (!(a->eps > 0) || !(a->mu > 0)) return dense_fail(ADP_ERR_ARG, "eps and mu must be > 0");
+  cudaStream_t st = (cudaStream_t)stream;
+  *res = adp_solve_result{};
+  int rc = prepare(P, lp->kernel, st);
+  if (rc) return rc;
+  const double tol = a->eps * a->mu;
+  const int64_t nbytes = P->N * (int64_t)sizeof(double);
+  // --- step size / Lipschitz constant (L_of_b, lower_solvers.py:90-96)
+  double lip, step;
+  res->norm_sq = a->norm_sq;
+  if (a->step_size > 0) {
+    step = a->step_size;
+    lip = 1.0 / step;
+  } else {
+    if (a->norm_sq < 0) {
+      if (!a->v0) return dense_fail(ADP_ERR_ARG, "fft solve: power-iteration start vector missing");
+      int pc = 0, pit = 0;
+      if ((rc = power(P, (const double*)a->v0, a->norm_max_iters, a->norm_tol, &res->norm_sq, &pc, &pit, st)))
+        return rc;
+      res->power_converged = pc;
+      res->power_iters = pit;
+    }
+    lip = 2.0 * res->norm_sq + lp->alpha * (8.0 / lp->nu);
+    step = 1.0 / lip;
+  }
+  res->lip = lip;
+  // buffers: X (iterate), XP (previous), Y (extrapolation), XC (candidate), G; buf[5] = residual
+  double* X = P->buf[0];
+  double* XP = P->buf[1];
+  double* Y = P->buf[2];
+  double* XC = P->buf[3];
+  double* G = P->buf[4];
+  cudaMemcpyAsync(X, x0, nbytes, cudaMemcpyDeviceToDevice, st);
+  cudaMemcpyAsync(XP, x0, nbytes, cudaMemcpyDeviceToDevice, st);
+  auto finish = [&](const double* xr, double gn2, int t, int conv) {
+    cudaMemcpyAsync(x_out, xr, nbytes, cudaMemcpyDeviceToDevice, st);
+    res->grad_norm = std::sqrt(gn2);
+    res->iters = t;
+    res->converged = conv;
+    const cudaError_t e = cudaStreamSynchronize(st);
+    return e == cudaSuccess ? ADP_OK : dense_fail(ADP_ERR_CUDA, cudaGetErrorString(e));
+  };
+  auto diverged = [&](int t) {
+    res->status = ADP_STATUS_DIVERGED;
+    res->fail_iter = t;
+    return ADP_OK;
+  };
+  // backtracked step from y (lower_solvers.py:170-177): XC = y - g / L_try
+  auto backtrack = [&](const double* yv, double h_y, double gn, double lip_try, double* step_out, int* ok) -> int {
+    for (int k = 0; k < 60; ++k) {
+      int r = vec(P, V_STEPDIV, lip_try, yv, nullptr, G, XC, nullptr, st);
+      if (r) return r;
+      double hv = 0.0;
+      if ((r = value(P, lp, XC, &hv, st))) return r;
+      res->value_evals++;
+      if (hv <= h_y - 0.5 * gn * gn / lip_try + 1e-15 * std::fabs(h_y)) {
+        *step_out = 1.0 / lip_try;
+        *ok = 1;
+        return ADP_OK;
+      }
+      lip_try *= 2.0;
+    }
+    *ok = 0;
+    return ADP_OK;
+  };
+  if (a->method == ADP_METHOD_PROXGRAD) {   // _gradient_descent (:154-167)
+    double h_x = 0.0, gn2 = 0.0;
+    if ((rc = vg(P, lp, X, G, &h_x, &gn2, st))) return rc;
+    res->vg_evals++;
+    for (int t = 0; t < a->max_iters; ++t) {
+      const double gn = std::sqrt(gn2);
+      if (!std::isfinite(gn)) return diverged(t);
+      if (gn <= tol) return finish(X, gn2, t, 1);
+      if (a->adaptive) {
+        int ok = 0;
+        double s = 0.0;
+        if ((rc = backtrack(X, h_x, gn, 1.0 / step, &s, &ok))) return rc;
+        if (!ok) { res->status = ADP_STATUS_BT_FAIL; return ADP_OK; }
+        step = s;
+        std::swap(X, XC);
+      } else {
+        if ((rc = vec(P, V_STEPMUL, step, X, nullptr, G, XC, nullptr, st))) return rc;
+        std::swap(X, XC);
+      }
+      if ((rc = vg(P, lp, X, G, &h_x, &gn2, st))) return rc;
+      res->vg_evals++;
+    }
+    return finish(X, gn2, a->max_iters, std::sqrt(gn2) <= tol);
+  }
+  // _accelerated (:180-213)
+  double theta = 0.0;
+  if (a->method == ADP_METHOD_FISTA_SC) {
+    const double q = std::min(a->mu / lip, 1.0);
+    theta = (1.0 - std::sqrt(q)) / (1.0 + std::sqrt(q));
+  }
+  double t_mom = 1.0, lip_t = lip;
+  bool xp_is_x = true;   // x_prev == x (start, and after a restart)
+  for (int t = 0; t < a->max_iters; ++t) {
+    double beta;
+    if (a->method == ADP_METHOD_FISTA_SC) {
+      beta = theta;
+    } else {
+      const double t_next = 0.5 * (1.0 + std::sqrt(1.0 + 4.0 * t_mom * t_mom));
+      beta = (t_mom - 1.0) / t_next;
+      t_mom = t_next;
+    }
+    if ((rc = vec(P, V_EXTRAP, beta, X, xp_is_x ? X : XP, nullptr, Y, nullptr, st))) return rc;
+    double h_y = 0.0, gn2 = 0.0;
+    if ((rc = vg(P, lp, Y, G, &h_y, &gn2, st))) return rc;
+    res->vg_evals++;
+    const double gn = std::sqrt(gn2);
+    if (!std::isfinite(gn)) return diverged(t);
+    if (gn <= tol) return finish(Y, gn2, t, 1);
+    // x_prev = x; x = step from y
+    if (a->adaptive) {
+      int ok = 0;
+      double s = 0.0;
+      if ((rc = backtrack(Y, h_y, gn, lip_t, &s, &ok))) return rc;
+      if (!ok) { res->status = ADP_STATUS_BT_FAIL; return ADP_OK; }
+      lip_t = std::max(1.0 / s * 0.9, lip * 1e-8);
+    } else {
+      if ((rc = vec(P, V_STEPDIV, lip_t, Y, nullptr, G, XC, nullptr, st))) return rc;
+    }
+    // rotate: XP <- X, X <- XC
+    std::swap(XP, X);
+    std::swap(X, XC);
+    xp_is_x = false;
+    if (a->method == ADP_METHOD_AGD) {   // gradient restart: vdot(g, x - x_prev) > 0
+      double d = 0.0;
+      if ((rc = vec(P, V_DOTDIFF, 0.0, X, XP, G, nullptr, &d, st))) return rc;
+      if (d > 0) {
+        t_mom = 1.0;
+        xp_is_x = true;
+        res->restarts++;
+      }
+    }
+  }
+  double gn2 = 0.0;
+  if ((rc = vg(P, lp, X, G, nullptr, &gn2, st))) return rc;
+  return finish(X, gn2, a->max_iters, std::sqrt(gn2) <= tol);
+}

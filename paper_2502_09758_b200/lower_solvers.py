@@ -81,11 +81,20 @@ def _check_reg_smooth(p: LowerProblem):
             reg._check_smooth()
 
 
+def _fft(p: LowerProblem) -> bool:
+    """FFT stencil mode applies to the depthwise 2-D operator."""
+    return nat.is_fft() and isinstance(p.op, ConvOperator)
+
+
 def lower_value(p: LowerProblem, x) -> float:
     """h(x) = sum((Bx - y)^2) + alpha * J(x) (lower_solvers.py:37-39)."""
     plan, s, keep = _native_lower(p)
     xd = nat.to_dev(x, p.op.signal_shape)
     val = ctypes.c_double()
+    if _fft(p):
+        nat.check(nat.lib().adp_fft_lower_value(p.op.fft_plan().handle, ctypes.byref(s), nat.ptr(xd),
+                                                ctypes.byref(val), nat.stream_ptr()), "lower_value")
+        return float(val.value)
     nat.check(nat.lib().adp_lower_value(plan.handle, ctypes.byref(s), nat.ptr(xd), ctypes.byref(val),
                                         nat.stream_ptr()), "lower_value")
     return float(val.value)
@@ -97,6 +106,10 @@ def lower_grad(p: LowerProblem, x):
     plan, s, keep = _native_lower(p)
     xd = nat.to_dev(x, p.op.signal_shape)
     g = nat.empty_like_dev(p.op.signal_shape)
+    if _fft(p):
+        nat.check(nat.lib().adp_fft_lower_value_and_grad(p.op.fft_plan().handle, ctypes.byref(s), nat.ptr(xd),
+                                                         None, nat.ptr(g), nat.stream_ptr()), "lower_grad")
+        return nat.like(g, x)
     nat.check(nat.lib().adp_lower_grad(plan.handle, ctypes.byref(s), nat.ptr(xd), nat.ptr(g), nat.stream_ptr()),
               "lower_grad")
     return nat.like(g, x)
@@ -109,8 +122,10 @@ def lower_value_and_grad(p: LowerProblem, x):
     xd = nat.to_dev(x, p.op.signal_shape)
     g = nat.empty_like_dev(p.op.signal_shape)
     val = ctypes.c_double()
-    nat.check(nat.lib().adp_lower_value_and_grad(plan.handle, ctypes.byref(s), nat.ptr(xd), ctypes.byref(val),
-                                                 nat.ptr(g), nat.stream_ptr()), "lower_value_and_grad")
+    fn = nat.lib().adp_fft_lower_value_and_grad if _fft(p) else nat.lib().adp_lower_value_and_grad
+    handle = p.op.fft_plan().handle if _fft(p) else plan.handle
+    nat.check(fn(handle, ctypes.byref(s), nat.ptr(xd), ctypes.byref(val), nat.ptr(g), nat.stream_ptr()),
+              "lower_value_and_grad")
     return float(val.value), nat.like(g, x)
 
 
@@ -182,8 +197,10 @@ def solve_lower(p: LowerProblem, x0, eps: float, mu: float, max_iters: int = 300
     v0 = nat.power_start(p.op.signal_shape)
     a.v0 = v0.data_ptr()
     r = nat.SolveResult()
-    nat.check(nat.lib().adp_lower_solve(plan.handle, ctypes.byref(s), nat.ptr(xd), nat.ptr(out), ctypes.byref(a),
-                                        ctypes.byref(r), nat.stream_ptr()), "solve_lower")
+    fn = nat.lib().adp_fft_lower_solve if _fft(p) else nat.lib().adp_lower_solve
+    handle = p.op.fft_plan().handle if _fft(p) else plan.handle
+    nat.check(fn(handle, ctypes.byref(s), nat.ptr(xd), nat.ptr(out), ctypes.byref(a), ctypes.byref(r),
+                 nat.stream_ptr()), "solve_lower")
     if step_size is None and p.op._norm_sq is None:
         if not r.power_converged:
             import warnings

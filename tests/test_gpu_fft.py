@@ -1,0 +1,132 @@
+"""FFT stencil mode: overlap-save tile FFTs for the
+depthwise correlation, the lower objective and the AGD solve.  A tolerance
+mode: primitives within 1e-12 of the reference arithmetic (CPU oracle =
+scipy.ndimage order, pinned to the real reference), short solves within
+1e-9, long solves to the same objective; fixed-order reductions make every
+run bitwise reproducible."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a, b = np.asarray(a, dtype=float), np.asarray(b, dtype=float)
+    return float(np.abs(a - b).max() / max(np.abs(b).max(), 1e-300))
+
+
+def gauss(k, sigma, c, rng=None):
+    g = np.arange(k) - k // 2
+    w = np.exp(-(g[:, None] ** 2 + g[None, :] ** 2) / (2 * sigma**2))
+    w = np.repeat(w[:, :, None], c, axis=2)
+    if rng is not None:
+        w = w * rng.uniform(0.5, 1.5, w.shape)
+    return w / w.sum(axis=(0, 1), keepdims=True)
+
+
+# (shape, K): single tile / one pair; 2 x 3 tiles (3 full pairs); 3 tiles (a pair with an empty slot);
+# K = 31 at the c5 tile geometry; non-square kernel
+CASES = [((100, 90, 3), (9, 9)), ((500, 1000, 1), (31, 31)), ((700, 300, 2), (15, 15)),
+         ((600, 620, 3), (31, 31)), ((257, 129, 1), (5, 11))]
+
+
+@pytest.fixture(autouse=True)
+def fft_mode(adp):
+    with adp.precision("float64", "fft"):
+        yield
+
+
+@pytest.mark.parametrize("shape,ks", CASES)
+def test_fft_apply_adjoint(adp, orc, shape, ks):
+    rng = np.random.default_rng(shape[0] + ks[0])
+    kern = rng.uniform(0.0, 1.0, ks + (shape[2],))
+    kern /= kern.sum(axis=(0, 1), keepdims=True)
+    x = rng.uniform(0.0, 1.0, shape)
+    v = rng.standard_normal(shape)
+    op = adp.ConvOperator(adp.Kernel(kern, adp.DEPTHWISE2D), shape)
+    bx, btv = op.apply(x), op.adjoint(v)
+    assert rel(bx, orc.correlate(x, kern)) <= 1e-13
+    assert rel(btv, orc.correlate(v, kern, flip=True)) <= 1e-13
+    lhs, rhs = float(np.vdot(bx, v)), float(np.vdot(x, btv))
+    assert abs(lhs - rhs) <= 1e-12 * abs(lhs)
+    assert np.array_equal(op.apply(x), bx)           # bitwise reproducible
+
+
+def _problem(adp, orc, shape, k, sigma, seed):
+    rng = np.random.default_rng(seed)
+    kern = gauss(k, sigma, shape[2], rng)
+    xt = rng.uniform(0.0, 1.0, shape)
+    y = orc.correlate(xt, kern) + 0.01 * rng.standard_normal(shape)
+    p = adp.LowerProblem(adp.ConvOperator(adp.Kernel(kern, adp.DEPTHWISE2D), shape), y, 0.6, adp.SmoothedTV(1e-4))
+    po = orc.Lower(orc.Conv(kern, shape), y, 0.6, orc.TV(1e-4))
+    return p, po, y, rng
+
+
+@pytest.mark.parametrize("shape,k", [((300, 260, 3), 15), ((520, 500, 1), 31)])
+def test_fft_lower_objective(adp, orc, shape, k):
+    p, po, y, rng = _problem(adp, orc, shape, k, k / 5.0, 5)
+    x = y + 0.05 * rng.standard_normal(shape)
+    v, g = adp.lower_value_and_grad(p, x)
+    vo, go = orc.lower_value_and_grad(po, x)
+    assert abs(v - vo) <= 1e-12 * abs(vo)
+    assert rel(g, go) <= 1e-11
+    assert abs(adp.lower_value(p, x) - orc.lower_value(po, x)) <= 1e-12 * abs(vo)
+    assert rel(adp.lower_grad(p, x), go) <= 1e-11
+
+
+def test_fft_op_norm_sq(adp, orc):
+    shape = (200, 230, 2)
+    rng = np.random.default_rng(2)
+    kern = gauss(31, 6.0, 2, rng)
+    op = adp.ConvOperator(adp.Kernel(kern, adp.DEPTHWISE2D), shape)
+    lam = adp.op_norm_sq(op, 300, 1e-4)
+    lam_o, _, _ = orc.op_norm_sq(orc.Conv(kern, shape), 300, 1e-4)
+    assert abs(lam - lam_o) <= 1e-10 * lam_o
+
+
+@pytest.mark.parametrize("shape,k,iters", [((160, 150, 3), 15, 12), ((300, 280, 1), 31, 12)])
+def test_fft_solve_short_matches_oracle(adp, orc, shape, k, iters):
+    """A few adaptive-AGD iterations: FFT rounding (1e-15) has not grown yet."""
+    p, po, y, _ = _problem(adp, orc, shape, k, k / 5.0, 9)
+    res = adp.solve_lower(p, y, 1e-12, 10.0, max_iters=iters, method="agd", adaptive=True)
+    xo, gno, it_o, _ = orc.solve_lower(po, y, 1e-12, 10.0, max_iters=iters, method="agd", adaptive=True)
+    assert res.iters == it_o == iters
+    assert rel(res.x_tilde, xo) <= 1e-9
+    assert abs(res.grad_norm - gno) <= 1e-7 * gno
+
+
+def test_fft_solve_long_objective_and_determinism(adp, orc):
+    """300 iterations: pixel trajectories separate at the TV's sensitivity
+    (SURVEY.md App. C), the objective reached agrees with the direct (fast)
+    device solve; two FFT runs are bitwise identical."""
+    shape, k = (256, 256, 1), 31
+    p, po, y, _ = _problem(adp, orc, shape, k, 6.0, 4)
+    r1 = adp.solve_lower(p, y, 1e-9, 10.0, max_iters=300, method="agd", adaptive=True)
+    r2 = adp.solve_lower(p, y, 1e-9, 10.0, max_iters=300, method="agd", adaptive=True)
+    assert np.array_equal(r1.x_tilde, r2.x_tilde) and r1.grad_norm == r2.grad_norm
+    with adp.precision("float64", "fast"):
+        p2 = adp.LowerProblem(adp.ConvOperator(p.op.kernel, shape), y, 0.6, adp.SmoothedTV(1e-4))
+        rd = adp.solve_lower(p2, y, 1e-9, 10.0, max_iters=300, method="agd", adaptive=True)
+        hd = adp.lower_value(p2, rd.x_tilde)
+    h1 = orc.lower_value(po, r1.x_tilde)
+    assert abs(h1 - hd) <= 1e-6 * abs(hd)
+    assert rel(r1.x_tilde, rd.x_tilde) <= 1e-3
+
+
+def test_fft_solve_methods_and_errors(adp, orc):
+    shape = (120, 100, 2)
+    p, po, y, _ = _problem(adp, orc, shape, 9, 2.0, 3)
+    for method, adaptive in (("proxgrad", False), ("proxgrad", True), ("agd", False), ("fista_sc", True)):
+        r = adp.solve_lower(p, y, 1e-12, 10.0, max_iters=8, method=method, adaptive=adaptive)
+        xo, gno, it_o, _ = orc.solve_lower(po, y, 1e-12, 10.0, max_iters=8, method=method, adaptive=adaptive)
+        assert r.iters == it_o
+        assert rel(r.x_tilde, xo) <= 1e-9, method
+    # converged solve returns the extrapolated point and its iteration index
+    _, gn10, _, _ = orc.solve_lower(po, y, 1e-12, 10.0, max_iters=10, adaptive=True)
+    eps = 1.5 * gn10 / 10.0
+    r = adp.solve_lower(p, y, eps, 10.0, max_iters=50, adaptive=True)
+    xo, gno, it_o, conv = orc.solve_lower(po, y, eps, 10.0, max_iters=50, adaptive=True)
+    assert conv and r.converged and r.iters == it_o < 10
+    assert rel(r.x_tilde, xo) <= 1e-9
+    with pytest.raises(ValueError):
+        adp.set_precision("float32", "fft")
