@@ -43,7 +43,7 @@ namespace fft {
 
 constexpr int T = 512;          // transform length (both axes)
 constexpr int RROWS = 4;        // rows per CTA in the row passes (64 threads per row)
-constexpr int CCOLS = 8;        // columns per CTA in the column pass (64 threads per column)
+constexpr int CCOLS = 4;        // columns per CTA in the column pass (64 threads per column)
 constexpr double kInvT2 = 1.0 / (512.0 * 512.0);   // exact power of two
 
 struct Geo {
@@ -88,57 +88,62 @@ __device__ __forceinline__ void dft8(double2* v) {
   v[7] = csub(c6, c7);
 }
 
-// 512-point Stockham FFTs of nb batches in shared memory.  Element e of batch
-// bi lives at buf[bi * bstride + e * estride].  Ping-pongs a -> b -> a -> b;
-// returns the buffer holding the result (b).  All threads of the CTA take
-// part; ends with a barrier.  BFAST: consecutive threads walk batches
-// (column passes, batches adjacent in memory).
-template <bool INV, bool BFAST>
-__device__ double2* fft512(double2* a, double2* b, int nb, int bstride, int estride, const double2* __restrict__ tw) {
-  double2* src = a;
-  double2* dst = b;
-  const int nwork = nb * 64;
-#pragma unroll 1
-  for (int st = 0, Ns = 1; st < 3; ++st, Ns *= 8) {
-    for (int t = threadIdx.x; t < nwork; t += blockDim.x) {
-      const int bi = BFAST ? (t % nb) : (t >> 6);
-      const int j = BFAST ? (t / nb) : (t & 63);
-      const int k = j & (Ns - 1);
-      double2* s = src + bi * bstride;
-      double2 v[8];
+// Register-resident 512-point FFT (radix-8 Stockham, 3 stages) of one batch.
+// The batch's 64 threads (j = 0..63) hold v[r] = element j + 64 r on entry
+// and output element j + 64 r on exit, so global loads and stores around it
+// are direct and coalesced; the two inter-stage exchanges go through the
+// batch's shared buffer `sm` (>= kPadB double2) with one pad slot per 8
+// elements (conflict-free 16-byte accesses).  Every thread of the CTA must
+// call it together (it contains CTA barriers; on return `sm` is free).
+constexpr int kPadB = 512 + 64 + 1;   // padded batch stride (odd: column batches land on distinct banks)
+__device__ __forceinline__ int pad8(int i) { return i + (i >> 3); }
+
+template <bool INV>
+__device__ __forceinline__ void twiddle(double2* v, int step, const double2* __restrict__ tw) {
 #pragma unroll
-      for (int r = 0; r < 8; ++r) v[r] = s[(j + r * 64) * estride];
-      if (st > 0) {
-        const int step = 64 / Ns;            // angle index m = r * k * 512 / (8 Ns)
-#pragma unroll
-        for (int r = 1; r < 8; ++r) {
-          double2 w = tw[(r * k * step) & 511];
-          if (INV) w.y = -w.y;
-          v[r] = cmul(v[r], w);
-        }
-      }
-      dft8<INV>(v);
-      double2* d = dst + bi * bstride;
-      const int base = (j - k) * 8 + k;
-#pragma unroll
-      for (int r = 0; r < 8; ++r) d[(base + r * Ns) * estride] = v[r];
-    }
-    __syncthreads();
-    double2* tmp = src;
-    src = dst;
-    dst = tmp;
+  for (int r = 1; r < 8; ++r) {
+    double2 w = __ldg(tw + ((r * step) & 511));   // exp(-2 pi i m / 512), m = r * step
+    if (INV) w.y = -w.y;
+    v[r] = cmul(v[r], w);
   }
-  return src;
 }
 
-__device__ __forceinline__ void load_twiddles(double2* tw_s, const double2* __restrict__ tw) {
-  for (int i = threadIdx.x; i < T; i += blockDim.x) tw_s[i] = tw[i];
+template <bool INV>
+__device__ __forceinline__ void fft512_reg(double2* v, double2* sm, int j, const double2* __restrict__ tw) {
+  dft8<INV>(v);                                   // stage 0 (Ns = 1): outputs to 8 j + r
+#pragma unroll
+  for (int r = 0; r < 8; ++r) sm[pad8(8 * j + r)] = v[r];
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 8; ++r) v[r] = sm[pad8(j + 64 * r)];
+  __syncthreads();
+  const int k = j & 7;                            // stage 1 (Ns = 8): outputs to (j - k) 8 + k + 8 r
+  twiddle<INV>(v, 8 * k, tw);
+  dft8<INV>(v);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) sm[pad8((j - k) * 8 + k + 8 * r)] = v[r];
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < 8; ++r) v[r] = sm[pad8(j + 64 * r)];
+  __syncthreads();
+  twiddle<INV>(v, j, tw);                         // stage 2 (Ns = 64): outputs to j + 64 r
+  dft8<INV>(v);
+}
+
+// Block index -> (pair, row/column group, channel); channel fastest so the
+// C CTAs that read (write) the same interleaved image rows run together.
+__device__ __forceinline__ void block_coords(int groups, int C, int& p, int& grp, int& c) {
+  const int b = blockIdx.x;
+  c = b % C;
+  const int q = b / C;
+  p = q / groups;
+  grp = q - p * groups;
 }
 
 // ---------------------------------------------------------------------------
-// K1: row pass.  grid (npairs * T / RROWS, C), 256 threads.
+// K1: row pass.  grid npairs * (T / RROWS) * C, 256 threads (64 per row).
 // mode 0: image tiles of x; mode 1: kernel embedding (spectrum setup; pair p:
-// p = 0 the kernel, p = 1 the flipped kernel, channel = grid.y).
+// p = 0 the kernel, p = 1 the flipped kernel).
 struct RowArgs {
   Geo g;
   const double* x;
@@ -155,50 +160,48 @@ __device__ __forceinline__ void tile_origin(const Geo& g, int t, int& h0, int& w
 }
 
 __global__ void __launch_bounds__(256) row_fwd_kernel(const __grid_constant__ RowArgs A) {
-  extern __shared__ __align__(16) double2 sm[];
-  double2* tw_s = sm;
-  double2* bufA = sm + T;
-  double2* bufB = bufA + RROWS * T;
+  __shared__ __align__(16) double2 sm[RROWS * kPadB];
   const Geo& g = A.g;
-  const int c = blockIdx.y;
-  const int rowgroups = T / RROWS;
-  const int p = blockIdx.x / rowgroups, row0 = (blockIdx.x - p * rowgroups) * RROWS;
-  load_twiddles(tw_s, A.tw);
+  int p, rg, c;
+  block_coords(T / RROWS, g.C, p, rg, c);
+  const int j = threadIdx.x & 63, rr = threadIdx.x >> 6, row = rg * RROWS + rr;
+  double2 v[8];
   if (A.mode == 0) {
     int h0a, w0a, h0b = 0, w0b = 0;
     tile_origin(g, 2 * p, h0a, w0a);
     const bool hasb = 2 * p + 1 < g.ntiles;
     if (hasb) tile_origin(g, 2 * p + 1, h0b, w0b);
-    for (int e = threadIdx.x; e < RROWS * T; e += blockDim.x) {
-      const int rr = e / T, col = e - rr * T;
-      const int ha = h0a - g.rh + row0 + rr, wa = w0a - g.rw + col;
+    const int ha = h0a - g.rh + row, hb = h0b - g.rh + row;
+    const bool rowa = ha >= 0 && ha < g.H, rowb = hasb && hb >= 0 && hb < g.H;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int col = j + 64 * r;
+      const int wa = w0a - g.rw + col, wb = w0b - g.rw + col;
       double re = 0.0, im = 0.0;
-      if (ha >= 0 && ha < g.H && wa >= 0 && wa < g.W) re = A.x[((int64_t)ha * g.W + wa) * g.C + c];
-      if (hasb) {
-        const int hb = h0b - g.rh + row0 + rr, wb = w0b - g.rw + col;
-        if (hb >= 0 && hb < g.H && wb >= 0 && wb < g.W) im = A.x[((int64_t)hb * g.W + wb) * g.C + c];
-      }
-      bufA[e] = make_double2(re, im);
+      if (rowa && wa >= 0 && wa < g.W) re = A.x[((int64_t)ha * g.W + wa) * g.C + c];
+      if (rowb && wb >= 0 && wb < g.W) im = A.x[((int64_t)hb * g.W + wb) * g.C + c];
+      v[r] = make_double2(re, im);
     }
   } else {
-    for (int e = threadIdx.x; e < RROWS * T; e += blockDim.x) {
-      const int rr = e / T, col = e - rr * T, i = row0 + rr;
-      double v = 0.0;
-      if (i < g.kh && col < g.kw) {
-        const int ii = p ? g.kh - 1 - i : i, jj = p ? g.kw - 1 - col : col;
-        v = A.kern[(ii * g.kw + jj) * g.C + c];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int col = j + 64 * r;
+      double val = 0.0;
+      if (row < g.kh && col < g.kw) {
+        const int ii = p ? g.kh - 1 - row : row, jj = p ? g.kw - 1 - col : col;
+        val = A.kern[(ii * g.kw + jj) * g.C + c];
       }
-      bufA[e] = make_double2(v, 0.0);
+      v[r] = make_double2(val, 0.0);
     }
   }
-  __syncthreads();
-  double2* res = fft512<false, false>(bufA, bufB, RROWS, T, 1, tw_s);
-  double2* S = A.S + (((int64_t)c * g.npairs + p) * T + row0) * T;
-  for (int e = threadIdx.x; e < RROWS * T; e += blockDim.x) S[e] = res[e];
+  fft512_reg<false>(v, sm + rr * kPadB, j, A.tw);
+  double2* S = A.S + (((int64_t)c * g.npairs + p) * T + row) * T;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) S[j + 64 * r] = v[r];
 }
 
 // ---------------------------------------------------------------------------
-// K2: column pass.  grid (npairs * T / CCOLS, C), 512 threads.
+// K2: column pass.  grid npairs * (T / CCOLS) * C, 64 * CCOLS threads.
 // mode 0: forward, multiply by the spectrum, inverse (a stencil);
 // mode 1: forward only, store conj (spectrum setup: S -> spec).
 struct ColArgs {
@@ -211,47 +214,33 @@ struct ColArgs {
   int npairs;            // pairs held in S for this pass
 };
 
-__global__ void __launch_bounds__(512) col_kernel(const __grid_constant__ ColArgs A) {
-  extern __shared__ __align__(16) double2 sm[];
-  double2* tw_s = sm;
-  double2* bufA = sm + T;
-  double2* bufB = bufA + CCOLS * T;
-  const int c = blockIdx.y;
-  const int strips = T / CCOLS;
-  const int p = blockIdx.x / strips, col0 = (blockIdx.x - p * strips) * CCOLS;
-  load_twiddles(tw_s, A.tw);
-  double2* S = A.S + ((int64_t)c * A.npairs + p) * T * T + col0;
-  for (int e = threadIdx.x; e < CCOLS * T; e += blockDim.x) {
-    const int r = e / CCOLS, q = e - r * CCOLS;
-    bufA[e] = S[(int64_t)r * T + q];
-  }
-  __syncthreads();
-  double2* f = fft512<false, true>(bufA, bufB, CCOLS, 1, CCOLS, tw_s);
+__global__ void __launch_bounds__(64 * CCOLS) col_kernel(const __grid_constant__ ColArgs A) {
+  __shared__ __align__(16) double2 sm[CCOLS * kPadB];
+  int p, strip, c;
+  block_coords(T / CCOLS, A.g.C, p, strip, c);
+  const int bi = threadIdx.x % CCOLS, j = threadIdx.x / CCOLS;
+  const int col = strip * CCOLS + bi;
+  double2* S = A.S + ((int64_t)c * A.npairs + p) * T * T + col;
+  double2 v[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) v[r] = S[(int64_t)(j + 64 * r) * T];
+  fft512_reg<false>(v, sm + bi * kPadB, j, A.tw);
   if (A.mode == 1) {
-    double2* o = A.spec_out + (((int64_t)p * A.g.C + c) * T) * T + col0;
-    for (int e = threadIdx.x; e < CCOLS * T; e += blockDim.x) {
-      const int r = e / CCOLS, q = e - r * CCOLS;
-      const double2 v = f[e];
-      o[(int64_t)r * T + q] = make_double2(v.x, -v.y);
-    }
+    double2* o = A.spec_out + ((int64_t)p * A.g.C + c) * T * T + col;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) o[(int64_t)(j + 64 * r) * T] = make_double2(v[r].x, -v[r].y);
     return;
   }
-  const double2* K = A.spec + (int64_t)c * T * T + col0;
-  for (int e = threadIdx.x; e < CCOLS * T; e += blockDim.x) {
-    const int r = e / CCOLS, q = e - r * CCOLS;
-    f[e] = cmul(f[e], K[(int64_t)r * T + q]);
-  }
-  __syncthreads();
-  double2* other = (f == bufA) ? bufB : bufA;
-  double2* res = fft512<true, true>(f, other, CCOLS, 1, CCOLS, tw_s);
-  for (int e = threadIdx.x; e < CCOLS * T; e += blockDim.x) {
-    const int r = e / CCOLS, q = e - r * CCOLS;
-    S[(int64_t)r * T + q] = res[e];
-  }
+  const double2* K = A.spec + (int64_t)c * T * T + col;
+#pragma unroll
+  for (int r = 0; r < 8; ++r) v[r] = cmul(v[r], __ldg(K + (int64_t)(j + 64 * r) * T));
+  fft512_reg<true>(v, sm + bi * kPadB, j, A.tw);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) S[(int64_t)(j + 64 * r) * T] = v[r];
 }
 
 // ---------------------------------------------------------------------------
-// K3: inverse row pass + crop + epilogue.  grid (npairs * T / RROWS, C), 256 threads.
+// K3: inverse row pass + crop + epilogue.  grid npairs * (T / RROWS) * C, 256 threads.
 enum Epi { E_STORE = 0, E_RESID = 1, E_GRAD = 2, E_VALUE = 3, E_POWER = 4 };
 
 struct InvArgs {
@@ -300,54 +289,54 @@ __device__ __forceinline__ TvTerms tv_at(const Geo& g, const double* __restrict_
   return t;
 }
 
+
 __global__ void __launch_bounds__(256) row_inv_kernel(const __grid_constant__ InvArgs A) {
-  extern __shared__ __align__(16) double2 sm[];
+  __shared__ __align__(16) double2 sm[RROWS * kPadB];
   __shared__ double red[40];
-  double2* tw_s = sm;
-  double2* bufA = sm + T;
-  double2* bufB = bufA + RROWS * T;
   const Geo& g = A.g;
-  const int c = blockIdx.y;
-  const int rowgroups = T / RROWS;
-  const int p = blockIdx.x / rowgroups, row0 = (blockIdx.x - p * rowgroups) * RROWS;
-  load_twiddles(tw_s, A.tw);
-  const double2* S = A.S + (((int64_t)c * g.npairs + p) * T + row0) * T;
-  for (int e = threadIdx.x; e < RROWS * T; e += blockDim.x) bufA[e] = S[e];
-  __syncthreads();
-  const double2* res = fft512<true, false>(bufA, bufB, RROWS, T, 1, tw_s);
+  int p, rg, c;
+  block_coords(T / RROWS, g.C, p, rg, c);
+  const int j = threadIdx.x & 63, rr = threadIdx.x >> 6, row = rg * RROWS + rr;
+  const double2* S = A.S + (((int64_t)c * g.npairs + p) * T + row) * T;
+  double2 v[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) v[r] = S[j + 64 * r];
+  fft512_reg<true>(v, sm + rr * kPadB, j, A.tw);
   double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll 1
   for (int half = 0; half < 2; ++half) {
     const int t = 2 * p + half;
-    if (t >= g.ntiles) break;
+    if (t >= g.ntiles || row >= g.Vh) break;
     int h0, w0;
     tile_origin(g, t, h0, w0);
-    for (int e = threadIdx.x; e < RROWS * T; e += blockDim.x) {
-      const int rr = e / T, q = e - rr * T;
-      const int h = h0 + row0 + rr, w = w0 + q;
-      if (row0 + rr >= g.Vh || q >= g.Vw || h >= g.H || w >= g.W) continue;
-      const double v = (half ? res[e].y : res[e].x) * kInvT2;
+    const int h = h0 + row;
+    if (h >= g.H) continue;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int q = j + 64 * r, w = w0 + q;
+      if (q >= g.Vw || w >= g.W) continue;
+      const double val = (half ? v[r].y : v[r].x) * kInvT2;
       const int64_t o = ((int64_t)h * g.W + w) * g.C + c;
       switch (A.epi) {
-        case E_STORE: A.out[o] = v; break;
-        case E_POWER: A.out[o] = v; acc0 = acc0 + v * v; break;
+        case E_STORE: A.out[o] = val; break;
+        case E_POWER: A.out[o] = val; acc0 = acc0 + val * val; break;
         case E_RESID: {
-          const double r = v - A.y[o];
-          A.out[o] = r;
-          acc0 = acc0 + r * r;
+          const double rs = val - A.y[o];
+          A.out[o] = rs;
+          acc0 = acc0 + rs * rs;
           break;
         }
         case E_GRAD: {   // g = 2 adj + alpha grad J (lower_solvers.py:54-62); vg TV form (regularizers.py:173-174)
           const TvTerms tv = tv_at(g, A.xp, h, w, c, A.nu, true);
-          const double gv = 2.0 * v + A.alpha * tv.grad;
+          const double gv = 2.0 * val + A.alpha * tv.grad;
           A.out[o] = gv;
           acc0 = acc0 + gv * gv;
           acc1 = acc1 + (tv.root0 + tv.root1);
           break;
         }
         case E_VALUE: {  // sum (Bx - y)^2 and tv_value = sum(sqrt(d^2 + nu^2) - nu) (regularizers.py:70-72)
-          const double r = v - A.y[o];
-          acc0 = acc0 + r * r;
+          const double rs = val - A.y[o];
+          acc0 = acc0 + rs * rs;
           const TvTerms tv = tv_at(g, A.xp, h, w, c, A.nu, false);
           acc1 = acc1 + ((tv.root0 - A.nu) + (tv.root1 - A.nu));
           break;
@@ -357,12 +346,11 @@ __global__ void __launch_bounds__(256) row_inv_kernel(const __grid_constant__ In
     }
   }
   if (A.part) {
-    const int cta = blockIdx.y * gridDim.x + blockIdx.x;
     const double s0 = block_sum(acc0, red);
     const double s1 = block_sum(acc1, red);
     if (threadIdx.x == 0) {
-      A.part[2 * cta] = s0;
-      A.part[2 * cta + 1] = s1;
+      A.part[2 * blockIdx.x] = s0;
+      A.part[2 * blockIdx.x + 1] = s1;
     }
   }
 }
@@ -442,19 +430,7 @@ struct adp_fft_plan {
 
 namespace {
 
-constexpr size_t kRowSmem = (size_t)(T + 2 * RROWS * T) * sizeof(double2);
-constexpr size_t kColSmem = (size_t)(T + 2 * CCOLS * T) * sizeof(double2);
-
-int setup_attrs() {
-  static int done = 0;
-  if (done) return ADP_OK;
-  if (cudaFuncSetAttribute(row_fwd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmem) != cudaSuccess ||
-      cudaFuncSetAttribute(row_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmem) != cudaSuccess ||
-      cudaFuncSetAttribute(col_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kColSmem) != cudaSuccess)
-    return dense_fail(ADP_ERR_CUDA, "fft: shared-memory attributes");
-  done = 1;
-  return ADP_OK;
-}
+int setup_attrs() { return ADP_OK; }   // static shared memory only
 
 int check_launch(const char* what) {
   const cudaError_t e = cudaGetLastError();
@@ -468,9 +444,9 @@ int build_spectra(adp_fft_plan* P, const double* kern, cudaStream_t st) {
   Geo kg = g;
   kg.npairs = 2;   // S slots: pair 0 = kernel, pair 1 = flipped kernel
   RowArgs ra{kg, nullptr, P->S, P->tw, 1, kern};
-  row_fwd_kernel<<<dim3(2 * T / RROWS, g.C), 256, kRowSmem, st>>>(ra);
+  row_fwd_kernel<<<2 * (T / RROWS) * g.C, 256, 0, st>>>(ra);
   ColArgs ca{kg, P->S, nullptr, P->spec, P->tw, 1, 2};
-  col_kernel<<<dim3(2 * T / CCOLS, g.C), 512, kColSmem, st>>>(ca);
+  col_kernel<<<2 * (T / CCOLS) * g.C, 64 * CCOLS, 0, st>>>(ca);
   return check_launch("fft spectra");
 }
 
@@ -478,13 +454,13 @@ int build_spectra(adp_fft_plan* P, const double* kern, cudaStream_t st) {
 int stencil(adp_fft_plan* P, int adj, const double* x, int epi, double* out, const double* y, const double* xp,
             double alpha, double nu, bool partials, cudaStream_t st) {
   const Geo& g = P->g;
-  const dim3 rgrid(g.npairs * T / RROWS, g.C);
+  const int rgrid = g.npairs * (T / RROWS) * g.C;
   RowArgs ra{g, x, P->S, P->tw, 0, nullptr};
-  row_fwd_kernel<<<rgrid, 256, kRowSmem, st>>>(ra);
+  row_fwd_kernel<<<rgrid, 256, 0, st>>>(ra);
   ColArgs ca{g, P->S, P->spec + (size_t)adj * g.C * T * T, nullptr, P->tw, 0, g.npairs};
-  col_kernel<<<dim3(g.npairs * T / CCOLS, g.C), 512, kColSmem, st>>>(ca);
+  col_kernel<<<g.npairs * (T / CCOLS) * g.C, 64 * CCOLS, 0, st>>>(ca);
   InvArgs ia{g, P->S, P->tw, out, y, xp, alpha, nu, epi, partials ? P->part : nullptr};
-  row_inv_kernel<<<rgrid, 256, kRowSmem, st>>>(ia);
+  row_inv_kernel<<<rgrid, 256, 0, st>>>(ia);
   return check_launch("fft stencil");
 }
 
