@@ -54,8 +54,8 @@ struct Geo {
 // radix-8 butterflies
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {   // FMA: this path is a tolerance mode
+  return make_double2(fma(a.x, b.x, -(a.y * b.y)), fma(a.x, b.y, a.y * b.x));
 }
 template <bool INV>
 __device__ __forceinline__ double2 mul_mi(double2 a) {   // forward: * (-i); inverse: * (+i)
@@ -95,7 +95,9 @@ __device__ __forceinline__ void dft8(double2* v) {
 // batch's shared buffer `sm` (>= kPadB double2) with one pad slot per 8
 // elements (conflict-free 16-byte accesses).  Every thread of the CTA must
 // call it together (it contains CTA barriers; on return `sm` is free).
-constexpr int kPadB = 512 + 64 + 1;   // padded batch stride (odd: column batches land on distinct banks)
+// padded batch stride = 2 mod 8 (16-byte units): the 8 threads of each quarter-warp phase of a
+// column pass (2 rows x 4 columns) land on 8 distinct bank groups
+constexpr int kPadB = 512 + 64 + 2;
 __device__ __forceinline__ int pad8(int i) { return i + (i >> 3); }
 
 template <bool INV>
@@ -159,7 +161,7 @@ __device__ __forceinline__ void tile_origin(const Geo& g, int t, int& h0, int& w
   w0 = tx * g.Vw;
 }
 
-__global__ void __launch_bounds__(256) row_fwd_kernel(const __grid_constant__ RowArgs A) {
+__global__ void __launch_bounds__(256, 3) row_fwd_kernel(const __grid_constant__ RowArgs A) {
   __shared__ __align__(16) double2 sm[RROWS * kPadB];
   const Geo& g = A.g;
   int p, rg, c;
@@ -214,7 +216,7 @@ struct ColArgs {
   int npairs;            // pairs held in S for this pass
 };
 
-__global__ void __launch_bounds__(64 * CCOLS) col_kernel(const __grid_constant__ ColArgs A) {
+__global__ void __launch_bounds__(64 * CCOLS, 3) col_kernel(const __grid_constant__ ColArgs A) {
   __shared__ __align__(16) double2 sm[CCOLS * kPadB];
   int p, strip, c;
   block_coords(T / CCOLS, A.g.C, p, strip, c);
@@ -290,7 +292,7 @@ __device__ __forceinline__ TvTerms tv_at(const Geo& g, const double* __restrict_
 }
 
 
-__global__ void __launch_bounds__(256) row_inv_kernel(const __grid_constant__ InvArgs A) {
+__global__ void __launch_bounds__(256, 3) row_inv_kernel(const __grid_constant__ InvArgs A) {
   __shared__ __align__(16) double2 sm[RROWS * kPadB];
   __shared__ double red[40];
   const Geo& g = A.g;
