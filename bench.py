@@ -381,11 +381,14 @@ def other_configs(args, flush):
     out = {}
     eps, mu = 1e-14, 10.0
 
-    def solve(up, iters):
-        x0 = nat.to_dev(up.x0)
-        xo = nat.empty_like_dev(up.x0.shape)
+    dev = {}   # x0 and the output buffer stay resident in HBM (inputs resident before the timed region)
+
+    def solve(up, iters, stats=None):
+        if id(up) not in dev:
+            dev[id(up)] = (nat.to_dev(up.x0), nat.empty_like_dev(up.x0.shape))
+        x0, xo = dev[id(up)]
         p = up.lower_problem(up.b0)
-        return adp.solve_lower(p, x0, eps, mu, max_iters=iters, method="agd", adaptive=True, x_out=xo)
+        return adp.solve_lower(p, x0, eps, mu, max_iters=iters, method="agd", adaptive=True, x_out=xo, stats=stats)
 
     up3 = configs.config3(0)
     solve(up3, 50)
@@ -394,6 +397,8 @@ def other_configs(args, flush):
     out["c3"] = {"value": up3.y_delta.size * r.iters / t / 1e9, "unit": UNIT, "iters": r.iters,
                  "ms_per_solve": 1e3 * t, "workload": "512x512x3, 15x15 line-Gaussian, 1200 AGD iterations"}
     ups = [configs.config3(seed) for seed in range(8)]
+    for u in ups:
+        solve(u, 2)
     flush.zero_()
 
     def c4():
@@ -403,6 +408,8 @@ def other_configs(args, flush):
                  "instances": len(ups), "ms": 1e3 * t,
                  "workload": "8 c3 instances (seeds 0-7) = one GPU's share of 64, 300 AGD iterations each, "
                              "no collectives (weak scaling over GPUs)"}
+    for u in ups:
+        dev.pop(id(u), None)
     del ups
     # IFT baseline on c1 (baselines.py:58-90 with defaults.cfg [ift]): upper iters/s
     up1 = configs.config1(0)
@@ -417,9 +424,10 @@ def other_configs(args, flush):
     up5 = configs.config5(0, size=args.c5_size)
     solve(up5, 2)
     flush.zero_()
-    r, t = _timed(lambda: solve(up5, args.c5_iters))
+    st5 = {}
+    r, t = _timed(lambda: solve(up5, args.c5_iters, st5))
     out["c5"] = {"value": up5.y_delta.size * r.iters / t / 1e9, "unit": UNIT, "iters": r.iters,
-                 "ms_per_solve": 1e3 * t,
+                 "ms_per_solve": 1e3 * t, "stats": {k: st5.get(k) for k in ("power_iters", "vg_evals", "value_evals")},
                  "workload": f"{args.c5_size}x{args.c5_size}x3, 31x31 Gaussian, {args.c5_iters} AGD iterations "
                              "(+ power iteration), one GPU"}
     out["c5_fft"] = c5_fft(args, up5, solve, flush)
@@ -436,6 +444,7 @@ def c5_fft(args, up5, solve, flush):
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
     p = up5.lower_problem(up5.b0)
     xd = nat.to_dev(up5.x0)
+    p.op.apply(xd)    # output buffer in the caching allocator before timing
 
     def stencil_ms(reps=3):
         p.op.apply(xd)
@@ -447,7 +456,8 @@ def c5_fft(args, up5, solve, flush):
         fft_ms = stencil_ms()
         solve(up5, 2)
         flush.zero_()
-        r, t = _timed(lambda: solve(up5, args.c5_iters))
+        stf = {}
+        r, t = _timed(lambda: solve(up5, args.c5_iters, stf))
         plan = p.op.fft_plan()
     H, W, C = up5.x0.shape
     kh = up5.b0.data.shape[0]
@@ -455,7 +465,10 @@ def c5_fft(args, up5, solve, flush):
     npairs = (-(-H // V) * -(-W // V) + 1) // 2
     sbytes = 16 * C * npairs * 512 * 512
     traffic = 5 * sbytes + 16 * H * W * C      # K1 write, K2 read+write+spectrum, K3 read; image in + out
+    n_sten = 2 * stf.get("power_iters", 0) + 2 * stf.get("vg_evals", 0) + stf.get("value_evals", 0)
     return {"value": up5.y_delta.size * r.iters / t / 1e9, "unit": UNIT, "iters": r.iters, "ms_per_solve": 1e3 * t,
+            "stats": {k: stf.get(k) for k in ("power_iters", "vg_evals", "value_evals")},
+            "stencils_per_solve": n_sten, "stencil_share": n_sten * fft_ms / (1e3 * t),
             "stencil_ms": {"direct_strict": direct_ms, "fft": fft_ms, "speedup": direct_ms / fft_ms},
             "fft_stencil_roofline": {"bound": "hbm", "achieved": traffic / (fft_ms * 1e-3) / 1e9, "peak": hbm,
                                      "unit": "GB/s", "frac": traffic / (fft_ms * 1e-3) / 1e9 / hbm,

@@ -146,6 +146,17 @@ __device__ __forceinline__ void block_coords(int groups, int C, int& p, int& grp
 // K1: row pass.  grid npairs * (T / RROWS) * C, 256 threads (64 per row).
 // mode 0: image tiles of x; mode 1: kernel embedding (spectrum setup; pair p:
 // p = 0 the kernel, p = 1 the flipped kernel).
+// Row-pass prologues: the elementwise solver step that produces the stencil's
+// input is computed while loading it (no separate pass over HBM).  The tile's
+// valid-region pixels (each image pixel exactly once) store the produced
+// iterate for the later passes.
+enum Pro {
+  P_NONE = 0,    // input = x
+  P_EXTRAP = 1,  // input = y = x + coef (x - x2), stored to wout        (lower_solvers.py:197)
+  P_STEP = 2,    // input = xc = x - x2 / coef (x = y, x2 = g), stored; partial sum g (xc - xold) (:173, :209)
+  P_SCALE = 3    // input = x / coef (power iteration v = w / lam, operators.py:162)
+};
+
 struct RowArgs {
   Geo g;
   const double* x;
@@ -153,6 +164,12 @@ struct RowArgs {
   const double2* tw;
   int mode;
   const double* kern;   // (kh, kw, C)
+  int pro;
+  const double* x2;
+  const double* xold;
+  double coef;
+  double* wout;
+  double* part;         // P_STEP: one partial per CTA
 };
 
 __device__ __forceinline__ void tile_origin(const Geo& g, int t, int& h0, int& w0) {
@@ -161,13 +178,37 @@ __device__ __forceinline__ void tile_origin(const Geo& g, int t, int& h0, int& w
   w0 = tx * g.Vw;
 }
 
+__device__ __forceinline__ double row_input(const RowArgs& A, int64_t o, bool valid, double& dot) {
+  const double xv = A.x[o];
+  switch (A.pro) {
+    case P_EXTRAP: {
+      const double u = xv + A.coef * (xv - A.x2[o]);
+      if (valid) A.wout[o] = u;
+      return u;
+    }
+    case P_STEP: {
+      const double gv = A.x2[o];
+      const double u = xv - gv / A.coef;
+      if (valid) {
+        A.wout[o] = u;
+        dot = dot + gv * (u - A.xold[o]);
+      }
+      return u;
+    }
+    case P_SCALE: return xv / A.coef;
+    default: return xv;
+  }
+}
+
 __global__ void __launch_bounds__(256, 3) row_fwd_kernel(const __grid_constant__ RowArgs A) {
   __shared__ __align__(16) double2 sm[RROWS * kPadB];
+  __shared__ double red[40];
   const Geo& g = A.g;
   int p, rg, c;
   block_coords(T / RROWS, g.C, p, rg, c);
   const int j = threadIdx.x & 63, rr = threadIdx.x >> 6, row = rg * RROWS + rr;
   double2 v[8];
+  double dot = 0.0;
   if (A.mode == 0) {
     int h0a, w0a, h0b = 0, w0b = 0;
     tile_origin(g, 2 * p, h0a, w0a);
@@ -175,14 +216,20 @@ __global__ void __launch_bounds__(256, 3) row_fwd_kernel(const __grid_constant__
     if (hasb) tile_origin(g, 2 * p + 1, h0b, w0b);
     const int ha = h0a - g.rh + row, hb = h0b - g.rh + row;
     const bool rowa = ha >= 0 && ha < g.H, rowb = hasb && hb >= 0 && hb < g.H;
+    const bool vrow = row >= g.rh && row - g.rh < g.Vh;     // valid-region row of both tiles
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
       const int col = j + 64 * r;
       const int wa = w0a - g.rw + col, wb = w0b - g.rw + col;
+      const bool vcol = vrow && col >= g.rw && col - g.rw < g.Vw;
       double re = 0.0, im = 0.0;
-      if (rowa && wa >= 0 && wa < g.W) re = A.x[((int64_t)ha * g.W + wa) * g.C + c];
-      if (rowb && wb >= 0 && wb < g.W) im = A.x[((int64_t)hb * g.W + wb) * g.C + c];
+      if (rowa && wa >= 0 && wa < g.W) re = row_input(A, ((int64_t)ha * g.W + wa) * g.C + c, vcol, dot);
+      if (rowb && wb >= 0 && wb < g.W) im = row_input(A, ((int64_t)hb * g.W + wb) * g.C + c, vcol, dot);
       v[r] = make_double2(re, im);
+    }
+    if (A.pro == P_STEP) {
+      const double s = block_sum(dot, red);
+      if (threadIdx.x == 0) A.part[blockIdx.x] = s;
     }
   } else {
 #pragma unroll
@@ -393,17 +440,27 @@ __global__ void __launch_bounds__(256) vec_kernel(int op, int64_t n, double a, c
   }
 }
 
-// Fixed-order fold of k interleaved partial streams (part[k * i + j], i < n):
-// one CTA, contiguous per-thread chunks, then block_sum.
-__global__ void __launch_bounds__(1024) fold_kernel(const double* __restrict__ part, int n, int k, double* out) {
+// Fixed-order folds of up to three partial buffers in one launch: source i
+// holds k_i interleaved streams (p[k_i * n + j], n < n_i); results in order.
+// One CTA, per-thread strided (coalesced) chains in a fixed order, then block_sum.
+struct FoldSrc {
+  const double* p;
+  int n, k;
+};
+
+__global__ void __launch_bounds__(1024) fold_kernel(FoldSrc a, FoldSrc b, FoldSrc c, double* out) {
   __shared__ double red[40];
-  const int per = (n + blockDim.x - 1) / blockDim.x;
-  for (int j = 0; j < k; ++j) {
-    double acc = 0.0;
-    const int i0 = threadIdx.x * per, i1 = min(n, i0 + per);
-    for (int i = i0; i < i1; ++i) acc = acc + part[(int64_t)k * i + j];
-    const double s = block_sum(acc, red);
-    if (threadIdx.x == 0) out[j] = s;
+  int o = 0;
+  for (int si = 0; si < 3; ++si) {
+    const FoldSrc f = si == 0 ? a : (si == 1 ? b : c);
+    for (int j = 0; j < f.k; ++j) {
+      double acc = 0.0;
+#pragma unroll 8
+      for (int i = threadIdx.x; i < f.n; i += blockDim.x) acc = acc + f.p[(int64_t)f.k * i + j];
+      const double s = block_sum(acc, red);
+      if (threadIdx.x == 0) out[o] = s;
+      ++o;
+    }
   }
 }
 
@@ -421,7 +478,10 @@ struct adp_fft_plan {
   double2* S = nullptr;        // (C, npairs, T, T)
   double2* spec = nullptr;     // (2, C, T, T): [0] apply, [1] adjoint
   double2* tw = nullptr;       // T twiddles exp(-2 pi i m / T)
-  double* part = nullptr;      // partials (2 per CTA)
+  double* partR = nullptr;     // residual-pass partials (2 per row CTA)
+  double* partG = nullptr;     // gradient / value / power-pass partials (2 per row CTA)
+  double* partK1 = nullptr;    // row-pass prologue partials (1 per row CTA)
+  double* partV = nullptr;     // vector-kernel partials (2 per CTA)
   double* red = nullptr;       // fold results (device)
   double* hred = nullptr;      // pinned host copy
   double* buf[6] = {};         // solver images
@@ -445,96 +505,119 @@ int build_spectra(adp_fft_plan* P, const double* kern, cudaStream_t st) {
   const Geo& g = P->g;
   Geo kg = g;
   kg.npairs = 2;   // S slots: pair 0 = kernel, pair 1 = flipped kernel
-  RowArgs ra{kg, nullptr, P->S, P->tw, 1, kern};
+  RowArgs ra{kg, nullptr, P->S, P->tw, 1, kern, P_NONE, nullptr, nullptr, 0.0, nullptr, nullptr};
   row_fwd_kernel<<<2 * (T / RROWS) * g.C, 256, 0, st>>>(ra);
   ColArgs ca{kg, P->S, nullptr, P->spec, P->tw, 1, 2};
   col_kernel<<<2 * (T / CCOLS) * g.C, 64 * CCOLS, 0, st>>>(ca);
   return check_launch("fft spectra");
 }
 
-// One stencil: out/epilogue from x with the apply (adj = 0) or adjoint (adj = 1) spectrum.
-int stencil(adp_fft_plan* P, int adj, const double* x, int epi, double* out, const double* y, const double* xp,
-            double alpha, double nu, bool partials, cudaStream_t st) {
+// Row-pass prologue of one stencil (see enum Pro).
+struct ProArgs {
+  int pro = P_NONE;
+  const double* x2 = nullptr;
+  const double* xold = nullptr;
+  double coef = 0.0;
+  double* wout = nullptr;
+};
+
+// One stencil: out/epilogue from (the prologue of) x with the apply (adj = 0) or adjoint (adj = 1)
+// spectrum; K3 partials to part3 (2 per CTA) when non-NULL, K1 partials (P_STEP) to P->partK1.
+int stencil(adp_fft_plan* P, int adj, const double* x, const ProArgs& pa, int epi, double* out, const double* y,
+            const double* xp, double alpha, double nu, double* part3, cudaStream_t st) {
   const Geo& g = P->g;
   const int rgrid = g.npairs * (T / RROWS) * g.C;
-  RowArgs ra{g, x, P->S, P->tw, 0, nullptr};
+  RowArgs ra{g, x, P->S, P->tw, 0, nullptr, pa.pro, pa.x2, pa.xold, pa.coef, pa.wout, P->partK1};
   row_fwd_kernel<<<rgrid, 256, 0, st>>>(ra);
   ColArgs ca{g, P->S, P->spec + (size_t)adj * g.C * T * T, nullptr, P->tw, 0, g.npairs};
   col_kernel<<<g.npairs * (T / CCOLS) * g.C, 64 * CCOLS, 0, st>>>(ca);
-  InvArgs ia{g, P->S, P->tw, out, y, xp, alpha, nu, epi, partials ? P->part : nullptr};
+  InvArgs ia{g, P->S, P->tw, out, y, xp, alpha, nu, epi, part3};
   row_inv_kernel<<<rgrid, 256, 0, st>>>(ia);
   return check_launch("fft stencil");
 }
 
-int fold(adp_fft_plan* P, int n, int k, double* host, cudaStream_t st) {
-  fold_kernel<<<1, 1024, 0, st>>>(P->part, n, k, P->red);
+int rowctas(const adp_fft_plan* P) { return P->g.npairs * (T / RROWS) * P->g.C; }
+
+// Fold up to three partial sources (one launch, one device->host read, one sync).
+int fold(adp_fft_plan* P, FoldSrc a, FoldSrc b, FoldSrc c, double* host, cudaStream_t st) {
+  const int k = a.k + b.k + c.k;
+  fold_kernel<<<1, 1024, 0, st>>>(a, b, c, P->red);
   cudaMemcpyAsync(P->hred, P->red, k * sizeof(double), cudaMemcpyDeviceToHost, st);
   const cudaError_t e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return dense_fail(ADP_ERR_CUDA, cudaGetErrorString(e));
   for (int j = 0; j < k; ++j) host[j] = P->hred[j];
   return ADP_OK;
 }
+FoldSrc src3(const adp_fft_plan* P, const double* part) { return FoldSrc{part, rowctas(P), 2}; }
+constexpr FoldSrc kNoSrc{nullptr, 0, 0};
 
 int vec(adp_fft_plan* P, int op, double a, const double* x, const double* xp, const double* g, double* out,
         double* host_red, cudaStream_t st) {
   const bool red = (op == V_DOTDIFF || op == V_NORM2);
-  vec_kernel<<<kVecGrid, 256, 0, st>>>(op, P->N, a, x, xp, g, out, red ? P->part : nullptr);
+  vec_kernel<<<kVecGrid, 256, 0, st>>>(op, P->N, a, x, xp, g, out, red ? P->partV : nullptr);
   int rc = check_launch("fft vec");
   if (rc != ADP_OK || !red) return rc;
   double r[2];
-  rc = fold(P, kVecGrid, 2, r, st);
+  rc = fold(P, FoldSrc{P->partV, kVecGrid, 2}, kNoSrc, kNoSrc, r, st);
   *host_red = r[0];
   return rc;
 }
 
-int rowctas(const adp_fft_plan* P) { return P->g.npairs * (T / RROWS) * P->g.C; }
-
-// value and gradient of the lower objective at x (lower_solvers.py:50-63):
-// r = Bx - y (stored in buf R), g = 2 B^T r + alpha grad TV(x); value = sum r^2 + alpha (sum root - nu * 2N)
-int vg(adp_fft_plan* P, const adp_lower* lp, const double* x, double* g, double* value, double* gn2,
-       cudaStream_t st) {
+// value and gradient of the lower objective (lower_solvers.py:50-63) at the stencil input
+// produced by `pa` from x (the point itself, or y = x + beta (x - x_prev) stored to pa.wout):
+// r = Bz - y (buf R), g = 2 B^T r + alpha grad TV(z); value = sum r^2 + alpha (sum root - nu * 2N)
+int vg(adp_fft_plan* P, const adp_lower* lp, const double* x, const ProArgs& pa, double* g, double* value,
+       double* gn2, cudaStream_t st) {
   double* R = P->buf[5];
-  int rc = stencil(P, 0, x, E_RESID, R, (const double*)lp->y, nullptr, 0.0, 0.0, true, st);
+  const double* z = pa.pro == P_NONE ? x : pa.wout;
+  int rc = stencil(P, 0, x, pa, E_RESID, R, (const double*)lp->y, nullptr, 0.0, 0.0, P->partR, st);
   if (rc) return rc;
-  double fit[2];
-  if ((rc = fold(P, rowctas(P), 2, fit, st))) return rc;
-  rc = stencil(P, 1, R, E_GRAD, g, nullptr, x, lp->alpha, lp->nu, true, st);
+  rc = stencil(P, 1, R, ProArgs{}, E_GRAD, g, nullptr, z, lp->alpha, lp->nu, P->partG, st);
   if (rc) return rc;
-  double gt[2];
-  if ((rc = fold(P, rowctas(P), 2, gt, st))) return rc;
-  const double tv = gt[1] - lp->nu * (double)(2 * P->N);
-  if (value) *value = fit[0] + lp->alpha * tv;
-  if (gn2) *gn2 = gt[0];
+  double t[4];
+  if ((rc = fold(P, src3(P, P->partR), src3(P, P->partG), kNoSrc, t, st))) return rc;
+  const double tv = t[3] - lp->nu * (double)(2 * P->N);
+  if (value) *value = t[0] + lp->alpha * tv;
+  if (gn2) *gn2 = t[2];
   return ADP_OK;
 }
 
-// lower_value (lower_solvers.py:37-39): sum (Bx - y)^2 + alpha tv_value(x)
-int value(adp_fft_plan* P, const adp_lower* lp, const double* x, double* val, cudaStream_t st) {
-  int rc = stencil(P, 0, x, E_VALUE, nullptr, (const double*)lp->y, x, 0.0, lp->nu, true, st);
+// lower_value (lower_solvers.py:37-39) at the stencil input produced by `pa`:
+// sum (Bz - y)^2 + alpha tv_value(z); with P_STEP also the restart dot sum g (xc - xold)
+int value(adp_fft_plan* P, const adp_lower* lp, const double* x, const ProArgs& pa, double* val, double* dot,
+          cudaStream_t st) {
+  const double* z = pa.pro == P_NONE ? x : pa.wout;
+  int rc = stencil(P, 0, x, pa, E_VALUE, nullptr, (const double*)lp->y, z, 0.0, lp->nu, P->partG, st);
   if (rc) return rc;
-  double t[2];
-  if ((rc = fold(P, rowctas(P), 2, t, st))) return rc;
+  double t[3];
+  const bool step = pa.pro == P_STEP;
+  if ((rc = fold(P, src3(P, P->partG), step ? FoldSrc{P->partK1, rowctas(P), 1} : kNoSrc, kNoSrc, t, st)))
+    return rc;
   *val = t[0] + lp->alpha * t[1];
+  if (dot) *dot = step ? t[2] : 0.0;
   return ADP_OK;
 }
 
-// op_norm_sq (operators.py:137-173)
+// op_norm_sq (operators.py:137-173); v = w / lam is the next row pass's prologue
 int power(adp_fft_plan* P, const double* v0, int max_iters, double tol, double* lam_out, int* conv_out,
           int* iters_out, cudaStream_t st) {
-  double* V = P->buf[3];
   double* Wb = P->buf[4];
   double* Bv = P->buf[5];
   double n2 = 0.0;
   int rc = vec(P, V_NORM2, 0.0, v0, nullptr, nullptr, nullptr, &n2, st);
   if (rc) return rc;
-  if ((rc = vec(P, V_DIVNORM, std::sqrt(n2), v0, nullptr, nullptr, V, nullptr, st))) return rc;
+  const double* vin = v0;      // v = vin / scale
+  double scale = std::sqrt(n2);
   double lam = 0.0;
   int converged = 0, it = 0;
   for (; it < max_iters; ++it) {
-    if ((rc = stencil(P, 0, V, E_STORE, Bv, nullptr, nullptr, 0.0, 0.0, false, st))) return rc;
-    if ((rc = stencil(P, 1, Bv, E_POWER, Wb, nullptr, nullptr, 0.0, 0.0, true, st))) return rc;
+    ProArgs pa;
+    pa.pro = P_SCALE;
+    pa.coef = scale;
+    if ((rc = stencil(P, 0, vin, pa, E_STORE, Bv, nullptr, nullptr, 0.0, 0.0, nullptr, st))) return rc;
+    if ((rc = stencil(P, 1, Bv, ProArgs{}, E_POWER, Wb, nullptr, nullptr, 0.0, 0.0, P->partG, st))) return rc;
     double w2[2];
-    if ((rc = fold(P, rowctas(P), 2, w2, st))) return rc;
+    if ((rc = fold(P, src3(P, P->partG), kNoSrc, kNoSrc, w2, st))) return rc;
     const double lam_new = std::sqrt(w2[0]);
     if (lam_new == 0.0) {
       lam = 0.0;
@@ -542,7 +625,8 @@ int power(adp_fft_plan* P, const double* v0, int max_iters, double tol, double* 
       ++it;
       break;
     }
-    if ((rc = vec(P, V_DIVNORM, lam_new, Wb, nullptr, nullptr, V, nullptr, st))) return rc;
+    vin = Wb;
+    scale = lam_new;
     if (std::fabs(lam_new - lam) <= tol * std::max(lam_new, 1e-300)) {
       lam = lam_new;
       converged = 1;
@@ -580,10 +664,13 @@ extern "C" int adp_fft_plan_create(adp_fft_plan** out, int32_t H, int32_t W, int
   // >= 2 pair slots: the spectrum setup transforms the kernel and its flip together
   const size_t sbytes = (size_t)C * std::max(2, g.npairs) * T * T * sizeof(double2);
   const size_t specb = (size_t)2 * C * T * T * sizeof(double2);
-  const int nparts = std::max(rowctas(P), kVecGrid);
+  const int nparts = rowctas(P);
   bool ok = cudaMalloc(&P->S, sbytes) == cudaSuccess && cudaMalloc(&P->spec, specb) == cudaSuccess &&
             cudaMalloc(&P->tw, T * sizeof(double2)) == cudaSuccess &&
-            cudaMalloc(&P->part, (size_t)2 * nparts * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&P->partR, (size_t)2 * nparts * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&P->partG, (size_t)2 * nparts * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&P->partK1, (size_t)nparts * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&P->partV, (size_t)2 * kVecGrid * sizeof(double)) == cudaSuccess &&
             cudaMalloc(&P->red, 8 * sizeof(double)) == cudaSuccess &&
             cudaMallocHost(&P->hred, 8 * sizeof(double)) == cudaSuccess;
   for (int i = 0; ok && i < 6; ++i) ok = cudaMalloc(&P->buf[i], (size_t)P->N * sizeof(double)) == cudaSuccess;
@@ -591,7 +678,7 @@ extern "C" int adp_fft_plan_create(adp_fft_plan** out, int32_t H, int32_t W, int
     adp_fft_plan_destroy(P);
     return dense_fail(ADP_ERR_CUDA, "fft plan: device allocation failed");
   }
-  P->bytes = sbytes + specb + (size_t)6 * P->N * sizeof(double) + 2 * nparts * sizeof(double);
+  P->bytes = sbytes + specb + (size_t)6 * P->N * sizeof(double) + (size_t)(5 * nparts + 2 * kVecGrid) * sizeof(double);
   // accurately rounded twiddles exp(-2 pi i m / T)
   std::vector<double2> tw(T);
   for (int m = 0; m < T; ++m) {
@@ -608,7 +695,10 @@ extern "C" void adp_fft_plan_destroy(adp_fft_plan* P) {
   cudaFree(P->S);
   cudaFree(P->spec);
   cudaFree(P->tw);
-  cudaFree(P->part);
+  cudaFree(P->partR);
+  cudaFree(P->partG);
+  cudaFree(P->partK1);
+  cudaFree(P->partV);
   cudaFree(P->red);
   if (P->hred) cudaFreeHost(P->hred);
   for (double* b : P->buf) cudaFree(b);
@@ -623,7 +713,8 @@ extern "C" int adp_fft_apply(adp_fft_plan* P, const void* kernel, int32_t adjoin
   cudaStream_t st = (cudaStream_t)stream;
   int rc = prepare(P, kernel, st);
   if (rc) return rc;
-  return stencil(P, adjoint ? 1 : 0, (const double*)x, E_STORE, (double*)out, nullptr, nullptr, 0.0, 0.0, false, st);
+  return stencil(P, adjoint ? 1 : 0, (const double*)x, ProArgs{}, E_STORE, (double*)out, nullptr, nullptr, 0.0, 0.0,
+                 nullptr, st);
 }
 
 extern "C" int adp_fft_lower_value(adp_fft_plan* P, const adp_lower* lp, const void* x, double* val, void* stream) {
@@ -632,7 +723,7 @@ extern "C" int adp_fft_lower_value(adp_fft_plan* P, const adp_lower* lp, const v
   cudaStream_t st = (cudaStream_t)stream;
   int rc = prepare(P, lp->kernel, st);
   if (rc) return rc;
-  return value(P, lp, (const double*)x, val, st);
+  return value(P, lp, (const double*)x, ProArgs{}, val, nullptr, st);
 }
 
 extern "C" int adp_fft_lower_value_and_grad(adp_fft_plan* P, const adp_lower* lp, const void* x, double* val,
@@ -643,7 +734,7 @@ extern "C" int adp_fft_lower_value_and_grad(adp_fft_plan* P, const adp_lower* lp
   int rc = prepare(P, lp->kernel, st);
   if (rc) return rc;
   double v = 0.0, gn2 = 0.0;
-  rc = vg(P, lp, (const double*)x, (double*)g, &v, &gn2, st);
+  rc = vg(P, lp, (const double*)x, ProArgs{}, (double*)g, &v, &gn2, st);
   if (val) *val = v;
   return rc;
 }
@@ -717,12 +808,20 @@ extern "C" int adp_fft_lower_solve(adp_fft_plan* P, const adp_lower* lp, const v
     return ADP_OK;
   };
   // backtracked step from y (lower_solvers.py:170-177): XC = y - g / L_try
+  // backtracked step from y (lower_solvers.py:170-177): XC = y - g / L_try is the value pass's
+  // row prologue, which also sums the restart dot g . (XC - X) (X = the current iterate)
+  double last_dot = 0.0;
   auto backtrack = [&](const double* yv, double h_y, double gn, double lip_try, double* step_out, int* ok) -> int {
     for (int k = 0; k < 60; ++k) {
-      int r = vec(P, V_STEPDIV, lip_try, yv, nullptr, G, XC, nullptr, st);
-      if (r) return r;
+      ProArgs pa;
+      pa.pro = P_STEP;
+      pa.x2 = G;
+      pa.xold = X;
+      pa.coef = lip_try;
+      pa.wout = XC;
       double hv = 0.0;
-      if ((r = value(P, lp, XC, &hv, st))) return r;
+      int r = value(P, lp, yv, pa, &hv, &last_dot, st);
+      if (r) return r;
       res->value_evals++;
       if (hv <= h_y - 0.5 * gn * gn / lip_try + 1e-15 * std::fabs(h_y)) {
         *step_out = 1.0 / lip_try;
@@ -736,7 +835,7 @@ extern "C" int adp_fft_lower_solve(adp_fft_plan* P, const adp_lower* lp, const v
   };
   if (a->method == ADP_METHOD_PROXGRAD) {   // _gradient_descent (:154-167)
     double h_x = 0.0, gn2 = 0.0;
-    if ((rc = vg(P, lp, X, G, &h_x, &gn2, st))) return rc;
+    if ((rc = vg(P, lp, X, ProArgs{}, G, &h_x, &gn2, st))) return rc;
     res->vg_evals++;
     for (int t = 0; t < a->max_iters; ++t) {
       const double gn = std::sqrt(gn2);
@@ -753,7 +852,7 @@ extern "C" int adp_fft_lower_solve(adp_fft_plan* P, const adp_lower* lp, const v
         if ((rc = vec(P, V_STEPMUL, step, X, nullptr, G, XC, nullptr, st))) return rc;
         std::swap(X, XC);
       }
-      if ((rc = vg(P, lp, X, G, &h_x, &gn2, st))) return rc;
+      if ((rc = vg(P, lp, X, ProArgs{}, G, &h_x, &gn2, st))) return rc;
       res->vg_evals++;
     }
     return finish(X, gn2, a->max_iters, std::sqrt(gn2) <= tol);
@@ -775,38 +874,42 @@ extern "C" int adp_fft_lower_solve(adp_fft_plan* P, const adp_lower* lp, const v
       beta = (t_mom - 1.0) / t_next;
       t_mom = t_next;
     }
-    if ((rc = vec(P, V_EXTRAP, beta, X, xp_is_x ? X : XP, nullptr, Y, nullptr, st))) return rc;
+    // y = x + beta (x - x_prev) is the residual pass's row prologue (stored to Y)
+    ProArgs pe;
+    pe.pro = P_EXTRAP;
+    pe.x2 = xp_is_x ? X : XP;
+    pe.coef = beta;
+    pe.wout = Y;
     double h_y = 0.0, gn2 = 0.0;
-    if ((rc = vg(P, lp, Y, G, &h_y, &gn2, st))) return rc;
+    if ((rc = vg(P, lp, X, pe, G, &h_y, &gn2, st))) return rc;
     res->vg_evals++;
     const double gn = std::sqrt(gn2);
     if (!std::isfinite(gn)) return diverged(t);
     if (gn <= tol) return finish(Y, gn2, t, 1);
     // x_prev = x; x = step from y
+    double d = 0.0;
     if (a->adaptive) {
       int ok = 0;
       double s = 0.0;
       if ((rc = backtrack(Y, h_y, gn, lip_t, &s, &ok))) return rc;
       if (!ok) { res->status = ADP_STATUS_BT_FAIL; return ADP_OK; }
       lip_t = std::max(1.0 / s * 0.9, lip * 1e-8);
+      d = last_dot;
     } else {
       if ((rc = vec(P, V_STEPDIV, lip_t, Y, nullptr, G, XC, nullptr, st))) return rc;
+      if (a->method == ADP_METHOD_AGD && (rc = vec(P, V_DOTDIFF, 0.0, XC, X, G, nullptr, &d, st))) return rc;
     }
     // rotate: XP <- X, X <- XC
     std::swap(XP, X);
     std::swap(X, XC);
     xp_is_x = false;
-    if (a->method == ADP_METHOD_AGD) {   // gradient restart: vdot(g, x - x_prev) > 0
-      double d = 0.0;
-      if ((rc = vec(P, V_DOTDIFF, 0.0, X, XP, G, nullptr, &d, st))) return rc;
-      if (d > 0) {
-        t_mom = 1.0;
-        xp_is_x = true;
-        res->restarts++;
-      }
+    if (a->method == ADP_METHOD_AGD && d > 0) {   // gradient restart: vdot(g, x - x_prev) > 0
+      t_mom = 1.0;
+      xp_is_x = true;
+      res->restarts++;
     }
   }
   double gn2 = 0.0;
-  if ((rc = vg(P, lp, X, G, nullptr, &gn2, st))) return rc;
+  if ((rc = vg(P, lp, X, ProArgs{}, G, nullptr, &gn2, st))) return rc;
   return finish(X, gn2, a->max_iters, std::sqrt(gn2) <= tol);
 }
