@@ -153,8 +153,9 @@ __device__ __forceinline__ void block_coords(int groups, int C, int& p, int& grp
 enum Pro {
   P_NONE = 0,    // input = x
   P_EXTRAP = 1,  // input = y = x + coef (x - x2), stored to wout        (lower_solvers.py:197)
-  P_STEP = 2,    // input = xc = x - x2 / coef (x = y, x2 = g), stored; partial sum g (xc - xold) (:173, :209)
-  P_SCALE = 3    // input = x / coef (power iteration v = w / lam, operators.py:162)
+  P_STEP = 2,    // input = xc = x - x2 * coef (x = y, x2 = g, coef = 1 / L), stored; partial sum g (xc - xold)
+                 // (:173, :209)
+  P_SCALE = 3    // input = x * coef (power iteration v = w / lam with coef = 1 / lam, operators.py:162)
 };
 
 struct RowArgs {
@@ -186,16 +187,16 @@ __device__ __forceinline__ double row_input(const RowArgs& A, int64_t o, bool va
       if (valid) A.wout[o] = u;
       return u;
     }
-    case P_STEP: {
+    case P_STEP: {   // coef = 1 / L: a multiply instead of the reference's division (tolerance mode)
       const double gv = A.x2[o];
-      const double u = xv - gv / A.coef;
+      const double u = xv - gv * A.coef;
       if (valid) {
         A.wout[o] = u;
         dot = dot + gv * (u - A.xold[o]);
       }
       return u;
     }
-    case P_SCALE: return xv / A.coef;
+    case P_SCALE: return xv * A.coef;   // coef = 1 / lam
     default: return xv;
   }
 }
@@ -317,22 +318,26 @@ __device__ __forceinline__ TvTerms tv_at(const Geo& g, const double* __restrict_
   const double x0 = X[o];
   const double d0 = (h + 1 < g.H) ? X[o + rs] - x0 : 0.0;
   const double d1 = (w + 1 < g.W) ? X[o + g.C] - x0 : 0.0;
+  // one reciprocal square root per difference: root = s * rsqrt(s), rho' = d * rsqrt(s)
+  // (a few ulp from sqrt / division; this path is a tolerance mode)
   TvTerms t;
-  t.root0 = sqrt(d0 * d0 + nu2);
-  t.root1 = sqrt(d1 * d1 + nu2);
+  const double s0 = d0 * d0 + nu2, s1 = d1 * d1 + nu2;
+  const double i0 = rsqrt(s0), i1 = rsqrt(s1);
+  t.root0 = s0 * i0;
+  t.root1 = s1 * i1;
   t.grad = 0.0;
   if (want_grad) {
     double acc = 0.0;
     if (h > 0) {
       const double du = x0 - X[o - rs];
-      acc = acc + du / sqrt(du * du + nu2);
+      acc = acc + du * rsqrt(du * du + nu2);
     }
-    acc = acc - d0 / t.root0;
+    acc = acc - d0 * i0;
     if (w > 0) {
       const double dl = x0 - X[o - g.C];
-      acc = acc + dl / sqrt(dl * dl + nu2);
+      acc = acc + dl * rsqrt(dl * dl + nu2);
     }
-    acc = acc - d1 / t.root1;
+    acc = acc - d1 * i1;
     t.grad = acc;
   }
   return t;
@@ -613,7 +618,7 @@ int power(adp_fft_plan* P, const double* v0, int max_iters, double tol, double* 
   for (; it < max_iters; ++it) {
     ProArgs pa;
     pa.pro = P_SCALE;
-    pa.coef = scale;
+    pa.coef = 1.0 / scale;
     if ((rc = stencil(P, 0, vin, pa, E_STORE, Bv, nullptr, nullptr, 0.0, 0.0, nullptr, st))) return rc;
     if ((rc = stencil(P, 1, Bv, ProArgs{}, E_POWER, Wb, nullptr, nullptr, 0.0, 0.0, P->partG, st))) return rc;
     double w2[2];
@@ -817,7 +822,7 @@ extern "C" int adp_fft_lower_solve(adp_fft_plan* P, const adp_lower* lp, const v
       pa.pro = P_STEP;
       pa.x2 = G;
       pa.xold = X;
-      pa.coef = lip_try;
+      pa.coef = 1.0 / lip_try;
       pa.wout = XC;
       double hv = 0.0;
       int r = value(P, lp, yv, pa, &hv, &last_dot, st);
