@@ -23,7 +23,10 @@ up = configs.config2(0)
 x0 = nat.to_dev(up.x0)
 out = nat.empty_like_dev(up.x0.shape)
 key = (nat.LAYOUT_DEPTHWISE2D, tuple(up.x0.shape), (9, 9))
-for tile in [(0, 0), (2, 128), (4, 128), (8, 128), (1, 256), (2, 256), (4, 256), (1, 128)]:
+tiles = [(0, 0), (2, 128), (4, 128), (8, 128), (1, 256), (2, 256), (4, 256), (1, 128)]
+if os.environ.get("ADP_RW") == "1":
+    tiles = [(2, 128), (4, 128), (1, 256), (2, 256), (1, 128)]
+for tile in tiles:
     nat.set_tile(key, tile)
     nat.clear_plans()
     try:
