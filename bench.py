@@ -462,6 +462,17 @@ def c5_fft(args, up5, solve, flush):
         stf = {}
         r, t = _timed(lambda: solve(up5, args.c5_iters, stf))
         plan = p.op.fft_plan()
+    # Jacobi-PCG on the lower Hessian (the hypergradient's CG), 10 iterations: direct strict vs fft
+    from paper_2502_09758_b200.hypergradient import hess_cg
+    rhs = xd * 0.5
+    cg_ms = {}
+    for mode in ("strict", "fft"):
+        with adp.precision("float64", mode):
+            pc = up5.lower_problem(up5.b0)
+            hess_cg(pc, xd, rhs, 1e-300, 2)
+            flush.zero_()
+            (cgr, _), tc = _timed(lambda: hess_cg(pc, xd, rhs, 1e-300, 10))
+            cg_ms[mode] = 1e3 * tc / max(cgr.iters, 1)
     H, W, C = up5.x0.shape
     kh = up5.b0.data.shape[0]
     V = 512 - kh + 1
@@ -473,6 +484,8 @@ def c5_fft(args, up5, solve, flush):
             "stats": {k: stf.get(k) for k in ("power_iters", "vg_evals", "value_evals")},
             "stencils_per_solve": n_sten, "stencil_share": n_sten * fft_ms / (1e3 * t),
             "stencil_ms": {"direct_strict": direct_ms, "fft": fft_ms, "speedup": direct_ms / fft_ms},
+            "cg_ms_per_iter": {"direct_strict": cg_ms["strict"], "fft": cg_ms["fft"],
+                               "note": "hess_cg (hypergradient CG) incl. setup and true residual, 10 iterations"},
             "fft_stencil_roofline": {"bound": "hbm", "achieved": traffic / (fft_ms * 1e-3) / 1e9, "peak": hbm,
                                      "unit": "GB/s", "frac": traffic / (fft_ms * 1e-3) / 1e9 / hbm,
                                      "bytes_per_stencil": traffic,

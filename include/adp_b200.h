@@ -221,6 +221,10 @@ int adp_fft_lower_value_and_grad(adp_fft_plan* p, const adp_lower* lp, const voi
 /* op_norm_sq power iteration (operators.py:137-173) */
 int adp_fft_op_norm_sq(adp_fft_plan* p, const void* kernel, const void* v0, int32_t max_iters, double tol,
                        double* lam, int32_t* converged, int32_t* iters, void* stream);
+/* cg_solve on lower_hess_vec with the lower_hess_diag Jacobi preconditioner (hypergradient.py:35-84 as called
+ * at 171-176): same arguments and result fields as adp_hess_cg */
+int adp_fft_hess_cg(adp_fft_plan* p, const adp_lower* lp, const void* x_tilde, const void* rhs, void* q, int32_t warm,
+                    const void* precond, double tol, int32_t max_iters, adp_cg_result* res, void* stream);
 /* solve_lower (lower_solvers.py:104-213): same arguments and result fields as adp_lower_solve */
 int adp_fft_lower_solve(adp_fft_plan* p, const adp_lower* lp, const void* x0, void* x_out, const adp_solve_args* args,
                         adp_solve_result* res, void* stream);

@@ -155,7 +155,8 @@ enum Pro {
   P_EXTRAP = 1,  // input = y = x + coef (x - x2), stored to wout        (lower_solvers.py:197)
   P_STEP = 2,    // input = xc = x - x2 * coef (x = y, x2 = g, coef = 1 / L), stored; partial sum g (xc - xold)
                  // (:173, :209)
-  P_SCALE = 3    // input = x * coef (power iteration v = w / lam with coef = 1 / lam, operators.py:162)
+  P_SCALE = 3,   // input = x * coef (power iteration v = w / lam with coef = 1 / lam, operators.py:162)
+  P_CGDIR = 4    // input = p' = minv * r + coef * p (x = r, x2 = minv, xold = p), stored to wout (hypergradient.py:79-80)
 };
 
 struct RowArgs {
@@ -197,6 +198,11 @@ __device__ __forceinline__ double row_input(const RowArgs& A, int64_t o, bool va
       return u;
     }
     case P_SCALE: return xv * A.coef;   // coef = 1 / lam
+    case P_CGDIR: {
+      const double u = A.x2[o] * xv + A.coef * A.xold[o];
+      if (valid) A.wout[o] = u;
+      return u;
+    }
     default: return xv;
   }
 }
@@ -291,7 +297,11 @@ __global__ void __launch_bounds__(64 * CCOLS, 3) col_kernel(const __grid_constan
 
 // ---------------------------------------------------------------------------
 // K3: inverse row pass + crop + epilogue.  grid npairs * (T / RROWS) * C, 256 threads.
-enum Epi { E_STORE = 0, E_RESID = 1, E_GRAD = 2, E_VALUE = 3, E_POWER = 4 };
+enum Epi {
+  E_STORE = 0, E_RESID = 1, E_GRAD = 2, E_VALUE = 3, E_POWER = 4,
+  E_HESS = 5,     // out = hv = 2 adj + alpha tvhess(v); partial <v, hv>     (lower_solvers.py:66-71)
+  E_HESSRES = 6   // d = hv - rhs: out = -d (r = rhs - H q) when out != NULL; partial ||d||^2 (hypergradient.py:56,83)
+};
 
 struct InvArgs {
   Geo g;
@@ -303,6 +313,8 @@ struct InvArgs {
   double alpha, nu;
   int epi;
   double* part;         // 2 partial sums per CTA: part[2 * cta + {0, 1}]
+  const double* w0;     // E_HESS*: TV curvature weights rho''(D x~), vertical / horizontal
+  const double* w1;
 };
 
 struct TvTerms {
@@ -388,6 +400,28 @@ __global__ void __launch_bounds__(256, 3) row_inv_kernel(const __grid_constant__
           acc1 = acc1 + (tv.root0 + tv.root1);
           break;
         }
+        case E_HESS:
+        case E_HESSRES: {   // TV hess_vec = D^T (w * D v), v = A.xp (regularizers.py:177-183)
+          const int64_t rs = (int64_t)g.W * g.C;
+          const double v0 = A.xp[o];
+          const double dv0 = (h + 1 < g.H) ? A.xp[o + rs] - v0 : 0.0;
+          const double dv1 = (w + 1 < g.W) ? A.xp[o + g.C] - v0 : 0.0;
+          double tvh = 0.0;
+          if (h > 0) tvh = tvh + A.w0[o - rs] * (v0 - A.xp[o - rs]);
+          tvh = tvh - A.w0[o] * dv0;
+          if (w > 0) tvh = tvh + A.w1[o - g.C] * (v0 - A.xp[o - g.C]);
+          tvh = tvh - A.w1[o] * dv1;
+          const double hv = 2.0 * val + A.alpha * tvh;
+          if (A.epi == E_HESS) {
+            A.out[o] = hv;
+            acc0 = acc0 + v0 * hv;
+          } else {
+            const double d = hv - A.y[o];
+            if (A.out) A.out[o] = -d;
+            acc0 = acc0 + d * d;
+          }
+          break;
+        }
         case E_VALUE: {  // sum (Bx - y)^2 and tv_value = sum(sqrt(d^2 + nu^2) - nu) (regularizers.py:70-72)
           const double rs = val - A.y[o];
           acc0 = acc0 + rs * rs;
@@ -469,6 +503,103 @@ __global__ void __launch_bounds__(1024) fold_kernel(FoldSrc a, FoldSrc b, FoldSr
   }
 }
 
+// ---------------------------------------------------------------------------
+// CG support (hypergradient.py:35-84 on lower_hess_vec / lower_hess_diag)
+// rho''(D x~) per pixel: w0 vertical, w1 horizontal (regularizers.py:34-36, 177-199)
+__global__ void __launch_bounds__(256) curv_kernel(Geo g, const double* __restrict__ x, double nu, double* w0,
+                                                   double* w1) {
+  const int64_t N = (int64_t)g.H * g.W * g.C, rs = (int64_t)g.W * g.C;
+  const double nu2 = nu * nu;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < N; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t hw = o / g.C;
+    const int h = (int)(hw / g.W), w = (int)(hw - (int64_t)h * g.W);
+    const double x0 = x[o];
+    const double d0 = (h + 1 < g.H) ? x[o + rs] - x0 : 0.0;
+    const double d1 = (w + 1 < g.W) ? x[o + g.C] - x0 : 0.0;
+    w0[o] = nu2 / pow(d0 * d0 + nu2, 1.5);
+    w1[o] = nu2 / pow(d1 * d1 + nu2, 1.5);
+  }
+}
+
+// Summed-area table of the flipped kernel squared, per channel: sat[(i * (kw + 1) + j) * C + c] =
+// sum_{i' < i, j' < j} kf[i', j', c]^2, kf = kernel[::-1, ::-1] (operators.py:98, 120-122)
+__global__ void sat_kernel(Geo g, const double* __restrict__ kern, double* sat) {
+  const int c = threadIdx.x;
+  if (c >= g.C) return;
+  const int W1 = g.kw + 1;
+  for (int j = 0; j < W1; ++j) sat[j * g.C + c] = 0.0;
+  for (int i = 1; i <= g.kh; ++i) {
+    double row = 0.0;
+    sat[(i * W1) * g.C + c] = 0.0;
+    for (int j = 1; j <= g.kw; ++j) {
+      const double k = kern[((g.kh - i) * g.kw + (g.kw - j)) * g.C + c];   // kf[i-1, j-1]
+      row = row + k * k;
+      sat[(i * W1 + j) * g.C + c] = sat[((i - 1) * W1 + j) * g.C + c] + row;
+    }
+  }
+}
+
+// d = 2 gram_diag + alpha hess_diag_TV (lower_solvers.py:74-79); partial max per CTA.
+// gram_diag = correlate(ones, kf^2): the in-image taps form an i- and a j-interval -> 4 SAT lookups.
+__global__ void __launch_bounds__(256) diag_kernel(Geo g, const double* __restrict__ sat, const double* __restrict__ w0,
+                                                   const double* __restrict__ w1, double alpha, double* d,
+                                                   double* part) {
+  __shared__ double red[40];
+  const int64_t N = (int64_t)g.H * g.W * g.C, rs = (int64_t)g.W * g.C;
+  const int W1 = g.kw + 1;
+  double mx = -INFINITY;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < N; o += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t hw = o / g.C;
+    const int c = (int)(o - hw * g.C);
+    const int h = (int)(hw / g.W), w = (int)(hw - (int64_t)h * g.W);
+    const int i0 = max(0, g.rh - h), i1 = min(g.kh, g.H - h + g.rh);   // 0 <= h + i - rh < H
+    const int j0 = max(0, g.rw - w), j1 = min(g.kw, g.W - w + g.rw);
+    const double gram = sat[(i1 * W1 + j1) * g.C + c] - sat[(i0 * W1 + j1) * g.C + c] -
+                        sat[(i1 * W1 + j0) * g.C + c] + sat[(i0 * W1 + j0) * g.C + c];
+    double tv = 0.0;
+    if (h + 1 < g.H) tv = tv + w0[o];
+    if (h > 0) tv = tv + w0[o - rs];
+    if (w + 1 < g.W) tv = tv + w1[o];
+    if (w > 0) tv = tv + w1[o - g.C];
+    const double v = 2.0 * gram + alpha * tv;
+    d[o] = v;
+    mx = fmax(mx, v);
+  }
+  const double m = block_max(mx, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = m;
+}
+
+// minv = 1 / max(d, floor) in place (lower_solvers.py:80; hypergradient.py:52-54)
+__global__ void __launch_bounds__(256) minv_kernel(int64_t n, double floor_, double* d) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = 1.0 / fmax(d[i], floor_);
+}
+
+// CG step (hypergradient.py:75-78): q += a p; r -= a hp; partials <r, minv r> and <r, r>.
+// With first != 0 (the start): r given, partials only.
+__global__ void __launch_bounds__(256) cg_update_kernel(int64_t n, double a, double* q, double* r,
+                                                        const double* __restrict__ p, const double* __restrict__ hp,
+                                                        const double* __restrict__ minv, int first, double* part) {
+  __shared__ double red[40];
+  double rz = 0.0, rr = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    double ri = r[i];
+    if (!first) {
+      q[i] = q[i] + a * p[i];
+      ri = ri - a * hp[i];
+      r[i] = ri;
+    }
+    rz = rz + ri * (minv[i] * ri);
+    rr = rr + ri * ri;
+  }
+  const double s0 = block_sum(rz, red);
+  const double s1 = block_sum(rr, red);
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = s0;
+    part[2 * blockIdx.x + 1] = s1;
+  }
+}
+
 }  // namespace fft
 }  // namespace adp
 
@@ -490,6 +621,8 @@ struct adp_fft_plan {
   double* red = nullptr;       // fold results (device)
   double* hred = nullptr;      // pinned host copy
   double* buf[6] = {};         // solver images
+  double* cgbuf[7] = {};       // CG images (allocated at first use): r, p0, p1, hp, minv, w0, w1
+  double* sat = nullptr;       // summed-area table of the flipped kernel squared
   int nrow_ctas = 0;
   const void* spec_kernel = nullptr;   // kernel pointer the spectra were built from (this call)
   size_t bytes = 0;
@@ -536,7 +669,7 @@ int stencil(adp_fft_plan* P, int adj, const double* x, const ProArgs& pa, int ep
   row_fwd_kernel<<<rgrid, 256, 0, st>>>(ra);
   ColArgs ca{g, P->S, P->spec + (size_t)adj * g.C * T * T, nullptr, P->tw, 0, g.npairs};
   col_kernel<<<g.npairs * (T / CCOLS) * g.C, 64 * CCOLS, 0, st>>>(ca);
-  InvArgs ia{g, P->S, P->tw, out, y, xp, alpha, nu, epi, part3};
+  InvArgs ia{g, P->S, P->tw, out, y, xp, alpha, nu, epi, part3, P->cgbuf[5], P->cgbuf[6]};
   row_inv_kernel<<<rgrid, 256, 0, st>>>(ia);
   return check_launch("fft stencil");
 }
@@ -707,6 +840,8 @@ extern "C" void adp_fft_plan_destroy(adp_fft_plan* P) {
   cudaFree(P->red);
   if (P->hred) cudaFreeHost(P->hred);
   for (double* b : P->buf) cudaFree(b);
+  for (double* b : P->cgbuf) cudaFree(b);
+  cudaFree(P->sat);
   delete P;
 }
 
@@ -917,4 +1052,109 @@ extern "C" int adp_fft_lower_solve(adp_fft_plan* P, const adp_lower* lp, const v
   double gn2 = 0.0;
   if ((rc = vg(P, lp, X, ProArgs{}, G, nullptr, &gn2, st))) return rc;
   return finish(X, gn2, a->max_iters, std::sqrt(gn2) <= tol);
+}
+
+// cg_solve on lower_hess_vec with the lower_hess_diag Jacobi preconditioner (hypergradient.py:35-84 as
+// called at 171-176), every Hessian product = two tile-FFT stencils with the TV term in the epilogue;
+// the next search direction p = minv r + beta p rides in the first stencil's row prologue.
+extern "C" int adp_fft_hess_cg(adp_fft_plan* P, const adp_lower* lp, const void* x_tilde, const void* rhs, void* q,
+                               int32_t warm, const void* precond, double tol, int32_t max_iters, adp_cg_result* res,
+                               void* stream) {
+  if (!P || !lp || !x_tilde || !rhs || !q || !res) return dense_fail(ADP_ERR_ARG, "fft hess_cg: null argument");
+  if (lp->reg != ADP_REG_TV) return dense_fail(ADP_ERR_UNSUPPORTED, "fft path: smoothed TV only");
+  if (!(tol > 0)) return dense_fail(ADP_ERR_ARG, "tol must be > 0");
+  cudaStream_t st = (cudaStream_t)stream;
+  *res = adp_cg_result{};
+  int rc = prepare(P, lp->kernel, st);
+  if (rc) return rc;
+  for (int i = 0; i < 7; ++i)
+    if (!P->cgbuf[i] && cudaMalloc(&P->cgbuf[i], (size_t)P->N * sizeof(double)) != cudaSuccess)
+      return dense_fail(ADP_ERR_CUDA, "fft hess_cg: device allocation failed");
+  if (!P->sat && cudaMalloc(&P->sat, (size_t)(P->g.kh + 1) * (P->g.kw + 1) * P->g.C * sizeof(double)) != cudaSuccess)
+    return dense_fail(ADP_ERR_CUDA, "fft hess_cg: device allocation failed");
+  const Geo& g = P->g;
+  const int64_t n = P->N;
+  double* R = P->cgbuf[0];
+  double* Pb[2] = {P->cgbuf[1], P->cgbuf[2]};
+  double* HP = P->cgbuf[3];
+  double* MINV = P->cgbuf[4];
+  double* Bp = P->buf[5];
+  double* Q = (double*)q;
+  const double* RHS = (const double*)rhs;
+  // curvature weights of x~ and the Jacobi diagonal
+  curv_kernel<<<kVecGrid, 256, 0, st>>>(g, (const double*)x_tilde, lp->nu, P->cgbuf[5], P->cgbuf[6]);
+  double floor_ = -1e308;
+  if (precond) {
+    cudaMemcpyAsync(MINV, precond, n * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  } else {
+    sat_kernel<<<1, 32, 0, st>>>(g, (const double*)lp->kernel, P->sat);
+    diag_kernel<<<kVecGrid, 256, 0, st>>>(g, P->sat, P->cgbuf[5], P->cgbuf[6], lp->alpha, MINV, P->partV);
+    if ((rc = check_launch("fft hess_cg diag"))) return rc;
+    // max over the per-CTA maxima (exact in any order)
+    std::vector<double> pm(kVecGrid);
+    cudaMemcpyAsync(pm.data(), P->partV, kVecGrid * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess) return dense_fail(ADP_ERR_CUDA, "fft hess_cg: diag");
+    double mx = -INFINITY;
+    for (double v : pm) mx = std::max(mx, v);
+    floor_ = 1e-12 * mx + 1e-300;
+  }
+  minv_kernel<<<kVecGrid, 256, 0, st>>>(n, floor_, MINV);
+  // r = rhs - H q (warm start) or q = 0, r = rhs
+  if (warm) {
+    if ((rc = stencil(P, 0, Q, ProArgs{}, E_STORE, Bp, nullptr, nullptr, 0.0, 0.0, nullptr, st))) return rc;
+    if ((rc = stencil(P, 1, Bp, ProArgs{}, E_HESSRES, R, RHS, Q, lp->alpha, lp->nu, P->partG, st))) return rc;
+    res->hv++;
+  } else {
+    cudaMemsetAsync(Q, 0, n * sizeof(double), st);
+    cudaMemcpyAsync(R, RHS, n * sizeof(double), cudaMemcpyDeviceToDevice, st);
+  }
+  cg_update_kernel<<<kVecGrid, 256, 0, st>>>(n, 0.0, Q, R, nullptr, nullptr, MINV, 1, P->partV);
+  double t2[2];
+  if ((rc = fold(P, FoldSrc{P->partV, kVecGrid, 2}, kNoSrc, kNoSrc, t2, st))) return rc;
+  double rs = t2[0], rr = t2[1], beta = 0.0;
+  int iters = 0, cur = 0;
+  const double* pold = MINV;   // p_1 = s_0 = minv r (+ 0 * a finite vector)
+  for (iters = 1; iters <= max_iters; ++iters) {
+    if (std::sqrt(rr) <= tol) {
+      iters -= 1;
+      break;
+    }
+    ProArgs pa;
+    pa.pro = P_CGDIR;
+    pa.x2 = MINV;
+    pa.xold = pold;
+    pa.coef = beta;
+    pa.wout = Pb[cur];
+    if ((rc = stencil(P, 0, R, pa, E_STORE, Bp, nullptr, nullptr, 0.0, 0.0, nullptr, st))) return rc;
+    if ((rc = stencil(P, 1, Bp, ProArgs{}, E_HESS, HP, nullptr, Pb[cur], lp->alpha, lp->nu, P->partG, st))) return rc;
+    res->hv++;
+    double cv[2];
+    if ((rc = fold(P, src3(P, P->partG), kNoSrc, kNoSrc, cv, st))) return rc;
+    const double curv = cv[0];
+    if (curv <= 0) {
+      res->status = ADP_STATUS_NEGCURV;
+      res->curv = curv;
+      res->iters = iters;
+      return ADP_OK;
+    }
+    const double a = rs / curv;
+    cg_update_kernel<<<kVecGrid, 256, 0, st>>>(n, a, Q, R, Pb[cur], HP, MINV, 0, P->partV);
+    if ((rc = fold(P, FoldSrc{P->partV, kVecGrid, 2}, kNoSrc, kNoSrc, t2, st))) return rc;
+    beta = t2[0] / rs;
+    rs = t2[0];
+    rr = t2[1];
+    pold = Pb[cur];
+    cur ^= 1;
+  }
+  if (iters > max_iters) iters = max_iters;
+  // true residual ||H q - rhs|| (hypergradient.py:83)
+  if ((rc = stencil(P, 0, Q, ProArgs{}, E_STORE, Bp, nullptr, nullptr, 0.0, 0.0, nullptr, st))) return rc;
+  if ((rc = stencil(P, 1, Bp, ProArgs{}, E_HESSRES, nullptr, RHS, Q, lp->alpha, lp->nu, P->partG, st))) return rc;
+  res->hv++;
+  double tr[2];
+  if ((rc = fold(P, src3(P, P->partG), kNoSrc, kNoSrc, tr, st))) return rc;
+  res->residual = std::sqrt(tr[0]);
+  res->iters = iters;
+  res->converged = res->residual <= tol;
+  return ADP_OK;
 }

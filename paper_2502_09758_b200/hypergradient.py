@@ -150,6 +150,7 @@ def mixed_second_transpose(x_tilde, b: Kernel, q, p: LowerProblem) -> np.ndarray
     xd = nat.to_dev(x_tilde, p.op.signal_shape)
     qd = nat.to_dev(q, p.op.signal_shape)
     out = nat.empty_like_dev(b.data.shape)
+    plan = plan or p.op.plan()   # fft mode: kernel-gradient correlations on the direct kernels
     nat.check(nat.lib().adp_mixed_T(plan.handle, ctypes.byref(s), nat.ptr(xd), nat.ptr(qd), nat.ptr(out),
                                     nat.stream_ptr()), "mixed_second_transpose")
     return nat.to_host(out).astype(float)
@@ -213,9 +214,12 @@ def hess_cg(p: LowerProblem, x_tilde, rhs, tol: float, max_iters: int, q0=None):
         q = nat.to_dev(q0, p.op.signal_shape).clone()
         warm = 1
     r = nat.CGResultC()
-    nat.check(nat.lib().adp_hess_cg(plan.handle, ctypes.byref(s), nat.ptr(xd), nat.ptr(rd), nat.ptr(q), warm,
-                                    ctypes.c_void_p(0), float(tol), int(max_iters), ctypes.byref(r),
-                                    nat.stream_ptr()), "hess_cg")
+    if plan is None:   # fft mode: Hessian products on the tile-FFT stencils
+        fn, handle = nat.lib().adp_fft_hess_cg, p.op.fft_plan().handle
+    else:
+        fn, handle = nat.lib().adp_hess_cg, plan.handle
+    nat.check(fn(handle, ctypes.byref(s), nat.ptr(xd), nat.ptr(rd), nat.ptr(q), warm, ctypes.c_void_p(0), float(tol),
+                 int(max_iters), ctypes.byref(r), nat.stream_ptr()), "hess_cg")
     if r.status == nat.STATUS_NEGCURV:
         raise _negcurv(float(r.curv))
     return CGResult(q, float(r.residual), int(r.iters), bool(r.converged)), int(r.hv)

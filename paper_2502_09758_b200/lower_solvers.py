@@ -52,7 +52,7 @@ def _native_lower(p: LowerProblem):
             raise ValueError("the depthwise 2-D operator is paired with SmoothedTV")
     else:
         raise TypeError(f"unsupported operator {type(op).__name__}")
-    plan = op.plan()
+    plan = None if (nat.is_fft() and isinstance(op, ConvOperator)) else op.plan()   # fft: tile-FFT plan instead
     s = reg.native()
     kd = _op_kernel(op).device()
     yd = _ydev(p)
@@ -136,6 +136,7 @@ def lower_hess_vec(p: LowerProblem, x, v):
     xd = nat.to_dev(x, p.op.signal_shape)
     vd = nat.to_dev(v, p.op.signal_shape)
     out = nat.empty_like_dev(p.op.signal_shape)
+    plan = plan or p.op.plan()   # fft mode: the Hessian product runs on the direct (fast) stencils
     nat.check(nat.lib().adp_lower_hess_vec(plan.handle, ctypes.byref(s), nat.ptr(xd), nat.ptr(vd), nat.ptr(out),
                                            nat.stream_ptr()), "lower_hess_vec")
     return nat.like(out, v)
@@ -148,6 +149,7 @@ def lower_hess_diag(p: LowerProblem, x):
     plan, s, keep = _native_lower(p)
     xd = nat.to_dev(x, p.op.signal_shape)
     out = nat.empty_like_dev(p.op.signal_shape)
+    plan = plan or p.op.plan()
     nat.check(nat.lib().adp_lower_hess_diag(plan.handle, ctypes.byref(s), nat.ptr(xd), nat.ptr(out),
                                             nat.stream_ptr()), "lower_hess_diag")
     return nat.like(out, x)

@@ -130,3 +130,45 @@ def test_fft_solve_methods_and_errors(adp, orc):
     assert rel(r.x_tilde, xo) <= 1e-9
     with pytest.raises(ValueError):
         adp.set_precision("float32", "fft")
+
+
+@pytest.mark.parametrize("warm", [False, True])
+def test_fft_hess_cg_matches_oracle(adp, orc, warm):
+    """Jacobi-PCG on the lower Hessian with FFT Hessian products (the TV
+    curvature term in the stencil epilogue, the SAT-based gram diagonal):
+    a few iterations track the oracle's cg_solve before the TV Hessian's
+    conditioning amplifies rounding (DESIGN.md, 2-D hypergradient)."""
+    from paper_2502_09758_b200.hypergradient import hess_cg
+    shape = (150, 140, 2)
+    p, po, y, rng = _problem(adp, orc, shape, 15, 3.0, 6)
+    xt = y + 0.02 * rng.standard_normal(shape)
+    rhs = rng.standard_normal(shape)
+    q0 = 0.01 * rng.standard_normal(shape) if warm else None
+    cg, hv = hess_cg(p, xt, rhs, 1e-30, 6, q0=q0)
+    qo, res_o, it_o, _ = orc.cg_solve(lambda v: orc.lower_hess_vec(po, xt, v), rhs, 1e-30, 6, x0=q0,
+                                      precond_diag=orc.lower_hess_diag(po, xt))
+    assert cg.iters == it_o == 6
+    assert rel(cg.q.cpu().numpy(), qo) <= 1e-8
+    assert abs(cg.residual - res_o) <= 1e-6 * res_o
+    assert hv == 6 + 1 + (1 if warm else 0)
+    # converged solve on an easy tolerance: same stopping iteration
+    tol = 0.5 * float(np.linalg.norm(rhs))
+    cg2, _ = hess_cg(p, xt, rhs, tol, 50)
+    q2, r2, it2, conv2 = orc.cg_solve(lambda v: orc.lower_hess_vec(po, xt, v), rhs, tol, 50,
+                                      precond_diag=orc.lower_hess_diag(po, xt))
+    assert cg2.iters == it2 and cg2.converged == conv2
+
+
+def test_fft_inexact_hypergradient_runs_and_agrees(adp, orc):
+    """Algorithm 1 end to end in fft mode on a small semi-blind problem: the
+    hypergradient agrees with the direct (fast) pipeline to the tolerance the
+    inexact solves allow."""
+    from paper_2502_09758_b200 import configs
+    up = configs.config3(0, size=96)
+    st = adp.WarmState(x=up.x0.copy(), q=None)
+    h = adp.inexact_hypergradient(up, up.b0, 1e-3, 1e-3, st, cg_max_iters=15)
+    with adp.precision("float64", "fast"):
+        st2 = adp.WarmState(x=up.x0.copy(), q=None)
+        h2 = adp.inexact_hypergradient(up, up.b0, 1e-3, 1e-3, st2, cg_max_iters=15)
+    assert h.cg_iters == h2.cg_iters
+    assert np.isfinite(h.z).all() and rel(h.z, h2.z) <= 1e-2
