@@ -225,6 +225,10 @@ int adp_fft_op_norm_sq(adp_fft_plan* p, const void* kernel, const void* v0, int3
  * at 171-176): same arguments and result fields as adp_hess_cg */
 int adp_fft_hess_cg(adp_fft_plan* p, const adp_lower* lp, const void* x_tilde, const void* rhs, void* q, int32_t warm,
                     const void* precond, double tol, int32_t max_iters, adp_cg_result* res, void* stream);
+/* UpperProblem.fit_value and ||upper_fit_grad|| (problems.py:48-50, hypergradient.py:87-89): same arguments as
+ * adp_upper_terms (grad_out may be NULL) */
+int adp_fft_upper_terms(adp_fft_plan* p, const void* A_kernel, const void* x, const void* y_delta, double* fit,
+                        double* grad_norm, void* grad_out, void* stream);
 /* solve_lower (lower_solvers.py:104-213): same arguments and result fields as adp_lower_solve */
 int adp_fft_lower_solve(adp_fft_plan* p, const adp_lower* lp, const void* x0, void* x_out, const adp_solve_args* args,
                         adp_solve_result* res, void* stream);

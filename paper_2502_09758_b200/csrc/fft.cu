@@ -300,7 +300,8 @@ __global__ void __launch_bounds__(64 * CCOLS, 3) col_kernel(const __grid_constan
 enum Epi {
   E_STORE = 0, E_RESID = 1, E_GRAD = 2, E_VALUE = 3, E_POWER = 4,
   E_HESS = 5,     // out = hv = 2 adj + alpha tvhess(v); partial <v, hv>     (lower_solvers.py:66-71)
-  E_HESSRES = 6   // d = hv - rhs: out = -d (r = rhs - H q) when out != NULL; partial ||d||^2 (hypergradient.py:56,83)
+  E_HESSRES = 6,  // d = hv - rhs: out = -d (r = rhs - H q) when out != NULL; partial ||d||^2 (hypergradient.py:56,83)
+  E_TWICE = 7     // out = 2 v (when out != NULL); partial ||2 v||^2 (upper_fit_grad, hypergradient.py:87-89)
 };
 
 struct InvArgs {
@@ -386,6 +387,12 @@ __global__ void __launch_bounds__(256, 3) row_inv_kernel(const __grid_constant__
       switch (A.epi) {
         case E_STORE: A.out[o] = val; break;
         case E_POWER: A.out[o] = val; acc0 = acc0 + val * val; break;
+        case E_TWICE: {
+          const double gv = 2.0 * val;
+          if (A.out) A.out[o] = gv;
+          acc0 = acc0 + gv * gv;
+          break;
+        }
         case E_RESID: {
           const double rs = val - A.y[o];
           A.out[o] = rs;
@@ -1156,5 +1163,25 @@ extern "C" int adp_fft_hess_cg(adp_fft_plan* P, const adp_lower* lp, const void*
   res->residual = std::sqrt(tr[0]);
   res->iters = iters;
   res->converged = res->residual <= tol;
+  return ADP_OK;
+}
+
+// UpperProblem.fit_value and ||upper_fit_grad|| (problems.py:48-50, hypergradient.py:87-89):
+// r = A x - y_delta (residual pass), grad = 2 A^T r (adjoint pass with the doubling in the epilogue)
+extern "C" int adp_fft_upper_terms(adp_fft_plan* P, const void* A_kernel, const void* x, const void* y_delta,
+                                   double* fit, double* grad_norm, void* grad_out, void* stream) {
+  if (!P || !A_kernel || !x || !y_delta || !fit || !grad_norm) return dense_fail(ADP_ERR_ARG, "fft upper_terms: null");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = prepare(P, A_kernel, st);
+  if (rc) return rc;
+  double* R = P->buf[5];
+  if ((rc = stencil(P, 0, (const double*)x, ProArgs{}, E_RESID, R, (const double*)y_delta, nullptr, 0.0, 0.0, P->partR,
+                    st)))
+    return rc;
+  if ((rc = stencil(P, 1, R, ProArgs{}, E_TWICE, (double*)grad_out, nullptr, nullptr, 0.0, 0.0, P->partG, st))) return rc;
+  double t[4];
+  if ((rc = fold(P, src3(P, P->partR), src3(P, P->partG), kNoSrc, t, st))) return rc;
+  *fit = t[0];
+  *grad_norm = std::sqrt(t[2]);
   return ADP_OK;
 }

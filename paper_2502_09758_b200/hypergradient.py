@@ -112,16 +112,17 @@ def cg_solve(hess_vec, rhs, tol: float, max_iters: int = 200, x0=None, precond_d
 
 def _upper_terms(A, x, y_delta, want_grad=False):
     """(sum((Ax - y)^2), ||2 A^T (Ax - y)||, optional grad) in one launch."""
-    from .operators import _op_kernel
-    plan = A.plan()
+    from .operators import ConvOperator, _op_kernel
+    fft = nat.is_fft() and isinstance(A, ConvOperator)   # tile-FFT stencils (SURVEY.md §8 f2)
+    plan = A.fft_plan() if fft else A.plan()
     xd = nat.to_dev(x, A.signal_shape)
     yd = y_delta if nat.is_torch(y_delta) and y_delta.is_cuda else _cached_dev(A, y_delta)
     g = nat.empty_like_dev(A.signal_shape) if want_grad else None
     fit = ctypes.c_double()
     gn = ctypes.c_double()
-    nat.check(nat.lib().adp_upper_terms(plan.handle, nat.ptr(_op_kernel(A).device()), nat.ptr(xd), nat.ptr(yd),
-                                        ctypes.byref(fit), ctypes.byref(gn), nat.ptr(g), nat.stream_ptr()),
-              "upper_terms")
+    fn = nat.lib().adp_fft_upper_terms if fft else nat.lib().adp_upper_terms
+    nat.check(fn(plan.handle, nat.ptr(_op_kernel(A).device()), nat.ptr(xd), nat.ptr(yd), ctypes.byref(fit),
+                 ctypes.byref(gn), nat.ptr(g), nat.stream_ptr()), "upper_terms")
     return float(fit.value), float(gn.value), g
 
 

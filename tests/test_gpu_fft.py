@@ -172,3 +172,20 @@ def test_fft_inexact_hypergradient_runs_and_agrees(adp, orc):
         h2 = adp.inexact_hypergradient(up, up.b0, 1e-3, 1e-3, st2, cg_max_iters=15)
     assert h.cg_iters == h2.cg_iters
     assert np.isfinite(h.z).all() and rel(h.z, h2.z) <= 1e-2
+
+
+def test_fft_upper_terms(adp, orc):
+    """fit_value and upper_fit_grad (problems.py:48-50, hypergradient.py:87-89) on FFT stencils."""
+    from paper_2502_09758_b200.hypergradient import _upper_terms
+    shape = (300, 200, 3)
+    rng = np.random.default_rng(8)
+    kern = gauss(31, 6.0, 3, rng)
+    A = adp.ConvOperator(adp.Kernel(kern, adp.DEPTHWISE2D), shape)
+    x, yd = rng.uniform(0, 1, shape), rng.uniform(0, 1, shape)
+    fit, gn, g = _upper_terms(A, x, yd, want_grad=True)
+    Ao = orc.Conv(kern, shape)
+    r = Ao.apply(x) - yd
+    go = orc.upper_fit_grad(x, Ao, yd)
+    assert abs(fit - orc.npsum(r * r)) <= 1e-12 * fit
+    assert rel(g.cpu().numpy(), go) <= 1e-12
+    assert abs(gn - orc.norm(go)) <= 1e-12 * gn
