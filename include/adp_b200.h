@@ -229,6 +229,9 @@ int adp_fft_hess_cg(adp_fft_plan* p, const adp_lower* lp, const void* x_tilde, c
  * adp_upper_terms (grad_out may be NULL) */
 int adp_fft_upper_terms(adp_fft_plan* p, const void* A_kernel, const void* x, const void* y_delta, double* fit,
                         double* grad_norm, void* grad_out, void* stream);
+/* mixed_second_transpose 2 [kgc(x~, B q) + kgc(q, B x~ - y)] (hypergradient.py:92-104, operators.py:198-220):
+ * same arguments as adp_mixed_T (out: device, kernel-shaped (kh, kw, C)) */
+int adp_fft_mixed_T(adp_fft_plan* p, const adp_lower* lp, const void* x_tilde, const void* q, void* out, void* stream);
 /* solve_lower (lower_solvers.py:104-213): same arguments and result fields as adp_lower_solve */
 int adp_fft_lower_solve(adp_fft_plan* p, const adp_lower* lp, const void* x0, void* x_out, const adp_solve_args* args,
                         adp_solve_result* res, void* stream);

@@ -102,6 +102,7 @@ SIGNATURES = {
     "adp_fft_op_norm_sq": (_I, [_P, _P, _P, _I, _D, ctypes.POINTER(_D), ctypes.POINTER(_I), ctypes.POINTER(_I), _P]),
     "adp_fft_hess_cg": (_I, [_P, ctypes.POINTER(Lower), _P, _P, _P, _I, _P, _D, _I, ctypes.POINTER(CGResultC), _P]),
     "adp_fft_upper_terms": (_I, [_P, _P, _P, _P, ctypes.POINTER(_D), ctypes.POINTER(_D), _P, _P]),
+    "adp_fft_mixed_T": (_I, [_P, ctypes.POINTER(Lower), _P, _P, _P, _P]),
     "adp_fft_lower_solve": (_I, [_P, ctypes.POINTER(Lower), _P, _P, ctypes.POINTER(SolveArgs),
                                  ctypes.POINTER(SolveResult), _P]),
     "adp_debug_trace": (_I, [_P, _I, _P]),

@@ -238,6 +238,21 @@ __global__ void __launch_bounds__(256, 3) row_fwd_kernel(const __grid_constant__
       const double s = block_sum(dot, red);
       if (threadIdx.x == 0) A.part[blockIdx.x] = s;
     }
+  } else if (A.mode == 2) {   // kgc: the tiles' own valid-region pixels v[h0 + a, w0 + b] (zero elsewhere)
+    int h0a, w0a, h0b = 0, w0b = 0;
+    tile_origin(g, 2 * p, h0a, w0a);
+    const bool hasb = 2 * p + 1 < g.ntiles;
+    if (hasb) tile_origin(g, 2 * p + 1, h0b, w0b);
+    const bool vrow = row < g.Vh;
+    const bool rowa = vrow && h0a + row < g.H, rowb = vrow && hasb && h0b + row < g.H;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int col = j + 64 * r;
+      double re = 0.0, im = 0.0;
+      if (rowa && col < g.Vw && w0a + col < g.W) re = A.x[((int64_t)(h0a + row) * g.W + w0a + col) * g.C + c];
+      if (rowb && col < g.Vw && w0b + col < g.W) im = A.x[((int64_t)(h0b + row) * g.W + w0b + col) * g.C + c];
+      v[r] = make_double2(re, im);
+    }
   } else {
 #pragma unroll
     for (int r = 0; r < 8; ++r) {
@@ -280,6 +295,12 @@ __global__ void __launch_bounds__(64 * CCOLS, 3) col_kernel(const __grid_constan
   double2 v[8];
 #pragma unroll
   for (int r = 0; r < 8; ++r) v[r] = S[(int64_t)(j + 64 * r) * T];
+  if (A.mode == 2) {   // inverse column FFTs only (kgc accumulator)
+    fft512_reg<true>(v, sm + bi * kPadB, j, A.tw);
+#pragma unroll
+    for (int r = 0; r < 8; ++r) S[(int64_t)(j + 64 * r) * T] = v[r];
+    return;
+  }
   fft512_reg<false>(v, sm + bi * kPadB, j, A.tw);
   if (A.mode == 1) {
     double2* o = A.spec_out + ((int64_t)p * A.g.C + c) * T * T + col;
@@ -293,6 +314,66 @@ __global__ void __launch_bounds__(64 * CCOLS, 3) col_kernel(const __grid_constan
   fft512_reg<true>(v, sm + bi * kPadB, j, A.tw);
 #pragma unroll
   for (int r = 0; r < 8; ++r) S[(int64_t)(j + 64 * r) * T] = v[r];
+}
+
+// kernel_gram_correlation by tile FFTs (operators.py:198-220, hypergradient.py:92-104):
+//   kgc(x, v)[i, j] = sum_tiles sum_{a,b} u_t[a + i, b + j] vt_t[a, b]
+// with u_t the tile's input window of x (the stencil row pass, mode 0) and vt_t the tile's own
+// pixels of v (mode 2): per pair Z_u conj(Z_v), whose inverse transform's real part is the sum
+// of the pair's two correlations (the cross terms are purely imaginary), summed over pairs in
+// the frequency domain; one inverse transform per channel gives the K^2 lags.
+__global__ void __launch_bounds__(64 * CCOLS, 2) col_corr_kernel(const __grid_constant__ ColArgs A,
+                                                                 const double2* __restrict__ Sv) {
+  __shared__ __align__(16) double2 sm[CCOLS * kPadB];
+  int p, strip, c;
+  block_coords(T / CCOLS, A.g.C, p, strip, c);
+  const int bi = threadIdx.x % CCOLS, j = threadIdx.x / CCOLS;
+  const int col = strip * CCOLS + bi;
+  const int64_t off = ((int64_t)c * A.npairs + p) * T * T + col;
+  double2* S = A.S + off;
+  double2 u[8], v[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) u[r] = S[(int64_t)(j + 64 * r) * T];
+  fft512_reg<false>(u, sm + bi * kPadB, j, A.tw);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) v[r] = Sv[off + (int64_t)(j + 64 * r) * T];
+  fft512_reg<false>(v, sm + bi * kPadB, j, A.tw);
+#pragma unroll
+  for (int r = 0; r < 8; ++r) S[(int64_t)(j + 64 * r) * T] = cmul(u[r], make_double2(v[r].x, -v[r].y));
+}
+
+// acc[c][i] (+)= sum over pairs p (in order) of S[c][p][i]
+__global__ void __launch_bounds__(256) pair_sum_kernel(const double2* __restrict__ S, int npairs, int C, int accumulate,
+                                                       double2* acc) {
+  const int64_t n = (int64_t)C * T * T;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = e / ((int64_t)T * T), i = e - c * T * T;
+    double2 s = accumulate ? acc[e] : make_double2(0.0, 0.0);
+    const double2* src = S + c * npairs * T * T + i;
+    for (int p = 0; p < npairs; ++p) s = cadd(s, src[(int64_t)p * T * T]);
+    acc[e] = s;
+  }
+}
+
+// rows i < kh of the column-inverted accumulator: inverse row FFT, out[i, j, c] = scale Re(.) for j < kw
+__global__ void __launch_bounds__(256) kgc_final_kernel(Geo g, const double2* __restrict__ acc,
+                                                        const double2* __restrict__ tw, double scale, double* out) {
+  __shared__ __align__(16) double2 sm[RROWS * kPadB];
+  const int groups = (g.kh + RROWS - 1) / RROWS;
+  const int c = blockIdx.x / groups, i0 = (blockIdx.x - c * groups) * RROWS;
+  const int j = threadIdx.x & 63, rr = threadIdx.x >> 6, i = i0 + rr;
+  const double2* row = acc + ((int64_t)c * T + min(i, T - 1)) * T;
+  double2 v[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) v[r] = row[j + 64 * r];
+  fft512_reg<true>(v, sm + rr * kPadB, j, tw);
+  if (i < g.kh) {
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int jj = j + 64 * r;
+      if (jj < g.kw) out[((int64_t)i * g.kw + jj) * g.C + c] = scale * v[r].x;
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -630,6 +711,8 @@ struct adp_fft_plan {
   double* buf[6] = {};         // solver images
   double* cgbuf[7] = {};       // CG images (allocated at first use): r, p0, p1, hp, minv, w0, w1
   double* sat = nullptr;       // summed-area table of the flipped kernel squared
+  double2* S2 = nullptr;       // kgc: second complex scratch (first use)
+  double2* acc = nullptr;      // kgc: (C, T, T) frequency-domain accumulator
   int nrow_ctas = 0;
   const void* spec_kernel = nullptr;   // kernel pointer the spectra were built from (this call)
   size_t bytes = 0;
@@ -849,6 +932,8 @@ extern "C" void adp_fft_plan_destroy(adp_fft_plan* P) {
   for (double* b : P->buf) cudaFree(b);
   for (double* b : P->cgbuf) cudaFree(b);
   cudaFree(P->sat);
+  cudaFree(P->S2);
+  cudaFree(P->acc);
   delete P;
 }
 
@@ -1184,4 +1269,43 @@ extern "C" int adp_fft_upper_terms(adp_fft_plan* P, const void* A_kernel, const 
   *fit = t[0];
   *grad_norm = std::sqrt(t[2]);
   return ADP_OK;
+}
+
+// mixed_second_transpose (hypergradient.py:92-104): 2 [kgc(x~, B q) + kgc(q, B x~ - y)] on tile FFTs;
+// out is the kernel-shaped (kh, kw, C) device array.
+extern "C" int adp_fft_mixed_T(adp_fft_plan* P, const adp_lower* lp, const void* x_tilde, const void* q, void* out,
+                               void* stream) {
+  if (!P || !lp || !x_tilde || !q || !out) return dense_fail(ADP_ERR_ARG, "fft mixed_T: null argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = prepare(P, lp->kernel, st);
+  if (rc) return rc;
+  const Geo& g = P->g;
+  const size_t sbytes = (size_t)g.C * std::max(2, g.npairs) * T * T * sizeof(double2);
+  if (!P->S2 && cudaMalloc(&P->S2, sbytes) != cudaSuccess) return dense_fail(ADP_ERR_CUDA, "fft mixed_T: allocation");
+  if (!P->acc && cudaMalloc(&P->acc, (size_t)g.C * T * T * sizeof(double2)) != cudaSuccess)
+    return dense_fail(ADP_ERR_CUDA, "fft mixed_T: allocation");
+  double* Bq = P->buf[3];
+  double* R = P->buf[4];
+  if ((rc = stencil(P, 0, (const double*)q, ProArgs{}, E_STORE, Bq, nullptr, nullptr, 0.0, 0.0, nullptr, st))) return rc;
+  if ((rc = stencil(P, 0, (const double*)x_tilde, ProArgs{}, E_RESID, R, (const double*)lp->y, nullptr, 0.0, 0.0, nullptr,
+                    st)))
+    return rc;
+  const int rgrid = g.npairs * (T / RROWS) * g.C;
+  const double* us[2] = {(const double*)x_tilde, (const double*)q};
+  const double* vs[2] = {Bq, R};
+  for (int k = 0; k < 2; ++k) {
+    RowArgs ru{g, us[k], P->S, P->tw, 0, nullptr, P_NONE, nullptr, nullptr, 0.0, nullptr, nullptr};
+    row_fwd_kernel<<<rgrid, 256, 0, st>>>(ru);
+    RowArgs rv{g, vs[k], P->S2, P->tw, 2, nullptr, P_NONE, nullptr, nullptr, 0.0, nullptr, nullptr};
+    row_fwd_kernel<<<rgrid, 256, 0, st>>>(rv);
+    ColArgs ca{g, P->S, nullptr, nullptr, P->tw, 0, g.npairs};
+    col_corr_kernel<<<g.npairs * (T / CCOLS) * g.C, 64 * CCOLS, 0, st>>>(ca, P->S2);
+    pair_sum_kernel<<<kVecGrid, 256, 0, st>>>(P->S, g.npairs, g.C, k, P->acc);
+  }
+  Geo ag = g;
+  ag.npairs = 1;
+  ColArgs ci{ag, P->acc, nullptr, nullptr, P->tw, 2, 1};
+  col_kernel<<<(T / CCOLS) * g.C, 64 * CCOLS, 0, st>>>(ci);
+  kgc_final_kernel<<<g.C * ((g.kh + RROWS - 1) / RROWS), 256, 0, st>>>(g, P->acc, P->tw, 2.0 * kInvT2, (double*)out);
+  return check_launch("fft mixed_T");
 }

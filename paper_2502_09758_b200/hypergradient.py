@@ -151,9 +151,12 @@ def mixed_second_transpose(x_tilde, b: Kernel, q, p: LowerProblem) -> np.ndarray
     xd = nat.to_dev(x_tilde, p.op.signal_shape)
     qd = nat.to_dev(q, p.op.signal_shape)
     out = nat.empty_like_dev(b.data.shape)
-    plan = plan or p.op.plan()   # fft mode: kernel-gradient correlations on the direct kernels
-    nat.check(nat.lib().adp_mixed_T(plan.handle, ctypes.byref(s), nat.ptr(xd), nat.ptr(qd), nat.ptr(out),
-                                    nat.stream_ptr()), "mixed_second_transpose")
+    if plan is None:   # fft mode: kernel-gradient correlations on tile FFTs
+        fn, handle = nat.lib().adp_fft_mixed_T, p.op.fft_plan().handle
+    else:
+        fn, handle = nat.lib().adp_mixed_T, plan.handle
+    nat.check(fn(handle, ctypes.byref(s), nat.ptr(xd), nat.ptr(qd), nat.ptr(out), nat.stream_ptr()),
+              "mixed_second_transpose")
     return nat.to_host(out).astype(float)
 
 

@@ -189,3 +189,15 @@ def test_fft_upper_terms(adp, orc):
     assert abs(fit - orc.npsum(r * r)) <= 1e-12 * fit
     assert rel(g.cpu().numpy(), go) <= 1e-12
     assert abs(gn - orc.norm(go)) <= 1e-12 * gn
+
+
+@pytest.mark.parametrize("shape,k", [((300, 260, 3), 15), ((600, 520, 1), 31), ((100, 90, 2), 9)])
+def test_fft_mixed_second_transpose(adp, orc, shape, k):
+    """2 [kgc(x~, Bq) + kgc(q, Bx~ - y)] from frequency-domain pair products vs the oracle."""
+    p, po, y, rng = _problem(adp, orc, shape, k, k / 5.0, 12)
+    xt = y + 0.02 * rng.standard_normal(shape)
+    q = rng.standard_normal(shape)
+    z = adp.mixed_second_transpose(xt, p.op.kernel, q, p)
+    zo = orc.mixed_second_transpose(xt, q, po, False, (k, k))
+    assert z.shape == zo.shape
+    assert rel(z, zo) <= 1e-11
