@@ -12,6 +12,7 @@ sys.path.insert(0, ROOT)
 ap = argparse.ArgumentParser()
 ap.add_argument("--size", type=int, default=4096)
 ap.add_argument("--iters", type=int, default=10)
+ap.add_argument("--config", default="c5")
 a = ap.parse_args()
 
 import torch  # noqa: E402
@@ -20,8 +21,8 @@ import paper_2502_09758_b200 as adp  # noqa: E402
 from paper_2502_09758_b200 import _native as nat  # noqa: E402
 from paper_2502_09758_b200 import configs  # noqa: E402
 
-adp.set_precision("float64", "fft")
-up = configs.config5(0, size=a.size)
+adp.set_precision("float64", os.environ.get("ADP_MODE", "fft"))
+up = configs.config5(0, size=a.size) if a.config == "c5" else configs.CONFIGS[a.config](0)
 x0 = nat.to_dev(up.x0)
 out = nat.empty_like_dev(up.x0.shape)
 
