@@ -43,7 +43,10 @@ namespace fft {
 
 constexpr int T = 512;          // transform length (both axes)
 constexpr int RROWS = 4;        // rows per CTA in the row passes (64 threads per row)
-constexpr int CCOLS = 4;        // columns per CTA in the column pass (64 threads per column)
+#ifndef FFT_CCOLS
+#define FFT_CCOLS 4
+#endif
+constexpr int CCOLS = FFT_CCOLS;   // columns per CTA in the column pass (64 threads per column)
 constexpr double kInvT2 = 1.0 / (512.0 * 512.0);   // exact power of two
 
 struct Geo {
