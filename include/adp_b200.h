@@ -98,6 +98,11 @@ typedef struct {
   int32_t norm_max_iters; /* L_of_b: 300 */
   double norm_tol;        /* L_of_b: 1e-4 */
   const void* v0;       /* power-iteration start vector (un-normalised), device */
+  /* injected AGD state (P2 lockstep): x_prev (NULL: x0), momentum t (<= 0: 1),
+   * backtracking Lipschitz estimate lip_t (<= 0: L; proxgrad: 1 / step) at the first iteration */
+  const void* x_prev0;
+  double t_mom0;
+  double lip_t0;
 } adp_solve_args;
 
 typedef struct {
@@ -112,6 +117,7 @@ typedef struct {
   int32_t power_iters;
   int32_t power_converged;
   int64_t vg_evals, value_evals, restarts;
+  double t_mom, lip_t;  /* AGD state at exit (momentum t; lip_t, or 1 / step for proxgrad) */
 } adp_solve_result;
 
 typedef struct {
@@ -154,6 +160,13 @@ int adp_lower_hess_diag(adp_plan* p, const adp_lower* lp, const void* x, void* o
 /* solve_lower -> _gradient_descent / _accelerated, one persistent launch  (:104-213) */
 int adp_lower_solve(adp_plan* p, const adp_lower* lp, const void* x0, void* x_out, const adp_solve_args* args,
                     adp_solve_result* res, void* stream);
+
+/* one lower-level iteration from an injected state (x, x_prev, t_mom, lip_t): adp_lower_solve with
+ * max_iters = 1 (P2 lockstep protocol).  x_out = the next x (or y when the
+ * convergence test fires); res: decisions (value_evals - 1 = backtracking retries, restarts,
+ * converged) and the next t_mom / lip_t.  args->max_iters is ignored. */
+int adp_lower_iter(adp_plan* p, const adp_lower* lp, const void* x, const void* x_prev, double t_mom, double lip_t,
+                   const adp_solve_args* args, void* x_out, adp_solve_result* res, void* stream);
 
 /* ---- hypergradient (hypergradient.py) ---- */
 /* cg_solve specialised to the lower Hessian at x_tilde with Jacobi preconditioner

@@ -34,6 +34,7 @@ from .lower_solvers import (
     lower_grad,
     lower_hess_diag,
     lower_hess_vec,
+    lower_iteration,
     lower_value,
     lower_value_and_grad,
     mu_of_b,
@@ -79,7 +80,7 @@ __all__ = [
     "UpperProblem", "WarmState", "build_deconv1d", "build_motion2d", "build_semiblind2d", "cg_solve",
     "gaussian_conv_matrix", "get_precision", "image_forward_diff", "image_forward_diff_adjoint",
     "inexact_hypergradient", "kernel_gram_correlation", "lip_upper_x", "lower_grad", "lower_hess_diag",
-    "lower_hess_vec", "lower_value", "lower_value_and_grad", "maid_run", "mixed_second_transpose", "mu_of_b",
+    "lower_hess_vec", "lower_iteration", "lower_value", "lower_value_and_grad", "maid_run", "mixed_second_transpose", "mu_of_b",
     "op_norm_sq", "operator_from_kernel", "piecewise_signal", "precision", "prox_grad_iterations", "prox_l1", "psi", "psi_value", "run_ift", "run_unrolled",
     "set_precision", "smoothed_abs_norm", "sobolev_grad", "sobolev_value", "solve_lower", "solve_lower_at",
     "tv_value", "unrolled_gradient", "upper_fit_grad",

@@ -45,7 +45,8 @@ class SolveArgs(ctypes.Structure):
     _fields_ = [("eps", ctypes.c_double), ("mu", ctypes.c_double), ("max_iters", ctypes.c_int32),
                 ("method", ctypes.c_int32), ("adaptive", ctypes.c_int32), ("step_size", ctypes.c_double),
                 ("norm_sq", ctypes.c_double), ("norm_max_iters", ctypes.c_int32),
-                ("norm_tol", ctypes.c_double), ("v0", ctypes.c_void_p)]
+                ("norm_tol", ctypes.c_double), ("v0", ctypes.c_void_p), ("x_prev0", ctypes.c_void_p),
+                ("t_mom0", ctypes.c_double), ("lip_t0", ctypes.c_double)]
 
 
 class SolveResult(ctypes.Structure):
@@ -53,7 +54,8 @@ class SolveResult(ctypes.Structure):
                 ("value", ctypes.c_double), ("iters", ctypes.c_int32), ("converged", ctypes.c_int32),
                 ("status", ctypes.c_int32), ("fail_iter", ctypes.c_int32), ("power_iters", ctypes.c_int32),
                 ("power_converged", ctypes.c_int32), ("vg_evals", ctypes.c_int64),
-                ("value_evals", ctypes.c_int64), ("restarts", ctypes.c_int64)]
+                ("value_evals", ctypes.c_int64), ("restarts", ctypes.c_int64), ("t_mom", ctypes.c_double),
+                ("lip_t", ctypes.c_double)]
 
 
 class CGResultC(ctypes.Structure):
@@ -84,6 +86,8 @@ SIGNATURES = {
     "adp_lower_hess_diag": (_I, [_P, ctypes.POINTER(Lower), _P, _P, _P]),
     "adp_lower_solve": (_I, [_P, ctypes.POINTER(Lower), _P, _P, ctypes.POINTER(SolveArgs),
                              ctypes.POINTER(SolveResult), _P]),
+    "adp_lower_iter": (_I, [_P, ctypes.POINTER(Lower), _P, _P, _D, _D, ctypes.POINTER(SolveArgs), _P,
+                            ctypes.POINTER(SolveResult), _P]),
     "adp_hess_cg": (_I, [_P, ctypes.POINTER(Lower), _P, _P, _P, _I, _P, _D, _I,
                          ctypes.POINTER(CGResultC), _P]),
     "adp_mixed_T": (_I, [_P, ctypes.POINTER(Lower), _P, _P, _P, _P]),

@@ -816,7 +816,11 @@ int adp_lower_solve(adp_plan* p, const adp_lower* lp, const void* x0, void* x_ou
   if (!(sa->mu > 0)) return fail(ADP_ERR_ARG, "mu must be > 0");
   if (sa->method < 0 || sa->method > 2) return fail(ADP_ERR_ARG, "unknown lower solver method");
   PlanImpl& P = p->impl;
-  if (IS_DENSE(p)) return dense_solve(P, lp, x0, x_out, sa, res, STREAM(stream));
+  const bool injected = sa->x_prev0 || sa->t_mom0 > 0 || sa->lip_t0 > 0;
+  if (IS_DENSE(p)) {
+    if (injected) return fail(ADP_ERR_UNSUPPORTED, "injected AGD state: depthwise 2-D plans only");
+    return dense_solve(P, lp, x0, x_out, sa, res, STREAM(stream));
+  }
   auto run = [&](auto tag) -> int {
     using T = decltype(tag);
     ConvArgs<T> a = conv_base<T>(P);
@@ -832,6 +836,9 @@ int adp_lower_solve(adp_plan* p, const adp_lower* lp, const void* x0, void* x_ou
     a.power_tol = sa->norm_tol;
     a.v0 = (const T*)sa->v0;
     a.x0 = (const T*)x0;
+    a.xprev0 = (const T*)sa->x_prev0;
+    a.t_mom0 = sa->t_mom0;
+    a.lip_t0 = sa->lip_t0;
     a.out = (T*)x_out;
     a.trace = P.d_trace;
     if (int e = launch_coop(P, P.k_solve, a, STREAM(stream))) return e;
@@ -851,9 +858,22 @@ int adp_lower_solve(adp_plan* p, const adp_lower* lp, const void* x0, void* x_ou
     res->vg_evals = o.vg_evals;
     res->value_evals = o.value_evals;
     res->restarts = o.restarts;
+    res->t_mom = o.t_mom;
+    res->lip_t = o.lip_t;
     return ADP_OK;
   };
   return P.d.dtype == ADP_DTYPE_F32 ? run(float()) : run(double());
+}
+
+int adp_lower_iter(adp_plan* p, const adp_lower* lp, const void* x, const void* x_prev, double t_mom, double lip_t,
+                   const adp_solve_args* args, void* x_out, adp_solve_result* res, void* stream) {
+  if (!args || !x_prev) return fail(ADP_ERR_ARG, "null argument");
+  adp_solve_args a = *args;
+  a.max_iters = 1;
+  a.x_prev0 = x_prev;
+  a.t_mom0 = t_mom;
+  a.lip_t0 = lip_t;
+  return adp_lower_solve(p, lp, x, x_out, &a, res, stream);
 }
 
 int adp_hess_cg(adp_plan* p, const adp_lower* lp, const void* x_tilde, const void* rhs, void* q, int32_t warm,

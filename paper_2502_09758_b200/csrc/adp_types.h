@@ -102,7 +102,7 @@ struct SolveOut {
   int64_t vg_evals;        // value+grad passes
   int64_t value_evals;     // value-only passes (backtracking)
   int64_t restarts;
-  int pad_[2];
+  double t_mom, lip_t;     // state at exit
 };
 
 struct CGOut {

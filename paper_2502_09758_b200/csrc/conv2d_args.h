@@ -42,6 +42,8 @@ struct ConvArgs {
   double power_tol;
   const T* v0;             // power-iteration start (un-normalised)
   const T* x0;             // warm start
+  const T* xprev0;         // injected x_prev (NULL: x0)
+  double t_mom0, lip_t0;   // injected momentum / Lipschitz estimate (<= 0: defaults)
   T* out;                  // x_tilde
   // workspace
   T* X[3];

@@ -141,18 +141,21 @@ __global__ void __launch_bounds__(512, 1) conv_solve_kernel(const __grid_constan
     step = 1.0 / lip;
   }
 
-  // ---- x = x_prev = x0
-  E.foreach_pixel([&](int64_t i, int, int, int) { a.X[0][i] = a.x0[i]; });
+  // ---- x = x_prev = x0 (or an injected x_prev, t_mom, lip_t: P2 lockstep)
+  E.foreach_pixel([&](int64_t i, int, int, int) {
+    a.X[0][i] = a.x0[i];
+    if (a.xprev0) a.X[1][i] = a.xprev0[i];
+  });
   E.gb.sync();
 
-  int ix = 0, ixp = 0, ic = 1;
-  double t_mom = 1.0, lip_t = lip;
+  int ix = 0, ixp = a.xprev0 ? 1 : 0, ic = a.xprev0 ? 2 : 1;
+  double t_mom = a.t_mom0 > 0.0 ? a.t_mom0 : 1.0, lip_t = a.lip_t0 > 0.0 ? a.lip_t0 : lip;
   double theta = 0.0;
   if (a.method == M_FISTA_SC) {
     const double q = fmin(a.mu / lip, 1.0);
     theta = (1.0 - sqrt(q)) / (1.0 + sqrt(q));
   }
-  double gd_step = step;   // _gradient_descent's `step`
+  double gd_step = (a.method == M_PROXGRAD && a.lip_t0 > 0.0) ? 1.0 / a.lip_t0 : step;   // _gradient_descent's `step`
   int status = ST_OK, fail_iter = -1, iters = a.max_iters, converged = 0;
   double gn = 0.0, h_y = 0.0, beta = 0.0;
   long long vg = 0, vals = 0, restarts = 0;
@@ -310,6 +313,8 @@ __global__ void __launch_bounds__(512, 1) conv_solve_kernel(const __grid_constan
     r->vg_evals = vg;
     r->value_evals = vals;
     r->restarts = restarts;
+    r->t_mom = t_mom;
+    r->lip_t = (a.method == M_PROXGRAD) ? 1.0 / gd_step : lip_t;
   }
 }
 

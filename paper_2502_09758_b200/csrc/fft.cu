@@ -1028,8 +1028,14 @@ extern "C" int adp_fft_lower_solve(adp_fft_plan* P, const adp_lower* lp, const v
   double* XC = P->buf[3];
   double* G = P->buf[4];
   cudaMemcpyAsync(X, x0, nbytes, cudaMemcpyDeviceToDevice, st);
-  cudaMemcpyAsync(XP, x0, nbytes, cudaMemcpyDeviceToDevice, st);
+  cudaMemcpyAsync(XP, a->x_prev0 ? a->x_prev0 : x0, nbytes, cudaMemcpyDeviceToDevice, st);
+  // injected state (P2 lockstep): momentum and backtracking estimate at the first iteration
+  double t_mom = a->t_mom0 > 0 ? a->t_mom0 : 1.0;
+  double lip_t = a->lip_t0 > 0 ? a->lip_t0 : lip;
+  if (a->method == ADP_METHOD_PROXGRAD && a->lip_t0 > 0) step = 1.0 / a->lip_t0;
   auto finish = [&](const double* xr, double gn2, int t, int conv) {
+    res->t_mom = t_mom;
+    res->lip_t = a->method == ADP_METHOD_PROXGRAD ? 1.0 / step : lip_t;
     cudaMemcpyAsync(x_out, xr, nbytes, cudaMemcpyDeviceToDevice, st);
     res->grad_norm = std::sqrt(gn2);
     res->iters = t;
@@ -1098,8 +1104,7 @@ extern "C" int adp_fft_lower_solve(adp_fft_plan* P, const adp_lower* lp, const v
     const double q = std::min(a->mu / lip, 1.0);
     theta = (1.0 - std::sqrt(q)) / (1.0 + std::sqrt(q));
   }
-  double t_mom = 1.0, lip_t = lip;
-  bool xp_is_x = true;   // x_prev == x (start, and after a restart)
+  bool xp_is_x = a->x_prev0 == nullptr;   // x_prev == x (start, and after a restart)
   for (int t = 0; t < a->max_iters; ++t) {
     double beta;
     if (a->method == ADP_METHOD_FISTA_SC) {

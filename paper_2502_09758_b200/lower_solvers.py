@@ -218,3 +218,51 @@ def solve_lower(p: LowerProblem, x0, eps: float, mu: float, max_iters: int = 300
                      lip=float(r.lip), power_iters=int(r.power_iters))
     gn = float(r.grad_norm)
     return LowerSolveResult(nat.like(out, x0), gn, int(r.iters), gn / mu, bool(r.converged))
+
+
+def lower_iteration(p: LowerProblem, x, x_prev, t_mom: float, lip_t: float, eps: float, mu: float,
+                    method: str = "agd", adaptive: bool = False, step_size: float | None = None) -> dict:
+    """ONE iteration of _accelerated (lower_solvers.py:191-211) from an injected
+    state (x, x_prev, t_mom, lip_t) — the P2 lockstep protocol of SURVEY.md
+    Appendix C.  Runs the production solve kernel with max_iters = 1.  Returns
+    the next state and the iteration's decisions: {"x", "x_prev", "t_mom",
+    "lip_t", "bt_tries", "restart", "converged", "grad_norm"} (on convergence
+    "x" is the extrapolated point y the solve would return)."""
+    if method not in ("agd", "fista_sc"):
+        raise ValueError("lower_iteration follows _accelerated (agd / fista_sc)")
+    _check_reg_smooth(p)
+    if step_size is None and p.op._norm_sq is None:
+        op_norm_sq(p.op, 300, 1e-4)          # L(b) outside the iteration, as the solve caches it
+    plan, s, keep = _native_lower(p)
+    xd = nat.to_dev(x, p.op.signal_shape)
+    xpd = nat.to_dev(x_prev, p.op.signal_shape)
+    out = nat.empty_like_dev(p.op.signal_shape)
+    a = nat.SolveArgs()
+    a.eps, a.mu = float(eps), float(mu)
+    a.max_iters = 1
+    a.method = nat.METHODS[method]
+    a.adaptive = 1 if adaptive else 0
+    a.step_size = float(step_size) if step_size is not None else 0.0
+    a.norm_sq = float(p.op._norm_sq) if p.op._norm_sq is not None else -1.0
+    a.norm_max_iters, a.norm_tol = 300, 1e-4
+    a.v0 = nat.power_start(p.op.signal_shape).data_ptr()
+    a.x_prev0 = xpd.data_ptr()
+    a.t_mom0, a.lip_t0 = float(t_mom), float(lip_t)
+    r = nat.SolveResult()
+    if _fft(p):
+        nat.check(nat.lib().adp_fft_lower_solve(p.op.fft_plan().handle, ctypes.byref(s), nat.ptr(xd), nat.ptr(out),
+                                                ctypes.byref(a), ctypes.byref(r), nat.stream_ptr()), "lower_iteration")
+    else:
+        nat.check(nat.lib().adp_lower_iter(plan.handle, ctypes.byref(s), nat.ptr(xd), nat.ptr(xpd), float(t_mom),
+                                           float(lip_t), ctypes.byref(a), nat.ptr(out), ctypes.byref(r),
+                                           nat.stream_ptr()), "lower_iteration")
+    if r.status == nat.STATUS_DIVERGED:
+        raise SolveDiverged("objective became non-finite at lower iteration 0")
+    if r.status == nat.STATUS_BT_FAIL:
+        raise SolveDiverged("backtracking line search failed to find a decreasing step")
+    converged = bool(r.converged) and r.iters == 0
+    restart = r.restarts > 0
+    xn = nat.like(out, x)
+    return {"x": xn, "x_prev": xn if restart else x, "t_mom": float(r.t_mom), "lip_t": float(r.lip_t),
+            "bt_tries": max(int(r.value_evals) - 1, 0) if adaptive else 0, "restart": restart,
+            "converged": converged, "grad_norm": float(r.grad_norm)}
