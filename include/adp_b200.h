@@ -127,6 +127,7 @@ typedef struct {
   int32_t converged;
   int32_t status;
   int32_t hv;
+  double rs;            /* <r, M^-1 r> at exit (the recurrence's rs) */
 } adp_cg_result;
 
 /* ---- plans ---- */
@@ -174,6 +175,11 @@ int adp_lower_iter(adp_plan* p, const adp_lower* lp, const void* x, const void* 
  * (hypergradient.py:35-84 as called at 171-176) */
 int adp_hess_cg(adp_plan* p, const adp_lower* lp, const void* x_tilde, const void* rhs, void* q, int32_t warm,
                 const void* precond, double tol, int32_t max_iters, adp_cg_result* res, void* stream);
+/* one PCG iteration from an injected state (q, r, p, rs) at iteration k of cg_solve (hypergradient.py:70-81):
+ * hp = H p, curv = <p, hp>, q += a p, r -= a hp, rs' = <r, M^-1 r> (res->rs, res->curv); q and r are updated in
+ * place (P2 lockstep protocol).  M = lower_hess_diag(x~) as in adp_hess_cg. */
+int adp_cg_iter(adp_plan* p, const adp_lower* lp, const void* x_tilde, void* q, void* r, const void* p_dir, double rs,
+                adp_cg_result* res, void* stream);
 /* mixed_second_transpose: out = 2 [kgc(x~, B q) + kgc(q, B x~ - y)]   (hypergradient.py:92-104) */
 int adp_mixed_T(adp_plan* p, const adp_lower* lp, const void* x_tilde, const void* q, void* out, void* stream);
 /* UpperProblem.fit_value (problems.py:48-50) and ||upper_fit_grad|| (hypergradient.py:87-89);

@@ -60,7 +60,8 @@ class SolveResult(ctypes.Structure):
 
 class CGResultC(ctypes.Structure):
     _fields_ = [("residual", ctypes.c_double), ("curv", ctypes.c_double), ("iters", ctypes.c_int32),
-                ("converged", ctypes.c_int32), ("status", ctypes.c_int32), ("hv", ctypes.c_int32)]
+                ("converged", ctypes.c_int32), ("status", ctypes.c_int32), ("hv", ctypes.c_int32),
+                ("rs", ctypes.c_double)]
 
 
 # Exported symbols and their signatures (kept in sync with include/adp_b200.h).
@@ -90,6 +91,7 @@ SIGNATURES = {
                             ctypes.POINTER(SolveResult), _P]),
     "adp_hess_cg": (_I, [_P, ctypes.POINTER(Lower), _P, _P, _P, _I, _P, _D, _I,
                          ctypes.POINTER(CGResultC), _P]),
+    "adp_cg_iter": (_I, [_P, ctypes.POINTER(Lower), _P, _P, _P, _P, _D, ctypes.POINTER(CGResultC), _P]),
     "adp_mixed_T": (_I, [_P, ctypes.POINTER(Lower), _P, _P, _P, _P]),
     "adp_upper_terms": (_I, [_P, _P, _P, _P, ctypes.POINTER(_D), ctypes.POINTER(_D), _P, _P]),
     "adp_dot": (_I, [_P, _P, _P, ctypes.POINTER(_D), _P]),

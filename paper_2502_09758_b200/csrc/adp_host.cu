@@ -876,8 +876,26 @@ int adp_lower_iter(adp_plan* p, const adp_lower* lp, const void* x, const void* 
   return adp_lower_solve(p, lp, x, x_out, &a, res, stream);
 }
 
+static int hess_cg_impl(adp_plan* p, const adp_lower* lp, const void* x_tilde, const void* rhs, void* q, int32_t warm,
+                        const void* precond, double tol, int32_t max_iters, adp_cg_result* res, void* r_io,
+                        const void* p_dir, double rs0, void* stream);
+
 int adp_hess_cg(adp_plan* p, const adp_lower* lp, const void* x_tilde, const void* rhs, void* q, int32_t warm,
                 const void* precond, double tol, int32_t max_iters, adp_cg_result* res, void* stream) {
+  return hess_cg_impl(p, lp, x_tilde, rhs, q, warm, precond, tol, max_iters, res, nullptr, nullptr, 0.0, stream);
+}
+
+int adp_cg_iter(adp_plan* p, const adp_lower* lp, const void* x_tilde, void* q, void* r, const void* p_dir, double rs,
+                adp_cg_result* res, void* stream) {
+  if (!q || !r || !p_dir) return fail(ADP_ERR_ARG, "null argument");
+  if (IS_DENSE(p)) return fail(ADP_ERR_UNSUPPORTED, "cg lockstep: depthwise 2-D plans only");
+  // tol tiny: the step is taken; rhs is only used by the true-residual pass (r stands in for it)
+  return hess_cg_impl(p, lp, x_tilde, r, q, 1, nullptr, 1e-300, 1, res, r, p_dir, rs, stream);
+}
+
+static int hess_cg_impl(adp_plan* p, const adp_lower* lp, const void* x_tilde, const void* rhs, void* q, int32_t warm,
+                        const void* precond, double tol, int32_t max_iters, adp_cg_result* res, void* r_io,
+                        const void* p_dir, double rs0, void* stream) {
   if (int e = check_lower(p, lp)) return e;
   if (!res) return fail(ADP_ERR_ARG, "null argument");
   if (!(tol > 0)) return fail(ADP_ERR_ARG, "tol must be > 0");
@@ -894,6 +912,9 @@ int adp_hess_cg(adp_plan* p, const adp_lower* lp, const void* x_tilde, const voi
     a.diag_in = (const T*)precond;
     a.tol = tol;
     a.max_iters = max_iters;
+    a.cg_r = (T*)r_io;
+    a.cg_p0 = (const T*)p_dir;
+    a.cg_rs0 = rs0;
     if (int e = launch_coop(P, P.k_cg, a, STREAM(stream))) return e;
     CK(cudaMemcpyAsync(P.h_cres, P.d_cres, sizeof(CGOut), cudaMemcpyDeviceToHost, STREAM(stream)));
     CK(cudaStreamSynchronize(STREAM(stream)));
@@ -904,6 +925,7 @@ int adp_hess_cg(adp_plan* p, const adp_lower* lp, const void* x_tilde, const voi
     res->converged = o.converged;
     res->status = o.status;
     res->hv = o.hv;
+    res->rs = o.rs;
     return ADP_OK;
   };
   return P.d.dtype == ADP_DTYPE_F32 ? run(float()) : run(double());

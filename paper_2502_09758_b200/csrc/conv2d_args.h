@@ -57,6 +57,10 @@ struct ConvArgs {
   T* WV; T* WH;            // rho'' weights
   T* P[2]; T* BP; T* HP; T* CR; T* CS;
   int warm;
+  // P2 lockstep of one CG iteration: injected r, p, rs (cg_p0 != NULL); r is written back to cg_r
+  T* cg_r;
+  const T* cg_p0;
+  double cg_rs0;
   // sums
   SumDev s_fit, s_tv, s_fitc, s_tvc;   // numpy-pairwise element sums (N, 2N, N, 2N)
   SumDev s_t0, s_t1, s_t2;             // per-tile partial sums (ddot-type)

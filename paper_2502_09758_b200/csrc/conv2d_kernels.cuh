@@ -499,8 +499,11 @@ __global__ void __launch_bounds__(512, 1) conv_cg_kernel(const __grid_constant__
     E.foreach_pixel([&](int64_t i, int, int, int) { a.DIAG[i] = T(1) / ldcg(a.DIAG + i); });
   }
   E.gb.sync();
-  // r = rhs - H q0 (warm) or rhs; q = q0 or 0
-  if (a.warm) {
+  // r = rhs - H q0 (warm) or rhs; q = q0 or 0; or the injected state (q, r, p) of a lockstep step,
+  // the direction entering as the "first" direction p = s
+  if (a.cg_p0) {
+    E.foreach_pixel([&](int64_t i, int, int, int) { a.CR[i] = a.cg_r[i]; a.CS[i] = a.cg_p0[i]; });
+  } else if (a.warm) {
     E.hess_vec(SrcLin<T>{a.Q}, a.P[1], tv, a.HP, nullptr, nullptr, nullptr);
     ++hv;
     E.gb.sync();
@@ -511,7 +514,7 @@ __global__ void __launch_bounds__(512, 1) conv_cg_kernel(const __grid_constant__
   // s = inv_diag * r ; rs = <r, s> ; rr = <r, r>
   E.foreach_pixel_sum([&](int64_t i, int, int, int) {
     const T r = ldcg(a.CR + i), s = ldcg(a.DIAG + i) * r;
-    a.CS[i] = s;
+    if (!a.cg_p0) a.CS[i] = s;
     return (double)r * (double)s;
   }, a.s_t1);
   E.foreach_pixel_sum([&](int64_t i, int, int, int) {
@@ -523,7 +526,7 @@ __global__ void __launch_bounds__(512, 1) conv_cg_kernel(const __grid_constant__
   {
     double o[2];
     E.reduce({&a.s_t1, &a.s_t2}, o);
-    rs = o[0];
+    rs = a.cg_p0 ? a.cg_rs0 : o[0];
     rr = o[1];
   }
   int iters = 0;
@@ -563,6 +566,10 @@ __global__ void __launch_bounds__(512, 1) conv_cg_kernel(const __grid_constant__
     rr = o[1];
   }
   if (iters > a.max_iters) iters = a.max_iters;
+  if (a.cg_p0) {
+    E.gb.sync();
+    E.foreach_pixel([&](int64_t i, int, int, int) { a.cg_r[i] = ldcg(a.CR + i); });
+  }
   double res = 0.0;
   int conv = 0;
   if (status == ST_OK) {

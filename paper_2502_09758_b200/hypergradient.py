@@ -263,3 +263,22 @@ def inexact_hypergradient(upper, b: Kernel, eps: float, delta: float, state: War
         cg_converged=cg.converged,
         mu=mu,
     )
+
+
+def cg_iteration(p: LowerProblem, x_tilde, q, r, p_dir, rs: float) -> dict:
+    """ONE Jacobi-PCG iteration of cg_solve on lower_hess_vec
+    (hypergradient.py:70-81) from an injected state (q, r, p, rs) — the P2
+    lockstep protocol of SURVEY.md Appendix C — in the production CG kernel.
+    Returns {"q", "r", "rs", "curv"} (q += a p, r -= a H p, rs = <r, M^-1 r>)."""
+    plan, s, keep = _native_lower(p)
+    plan = plan or p.op.plan()
+    xd = nat.to_dev(x_tilde, p.op.signal_shape)
+    qd = nat.to_dev(q, p.op.signal_shape).clone()
+    rd = nat.to_dev(r, p.op.signal_shape).clone()
+    pd = nat.to_dev(p_dir, p.op.signal_shape)
+    res = nat.CGResultC()
+    nat.check(nat.lib().adp_cg_iter(plan.handle, ctypes.byref(s), nat.ptr(xd), nat.ptr(qd), nat.ptr(rd), nat.ptr(pd),
+                                    float(rs), ctypes.byref(res), nat.stream_ptr()), "cg_iteration")
+    if res.status == nat.STATUS_NEGCURV:
+        raise _negcurv(float(res.curv))
+    return {"q": nat.like(qd, q), "r": nat.like(rd, r), "rs": float(res.rs), "curv": float(res.curv)}

@@ -60,3 +60,31 @@ def test_lower_iteration_lockstep(adp, orc, mode, shape, k, tol):
             restarts += rec.restart[it]
             checked += 1
     assert checked == 20 and retries > 0
+
+
+@pytest.mark.parametrize("mode,tol", [("strict", 1e-11), ("fast", 1e-11)])
+def test_cg_iteration_lockstep(adp, orc, mode, tol):
+    """One Jacobi-PCG iteration of the production CG kernel from the oracle's
+    state (q, r, p, rs) at iteration k reproduces the oracle's (q, r, rs) at
+    k + 1 and its curvature <p, Hp>; the Jacobi diagonal (np.power in rho'')
+    and the ddot order are tolerance sites (App. B), so the bar is 1e-11."""
+    from paper_2502_09758_b200.hypergradient import cg_iteration
+    shape, k = (80, 72, 2), 9
+    kern, y, rec, lam = _record(orc, shape, k, 5, 5)
+    rng = np.random.default_rng(3)
+    xt = y + 0.02 * rng.standard_normal(shape)
+    rhs = rng.standard_normal(shape)
+    po = orc.Lower(orc.Conv(kern, shape), y, 0.6, orc.TV(1e-4))
+    states = []
+    orc.cg_solve(lambda v: orc.lower_hess_vec(po, xt, v), rhs, 1e-30, 30,
+                 precond_diag=orc.lower_hess_diag(po, xt), record=states)
+    with adp.precision("float64", mode):
+        p = adp.LowerProblem(adp.ConvOperator(adp.Kernel(kern, adp.DEPTHWISE2D), shape), y, 0.6,
+                             adp.SmoothedTV(1e-4))
+        for it in (0, 1, 7, 18, 28):
+            q, r, pd, rs, curv = states[it]
+            out = cg_iteration(p, xt, q, r, pd, rs)
+            qn, rn, _, rsn, _ = states[it + 1]
+            assert abs(out["curv"] - curv) <= tol * abs(curv), it
+            assert abs(out["rs"] - rsn) <= tol * abs(rsn), it
+            assert rel(out["q"], qn) <= tol and rel(out["r"], rn) <= tol, it
