@@ -117,6 +117,27 @@ def metric_cases():
     save("metrics.npz", **out)
 
 
+def maid_p3():
+    """P3 lockstep: the reference maid_run on the scripted stand-ins of tests/maid_fakes.py."""
+    sys.path.insert(0, os.path.dirname(HERE))
+    import maid_fakes as F
+    out = {}
+    for seed in (0, 1, 2):
+        w = F.World(O.Kernel, O.DEPTHWISE2D, seed)
+        M.inexact_hypergradient = w.hypergradient
+        M._solve_candidate = w.candidate
+        M.upper_fit_grad = lambda x, A, y, w=w: 2.0 * (np.asarray(x) - F.TARGET)
+        M.lip_upper_x = lambda A, *a, **k: 3.7
+        b, x, tr = M.maid_run(w.upper, F.config(M.MAIDConfig))
+        for f in ("k", "loss", "grad_norm", "eps", "delta", "alpha", "lower_iters_cum", "cg_iters_cum"):
+            out[f"s{seed}_{f}"] = np.asarray(getattr(tr, f))
+        out[f"s{seed}_final"] = tr.final_loss
+        out[f"s{seed}_b"] = b.data
+        out[f"s{seed}_calls"] = w.calls
+        print("seed", seed, "accepted", len(tr), "calls", w.calls, "final", tr.final_loss)
+    save("maid_p3.npz", **out)
+
+
 def solver_cases():
     # 2-D adaptive AGD on a small semi-blind instance (motion2d semantics)
     up = P.build_semiblind2d(size=(40, 48), seed=3)
@@ -249,3 +270,4 @@ if __name__ == "__main__":
     config_cases()
     baseline_cases()
     metric_cases()
+    maid_p3()
