@@ -615,9 +615,8 @@ __global__ void __launch_bounds__(256) curv_kernel(Geo g, const double* __restri
 // Summed-area table of the flipped kernel squared, per channel: sat[(i * (kw + 1) + j) * C + c] =
 // sum_{i' < i, j' < j} kf[i', j', c]^2, kf = kernel[::-1, ::-1] (operators.py:98, 120-122)
 __global__ void sat_kernel(Geo g, const double* __restrict__ kern, double* sat) {
-  const int c = threadIdx.x;
-  if (c >= g.C) return;
   const int W1 = g.kw + 1;
+  for (int c = threadIdx.x; c < g.C; c += blockDim.x) {
   for (int j = 0; j < W1; ++j) sat[j * g.C + c] = 0.0;
   for (int i = 1; i <= g.kh; ++i) {
     double row = 0.0;
@@ -627,6 +626,7 @@ __global__ void sat_kernel(Geo g, const double* __restrict__ kern, double* sat) 
       row = row + k * k;
       sat[(i * W1 + j) * g.C + c] = sat[((i - 1) * W1 + j) * g.C + c] + row;
     }
+  }
   }
 }
 
