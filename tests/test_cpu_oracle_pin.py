@@ -165,3 +165,17 @@ def test_trace_csv_roundtrip(tmp_path):
         mi.read_trace_csv(tmp_path / "missing.csv")
     assert mi.loss_axis_scale([[1.0, 2e3], [5.0]]) == "log"
     assert mi.loss_axis_scale([[1.0, 2.0], [-1.0]]) == "linear"
+
+
+def test_png_io_roundtrip(tmp_path):
+    """save_png / load_png / save_kernel_image (metrics_io.py:163-199): host file utilities."""
+    pytest.importorskip("PIL")
+    from paper_2502_09758_b200 import metrics_io as mi
+    img = np.linspace(-0.2, 1.2, 48).reshape(6, 8)
+    mi.save_png(img, tmp_path / "a.png")
+    back = mi.load_png(tmp_path / "a.png")
+    assert np.array_equal(back, np.round(np.clip(img, 0, 1) * 255) / 255)
+    mi.save_kernel_image(np.arange(9.0).reshape(3, 3, 1), tmp_path / "k.png")
+    assert mi.load_png(tmp_path / "k.png").max() == 1.0
+    with pytest.raises(OSError, match="cannot read image"):
+        mi.load_png(tmp_path / "missing.png")
