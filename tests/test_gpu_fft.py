@@ -201,3 +201,21 @@ def test_fft_mixed_second_transpose(adp, orc, shape, k):
     zo = orc.mixed_second_transpose(xt, q, po, False, (k, k))
     assert z.shape == zo.shape
     assert rel(z, zo) <= 1e-11
+
+
+def test_fft_maid_run_end_to_end(adp):
+    """MAID in fft mode (every image-space call on tile-FFT stencils: lower
+    solves, CG, mixed derivative, upper terms) on a c2-type instance with the
+    BASELINE MAID settings: two accepted steps that decrease the upper loss,
+    final loss close to the strict run's."""
+    from dataclasses import replace
+
+    from paper_2502_09758_b200 import configs
+    cfg = replace(configs.maid_config("c2"), max_upper_iters=2)
+    up = configs.config2(0, size=128)
+    b, x, tr = adp.maid_run(up, cfg)
+    assert len(tr) == 2 and np.isfinite(tr.loss).all() and np.isfinite(x).all()
+    assert tr.final_loss < tr.loss[0]
+    with adp.precision("float64", "strict"):
+        b2, x2, tr2 = adp.maid_run(configs.config2(0, size=128), cfg)
+    assert abs(tr.final_loss - tr2.final_loss) <= 1e-3 * tr2.final_loss
