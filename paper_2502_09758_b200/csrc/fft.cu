@@ -514,6 +514,7 @@ __global__ void __launch_bounds__(256, 3) row_inv_kernel(const __grid_constant__
           break;
         }
         case E_VALUE: {  // sum (Bx - y)^2 and tv_value = sum(sqrt(d^2 + nu^2) - nu) (regularizers.py:70-72)
+          if (A.out) A.out[o] = val;   // keep B x (the solver's linear extrapolation of B y)
           const double rs = val - A.y[o];
           acc0 = acc0 + rs * rs;
           const TvTerms tv = tv_at(g, A.xp, h, w, c, A.nu, false);
@@ -568,6 +569,27 @@ __global__ void __launch_bounds__(256) vec_kernel(int op, int64_t n, double a, c
     const double s = block_sum(acc, red);
     if (threadIdx.x == 0) part[2 * blockIdx.x] = s;
   }
+}
+
+// Residual by linearity (the adaptive accelerated FFT solve): y = x + beta (x - xp) and
+// B y = Bx + beta (Bx - Bxp) from the kept B x / B x_prev, r = B y - data; partial sum r^2.
+// (B y is a linear combination of two fresh transforms: no error accumulates over iterations.)
+__global__ void __launch_bounds__(256) resid_lin_kernel(int64_t n, double beta, const double* __restrict__ x,
+                                                        const double* __restrict__ xp, const double* __restrict__ bx,
+                                                        const double* __restrict__ bxp,
+                                                        const double* __restrict__ data, double* y, double* r,
+                                                        double* part) {
+  __shared__ double red[40];
+  double acc = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double xv = x[i], bv = bx[i];
+    y[i] = xv + beta * (xv - xp[i]);
+    const double rv = (bv + beta * (bv - bxp[i])) - data[i];
+    r[i] = rv;
+    acc = acc + rv * rv;
+  }
+  const double s = block_sum(acc, red);
+  if (threadIdx.x == 0) part[2 * blockIdx.x] = s;
 }
 
 // Fixed-order folds of up to three partial buffers in one launch: source i
@@ -713,6 +735,7 @@ struct adp_fft_plan {
   double* hred = nullptr;      // pinned host copy
   double* buf[6] = {};         // solver images
   double* cgbuf[7] = {};       // CG images (allocated at first use): r, p0, p1, hp, minv, w0, w1
+  double* lin[3] = {};         // adaptive accelerated solve: B x, B x_prev, B x_candidate (first use)
   double* sat = nullptr;       // summed-area table of the flipped kernel squared
   double2* S2 = nullptr;       // kgc: second complex scratch (first use)
   double2* acc = nullptr;      // kgc: (C, T, T) frequency-domain accumulator
@@ -813,12 +836,30 @@ int vg(adp_fft_plan* P, const adp_lower* lp, const double* x, const ProArgs& pa,
   return ADP_OK;
 }
 
+// value and gradient at y = x + beta (x - xp) with B y from the kept B x, B xp (resid_lin_kernel):
+// one elementwise pass + the adjoint stencil instead of two stencils
+int vg_lin(adp_fft_plan* P, const adp_lower* lp, double beta, const double* x, const double* xp, const double* bx,
+           const double* bxp, double* y, double* g, double* value, double* gn2, cudaStream_t st) {
+  double* R = P->buf[5];
+  resid_lin_kernel<<<kVecGrid, 256, 0, st>>>(P->N, beta, x, xp, bx, bxp, (const double*)lp->y, y, R, P->partV);
+  int rc = check_launch("fft resid_lin");
+  if (rc) return rc;
+  rc = stencil(P, 1, R, ProArgs{}, E_GRAD, g, nullptr, y, lp->alpha, lp->nu, P->partG, st);
+  if (rc) return rc;
+  double t[4];
+  if ((rc = fold(P, FoldSrc{P->partV, kVecGrid, 2}, src3(P, P->partG), kNoSrc, t, st))) return rc;
+  const double tv = t[3] - lp->nu * (double)(2 * P->N);
+  if (value) *value = t[0] + lp->alpha * tv;
+  if (gn2) *gn2 = t[2];
+  return ADP_OK;
+}
+
 // lower_value (lower_solvers.py:37-39) at the stencil input produced by `pa`:
 // sum (Bz - y)^2 + alpha tv_value(z); with P_STEP also the restart dot sum g (xc - xold)
 int value(adp_fft_plan* P, const adp_lower* lp, const double* x, const ProArgs& pa, double* val, double* dot,
-          cudaStream_t st) {
+          cudaStream_t st, double* bx_out = nullptr) {
   const double* z = pa.pro == P_NONE ? x : pa.wout;
-  int rc = stencil(P, 0, x, pa, E_VALUE, nullptr, (const double*)lp->y, z, 0.0, lp->nu, P->partG, st);
+  int rc = stencil(P, 0, x, pa, E_VALUE, bx_out, (const double*)lp->y, z, 0.0, lp->nu, P->partG, st);
   if (rc) return rc;
   double t[3];
   const bool step = pa.pro == P_STEP;
@@ -934,6 +975,7 @@ extern "C" void adp_fft_plan_destroy(adp_fft_plan* P) {
   if (P->hred) cudaFreeHost(P->hred);
   for (double* b : P->buf) cudaFree(b);
   for (double* b : P->cgbuf) cudaFree(b);
+  for (double* b : P->lin) cudaFree(b);
   cudaFree(P->sat);
   cudaFree(P->S2);
   cudaFree(P->acc);
@@ -1052,6 +1094,7 @@ extern "C" int adp_fft_lower_solve(adp_fft_plan* P, const adp_lower* lp, const v
   // backtracked step from y (lower_solvers.py:170-177): XC = y - g / L_try is the value pass's
   // row prologue, which also sums the restart dot g . (XC - X) (X = the current iterate)
   double last_dot = 0.0;
+  double* bx_keep = nullptr;   // set: each candidate's B x_c is stored there (the linear B y path)
   auto backtrack = [&](const double* yv, double h_y, double gn, double lip_try, double* step_out, int* ok) -> int {
     for (int k = 0; k < 60; ++k) {
       ProArgs pa;
@@ -1061,7 +1104,7 @@ extern "C" int adp_fft_lower_solve(adp_fft_plan* P, const adp_lower* lp, const v
       pa.coef = 1.0 / lip_try;
       pa.wout = XC;
       double hv = 0.0;
-      int r = value(P, lp, yv, pa, &hv, &last_dot, st);
+      int r = value(P, lp, yv, pa, &hv, &last_dot, st, bx_keep);
       if (r) return r;
       res->value_evals++;
       if (hv <= h_y - 0.5 * gn * gn / lip_try + 1e-15 * std::fabs(h_y)) {
@@ -1105,6 +1148,22 @@ extern "C" int adp_fft_lower_solve(adp_fft_plan* P, const adp_lower* lp, const v
     theta = (1.0 - std::sqrt(q)) / (1.0 + std::sqrt(q));
   }
   bool xp_is_x = a->x_prev0 == nullptr;   // x_prev == x (start, and after a restart)
+  // Adaptive: every accepted x is a backtracking candidate whose B x_c the value pass already
+  // computed, so B y = B x + beta (B x - B x_prev) needs no forward stencil (vg_lin).
+  const bool lin = a->adaptive != 0;
+  double *BX = nullptr, *BXP = nullptr, *BXC = nullptr;
+  if (lin) {
+    for (double*& b : P->lin)
+      if (!b && cudaMalloc(&b, (size_t)P->N * sizeof(double)) != cudaSuccess)
+        return dense_fail(ADP_ERR_CUDA, "fft solve: device allocation failed");
+    BX = P->lin[0];
+    BXP = P->lin[1];
+    BXC = P->lin[2];
+    if ((rc = stencil(P, 0, X, ProArgs{}, E_STORE, BX, nullptr, nullptr, 0.0, 0.0, nullptr, st))) return rc;
+    if (!xp_is_x && (rc = stencil(P, 0, XP, ProArgs{}, E_STORE, BXP, nullptr, nullptr, 0.0, 0.0, nullptr, st)))
+      return rc;
+    bx_keep = BXC;
+  }
   for (int t = 0; t < a->max_iters; ++t) {
     double beta;
     if (a->method == ADP_METHOD_FISTA_SC) {
@@ -1121,7 +1180,9 @@ extern "C" int adp_fft_lower_solve(adp_fft_plan* P, const adp_lower* lp, const v
     pe.coef = beta;
     pe.wout = Y;
     double h_y = 0.0, gn2 = 0.0;
-    if ((rc = vg(P, lp, X, pe, G, &h_y, &gn2, st))) return rc;
+    if (lin) rc = vg_lin(P, lp, beta, X, xp_is_x ? X : XP, BX, xp_is_x ? BX : BXP, Y, G, &h_y, &gn2, st);
+    else rc = vg(P, lp, X, pe, G, &h_y, &gn2, st);
+    if (rc) return rc;
     res->vg_evals++;
     const double gn = std::sqrt(gn2);
     if (!std::isfinite(gn)) return diverged(t);
@@ -1139,9 +1200,14 @@ extern "C" int adp_fft_lower_solve(adp_fft_plan* P, const adp_lower* lp, const v
       if ((rc = vec(P, V_STEPDIV, lip_t, Y, nullptr, G, XC, nullptr, st))) return rc;
       if (a->method == ADP_METHOD_AGD && (rc = vec(P, V_DOTDIFF, 0.0, XC, X, G, nullptr, &d, st))) return rc;
     }
-    // rotate: XP <- X, X <- XC
+    // rotate: XP <- X, X <- XC (and their images under B)
     std::swap(XP, X);
     std::swap(X, XC);
+    if (lin) {
+      std::swap(BXP, BX);
+      std::swap(BX, BXC);
+      bx_keep = BXC;
+    }
     xp_is_x = false;
     if (a->method == ADP_METHOD_AGD && d > 0) {   // gradient restart: vdot(g, x - x_prev) > 0
       t_mom = 1.0;
@@ -1150,7 +1216,9 @@ extern "C" int adp_fft_lower_solve(adp_fft_plan* P, const adp_lower* lp, const v
     }
   }
   double gn2 = 0.0;
-  if ((rc = vg(P, lp, X, ProArgs{}, G, nullptr, &gn2, st))) return rc;
+  if (lin) rc = vg_lin(P, lp, 0.0, X, X, BX, BX, Y, G, nullptr, &gn2, st);
+  else rc = vg(P, lp, X, ProArgs{}, G, nullptr, &gn2, st);
+  if (rc) return rc;
   return finish(X, gn2, a->max_iters, std::sqrt(gn2) <= tol);
 }
 
