@@ -88,3 +88,25 @@ def test_cg_iteration_lockstep(adp, orc, mode, tol):
             assert abs(out["curv"] - curv) <= tol * abs(curv), it
             assert abs(out["rs"] - rsn) <= tol * abs(rsn), it
             assert rel(out["q"], qn) <= tol and rel(out["r"], rn) <= tol, it
+
+
+@pytest.mark.parametrize("name,iters,check", [("c2", 30, (0, 7, 19, 28)), ("c3", 5, (1, 3))])
+def test_lower_iteration_lockstep_at_config_shapes(adp, orc, name, iters, check):
+    """P2 at the BASELINE config shapes (c2 256x256x1 K = 9, c3 512x512x3 K = 15)
+    on the config's own data and initial kernel: strict mode bitwise."""
+    from paper_2502_09758_b200 import configs
+    up = configs.CONFIGS[name](0)
+    y = np.asarray(up.y_delta, dtype=float)
+    kern = up.b0.data
+    po = orc.Lower(orc.Conv(kern, y.shape), y, up.alpha, orc.TV(up.reg.nu))
+    rec = types.SimpleNamespace(gn=[], h_y=[], bt_tries=[], restart=[], states=[])
+    orc.solve_lower(po, y, 1e-14, 10.0, max_iters=iters + 1, method="agd", adaptive=True, record=rec)
+    p = up.lower_problem(up.b0)
+    p.op._norm_sq = po.op.norm_sq
+    for it in check:
+        x, xp, t_mom, lip_t = rec.states[it]
+        out = adp.lower_iteration(p, x, xp, t_mom, lip_t, 1e-14, 10.0, adaptive=True)
+        xn, _, tn, ln = rec.states[it + 1]
+        assert out["bt_tries"] == rec.bt_tries[it] and out["restart"] == rec.restart[it], it
+        assert out["t_mom"] == tn and out["lip_t"] == ln, it
+        assert np.array_equal(out["x"], xn), it
