@@ -225,3 +225,16 @@ def test_fft_maid_run_end_to_end(adp):
     with adp.precision("float64", "strict"):
         b2, x2, tr2 = adp.maid_run(configs.config2(0, size=128), cfg)
     assert abs(tr.final_loss - tr2.final_loss) <= 1e-3 * tr2.final_loss
+
+
+@pytest.mark.parametrize("shape,ks", [((5, 7, 1), (9, 9)), ((1, 40, 2), (3, 5)), ((33, 1, 4), (7, 1)),
+                                      ((483, 482, 1), (31, 31)), ((964, 20, 2), (31, 31)), ((2, 2, 3), (1, 1))])
+def test_fft_edge_geometries(adp, orc, shape, ks):
+    """Images smaller than the kernel, single rows/columns, 1x1 kernels, tile
+    counts at the valid-region boundary (482 = 512 - 31 + 1) and odd tile counts."""
+    rng = np.random.default_rng(sum(shape) + ks[0])
+    kern = rng.uniform(-0.5, 1.0, ks + (shape[2],))
+    x = rng.standard_normal(shape)
+    op = adp.ConvOperator(adp.Kernel(kern, adp.DEPTHWISE2D), shape)
+    assert rel(op.apply(x), orc.correlate(x, kern)) <= 1e-13
+    assert rel(op.adjoint(x), orc.correlate(x, kern, flip=True)) <= 1e-13
