@@ -43,7 +43,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
-    ap.add_argument("--mode", default="strict", choices=["strict", "fast", "fp32"])
+    ap.add_argument("--mode", default="strict", choices=["strict", "fast", "fp32", "fft"],
+                    help="fft: tile-FFT stencils (SURVEY.md §8 f2); single GPU for --workload c5")
     ap.add_argument("--iters", type=int, default=1200)
     ap.add_argument("--size", type=int, default=256)
     ap.add_argument("--maid-steps", type=int, default=2, help="accepted MAID steps for upper iters/s (0: skip)")
@@ -531,10 +532,22 @@ def run_c5(args):
     up = configs.config5(0, size=args.c5_size)
     N = up.y_delta.size
     x0 = np.ascontiguousarray(up.x0)
+    if mode == "fft" and ws > 1:
+        raise SystemExit("--mode fft runs the c5 workload on one GPU (the row-slab path uses the direct stencils)")
     comm = multigpu.DistComm() if ws > 1 else multigpu.LocalComm()
-    sv = multigpu.SlabSolver(up.lower_problem(up.b0), ws, ranks=[rank] if ws > 1 else None, comm=comm)
+    sv = None
+    if mode != "fft":
+        sv = multigpu.SlabSolver(up.lower_problem(up.b0), ws, ranks=[rank] if ws > 1 else None, comm=comm)
+    from paper_2502_09758_b200 import _native as nat
+    x0d, xo = nat.to_dev(x0), nat.empty_like_dev(x0.shape)
+    fft_stats = {}
 
     def step():
+        if sv is None:   # one GPU, tile-FFT stencils: the solve_lower drop-in in fft mode
+            fft_stats.clear()
+            r = adp.solve_lower(up.lower_problem(up.b0), x0d, 1e-14, 10.0, max_iters=args.c5_iters,
+                                adaptive=True, x_out=xo, stats=fft_stats)
+            return None, r.grad_norm, r.iters, r.converged
         sv.p = up.lower_problem(up.b0)      # fresh operator: power iteration included
         return sv.solve(x0, 1e-14, 10.0, max_iters=args.c5_iters)
 
@@ -548,6 +561,11 @@ def run_c5(args):
             (xs, gn, it, conv), dt = _timed(step)
             times.append(dt)
             units += N * it
+            if sv is None:   # fft: 3 row/column/inverse passes per stencil + folds and vector passes
+                n_st = 2 * fft_stats.get("power_iters", 0) + fft_stats.get("vg_evals", 0) + \
+                    fft_stats.get("value_evals", 0) + 1
+                launches += 3 * n_st + 2 * fft_stats.get("vg_evals", 0) + fft_stats.get("value_evals", 0) + 2
+                continue
             st = sv.stats
             n_steps = 1 + st["power_iters"] + st["value_evals"] + (0 if conv or it < args.c5_iters else 1)
             launches += 2 * n_steps          # one slab step + one unit fold per reduction point
@@ -563,7 +581,8 @@ def run_c5(args):
             "config": {"workload": f"c5: {args.c5_size}x{args.c5_size}x3 image, 31x31 stencil, smoothed TV, "
                                    f"adaptive AGD, {args.c5_iters} lower iterations per solve (+ power iteration)",
                        "mode": mode, "l2": "inputs larger than L2",
-                       "parallelism": f"row slabs x{ws} (ghost {sv.slabs[0].ghost_bot if ws > 1 else 0} rows)"},
+                       "parallelism": ("tile-FFT stencils, one GPU" if sv is None else
+                                       f"row slabs x{ws} (ghost {sv.slabs[0].ghost_bot if ws > 1 else 0} rows)")},
             "gpu_launches": launches, "clocks": clk.summary()}
     if rank == 0:
         print(json.dumps(line), flush=True)
