@@ -12,20 +12,29 @@
 // correlation acts on both parts independently.
 //
 // Passes (one stencil = three launches, all in HBM-resident complex scratch):
-//   K1 row pass     : load the two tiles' rows (zero padded), FFT-512 per row
+//   K1 row pass     : load the two tiles' rows (zero padded), FFT-512 per row;
+//                     a load prologue can produce the input on the fly (the
+//                     AGD extrapolation, the backtracking candidate with the
+//                     restart dot, the power iteration's w / lam, the CG
+//                     direction) and store it for the later passes
 //   K2 column pass  : FFT-512 per column, multiply by conj(FFT2(kernel)),
-//                     inverse FFT-512 per column (one shared-memory round trip)
+//                     inverse FFT-512 per column (registers + two padded
+//                     shared-memory exchanges per transform)
 //   K3 inverse rows : inverse FFT-512 per row, crop the valid outputs, fused
 //                     epilogue (residual, gradient with the TV term, value
-//                     terms, power-iteration norm) with per-CTA partial sums
-// The FFT is a radix-8 Stockham autosort transform in shared memory
-// (3 stages for 512 points) with an accurately rounded twiddle table.
+//                     terms, power-iteration norm, Hessian products, upper
+//                     terms) with per-CTA partial sums
+// The FFT is a register-resident radix-8 Stockham transform (3 stages for 512
+// points; each of 64 threads owns elements j + 64 r) with an accurately
+// rounded twiddle table.  Also here: the host-driven solvers on these passes
+// (solve_lower, the hypergradient's PCG, op_norm_sq), the kernel-gradient
+// correlation by frequency-domain pair products, the upper terms.
 //
-// Arithmetic: float64 with FMA contraction off (library-wide --fmad=false);
-// results differ from the direct strict stencil by FFT rounding (~1e-15
-// relative to the output scale): a tolerance-only mode, like "fast".
-// Reductions are fixed-order (per-CTA trees, then a fixed fold), so every run
-// is bitwise reproducible.
+// Arithmetic: float64; complex multiplies use FMA and the TV terms use rsqrt
+// (a tolerance-only mode, like "fast": results differ from the direct strict
+// stencil by FFT rounding, ~1e-15 of the output scale).  Reductions are
+// fixed-order (per-CTA trees, then a fixed fold), so every run is bitwise
+// reproducible.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
