@@ -501,7 +501,8 @@ static int conv_plan_init(PlanImpl& P) {
   ConvKernelSet ks = conv_kernels(P.d.dtype, P.d.mode, P.g.rwb);
   {
     const char* ev = getenv("ADP_K9");
-    if (g.C == 1 && g.kh == 9 && g.kw == 9 && g.rwb == 2 && P.d.dtype == ADP_DTYPE_F64 && !(ev && atoi(ev) == 0))
+    if (g.C == 1 && g.kh == 9 && g.kw == 9 && g.rwb == 2 && g.threads <= kSolveKSThreads &&
+        P.d.dtype == ADP_DTYPE_F64 && !(ev && atoi(ev) == 0))
       ks.solve = conv_solve_k9(P.d.mode == ADP_MODE_FAST);
   }
   const int maxg = g.nTiles;

@@ -102,6 +102,9 @@ ConvKernelSet conv_kernels_f64s_rw1();
 ConvKernelSet conv_kernels_f64f_rw1();
 // solve kernels specialised to a 9x9 stencil at RW = 2 (c2), float64
 const void* conv_solve_k9(int fast);
+// thread bound of the compile-time-stencil solve kernel (the host selects it
+// only for CTAs of at most this many threads)
+constexpr int kSolveKSThreads = 256;
 inline ConvKernelSet conv_kernels(int dtype, int mode, int rw) {
   if (dtype == 1) return conv_kernels_f32();
   const bool fast = mode == 1;

@@ -120,8 +120,11 @@ struct ConvOps : Conv<T, FAST, RW, KS> {
 
 // ---------------------------------------------------------------------------
 // solve_lower (lower_solvers.py:104-213) as one persistent kernel.
+// The compile-time-stencil instance (KS > 0: the c2 kernel, <= 256 threads,
+// see kSolveKSThreads) is bounded at 256 threads so it gets the full
+// 255-register file instead of spilling at the 512-thread cap of 128.
 template <typename T, bool FAST, int RW, int KS = 0>
-__global__ void __launch_bounds__(512, 1) conv_solve_kernel(const __grid_constant__ ConvArgs<T> a) {
+__global__ void __launch_bounds__(KS > 0 ? kSolveKSThreads : 512, 1) conv_solve_kernel(const __grid_constant__ ConvArgs<T> a) {
   ConvOps<T, FAST, RW, KS> E(a);
   const ConvGeom& g = a.g;
   E.load_weights(a.kern);
