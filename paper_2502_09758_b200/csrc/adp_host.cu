@@ -504,6 +504,8 @@ static int conv_plan_init(PlanImpl& P) {
     if (g.C == 1 && g.kh == 9 && g.kw == 9 && g.rwb == 2 && g.threads <= kSolveKSThreads &&
         P.d.dtype == ADP_DTYPE_F64 && !(ev && atoi(ev) == 0))
       ks.solve = conv_solve_k9(P.d.mode == ADP_MODE_FAST);
+    else if (g.rwb == 4 && g.threads <= kSolveT384 && !(getenv("ADP_T384") && atoi(getenv("ADP_T384")) == 0))
+      ks.solve = conv_solve_t384(P.d.dtype, P.d.mode == ADP_MODE_FAST);
   }
   const int maxg = g.nTiles;
   if (int e = setup_kernel(P, P.k_solve, ks.solve, g.threads, P.smem, maxg)) return e;

@@ -105,6 +105,10 @@ const void* conv_solve_k9(int fast);
 // thread bound of the compile-time-stencil solve kernel (the host selects it
 // only for CTAs of at most this many threads)
 constexpr int kSolveKSThreads = 256;
+// RW = 4 solve kernels bounded at kSolveT384 threads (168 registers instead
+// of 128; the host selects them for CTAs of at most that many threads)
+constexpr int kSolveT384 = 384;
+const void* conv_solve_t384(int dtype, int fast);
 inline ConvKernelSet conv_kernels(int dtype, int mode, int rw) {
   if (dtype == 1) return conv_kernels_f32();
   const bool fast = mode == 1;

@@ -123,8 +123,10 @@ struct ConvOps : Conv<T, FAST, RW, KS> {
 // The compile-time-stencil instance (KS > 0: the c2 kernel, <= 256 threads,
 // see kSolveKSThreads) is bounded at 256 threads so it gets the full
 // 255-register file instead of spilling at the 512-thread cap of 128.
-template <typename T, bool FAST, int RW, int KS = 0>
-__global__ void __launch_bounds__(KS > 0 ? kSolveKSThreads : 512, 1) conv_solve_kernel(const __grid_constant__ ConvArgs<T> a) {
+// MAXT < 512: instances for CTAs of at most MAXT threads (c3-c5 run 384),
+// more registers per thread for the same reason.
+template <typename T, bool FAST, int RW, int KS = 0, int MAXT = 512>
+__global__ void __launch_bounds__(KS > 0 ? kSolveKSThreads : MAXT, 1) conv_solve_kernel(const __grid_constant__ ConvArgs<T> a) {
   ConvOps<T, FAST, RW, KS> E(a);
   const ConvGeom& g = a.g;
   E.load_weights(a.kern);
