@@ -125,12 +125,15 @@ struct Conv {
   const ConvArgs<T>& a;
   int ch, ty, tx;                // this thread's channel, tile row, column group
 
+  __device__ __forceinline__ int nC() const { return KS > 0 ? 1 : a.g.C; }
   __device__ static __forceinline__ int sk(int col) { return RW == 1 ? col : col + (col >> kShift); }
   __device__ static __forceinline__ int skr(int m) { return RW == 1 ? m : m + (m >> kShift); }
 
   __device__ explicit Conv(const ConvArgs<T>& a_) : a(a_) {
     const int tpr = a.g.TW / RW;
-    ch = threadIdx.x / a.g.tpc;
+    // KS > 0 instances serve single-channel images only (host check), so the
+    // channel index and count are compile-time
+    ch = KS > 0 ? 0 : (int)(threadIdx.x / a.g.tpc);
     const int r = threadIdx.x - ch * a.g.tpc;
     ty = r / tpr;
     tx = r - ty * tpr;
@@ -148,7 +151,7 @@ struct Conv {
 
   // ---- weights: ws[c][i][j] = kern[i][j][c] (|w| <= eps -> 0), wf flipped
   __device__ void load_weights(const T* kern) {
-    const int kh = a.g.kh, kw = a.g.kw, C = a.g.C, nk = kh * kw * C;
+    const int kh = a.g.kh, kw = a.g.kw, C = nC(), nk = kh * kw * C;
     T* s = ws();
     T* f = wf();
     for (int e = threadIdx.x; e < nk; e += blockDim.x) {
@@ -162,7 +165,7 @@ struct Conv {
   }
   // squared flipped taps (gram_diag: correlate(ones, flipped**2), operators.py:120-122)
   __device__ void load_weights_sq(const T* kern) {
-    const int kh = a.g.kh, kw = a.g.kw, C = a.g.C, nk = kh * kw * C;
+    const int kh = a.g.kh, kw = a.g.kw, C = nC(), nk = kh * kw * C;
     T* f = wf();
     __syncthreads();
     for (int e = threadIdx.x; e < nk; e += blockDim.x) {
@@ -184,7 +187,7 @@ struct Conv {
     w0 = (tile - tr * a.g.tilesW) * a.g.TW;
   }
   __device__ __forceinline__ int64_t gidx(int h, int w, int c) const {
-    return ((int64_t)h * a.g.W + w) * a.g.C + c;
+    return ((int64_t)h * a.g.W + w) * nC() + c;
   }
 
   // ---- load tile + (r+1) halo of all channels into the planes.  One warp
@@ -193,7 +196,7 @@ struct Conv {
   // element k of the flattened (row, interleaved column) tile box -> global
   // index (or -1 when outside the image) and plane offset
   __device__ __forceinline__ void box_elem(int k, int gh0, int gw0, int64_t& gi, int& off) const {
-    const int C = a.g.C, rowE = (a.g.TW + 2 * a.g.rw + 2) * C;
+    const int C = nC(), rowE = (a.g.TW + 2 * a.g.rw + 2) * C;
     const int sr = (int)(((unsigned long long)k * a.g.magicRow) >> 32);
     const int e = k - sr * rowE;
     const int px = (int)(((unsigned long long)e * a.g.magicC) >> 20);
@@ -209,7 +212,7 @@ struct Conv {
   static constexpr int kJ = 8;   // lane steps per row handled per pass (rows longer than 256 loop)
   template <class Src>
   __device__ void load_full(int h0, int w0, const Src& src, T* dst_region = nullptr) const {
-    const int C = a.g.C, H = a.g.H, W = a.g.W, SH = a.g.SH, SWP = a.g.SWP;
+    const int C = nC(), H = a.g.H, W = a.g.W, SH = a.g.SH, SWP = a.g.SWP;
     const unsigned mC = a.g.magicC;
     const int rowE = (a.g.TW + 2 * a.g.rw + 2) * C, planeSz = SH * SWP;
     const int gh0 = h0 - a.g.rh - 1, gw0 = w0 - a.g.rw - 1;
@@ -281,7 +284,7 @@ struct Conv {
   // plain copies: asynchronous global -> shared (LDGSTS), zero fill outside;
   // the caller's __syncthreads() after cp_async_wait_all() publishes them
   __device__ void load_copy(int h0, int w0, const T* x) const {
-    const int total = a.g.SH * (a.g.TW + 2 * a.g.rw + 2) * a.g.C;
+    const int total = a.g.SH * (a.g.TW + 2 * a.g.rw + 2) * nC();
     const int gh0 = h0 - a.g.rh - 1, gw0 = w0 - a.g.rw - 1;
     T* dst = pa();
     for (int k = threadIdx.x; k < total; k += blockDim.x) {
@@ -480,7 +483,7 @@ struct Conv {
     if (!tile_owned(h0)) return;   // CTA-uniform
     __syncthreads();
     // fused layouts have TW | W, so every tile row holds segs whole leaves
-    const int C = a.g.C, L = a.g.leafL;
+    const int C = nC(), L = a.g.leafL;
     const int rows = min(a.g.TH, a.g.H - h0);
     const int segs = a.g.segs;
     const int per_buf = rows * segs * 8;
@@ -518,7 +521,7 @@ struct Conv {
     }
   }
   __device__ __forceinline__ void put_term(int buf, int r, int q, double v) const {
-    tm()[(size_t)buf * a.g.TH * a.g.TW * a.g.C + ((size_t)r * a.g.TW + q) * a.g.C + ch] = v;
+    tm()[(size_t)buf * a.g.TH * a.g.TW * nC() + ((size_t)r * a.g.TW + q) * nC() + ch] = v;
   }
 
   // =========================================================================
@@ -536,7 +539,7 @@ struct Conv {
   __device__ __forceinline__ void tileA(const T* pr, T* qr, int tb, int h0, int w0, const T (&ypre)[RW], T* Rout,
                                         bool tv, T* TV2out, T* TVGout, bool fused, const T* pre_acc = nullptr) {
     const T nu = T(a.nu), nu2 = nu * nu;
-    const int H = a.g.H, W = a.g.W, TH = a.g.TH, TW = a.g.TW, C = a.g.C;
+    const int H = a.g.H, W = a.g.W, TH = a.g.TH, TW = a.g.TW, C = nC();
     const int64_t N = a.g.N;
     const int h = h0 + ty;
     T acc[RW];

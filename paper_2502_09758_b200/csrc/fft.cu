@@ -219,7 +219,10 @@ __device__ __forceinline__ double row_input(const RowArgs& A, int64_t o, bool va
   }
 }
 
-__global__ void __launch_bounds__(256, 3) row_fwd_kernel(const __grid_constant__ RowArgs A) {
+#ifndef FFT_ROW_MINB
+#define FFT_ROW_MINB 3
+#endif
+__global__ void __launch_bounds__(256, FFT_ROW_MINB) row_fwd_kernel(const __grid_constant__ RowArgs A) {
   __shared__ __align__(16) double2 sm[RROWS * kPadB];
   __shared__ double red[40];
   const Geo& g = A.g;
@@ -297,7 +300,10 @@ struct ColArgs {
   int npairs;            // pairs held in S for this pass
 };
 
-__global__ void __launch_bounds__(64 * CCOLS, 3) col_kernel(const __grid_constant__ ColArgs A) {
+#ifndef FFT_COL_MINB
+#define FFT_COL_MINB 3
+#endif
+__global__ void __launch_bounds__(64 * CCOLS, FFT_COL_MINB) col_kernel(const __grid_constant__ ColArgs A) {
   __shared__ __align__(16) double2 sm[CCOLS * kPadB];
   int p, strip, c;
   block_coords(T / CCOLS, A.g.C, p, strip, c);
@@ -450,7 +456,7 @@ __device__ __forceinline__ TvTerms tv_at(const Geo& g, const double* __restrict_
 }
 
 
-__global__ void __launch_bounds__(256, 3) row_inv_kernel(const __grid_constant__ InvArgs A) {
+__global__ void __launch_bounds__(256, FFT_ROW_MINB) row_inv_kernel(const __grid_constant__ InvArgs A) {
   __shared__ __align__(16) double2 sm[RROWS * kPadB];
   __shared__ double red[40];
   const Geo& g = A.g;
