@@ -480,7 +480,16 @@ __device__ __forceinline__ void reduce_k(const SumDev* const (&ss)[K], double* o
     total += (P[i] + 1) & ~1;
   }
   if (!fast || total > kTreeStage) {
-    reduce_list(ss, K, out, sv, gb, tr);
+    // the out-of-line routine takes addresses: give it its own copies so the
+    // caller's descriptor and result arrays stay in registers on the fast
+    // path (a stack copy is re-read from L2 after the grid barrier's acquire)
+    const SumDev* tss[K];
+    double tout[K];
+#pragma unroll
+    for (int i = 0; i < K; ++i) tss[i] = ss[i];
+    reduce_list(tss, K, tout, sv, gb, tr);
+#pragma unroll
+    for (int i = 0; i < K; ++i) out[i] = tout[i];
     return;
   }
   if (two) {
