@@ -453,7 +453,10 @@ static __device__ __noinline__ void reduce_list(const SumDev* const* ss, int k, 
 // all descriptor reads, copies, folds and shuffles of the K sums are
 // independent (unrolled) so their latencies overlap; otherwise the generic
 // out-of-line routine runs.  Same tree order, same results.
-template <int K>
+// OWN: give the out-of-line fallback its own stack copies (see below); used by
+// the register-rich c2 kernel, while the 168-register RW = 4 kernels keep the
+// shared arrays (the copies cost them spills).
+template <int K, bool OWN = false>
 __device__ __forceinline__ void reduce_k(const SumDev* const (&ss)[K], double* out, double* sv, GridBarrier& gb,
                                          unsigned long long* tr) {
   const bool stamp = tr && blockIdx.x == 0 && threadIdx.x == 0;
@@ -478,6 +481,10 @@ __device__ __forceinline__ void reduce_k(const SumDev* const (&ss)[K], double* o
     P[i] = n[i] <= 1 ? 1 : 1 << (32 - __clz(n[i] - 1));
     src[i] = s.nSub > 1 ? s.sub_vals : s.leaf_vals;
     total += (P[i] + 1) & ~1;
+  }
+  if ((!fast || total > kTreeStage) && !OWN) {
+    reduce_list(ss, K, out, sv, gb, tr);
+    return;
   }
   if (!fast || total > kTreeStage) {
     // the out-of-line routine takes addresses: give it its own copies so the

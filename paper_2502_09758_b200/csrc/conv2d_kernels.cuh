@@ -32,7 +32,7 @@ struct ConvOps : Conv<T, FAST, RW, KS> {
       const ptrdiff_t j = l[i] - &a.s_fit;
       ss[i] = (j >= 0 && j < kNumSums) ? ssm + j : l[i];
     }
-    reduce_k<K>(ss, out, this->sv(), gb, a.trace ? a.trace + 1088 : nullptr);
+    reduce_k<K, (KS > 0)>(ss, out, this->sv(), gb, a.trace ? a.trace + 1088 : nullptr);
   }
   // phase 1 only (subtrees of two-level sums), for the row-slab steps
   template <int K>
