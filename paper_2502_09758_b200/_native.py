@@ -262,11 +262,17 @@ def set_tile(shape_key, tile):
     _tile_override[shape_key] = tile
 
 
+def current_device() -> int:
+    """CUDA device of the calling thread: every device-side cache is keyed by it."""
+    import torch
+    return torch.cuda.current_device()
+
+
 def plan_for(layout, shape, ksize=(0, 0), slot=None) -> Plan:
     """Cached plan per (layout, shape, kernel size, precision, thread/slot)."""
     tile = _tile_override.get((layout, tuple(int(s) for s in shape), tuple(int(k) for k in ksize)), (0, 0))
     key = (layout, tuple(int(s) for s in shape), tuple(int(k) for k in ksize), _settings["dtype"],
-           _settings["mode"], threading.get_ident() if slot is None else slot, tuple(tile))
+           _settings["mode"], threading.get_ident() if slot is None else slot, tuple(tile), current_device())
     p = _plans.get(key)
     if p is None:
         p = Plan(layout, shape, ksize, _settings["dtype"], _settings["mode"], tile)
@@ -404,7 +410,7 @@ def power_start(shape):
     """The reference's power-iteration start vector (operators.py:145-149):
     ones + 0.01 * standard_normal from default_rng(0), un-normalised.  A
     constant of the algorithm generated once per shape and kept on device."""
-    key = (tuple(shape), _settings["dtype"])
+    key = (tuple(shape), _settings["dtype"], current_device())
     t = _v0_cache.get(key)
     if t is None:
         rng = np.random.default_rng(0)

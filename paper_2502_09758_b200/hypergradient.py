@@ -129,12 +129,13 @@ def _upper_terms(A, x, y_delta, want_grad=False):
 def _cached_dev(owner, arr):
     """Device copy of a host array held by `owner` (e.g. y_delta), cached."""
     cache = owner.__dict__.setdefault("_devcache", {})
-    key = (id(arr), nat.get_precision()["dtype"])
+    key = (id(arr), nat.get_precision()["dtype"], nat.current_device())
+    ver = arr._version if nat.is_torch(arr) else None   # in-place edits of a tensor re-copy
     hit = cache.get(key)
-    if hit is None or hit[0] is not arr:
-        hit = (arr, nat.to_dev(arr, owner.signal_shape))
+    if hit is None or hit[0] is not arr or hit[1] != ver:
+        hit = (arr, ver, nat.to_dev(arr, owner.signal_shape))
         cache[key] = hit
-    return hit[1]
+    return hit[2]
 
 
 def upper_fit_grad(x, A, y_delta):
@@ -246,10 +247,10 @@ def inexact_hypergradient(upper, b: Kernel, eps: float, delta: float, state: War
     )
     host = not nat.is_torch(state.x)   # numpy state in -> numpy state out (reference types)
     x_t = res.x_tilde
+    state.x = nat.to_host(x_t).astype(float) if host else x_t   # before the CG, as hypergradient.py:169
     _, _, rhs = _upper_terms(upper.A, x_t, upper.y_delta, want_grad=True)
     cg, _ = hess_cg(p, x_t, rhs, delta, cg_max_iters, q0=state.q)
     z = -mixed_second_transpose(x_t, b, cg.q, p) + sobolev_grad(b, upper.a, upper.beta)
-    state.x = nat.to_host(x_t).astype(float) if host else x_t
     state.q = nat.to_host(cg.q).astype(float) if host else cg.q
     return HypergradResult(
         z=z,

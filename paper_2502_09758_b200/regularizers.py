@@ -113,10 +113,19 @@ class SmoothedElasticNet:
         return s
 
     def _call(self, op, x, v=None, want_out=True):
-        shape = tuple(np.shape(x))
-        if len(shape) != 1:
-            raise ValueError("the device elastic net acts on 1-D signals")
-        return _reg_call(self.native(), nat.LAYOUT_DENSE1D, shape, (0, 0), op, x, v, want_out)
+        """Elementwise on any shape, as the reference (regularizers.py:75-134):
+        the C-order flattening is exactly what np.sum reduces over, so the
+        device runs the 1-D form on the flat view and the result takes x's
+        shape back."""
+        shape = tuple(int(s) for s in np.shape(x))
+        if v is not None and tuple(np.shape(v)) != shape:
+            raise ValueError(f"shape mismatch: x {shape}, v {tuple(np.shape(v))}")
+        n = int(np.prod(shape)) if shape else 1
+        xf = x.reshape(n) if nat.is_torch(x) else np.ascontiguousarray(np.asarray(x, dtype=float)).reshape(n)
+        vf = None if v is None else (v.reshape(n) if nat.is_torch(v) else
+                                     np.ascontiguousarray(np.asarray(v, dtype=float)).reshape(n))
+        val, out = _reg_call(self.native(), nat.LAYOUT_DENSE1D, (n,), (0, 0), op, xf, vf, want_out)
+        return val, (out.reshape(shape) if out is not None else None)
 
     def value(self, x) -> float:
         return self._call(0, x, want_out=False)[0]

@@ -256,6 +256,83 @@ def baseline_cases():
          unr_gnorm=np.array(utr.grad_norm), unr_final=utr.final_loss)
 
 
+def _sha(a) -> str:
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(np.asarray(a, dtype=np.float64)).tobytes()).hexdigest()
+
+
+def k31_inputs(shape, seed):
+    """Inputs of the large K = 31 fixture, regenerated bit for bit by the test
+    from the seed (PCG64 streams are platform-independent)."""
+    rng = np.random.default_rng(seed)
+    return rng.uniform(0.0, 1.0, shape), rng.standard_normal(shape), rng.uniform(0.0, 1.0, shape)
+
+
+def conv_k31_cases():
+    """c5-geometry stencils (K = 31): a random kernel with tiny taps on
+    96x80x3 (full arrays) and the c5 Gaussian (sigma 6) on 300x260x3 (inputs
+    from a seed; bitwise outputs as SHA-256 of their bytes, tolerance outputs
+    in full)."""
+    conv_case("conv_k31.npz", (96, 80, 3), 31, 14)
+    shape, seed = (300, 260, 3), 15
+    kern = P.gaussian_kernel_2d(31, 6.0, 3).data
+    x, v, y = k31_inputs(shape, seed)
+    op = O.ConvOperator(O.Kernel(kern, O.DEPTHWISE2D), shape)
+    p = L.LowerProblem(op, y, 0.6, R.SmoothedTV(1e-4))
+    vg_val, vg_g = L.lower_value_and_grad(p, x)
+    lam = O.op_norm_sq(O.ConvOperator(O.Kernel(kern, O.DEPTHWISE2D), shape), 300, 1e-4)
+    save("conv_k31_g6.npz", kern=kern, shape=np.array(shape), seed=seed, alpha=0.6, nu=1e-4,
+         apply_sha=_sha(op.apply(x)), adjoint_sha=_sha(op.adjoint(v)), gram_diag_sha=_sha(op.gram_diag()),
+         vg_g_sha=_sha(vg_g), lower_grad_sha=_sha(L.lower_grad(p, x)), vg_val=vg_val,
+         lower_value=L.lower_value(p, x), apply_probe=op.apply(x)[::37, ::41],
+         hess_vec=L.lower_hess_vec(p, x, v), hess_diag=L.lower_hess_diag(p, x), norm_sq=lam,
+         kgc=O.kernel_gram_correlation(x, v, op.kernel), mixed=H.mixed_second_transpose(x, op.kernel, v, p))
+
+
+def _maid2d_run(tag, perturb_seed):
+    """One reference maid_run on the reduced c2 (96x96x1, c2 kernels and the
+    reference 2-D MAID settings, 3 accepted upper steps); perturb_seed > 0:
+    y_delta * (1 + 1e-15 N(0, 1)) (SURVEY.md App. C band calibration)."""
+    from adp import metrics_io as MI
+    from paper_2502_09758_b200 import configs as C
+
+    def ref_blur(x, kernel):
+        return O.ConvOperator(O.Kernel(kernel.data, O.DEPTHWISE2D), x.shape).apply(x)
+    up2 = C.config2(0, size=96, blur_fn=ref_blur)
+    y = np.array(up2.y_delta)
+    if perturb_seed:
+        y = y * (1.0 + 1e-15 * np.random.default_rng(1000 + perturb_seed).standard_normal(y.shape))
+    ref2 = P.UpperProblem(name="c2s", A=O.ConvOperator(O.Kernel(up2.a.data, O.DEPTHWISE2D), y.shape),
+                          a=O.Kernel(up2.a.data, O.DEPTHWISE2D), y_delta=y, beta=0.3, alpha=0.6,
+                          reg=R.SmoothedTV(1e-4), b0=O.Kernel(up2.b0.data, O.DEPTHWISE2D), x0=y.copy(),
+                          mu_floor=10.0, lower_method="agd", lower_max_iters=1200, lower_adaptive=True)
+    cfg = M.MAIDConfig(eps0=0.25, delta0=0.25, alpha0=2e-5, max_bt=2, cg_max_iters=100, max_upper_iters=3)
+    b, x, tr = M.maid_run(ref2, cfg)
+    out = {f"{tag}_{f}": np.asarray(getattr(tr, f)) for f in
+           ("loss", "grad_norm", "eps", "delta", "alpha", "lower_iters_cum", "cg_iters_cum")}
+    out[f"{tag}_final"] = tr.final_loss
+    out[f"{tag}_psnr"] = MI.psnr(x, up2.ground_truth)
+    out[f"{tag}_b"] = b.data
+    out[f"{tag}_x"] = x
+    if not perturb_seed:
+        out["y_delta"] = y
+        out["x_true"] = up2.ground_truth
+        out["a"] = up2.a.data
+    return out
+
+
+def maid2d_p4():
+    """P4 full-run fixture for 2-D MAID: the reference run plus three
+    1e-15-perturbed replicas (the reference's intrinsic reproducibility band)."""
+    import multiprocessing as mp
+    with mp.get_context("fork").Pool(4) as pool:
+        parts = pool.starmap(_maid2d_run, [("ref", 0), ("rep1", 1), ("rep2", 2), ("rep3", 3)])
+    out = {}
+    for d in parts:
+        out.update(d)
+    save("maid2d_p4.npz", **out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:

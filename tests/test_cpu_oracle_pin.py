@@ -21,7 +21,7 @@ def test_reductions_bitwise(orc, golden, n):
     assert orc.norm(a) == float(d[f"norm{n}"])
 
 
-@pytest.mark.parametrize("name", ["conv_small.npz", "conv_k9.npz", "conv_k15.npz"])
+@pytest.mark.parametrize("name", ["conv_small.npz", "conv_k9.npz", "conv_k15.npz", "conv_k31.npz"])
 def test_conv_primitives(orc, golden, name):
     d = golden(name)
     op = orc.Conv(d["kern"], d["x"].shape)
@@ -39,6 +39,24 @@ def test_conv_primitives(orc, golden, name):
     assert rel(orc.kgc(d["x"], d["v"], False, d["kern"].shape[:2]), d["kgc"]) <= 1e-13
     lam, conv, _ = orc.op_norm_sq(orc.Conv(d["kern"], d["x"].shape), 300, 1e-4)
     assert lam == float(d["norm_sq"])
+
+
+def test_conv_k31_gaussian_pin(orc, golden):
+    """The oracle's ndimage restatement at K = 31 on 300x260x3 (c5 kernel),
+    pinned by the SHA-256 of the reference's outputs."""
+    import hashlib
+    d = golden("conv_k31_g6.npz")
+    shape, seed = tuple(int(s) for s in d["shape"]), int(d["seed"])
+    rng = np.random.default_rng(seed)
+    x, v = rng.uniform(0.0, 1.0, shape), rng.standard_normal(shape)
+    op = orc.Conv(d["kern"], shape)
+
+    def sha(a):
+        return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
+    ap = op.apply(x)
+    assert np.array_equal(ap[::37, ::41], d["apply_probe"])
+    assert sha(ap) == str(d["apply_sha"])
+    assert sha(op.adjoint(v)) == str(d["adjoint_sha"])
 
 
 def test_dense_primitives(orc, golden):
