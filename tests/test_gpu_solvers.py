@@ -130,7 +130,14 @@ def test_config1_full_maid_run(adp, golden):
     assert len(tr) == len(d["maid_loss"])
     assert tr.lower_iters_cum == [int(v) for v in d["maid_lower_cum"]]
     assert tr.cg_iters_cum == [int(v) for v in d["maid_cg_cum"]]
-    assert rel(tr.alpha, d["maid_alpha"]) <= 1e-12
-    assert rel(tr.loss, d["maid_loss"]) <= 1e-9
-    assert rel(b.data, d["maid_b"]) <= 1e-9
-    assert rel(x, d["maid_x"]) <= 1e-8
+    e = {"alpha": rel(tr.alpha, d["maid_alpha"]), "loss": rel(tr.loss, d["maid_loss"]),
+         "b": rel(b.data, d["maid_b"]), "x": rel(x, d["maid_x"]), "final": abs(tr.final_loss - float(d["maid_final"]))
+         / abs(float(d["maid_final"]))}
+    from _report import report
+    report("c1_full_maid_run", **e)
+    assert e["alpha"] <= 1e-12
+    assert e["loss"] <= 1e-9 and e["final"] <= 1e-9
+    assert e["b"] <= 1e-9
+    # x: 1e-9 as the north star asks; SURVEY App. C measured the reference's own x reproducibility under
+    # 1e-15 input noise at up to 1.06e-9 on c1, so the measured value is reported (parity_report.jsonl)
+    assert e["x"] <= 1e-9, e["x"]
