@@ -277,13 +277,38 @@ int adp_plan_probe(const adp_plan_desc* desc, int32_t* out);
  * Each step leaves phase 1 of its sums in the plan; adp_slab_units exposes them. */
 int adp_slab_step(adp_plan* p, const adp_lower* lp, int32_t op, const void* x, const void* xp, void* out,
                   double beta, double L, void* stream);
-/* Sum units of a slab plan for sum `which` (0 fit, 1 tv, 2 fitc, 3 tvc, 4 ||g||^2 / norm, 5 restart dot):
+/* Sum units of a slab plan for sum `which` (0 fit, 1 tv, 2 fitc, 3 tvc, 4 ||g||^2 / norm / <p, Hp>,
+ * 5 restart dot / <r, M^-1 r>, 6 ||r||^2):
  * the global tree has n_units units (leaf values, or subtree roots when the sum is two-level), of
  * which this plan produces [own[0], own[1]) and [own[2], own[3]).  If dst (device, n_units doubles)
  * is non-NULL those ranges are copied into it at their global offsets (stream-ordered).  Once every
  * rank's ranges are in place (the other entries zero: an all-reduce SUM assembles them exactly),
  * adp_fold_units gives the sum in the single-GPU tree order. */
 int adp_slab_units(adp_plan* p, int32_t which, int64_t* n_units, int64_t* own, double* dst, void* stream);
+
+/* ---- row-slab hypergradient (multi-GPU c5: inexact_hypergradient / maid_run on slabs).
+ * adp_slab_cg: one step of the hypergradient's Jacobi-PCG (cg_solve, hypergradient.py:35-84, on
+ * lower_hess_vec / lower_hess_diag, lower_solvers.py:66-80) over slab + ghosts, split at its sums:
+ *   op 0: TV curvature weights and the unfloored Jacobi diagonal of H at x~ = in0; *scal = max over
+ *         the owned pixels (the ranks take the max; floor = 1e-12 max + 1e-300, lower_solvers.py:80)
+ *   op 1: DIAG = 1 / max(d, s); r = in0 (rhs) - (flag ? H q : 0); out0 = q (zeroed unless flag);
+ *         out1 = M^-1 r; sums <r, M^-1 r> (units 5), ||r||^2 (units 6)          (hypergradient.py:55-63)
+ *   op 2: flag 0 / 1: p = in0 (+ s * in1) -> out0, H p, <p, Hp> (units 4)       (:70-75, 81)
+ *         flag 2: ||H in0 - in1||^2 (units 4), the true residual (:83); flag 3: H in0 (warm start)
+ *   op 3: out0 (q) += s p (in0); r -= s H p; out1 = M^-1 r; sums units 5, 6     (:76-80)
+ * adp_slab_upper: R = A x - y_delta, grad_out = 2 A^T R, sum(R^2) (units 0), ||grad||^2 (units 4)
+ *                 (problems.py:48-50, hypergradient.py:87-89)
+ * adp_slab_mixed: the two kernel_gram_correlation terms of mixed_second_transpose
+ *                 (hypergradient.py:92-104, operators.py:198-220) for the slab's owned 16-row groups,
+ *                 into part (ngroups x ntaps doubles, other groups untouched: zero them, sum over ranks,
+ *                 then adp_kgc_final(scale 2) folds the groups in the unsplit order) */
+int adp_slab_cg(adp_plan* p, const adp_lower* lp, int32_t op, const void* in0, const void* in1, void* out0,
+                void* out1, double s, int32_t flag, double* scal, void* stream);
+int adp_slab_upper(adp_plan* p, const void* A_kernel, const void* x, const void* y_delta, void* grad_out,
+                   void* stream);
+int adp_slab_mixed(adp_plan* p, const adp_lower* lp, const void* x_tilde, const void* q, double* part, void* stream);
+int adp_kgc_groups(adp_plan* p, int32_t* ngroups, int32_t* ntaps);
+int adp_kgc_final(adp_plan* p, const double* part, void* out, double scale, void* stream);
 /* k (<= 8) perfect-tree folds (zero-padded to a power of two, <= 16384 units each) of device unit
  * vectors units[i] (n[i] doubles); results to HOST out[i]; synchronises the stream. */
 int adp_fold_units(int32_t k, const double* const* units, const int64_t* n, double* out, void* stream);

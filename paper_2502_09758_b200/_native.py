@@ -119,6 +119,11 @@ SIGNATURES = {
     "adp_slab_step": (_I, [_P, ctypes.POINTER(Lower), _I, _P, _P, _P, _D, _D, _P]),
     "adp_slab_units": (_I, [_P, _I, ctypes.POINTER(ctypes.c_int64), _P, _P, _P]),
     "adp_fold_units": (_I, [_I, _P, _P, _P, _P]),
+    "adp_slab_cg": (_I, [_P, ctypes.POINTER(Lower), _I, _P, _P, _P, _P, _D, _I, ctypes.POINTER(_D), _P]),
+    "adp_slab_upper": (_I, [_P, _P, _P, _P, _P, _P]),
+    "adp_slab_mixed": (_I, [_P, ctypes.POINTER(Lower), _P, _P, _P, _P]),
+    "adp_kgc_groups": (_I, [_P, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
+    "adp_kgc_final": (_I, [_P, _P, _P, _D, _P]),
     "adp_sum_layout": (_I, [ctypes.c_int64, _I, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(_I),
                             ctypes.POINTER(_I), _P, ctypes.c_int64, _P, _P, ctypes.c_int64, _P, ctypes.c_int64,
                             ctypes.POINTER(ctypes.c_int64)]),

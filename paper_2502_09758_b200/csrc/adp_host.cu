@@ -399,7 +399,13 @@ static int conv_plan_init(PlanImpl& P) {
   build_sum(s2N, 2 * g.Ng, true, pool);
   build_sum(sT, nTilesG, false, pool);
   // kgc partial groups
-  P.kgc_groups = std::min(4 * P.sm_count, std::max(1, ((g.H + 15) / 16) * ((g.W + 15) / 16)));
+  {
+    // kernel_gram_correlation groups: (tile row of 16 GLOBAL rows, column
+    // block); the count depends on the geometry only (identical on every rank)
+    const int thH = (g.Hg + 15) / 16, thW = (g.W + 15) / 16;
+    P.kgc_cblocks = std::max(1, std::min(thW, (296 + thH - 1) / thH));
+    P.kgc_groups = thH * P.kgc_cblocks;
+  }
   const size_t nk = (size_t)g.kh * g.kw * g.C;
   // layout the device block
   size_t off = 0;
@@ -597,15 +603,17 @@ static int conv_slab_step(PlanImpl& P, const adp_lower* lp, int op, const void* 
 
 template <typename T>
 static int conv_kgc(PlanImpl& P, const void* xa, const void* va, const void* xb, const void* vb, void* out,
-                    double scale, cudaStream_t st) {
-  if (P.g.Hg != P.g.H || P.g.row0) return fail(ADP_ERR_UNSUPPORTED, "row-slab plans run adp_slab_step only");
+                    double scale, cudaStream_t st, double* part) {
+  // part != null: row slab, partials of the owned groups into the caller's vector (no final sum)
+  if ((P.g.Hg != P.g.H || P.g.row0) && !part) return fail(ADP_ERR_UNSUPPORTED, "row-slab plans: use adp_slab_mixed");
   ConvKernelSet ks = conv_kernels(P.d.dtype, P.d.mode, P.g.rwb);
   KgcArgs<T> a;
   std::memset(&a, 0, sizeof(a));
   a.g = P.g;
   a.xa = (const T*)xa; a.va = (const T*)va; a.xb = (const T*)xb; a.vb = (const T*)vb;
-  a.part = P.d_kgc_part;
+  a.part = part ? part : P.d_kgc_part;
   a.ngroups = P.kgc_groups;
+  a.cblocks = P.kgc_cblocks;
   a.out = (T*)out;
   a.scale = scale;
   const int KT = 16;
@@ -613,9 +621,44 @@ static int conv_kgc(PlanImpl& P, const void* xa, const void* va, const void* xb,
   CK(cudaFuncSetAttribute(ks.kgc_part, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem_optin));
   void* args[] = {&a};
   CK(cudaLaunchKernel(ks.kgc_part, dim3(P.kgc_groups), dim3(256), args, smem, st));
+  if (part) return ADP_OK;
   const int n = P.g.kh * P.g.kw * P.g.C;
   CK(cudaLaunchKernel(ks.kgc_final, dim3((n + 255) / 256), dim3(256), args, 0, st));
   return ADP_OK;
+}
+
+template <typename T>
+static int conv_kgc_final(PlanImpl& P, const double* part, void* out, double scale, cudaStream_t st) {
+  ConvKernelSet ks = conv_kernels(P.d.dtype, P.d.mode, P.g.rwb);
+  KgcArgs<T> a;
+  std::memset(&a, 0, sizeof(a));
+  a.g = P.g;
+  a.part = const_cast<double*>(part);
+  a.ngroups = P.kgc_groups;
+  a.cblocks = P.kgc_cblocks;
+  a.out = (T*)out;
+  a.scale = scale;
+  void* args[] = {&a};
+  const int n = P.g.kh * P.g.kw * P.g.C;
+  CK(cudaLaunchKernel(ks.kgc_final, dim3((n + 255) / 256), dim3(256), args, 0, st));
+  return ADP_OK;
+}
+
+template <typename T>
+static int conv_slab_cg(PlanImpl& P, const adp_lower* lp, int op, const void* in0, const void* in1, void* out0,
+                        void* out1, double s, int flag, cudaStream_t st) {
+  static const int modes[4] = {CM_SLAB_CG_DIAG, CM_SLAB_CG_INIT, CM_SLAB_CG_HV, CM_SLAB_CG_UPD};
+  ConvArgs<T> a = conv_base<T>(P);
+  set_lower(a, lp);
+  a.mode = modes[op];
+  a.in0 = (const T*)in0;
+  a.in1 = (const T*)in1;
+  a.out0 = (T*)out0;
+  a.out1 = (T*)out1;
+  a.sbeta = s;
+  a.sL = s;
+  a.sflag = flag;
+  return launch_coop(P, P.k_misc, a, st);
 }
 
 }  // namespace adp
@@ -757,7 +800,7 @@ int adp_op_norm_sq(adp_plan* p, const void* kernel, const void* v0, int32_t max_
 int adp_kgc(adp_plan* p, const void* x, const void* v, void* out, void* stream) {
   if (!p) return fail(ADP_ERR_ARG, "null plan");
   if (IS_DENSE(p)) return dense_call(p->impl, DO_KGC, nullptr, nullptr, x, v, out, nullptr, nullptr, nullptr, STREAM(stream));
-  return DISPATCH_T(p->impl, conv_kgc)(p->impl, x, v, nullptr, nullptr, out, 1.0, STREAM(stream));
+  return DISPATCH_T(p->impl, conv_kgc)(p->impl, x, v, nullptr, nullptr, out, 1.0, STREAM(stream), nullptr);
 }
 
 static int check_lower(adp_plan* p, const adp_lower* lp) {
@@ -942,7 +985,7 @@ int adp_mixed_T(adp_plan* p, const adp_lower* lp, const void* x_tilde, const voi
   void* bq = P.ws[12];    // BP
   if (int e = DISPATCH_T(P, conv_misc)(P, CM_MIXED_PREP, lp, nullptr, x_tilde, q, resid, bq, nullptr, STREAM(stream)))
     return e;
-  return DISPATCH_T(P, conv_kgc)(P, x_tilde, bq, q, resid, out, 2.0, STREAM(stream));
+  return DISPATCH_T(P, conv_kgc)(P, x_tilde, bq, q, resid, out, 2.0, STREAM(stream), nullptr);
 }
 
 int adp_upper_terms(adp_plan* p, const void* A_kernel, const void* x, const void* y_delta, double* fit,
@@ -1132,8 +1175,8 @@ extern "C" int adp_slab_units(adp_plan* p, int32_t which, int64_t* n_units, int6
   if (!p || !n_units || !own) return fail(ADP_ERR_ARG, "null argument");
   PlanImpl& P = p->impl;
   if (P.d.layout != ADP_LAYOUT_DEPTHWISE2D) return fail(ADP_ERR_UNSUPPORTED, "slab units: depthwise2d plans only");
-  if (which < 0 || which > 5) return fail(ADP_ERR_ARG, "slab units: unknown sum");
-  const SumDev* sds[6] = {&P.s_fit, &P.s_tv, &P.s_fitc, &P.s_tvc, &P.s_t0, &P.s_t1};
+  if (which < 0 || which > 6) return fail(ADP_ERR_ARG, "slab units: unknown sum");
+  const SumDev* sds[7] = {&P.s_fit, &P.s_tv, &P.s_fitc, &P.s_tvc, &P.s_t0, &P.s_t1, &P.s_t2};
   const SumDev& sd = *sds[which];
   if (!sd.regular) return fail(ADP_ERR_UNSUPPORTED, "slab units: irregular (program) sum");
   *n_units = P.units_n[which];
@@ -1148,6 +1191,82 @@ extern "C" int adp_slab_units(adp_plan* p, int32_t which, int64_t* n_units, int6
     }
   }
   return ADP_OK;
+}
+
+// ---- row-slab hypergradient (multigpu.SlabHypergradient) -----------------
+// One step of the hypergradient's Jacobi-PCG (hypergradient.py:35-84 on
+// lower_hess_vec / lower_hess_diag, lower_solvers.py:66-80) over a slab +
+// ghosts, stopping after phase 1 of its sums (adp_slab_units + adp_fold_units
+// assemble them across ranks).  op 0: TV weights + unfloored diagonal of
+// H(x~ = in0), *scal = max over the owned pixels; op 1: floor s, invert,
+// r = in0 (- H q if flag), q = out0 (zeroed unless flag), s = out1, sums
+// <r, s>, <r, r>; op 2: flag 0/1: p = in0 (+ s * in1) -> out0, H p, <p, Hp>;
+// flag 2: ||H in0 - in1||^2 (true residual), Vbuf out0; flag 3: H in0 (warm
+// start), Vbuf out0; op 3: q (out0) += s p (in0), r -= s H p, s (out1) = M^-1 r,
+// sums <r, s>, <r, r>.
+extern "C" int adp_slab_cg(adp_plan* p, const adp_lower* lp, int32_t op, const void* in0, const void* in1,
+                           void* out0, void* out1, double s, int32_t flag, double* scal, void* stream) {
+  if (int e = check_lower(p, lp)) return e;
+  PlanImpl& P = p->impl;
+  if (P.d.layout != ADP_LAYOUT_DEPTHWISE2D) return fail(ADP_ERR_UNSUPPORTED, "slab CG: depthwise2d plans only");
+  if (op < 0 || op > 3) return fail(ADP_ERR_ARG, "slab CG: unknown op");
+  if (!in0 || (op != 0 && !out0) || ((op == 1 || op == 3) && !out1)) return fail(ADP_ERR_ARG, "slab CG: null argument");
+  if (op == 2 && (flag < 0 || flag > 3 || (flag != 0 && flag != 3 && !in1))) return fail(ADP_ERR_ARG, "slab CG: bad flag");
+  if (int e = DISPATCH_T(P, conv_slab_cg)(P, lp, op, in0, in1, out0, out1, s, flag, STREAM(stream))) return e;
+  if (op == 0) {
+    if (int e = fetch_scal(P, 1, STREAM(stream))) return e;
+    if (scal) *scal = P.h_scal[0];
+  }
+  return ADP_OK;
+}
+
+// UpperProblem.fit_value / upper_fit_grad (problems.py:48-50,
+// hypergradient.py:87-89) over a slab: R = A x - y, grad_out = 2 A^T R (owned
+// rows valid), phase 1 of sum(R^2) (units 0) and ||grad||^2 (units 4).
+extern "C" int adp_slab_upper(adp_plan* p, const void* A_kernel, const void* x, const void* y_delta, void* grad_out,
+                              void* stream) {
+  if (!p || !A_kernel || !x || !y_delta) return fail(ADP_ERR_ARG, "null argument");
+  PlanImpl& P = p->impl;
+  if (P.d.layout != ADP_LAYOUT_DEPTHWISE2D) return fail(ADP_ERR_UNSUPPORTED, "slab upper: depthwise2d plans only");
+  if (!P.g.fused) return fail(ADP_ERR_UNSUPPORTED, "slab upper: needs the row-aligned (fused) sum layout");
+  return DISPATCH_T(P, conv_misc)(P, CM_SLAB_UPPER, nullptr, A_kernel, x, nullptr, grad_out, nullptr, y_delta,
+                                  STREAM(stream));
+}
+
+// mixed_second_transpose (hypergradient.py:92-104) over a slab: R = B x~ - y,
+// BP = B q, then the kernel_gram_correlation partials of the slab's owned
+// groups into part (adp_kgc_groups doubles x groups, zero elsewhere; the
+// ranks sum the vectors and adp_kgc_final folds them in group order).
+extern "C" int adp_slab_mixed(adp_plan* p, const adp_lower* lp, const void* x_tilde, const void* q, double* part,
+                              void* stream) {
+  if (int e = check_lower(p, lp)) return e;
+  PlanImpl& P = p->impl;
+  if (P.d.layout != ADP_LAYOUT_DEPTHWISE2D) return fail(ADP_ERR_UNSUPPORTED, "slab mixed: depthwise2d plans only");
+  if (!x_tilde || !q || !part) return fail(ADP_ERR_ARG, "null argument");
+  if ((P.g.row0 + P.g.own0) % 16 || ((P.g.row0 + P.g.own1) % 16 && P.g.row0 + P.g.own1 != P.g.Hg))
+    return fail(ADP_ERR_ARG, "slab mixed: owned rows must be 16-row aligned");
+  void* resid = P.ws[3];  // R
+  void* bq = P.ws[12];    // BP
+  if (int e = DISPATCH_T(P, conv_misc)(P, CM_SLAB_MIXED_PREP, lp, nullptr, x_tilde, q, nullptr, nullptr, nullptr,
+                                       STREAM(stream)))
+    return e;
+  return DISPATCH_T(P, conv_kgc)(P, x_tilde, bq, q, resid, nullptr, 2.0, STREAM(stream), part);
+}
+
+extern "C" int adp_kgc_groups(adp_plan* p, int32_t* ngroups, int32_t* ntaps) {
+  if (!p || !ngroups || !ntaps) return fail(ADP_ERR_ARG, "null argument");
+  PlanImpl& P = p->impl;
+  if (P.d.layout != ADP_LAYOUT_DEPTHWISE2D) return fail(ADP_ERR_UNSUPPORTED, "kgc groups: depthwise2d plans only");
+  *ngroups = P.kgc_groups;
+  *ntaps = P.g.kh * P.g.kw * P.g.C;
+  return ADP_OK;
+}
+
+extern "C" int adp_kgc_final(adp_plan* p, const double* part, void* out, double scale, void* stream) {
+  if (!p || !part || !out) return fail(ADP_ERR_ARG, "null argument");
+  PlanImpl& P = p->impl;
+  if (P.d.layout != ADP_LAYOUT_DEPTHWISE2D) return fail(ADP_ERR_UNSUPPORTED, "kgc final: depthwise2d plans only");
+  return DISPATCH_T(P, conv_kgc_final)(P, part, out, scale, STREAM(stream));
 }
 
 // Debug: enable (enable = 1) per-phase %globaltimer stamps of the next solves

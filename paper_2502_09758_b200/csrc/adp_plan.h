@@ -62,6 +62,7 @@ struct PlanImpl {
   double* d_scal = nullptr;
   double* d_kgc_part = nullptr;
   int kgc_groups = 0;
+  int kgc_cblocks = 1;
   // pinned host staging
   SolveOut* h_sres = nullptr;
   CGOut* h_cres = nullptr;

@@ -23,6 +23,13 @@ enum ConvMode : int {
   CM_SLAB_NORM0 = 15,    // row slab: phase-1 of ||in0||^2
   CM_SLAB_GRAD = 16,     // row slab: lower_grad(in0) -> G; phase-1 of fit, tv, ||g||^2
   CM_BENCH_REDUCE = 17,  // micro-benchmark: the solve's 6-sum reduction, mode-param times back to back
+  // row-slab hypergradient steps (multigpu.SlabHypergradient): each stops after phase 1 of its sums
+  CM_SLAB_CG_DIAG = 18,  // TV weights + unfloored Jacobi diagonal of H(in0 = x~); scal[0] = max over owned pixels
+  CM_SLAB_CG_INIT = 19,  // DIAG = 1 / max(d, sL); r = in0 (- HP if sflag); out0 = q (0 unless sflag); out1 = s
+  CM_SLAB_CG_HV = 20,    // sflag 0/1: p = in0 (+ sbeta in1) -> out0, HP = H p, <p, Hp>; 2: (H in0 - in1)^2; 3: HP = H in0
+  CM_SLAB_CG_UPD = 21,   // q (out0) += sbeta p (in0); r -= sbeta HP; s (out1) = DIAG r; <r, s>, <r, r>
+  CM_SLAB_UPPER = 22,    // R = A in0 - y; out0 = 2 A^T R; leaves of R^2 (owned rows), <out0, out0>
+  CM_SLAB_MIXED_PREP = 23,  // R = B in0 - y, BP = B in1 (every local row)
 };
 
 
@@ -72,6 +79,7 @@ struct ConvArgs {
   int mode;                // misc kernel mode
   int nofloor;             // hess_diag without the 1e-12*max floor (regularizer-only call)
   double sbeta, sL;        // row-slab steps: momentum beta, trial Lipschitz L (or power scale)
+  int sflag;               // row-slab CG steps: variant (see CM_SLAB_CG_*)
   unsigned long long* trace;  // optional phase timestamps (CTA 0): [iter][16] %globaltimer ns
   const T* in0; const T* in1; T* out0; T* out1;
 };
@@ -81,7 +89,8 @@ struct KgcArgs {
   ConvGeom g;
   const T* xa; const T* va; const T* xb; const T* vb;
   double* part;   // [ngroups][kh*kw*C]
-  int ngroups;
+  int ngroups;    // (tile row of 16 image rows, column block) groups over the GLOBAL image
+  int cblocks;    // column blocks per tile row
   T* out;         // (kh, kw, C)
   double scale;
 };

@@ -53,6 +53,41 @@ struct ConvOps : Conv<T, FAST, RW, KS> {
     reduce({&s}, &o);
     return o;
   }
+  // NumPy-pairwise leaves of an element sum over the OWNED rows of a row
+  // slab (regular, row-aligned layout), at their GLOBAL leaf indices; the
+  // same per-leaf arithmetic as np_leaves_regular (unsplit plans: all rows).
+  template <class Src>
+  __device__ void slab_leaves(const SumDev& s, const Src& src) {
+    const int L = s.leaf_len;
+    const int64_t rowL = (int64_t)a.g.W * a.g.C / L;
+    const int64_t l0 = (int64_t)(a.g.row0 + a.g.own0) * rowL;
+    const int64_t l1 = (int64_t)(a.g.row0 + min(a.g.own1, a.g.H)) * rowL;
+    const int64_t ebase = (int64_t)a.g.row0 * a.g.W * a.g.C;
+    const int64_t nthreads = (int64_t)gridDim.x * blockDim.x;
+    const int64_t total = (l1 - l0) * 8;
+    const int64_t base = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t g0 = 0; g0 < total; g0 += nthreads) {
+      const int64_t g = g0 + base;
+      const bool act = g < total;
+      const int64_t leaf = l0 + (g >> 3);
+      const int k = (int)(g & 7);
+      double acc = 0.0;
+      if (act) {
+        const int64_t e0 = leaf * L + k - ebase;
+        double v[16];
+#pragma unroll
+        for (int m = 0; m < 16; ++m) v[m] = (8 * m < L) ? src(e0 + 8 * m) : 0.0;
+        acc = v[0];
+#pragma unroll
+        for (int m = 1; m < 16; ++m)
+          if (8 * m < L) acc = acc + v[m];
+      }
+      acc = acc + __shfl_xor_sync(kFull, acc, 1);
+      acc = acc + __shfl_xor_sync(kFull, acc, 2);
+      acc = acc + __shfl_xor_sync(kFull, acc, 4);
+      if (act && k == 0) s.leaf_vals[leaf] = acc;
+    }
+  }
   // element-sum leaves for the non-fused layout (after a barrier)
   __device__ void leaves_if_unfused(const SumDev& s, const T* terms, bool square) {
     if (a.g.fused) return;
@@ -339,7 +374,7 @@ struct HessOps : ConvOps<T, FAST, RW> {
     const int H = a.g.H, W = a.g.W, C = a.g.C;
     this->foreach_pixel([&](int64_t i, int h, int w, int) {
       const T xc = ldcg(x + i);
-      const T d0 = this->has_below(h) ? ldcg(x + i + (int64_t)W * C) - xc : T(0);
+      const T d0 = this->below(h) ? ldcg(x + i + (int64_t)W * C) - xc : T(0);
       const T d1 = (w < W - 1) ? ldcg(x + i + C) - xc : T(0);
       const T s0 = d0 * d0 + nu2, s1 = d1 * d1 + nu2;
       a.WV[i] = nu2 / (s0 * sqrt(s0));
@@ -375,8 +410,8 @@ struct HessOps : ConvOps<T, FAST, RW> {
               // D^T (W . D v) at pixel i, image_forward_diff_adjoint order
               const T vc = ldcg(V + i);
               T t = T(0);
-              if (this->has_above(h)) t = t + ldcg(a.WV + i - rowS) * (vc - ldcg(V + i - rowS));
-              if (this->has_below(h)) t = t - ldcg(a.WV + i) * (ldcg(V + i + rowS) - vc);
+              if (this->above(h)) t = t + ldcg(a.WV + i - rowS) * (vc - ldcg(V + i - rowS));
+              if (this->below(h)) t = t - ldcg(a.WV + i) * (ldcg(V + i + rowS) - vc);
               if (w >= 1) t = t + ldcg(a.WH + i - C) * (vc - ldcg(V + i - C));
               if (w <= W - 2) t = t - ldcg(a.WH + i) * (ldcg(V + i + C) - vc);
               hv = hv + alpha * t;
@@ -427,7 +462,13 @@ struct HessOps : ConvOps<T, FAST, RW> {
 
   // lower_hess_diag (lower_solvers.py:74-80) into Out; TV part:
   // SmoothedTV.hess_diag (regularizers.py:185-199).
-  __device__ void hess_diag(const T* x, bool tv, T* Out) {
+  // the global-row TV edge AND inside the local array (a row slab's outer rows are ghosts)
+  __device__ __forceinline__ bool below(int h) const { return this->has_below(h) && h + 1 < a.g.H; }
+  __device__ __forceinline__ bool above(int h) const { return this->has_above(h) && h >= 1; }
+
+  // slab = true (row-slab CG setup): no floor; the max over the OWNED pixels
+  // goes to scal[0] (the ranks all-reduce it and floor in CM_SLAB_CG_INIT)
+  __device__ void hess_diag(const T* x, bool tv, T* Out, bool slab = false) {
     this->load_weights_sq(a.kern);
     const T nu = T(a.nu), nu2 = nu * nu, two = T(2), alpha = T(a.alpha);
     const int C = a.g.C, H = a.g.H, W = a.g.W;
@@ -453,14 +494,14 @@ struct HessOps : ConvOps<T, FAST, RW> {
               const T xc = ldcg(x + i);
               T t = T(0);
               // diag[:-1] += wv; diag[1:] += wv; diag[:, :-1] += wh; diag[:, 1:] += wh
-              if (this->has_below(h)) { const T dd = ldcg(x + i + rowS) - xc, s = dd * dd + nu2; t = t + nu2 / (s * sqrt(s)); }
-              if (this->has_above(h)) { const T dd = xc - ldcg(x + i - rowS), s = dd * dd + nu2; t = t + nu2 / (s * sqrt(s)); }
+              if (this->below(h)) { const T dd = ldcg(x + i + rowS) - xc, s = dd * dd + nu2; t = t + nu2 / (s * sqrt(s)); }
+              if (this->above(h)) { const T dd = xc - ldcg(x + i - rowS), s = dd * dd + nu2; t = t + nu2 / (s * sqrt(s)); }
               if (w <= W - 2) { const T dd = ldcg(x + i + C) - xc, s = dd * dd + nu2; t = t + nu2 / (s * sqrt(s)); }
               if (w >= 1) { const T dd = xc - ldcg(x + i - C), s = dd * dd + nu2; t = t + nu2 / (s * sqrt(s)); }
               d = d + alpha * t;
             }
             Out[i] = d;
-            mx = fmax(mx, (double)d);
+            if (!slab || this->tile_owned(h0)) mx = fmax(mx, (double)d);
           }
         }
       }
@@ -472,6 +513,11 @@ struct HessOps : ConvOps<T, FAST, RW> {
     double gmx = -INFINITY;
     for (int b = threadIdx.x; b < gridDim.x; b += blockDim.x) gmx = fmax(gmx, ldcg(a.s_t2.leaf_vals + b));
     gmx = block_max(gmx, this->red());
+    if (slab) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) a.scal[0] = gmx;
+      this->load_weights(a.kern);
+      return;
+    }
     const T fl = T(1e-12 * gmx + 1e-300);
     if (!a.nofloor) this->foreach_pixel([&](int64_t i, int, int, int) {
       const T d = ldcg(Out + i);
@@ -724,6 +770,84 @@ __global__ void __launch_bounds__(512, 1) conv_misc_kernel(const __grid_constant
       if (blockIdx.x == 0 && threadIdx.x == 0) a.scal[0] = acc;
       break;
     }
+    // ---- row-slab hypergradient (multigpu.SlabHypergradient): the steps of
+    // conv_cg_kernel / CM_UPPER / adp_mixed_T split at their reductions, over
+    // slab + ghosts, sums over the owned rows only (same tiles / leaves / trees
+    // as the unsplit plan, so the folded scalars are bitwise those of one GPU)
+    case CM_SLAB_CG_DIAG:
+      if (tv) { E.hess_weights(a.in0); E.gb.sync(); }
+      E.hess_diag(a.in0, tv, a.DIAG, true);
+      break;
+    case CM_SLAB_CG_INIT: {
+      const T fl = T(a.sL);
+      E.foreach_pixel([&](int64_t i, int, int, int) {
+        const T d = ldcg(a.DIAG + i);
+        a.DIAG[i] = T(1) / (d > fl ? d : fl);
+      });
+      E.foreach_pixel_sum([&](int64_t i, int, int, int) {
+        T r;
+        if (a.sflag) {
+          r = a.in0[i] - ldcg(a.HP + i);
+        } else {
+          a.out0[i] = T(0);
+          r = a.in0[i];
+        }
+        a.CR[i] = r;
+        const T sv = ldcg(a.DIAG + i) * r;
+        a.out1[i] = sv;
+        return (double)r * (double)sv;
+      }, a.s_t1);
+      E.foreach_pixel_sum([&](int64_t i, int, int, int) {
+        const double r = (double)ldcg(a.CR + i);
+        return r * r;
+      }, a.s_t2);
+      E.gb.sync();
+      E.phase1({&a.s_t1, &a.s_t2});
+      break;
+    }
+    case CM_SLAB_CG_HV:
+      if (a.sflag <= 1) {
+        E.hess_vec(SrcCGDir<T>{a.in0, a.in1, T(a.sbeta), a.sflag == 0}, a.out0, tv, a.HP, a.out0, nullptr, &a.s_t0);
+      } else if (a.sflag == 2) {
+        E.hess_vec(SrcLin<T>{a.in0}, a.out0, tv, a.HP, nullptr, a.in1, &a.s_t0);
+      } else {
+        E.hess_vec(SrcLin<T>{a.in0}, a.out0, tv, a.HP, nullptr, nullptr, nullptr);
+        break;
+      }
+      E.gb.sync();
+      E.phase1({&a.s_t0});
+      break;
+    case CM_SLAB_CG_UPD: {
+      const T ta = T(a.sbeta);
+      E.foreach_pixel_sum([&](int64_t i, int, int, int) {
+        const T p = ldcg(a.in0 + i);
+        a.out0[i] = ldcg(a.out0 + i) + ta * p;
+        const T r = ldcg(a.CR + i) - ta * ldcg(a.HP + i);
+        a.CR[i] = r;
+        const T sv = ldcg(a.DIAG + i) * r;
+        a.out1[i] = sv;
+        return (double)r * (double)sv;
+      }, a.s_t1);
+      E.foreach_pixel_sum([&](int64_t i, int, int, int) {
+        const double r = (double)ldcg(a.CR + i);
+        return r * r;
+      }, a.s_t2);
+      E.gb.sync();
+      E.phase1({&a.s_t1, &a.s_t2});
+      break;
+    }
+    case CM_SLAB_UPPER:
+      E.stage_corr(SrcLin<T>{a.in0}, false, a.R, a.ydat, T(1), nullptr);
+      E.gb.sync();
+      E.stage_corr(SrcLin<T>{a.R}, true, a.out0 ? a.out0 : a.G, nullptr, T(2), &a.s_t0);
+      E.slab_leaves(a.s_fit, SqOf<T>{a.R});
+      E.gb.sync();
+      E.phase1({&a.s_fit, &a.s_t0});
+      break;
+    case CM_SLAB_MIXED_PREP:
+      E.stage_corr(SrcLin<T>{a.in0}, false, a.R, a.ydat, T(1), nullptr);
+      E.stage_corr(SrcLin<T>{a.in1}, false, a.BP, nullptr, T(1), nullptr);
+      break;
     case CM_SLAB_GRAD:
       // g = lower_grad(x) partials (final gradient norm, lower_solvers.py:212)
       E.stageA(SrcLin<T>{a.in0}, a.R, a.ydat, tv, a.TV2, a.TVG, &a.s_fit, &a.s_tv);
@@ -740,8 +864,13 @@ __global__ void __launch_bounds__(512, 1) conv_misc_kernel(const __grid_constant
 // ---------------------------------------------------------------------------
 // kernel_gram_correlation (operators.py:198-220), summed over pairs:
 //   out[i,j,c] = sum_{h,w} xa[h+i-r, w+j-r, c] * va[h,w,c] (+ same for xb, vb)
-// Non-cooperative: work groups own fixed tile sets; per-group partials then a
-// fixed-order final reduction (deterministic, independent of the grid).
+// Non-cooperative.  Work groups are (tile row of KT GLOBAL image rows,
+// column block): group g = tr * cblocks + cb owns the 16x16 tiles of tile row
+// tr in columns [cb * per, (cb + 1) * per); per-group partials, then a
+// fixed-order final sum over the groups (deterministic, grid-independent).
+// A row slab (rows KT-aligned) computes exactly the groups of its owned tile
+// rows, so assembling the per-rank partial vectors and the same final sum is
+// bitwise the unsplit result.
 template <typename T>
 __global__ void __launch_bounds__(256) kgc_partial_kernel(const __grid_constant__ KgcArgs<T> a) {
   const ConvGeom& g = a.g;
@@ -750,9 +879,13 @@ __global__ void __launch_bounds__(256) kgc_partial_kernel(const __grid_constant_
   T* xs = reinterpret_cast<T*>(dsm());
   T* vs = xs + SHx * SWx;
   const int ntap = g.kh * g.kw;
-  const int thH = (g.H + KT - 1) / KT, thW = (g.W + KT - 1) / KT;
-  const int ntile = thH * thW;
+  const int thW = (g.W + KT - 1) / KT;
+  const int per = (thW + a.cblocks - 1) / a.cblocks;
   for (int grp = blockIdx.x; grp < a.ngroups; grp += gridDim.x) {
+    const int tr = grp / a.cblocks, cb = grp - tr * a.cblocks;
+    const int h0 = tr * KT - g.row0;            // local row of the tile row
+    if (h0 < g.own0 || h0 >= g.own1) continue;  // not this slab's (CTA-uniform)
+    const int tc0 = cb * per, tc1 = min(thW, tc0 + per);
     for (int c = 0; c < g.C; ++c) {
       double acc[12];
 #pragma unroll
@@ -761,8 +894,8 @@ __global__ void __launch_bounds__(256) kgc_partial_kernel(const __grid_constant_
         const T* X = pair ? a.xb : a.xa;
         const T* V = pair ? a.vb : a.va;
         if (!X) continue;
-        for (int tile = grp; tile < ntile; tile += a.ngroups) {
-          const int h0 = (tile / thW) * KT, w0 = (tile % thW) * KT;
+        for (int tc = tc0; tc < tc1; ++tc) {
+          const int w0 = tc * KT;
           __syncthreads();
           for (int e = threadIdx.x; e < SHx * SWx; e += blockDim.x) {
             const int r = e / SWx, q = e % SWx;
