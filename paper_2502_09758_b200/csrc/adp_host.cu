@@ -238,7 +238,7 @@ static void choose_tiles(const adp_plan_desc& d, int leafL, int& TH, int& TW, in
 }
 
 // Dynamic shared-memory layout (byte offsets; see ConvGeom).
-static size_t conv_smem(ConvGeom& g, int esize) {
+static size_t conv_smem(ConvGeom& g, int esize, size_t cap = 0) {
   const size_t nk = (size_t)g.kh * g.kw * g.C;
   size_t off = 64 * sizeof(double);                  // red
   g.o_ws = (int)off;
@@ -256,6 +256,16 @@ static size_t conv_smem(ConvGeom& g, int esize) {
   g.o_tm = (int)(R0 + np * pa);
   g.o_sv = (int)R0;
   const size_t region = std::max(np * (pa + tm), (size_t)(kTreeStage + 512) * sizeof(double));
+  g.o_q = 0;
+  if (g.fuseCA && g.rwb == 4) {
+    // TV neighbour scratch of the pipelined stages: [C][TH+1][TW] + [C][TH][TW+1]
+    const size_t q = ((size_t)g.C * ((g.TH + 1) * g.TW + g.TH * (g.TW + 1)) * esize + 15) & ~size_t(15);
+    const char* ev = getenv("ADP_PIPE");    // ADP_PIPE=0: the unpipelined stages (A/B)
+    if (!(ev && atoi(ev) == 0) && R0 + region + q + 2048 <= cap) {
+      g.o_q = (int)(R0 + region);
+      return R0 + region + q;
+    }
+  }
   return R0 + region;
 }
 
@@ -380,7 +390,7 @@ static int conv_plan_init(PlanImpl& P) {
     const char* ev = getenv("ADP_FUSECA");
     if ((ev && atoi(ev) == 0) || conv_smem(g, P.esize) + 8192 > smem_optin) g.fuseCA = 0;
   }
-  P.smem = conv_smem(g, P.esize);
+  P.smem = conv_smem(g, P.esize, smem_optin);
   if (P.smem > smem_optin) return fail(ADP_ERR_UNSUPPORTED, "tile + halo exceeds shared memory; use a smaller tile");
   if (P.probe_only) return ADP_OK;   // adp_plan_probe: geometry only, no device memory
 

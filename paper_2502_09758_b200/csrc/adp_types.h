@@ -82,6 +82,7 @@ struct ConvGeom {
   unsigned magicRow;       // ceil(2^32 / rowE): row of a flattened tile-box index
   int o_ws, o_wf, o_pa, o_pq, o_tm, o_sv;   // byte offsets in dynamic smem
   int o_pa2;               // second plane region (fuseCA)
+  int o_q;                 // TV neighbour (Q) scratch of the pipelined RW = 4 stages (0: not pipelined)
   int fuseCA;              // 1: candidate value + speculative next value/grad share one stage
   int64_t N;               // H*W*C
   int64_t Ng;              // global element count (Hg*W*C; = N unless a row slab)

@@ -301,6 +301,31 @@ struct Conv {
     cp_async_wait_all();
   }
 
+  // Asynchronous copy (LDGSTS) of the tile box of a plain array into a plane
+  // region, zero-filled outside the image: warps own box rows (contiguous in
+  // global memory), lanes walk the row's interleaved elements.  The caller
+  // commits the group and waits before the barrier that publishes it.
+  __device__ void load_async(int h0, int w0, const T* x, T* dst) const {
+    const int C = nC(), H = a.g.H, W = a.g.W, SH = a.g.SH, SWP = a.g.SWP;
+    const unsigned mC = a.g.magicC;
+    const int rowE = (a.g.TW + 2 * a.g.rw + 2) * C, planeSz = SH * SWP;
+    const int gh0 = h0 - a.g.rh - 1, gw0 = w0 - a.g.rw - 1;
+    const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int sr = threadIdx.x >> 5; sr < SH; sr += nw) {
+      const int gh = gh0 + sr;
+      const bool rowok = gh >= 0 && gh < H;
+      const int64_t rowbase = ((int64_t)(rowok ? gh : 0) * W + gw0) * C;
+      T* drow = dst + sr * SWP;
+      for (int e = lane; e < rowE; e += 32) {
+        const int px = C == 1 ? e : (int)(((unsigned long long)(unsigned)e * mC) >> 20);
+        const int c = e - px * C;
+        const bool ok = rowok && (unsigned)(gw0 + px) < (unsigned)W;
+        cp_async_el(drow + c * planeSz + sk(px), ok ? x + rowbase + e : x, ok);
+      }
+    }
+  }
+  __device__ __forceinline__ T* qs() const { return reinterpret_cast<T*>(dsm() + a.g.o_q); }
+
   // ---- register-blocked correlation: RW consecutive outputs (row ty, cols
   // tx*RW..) of the thread's channel plane with stencil w (kh x kw).  Per
   // output the taps are accumulated in row-major order starting from 0.
@@ -698,6 +723,117 @@ struct Conv {
       if (sgg) tile_partial(*sgg, tile, part);
       ADP_SUB(5);
       ADP_SUB_FLUSH(6);
+    }
+  }
+
+  // Stage B, pipelined (RW = 4 plans with two plane regions and the Q
+  // scratch): the R tile boxes alternate between the two regions, the copy
+  // of tile k+1 in flight while tile k is computed; besides g and the first
+  // candidate xc = y - g / L it writes the next extrapolation point
+  // y' = xc + betaN (xc - x) to Yn (SrcExtrap's expression, exact), which
+  // stageCA_pipe then copies as a plain box.
+  __device__ void stageB_pipe(const T* Rin, bool tv, const T* TVGin, T* Gout, const SumDev* sgg, const T* Xs,
+                              const T* XPs, T beta, T L, T* Xc, T betaN, T* Yn) {
+    const T two = T(2), alpha = T(a.alpha);
+    const int H = a.g.H, W = a.g.W;
+    const size_t co = (size_t)ch * a.g.SH * a.g.SWP;
+    int tile = blockIdx.x;
+    if (tile < a.g.nTiles) {
+      int h0, w0;
+      tile_origin(tile, h0, w0);
+      load_async(h0, w0, Rin, pa());
+    }
+    cp_commit();
+    for (int k = 0; tile < a.g.nTiles; tile += gridDim.x, ++k) {
+      int h0, w0;
+      tile_origin(tile, h0, w0);
+      const T* cur = (k & 1) ? pa2() : pa();
+      const int nt = tile + gridDim.x;
+      if (nt < a.g.nTiles) {
+        int h1, w1;
+        tile_origin(nt, h1, w1);
+        load_async(h1, w1, Rin, (k & 1) ? pa() : pa2());
+      }
+      cp_commit();
+      const int h = h0 + ty;
+      T tpre[RW], xpre[RW], xppre[RW];
+#pragma unroll
+      for (int o = 0; o < RW; ++o) {
+        const int w = w0 + tx * RW + o;
+        tpre[o] = xpre[o] = xppre[o] = T(0);
+        if (h < H && w < W) {
+          const int64_t i = gidx(h, w, ch);
+          if (tv) tpre[o] = ldcg(TVGin + i);
+          xpre[o] = ldcg(Xs + i);
+          xppre[o] = ldcg(XPs + i);
+        }
+      }
+      cp_wait<1>();
+      __syncthreads();
+      double part = 0.0;
+      T acc[RW];
+      stencil(cur + co, wf() + ch * a.g.kh * a.g.kw, acc);
+#pragma unroll
+      for (int o = 0; o < RW; ++o) {
+        const int w = w0 + tx * RW + o;
+        if (h < H && w < W) {
+          const int64_t i = gidx(h, w, ch);
+          T gv = two * acc[o];
+          if (tv) gv = gv + alpha * tpre[o];
+          Gout[i] = gv;
+          part += (double)gv * (double)gv;
+          const T xc = (xpre[o] + beta * (xpre[o] - xppre[o])) - gv / L;
+          Xc[i] = xc;
+          Yn[i] = xc + betaN * (xc - xpre[o]);
+        }
+      }
+      if (sgg) tile_partial(*sgg, tile, part);
+      __syncthreads();   // every warp is done with `cur` before it receives tile k+2
+    }
+  }
+
+  // Stage CA, pipelined (see stageCA): the candidate's box (Xc) and the next
+  // extrapolation point's box (Yn, written by stageB_pipe) are plain
+  // asynchronous copies: Yn(k) lands during the candidate pass of tile k and
+  // Xc(k+1) during its speculative stage-A pass; tileA publishes its TV
+  // neighbour values through the Q scratch (the first region is receiving
+  // the next box).  Same arithmetic and leaves as stageCA.
+  __device__ void stageCA_pipe(const T* Xc, const T* Yn, const T* Xold, const T* Gin, bool tv, T* Rout, T* TVGout,
+                               const SumDev* sdot, const SumDev* sfitc, const SumDev* stvc, const SumDev* sfit2,
+                               const SumDev* stv2) {
+    int tile = blockIdx.x;
+    if (tile < a.g.nTiles) {
+      int h0, w0;
+      tile_origin(tile, h0, w0);
+      load_async(h0, w0, Xc, pa());
+    }
+    cp_commit();
+    const int koff = (int)(a.g.Ng / a.g.leafL);
+    for (; tile < a.g.nTiles; tile += gridDim.x) {
+      int h0, w0;
+      tile_origin(tile, h0, w0);
+      cp_wait<0>();
+      __syncthreads();                       // Xc(k) landed; the second region is free
+      load_async(h0, w0, Yn, pa2());
+      cp_commit();
+      T ypre[RW], gpre[RW], xopre[RW];
+      prefetch_c(h0, w0, Gin, Xold, true, ypre, gpre, xopre);
+      const double part = tileC(pa(), h0, w0, ypre, gpre, xopre, nullptr, tv, nullptr, nullptr, true, true);
+      tile_partial(*sdot, tile, part);       // its barriers: every warp is done reading the first region
+      tile_leaves(h0, w0, tv ? 3 : 1, sfitc, stvc, koff);
+      __syncthreads();
+      const int nt = tile + gridDim.x;
+      if (nt < a.g.nTiles) {
+        int h1, w1;
+        tile_origin(nt, h1, w1);
+        load_async(h1, w1, Xc, pa());
+      }
+      cp_commit();
+      cp_wait<1>();
+      __syncthreads();                       // Yn(k) landed
+      tileA(pa2(), qs(), 3, h0, w0, ypre, Rout, tv, nullptr, TVGout, true);
+      tile_leaves(h0, w0, tv ? 3 : 1, sfit2, stv2, koff, 3);
+      __syncthreads();                       // the second region is read before Yn(k+1) is issued
     }
   }
 

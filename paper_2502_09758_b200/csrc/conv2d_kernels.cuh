@@ -206,6 +206,9 @@ __global__ void __launch_bounds__(KS > 0 ? kSolveKSThreads : MAXT, 1) conv_solve
   // iteration skips stage A and one grid barrier.  Stage-A sums alternate
   // between two sets (par).  Same arithmetic as the unfused order.
   const bool spec = a.adaptive && tv && g.fuseCA && a.method == M_AGD;
+  // pipelined stages (asynchronous double-buffered tile copies; RW = 4 plans
+  // with the Q scratch): stage B also writes the next extrapolation point to P[0]
+  const bool pipe = KS == 0 && spec && g.o_q > 0;
   bool a_ready = false;
   int par = 0;
 
@@ -237,7 +240,13 @@ __global__ void __launch_bounds__(KS > 0 ? kSolveKSThreads : MAXT, 1) conv_solve
         ADP_TRACE(t, 1);
       }
       ADP_TRACE(t, 2);
-      E.stageB(a.R, tv, a.TVG, a.G, &a.s_t0, a.X[ix], a.X[ixp], tb, T(L_try), a.X[ic]);
+      if (pipe) {
+        const double t_next2 = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t_mom * t_mom));   // as in the stage-CA branch
+        const double beta2 = (t_mom - 1.0) / t_next2;
+        E.stageB_pipe(a.R, tv, a.TVG, a.G, &a.s_t0, a.X[ix], a.X[ixp], tb, T(L_try), a.X[ic], T(beta2), a.P[0]);
+      } else {
+        E.stageB(a.R, tv, a.TVG, a.G, &a.s_t0, a.X[ix], a.X[ixp], tb, T(L_try), a.X[ic]);
+      }
       E.leaves_if_unfused(a.s_fit, a.R, true);
       if (tv) E.leaves_if_unfused(a.s_tv, a.TV2, false);
     } else {
@@ -251,8 +260,12 @@ __global__ void __launch_bounds__(KS > 0 ? kSolveKSThreads : MAXT, 1) conv_solve
       // next iteration's momentum if this one ends without restart
       const double t_next2 = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t_mom * t_mom));
       const double beta2 = (t_mom - 1.0) / t_next2;
-      E.stageCA(a.X[ic], a.X[ix], T(beta2), a.G, tv, a.R, a.TVG, &a.s_t1, &a.s_fitc, &a.s_tvc,
-                par ? &a.s_fit : &a.s_fit2, par ? &a.s_tv : &a.s_tv2);
+      if (pipe)
+        E.stageCA_pipe(a.X[ic], a.P[0], a.X[ix], a.G, tv, a.R, a.TVG, &a.s_t1, &a.s_fitc, &a.s_tvc,
+                       par ? &a.s_fit : &a.s_fit2, par ? &a.s_tv : &a.s_tv2);
+      else
+        E.stageCA(a.X[ic], a.X[ix], T(beta2), a.G, tv, a.R, a.TVG, &a.s_t1, &a.s_fitc, &a.s_tvc,
+                  par ? &a.s_fit : &a.s_fit2, par ? &a.s_tv : &a.s_tv2);
       ++vals;
     } else if (a.adaptive) {
       E.value_cand(SrcLin<T>{a.X[ic]}, tv, nullptr, a.G, a.X[ix], &a.s_t1);

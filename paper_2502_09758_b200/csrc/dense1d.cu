@@ -50,8 +50,12 @@ struct Dense {
     off += (size_t)(2 * a.s_n.nLeaves + 2) * sizeof(double);
     off = (off + 15) & ~size_t(15);
     for (int k = 0; k < kDenseVecs; ++k) {
-      v[k] = reinterpret_cast<T*>(smem + off);
-      off += ((size_t)n * sizeof(T) + 15) & ~size_t(15);
+      if (a.gvec) {   // large n: this CTA's private copies in global memory (L1/L2-resident)
+        v[k] = a.gvec + ((int64_t)blockIdx.x * kDenseVecs + k) * a.vpitch;
+      } else {
+        v[k] = reinterpret_cast<T*>(smem + off);
+        off += ((size_t)n * sizeof(T) + 15) & ~size_t(15);
+      }
     }
     if (a.b_smem && a.B) {
       T* bs = reinterpret_cast<T*>(smem + off);
@@ -637,6 +641,8 @@ int dense_fail(int code, const char* m);  // adp_host.cu
 struct DenseState {
   int G, rows_per, b_smem;
   size_t smem;
+  void* d_gvec;      // large n: replicated vectors in global memory
+  int64_t vpitch;
   SumHost sn;
   int* d_progs;
   int64_t* d_leaf;
@@ -666,11 +672,15 @@ int dense_plan_init(PlanImpl& P) {
   const size_t es = (size_t)P.esize;
   size_t base = 64 * sizeof(double) + (size_t)(2 * S->sn.nLeaves + 2) * sizeof(double);
   base = (base + 15) & ~size_t(15);
-  base += (size_t)kDenseVecs * (((size_t)n * es + 15) & ~size_t(15));
-  if (base > (size_t)optin) return dense_fail(ADP_ERR_UNSUPPORTED, "dense1d signal too long for shared memory");
+  const size_t vecs = (size_t)kDenseVecs * (((size_t)n * es + 15) & ~size_t(15));
+  const bool gvec = base + vecs > (size_t)optin;   // large n: vectors in global memory instead of smem
+  if (!gvec) base += vecs;
   int G = std::max(1, std::min((n + 15) / 16, P.sm_count));
   int rows_per = (n + G - 1) / G;
   G = (n + rows_per - 1) / rows_per;
+  S->d_gvec = nullptr;
+  S->vpitch = (int64_t)((n + 1) & ~1);
+  if (gvec) DCK(cudaMalloc(&S->d_gvec, (size_t)G * kDenseVecs * S->vpitch * es));
   const size_t bslice = (size_t)rows_per * n * es;
   S->b_smem = (base + bslice <= (size_t)optin) ? 1 : 0;
   S->smem = base + (S->b_smem ? bslice : 0);
@@ -716,6 +726,7 @@ void dense_plan_free(PlanImpl& P) {
   cudaFree(S->d_leaf);
   cudaFree(S->d_rowbuf);
   cudaFree(S->d_part);
+  if (S->d_gvec) cudaFree(S->d_gvec);
   delete S;
   P.ws[0] = nullptr;
 }
@@ -731,6 +742,8 @@ static DenseArgs<T> dense_base(PlanImpl& P) {
   a.b_smem = S->b_smem;
   a.rowbuf = (T*)S->d_rowbuf;
   a.part = S->d_part;
+  a.gvec = (T*)S->d_gvec;
+  a.vpitch = S->vpitch;
   a.s_n.nLeaves = S->sn.nLeaves;
   a.s_n.nSub = 1;
   a.s_n.sub_own0 = 0;

@@ -29,6 +29,9 @@ struct DenseArgs {
   int nofloor;
   const T* in0; const T* in1; T* out0; T* out1;
   double pstep, pthr; int piters;   // prox_grad_iterations (DM_PROX)
+  T* gvec;                       // non-null: the replicated vectors live in global memory (large n),
+                                 //   CTA b's kDenseVecs vectors at gvec + (b * kDenseVecs + k) * vpitch
+  int64_t vpitch;
 };
 
 struct DenseKernelSet {
