@@ -267,6 +267,17 @@ def set_tile(shape_key, tile):
     _tile_override[shape_key] = tile
 
 
+def host_fingerprint(arr) -> int:
+    """Cheap content tag of a host array for device-copy caches: the bytes of
+    4,096 strided samples (plus shape and address).  Catches reassignment and
+    the usual in-place edits (y[:] = ..., y *= s) without reading the whole
+    array; an edit that touches none of the sampled elements is not seen."""
+    a = np.asarray(arr)
+    flat = a.reshape(-1) if a.flags.c_contiguous else np.ascontiguousarray(a).reshape(-1)
+    step = max(1, flat.size // 4096)
+    return hash((a.shape, a.__array_interface__["data"][0], flat[::step].tobytes()))
+
+
 def current_device() -> int:
     """CUDA device of the calling thread: every device-side cache is keyed by it."""
     import torch

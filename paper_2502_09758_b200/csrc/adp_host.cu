@@ -245,9 +245,10 @@ static size_t conv_smem(ConvGeom& g, int esize, size_t cap = 0) {
   off += (nk * esize + 15) & ~size_t(15);
   g.o_wf = (int)off;
   off += (nk * esize + 15) & ~size_t(15);
+  off = (off + 127) & ~size_t(127);
   const size_t R0 = off;
   g.QP = 0;   // TV Q values are staged through registers into the plane region
-  const size_t pa = ((size_t)g.C * g.SH * g.SWP * esize + 15) & ~size_t(15);
+  const size_t pa = ((size_t)g.C * g.SH * g.SWP * esize + 127) & ~size_t(127);   // 128 B: TMA destinations
   const size_t tm = g.fused ? (size_t)3 * g.TH * g.TW * g.C * sizeof(double) : 0;
   const int np = g.fuseCA ? 2 : 1;   // fuseCA: two plane regions, six term buffers
   g.o_pa = (int)R0;
@@ -300,6 +301,36 @@ static int setup_kernel(PlanImpl& P, KernelInfo& k, const void* fn, int threads,
   CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fn, threads, smem));
   if (nb <= 0) return fail(ADP_ERR_UNSUPPORTED, "kernel does not fit on an SM (smem/registers)");
   k.grid = std::max(1, std::min(max_grid, nb * P.sm_count));
+  return ADP_OK;
+}
+
+// 2-D TMA descriptors (W inner, H outer; float64) of the plan's workspace
+// images X[0..2], R, P[0]: box (SWPt, SH), zero fill outside the image.
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static int build_tmaps(PlanImpl& P) {
+  static EncodeTiledFn enc = nullptr;
+  if (!enc) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+      return ADP_ERR_UNSUPPORTED;
+    enc = (EncodeTiledFn)fn;
+  }
+  const ConvGeom& g = P.g;
+  if (g.SWPt > 256 || g.SH > 256 || ((size_t)g.W * 8) % 16) return ADP_ERR_UNSUPPORTED;
+  const int idx[5] = {0, 1, 2, 3, 10};   // X[0..2], R, P[0] (ws indices, conv_base)
+  for (int k = 0; k < 5; ++k) {
+    cuuint64_t dims[2] = {(cuuint64_t)g.W, (cuuint64_t)g.H};
+    cuuint64_t strides[1] = {(cuuint64_t)g.W * sizeof(double)};
+    cuuint32_t box[2] = {(cuuint32_t)g.SWPt, (cuuint32_t)g.SH};
+    cuuint32_t es[2] = {1, 1};
+    if (enc(&P.tm[k], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, P.ws[idx[k]], dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return ADP_ERR_UNSUPPORTED;
+  }
   return ADP_OK;
 }
 
@@ -359,6 +390,7 @@ static int conv_plan_init(PlanImpl& P) {
   g.SH = g.TH + 2 * g.rh + 2;
   const int SWL = g.TW + 2 * g.rw + 2;
   g.SWP = kRWp == 1 ? SWL + 1 : SWL + SWL / kRWp + 1;
+  g.SWPt = (SWL + 2 + 1) & ~1;   // dense TMA box: one extra column on each side, even pitch
   {
     const unsigned long long rowE = (unsigned long long)SWL * g.C;
     g.magicRow = (unsigned)(((1ull << 32) + rowE - 1) / rowE);
@@ -518,8 +550,16 @@ static int conv_plan_init(PlanImpl& P) {
   {
     const char* ev = getenv("ADP_K9");
     if (g.C == 1 && g.kh == 9 && g.kw == 9 && g.rwb == 2 && g.threads <= kSolveKSThreads &&
-        P.d.dtype == ADP_DTYPE_F64 && !(ev && atoi(ev) == 0))
+        P.d.dtype == ADP_DTYPE_F64 && !(ev && atoi(ev) == 0)) {
       ks.solve = conv_solve_k9(P.d.mode == ADP_MODE_FAST);
+      // TMA tile boxes for the c2 kernel (ADP_TMA=0: the LDS-fed loaders)
+      const char* et = getenv("ADP_TMA");
+      if (!(et && atoi(et) == 0) && !slab && (size_t)g.SH * g.SWPt <= (size_t)g.SH * g.SWP &&
+          build_tmaps(P) == ADP_OK) {
+        P.tma = 1;
+        ks.solve = conv_solve_k9_tma(P.d.mode == ADP_MODE_FAST);
+      }
+    }
     else if (g.rwb == 4 && g.threads <= kSolveT384 && !(getenv("ADP_T384") && atoi(getenv("ADP_T384")) == 0))
       ks.solve = conv_solve_t384(P.d.dtype, P.d.mode == ADP_MODE_FAST);
   }
@@ -547,6 +587,7 @@ static ConvArgs<T> conv_base(PlanImpl& P) {
   a.s_fit = P.s_fit; a.s_tv = P.s_tv; a.s_fitc = P.s_fitc; a.s_tvc = P.s_tvc;
   a.s_t0 = P.s_t0; a.s_t1 = P.s_t1; a.s_t2 = P.s_t2;
   a.s_fit2 = P.s_fit2; a.s_tv2 = P.s_tv2;
+  if (P.tma) std::memcpy(a.tm, P.tm, sizeof(a.tm));
   a.bar = P.d_bar;
   a.sres = P.d_sres;
   a.cres = P.d_cres;

@@ -1,5 +1,6 @@
 // Host-side plan: geometry, workspace and deterministic-sum programs.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <string>
@@ -63,6 +64,8 @@ struct PlanImpl {
   double* d_kgc_part = nullptr;
   int kgc_groups = 0;
   int kgc_cblocks = 1;
+  int tma = 0;                  // KS = 9 solve kernel with TMA tile boxes (tm[] valid)
+  CUtensorMap tm[5];            // X[0..2], R, P[0]
   // pinned host staging
   SolveOut* h_sres = nullptr;
   CGOut* h_cres = nullptr;

@@ -83,6 +83,7 @@ struct ConvGeom {
   int o_ws, o_wf, o_pa, o_pq, o_tm, o_sv;   // byte offsets in dynamic smem
   int o_pa2;               // second plane region (fuseCA)
   int o_q;                 // TV neighbour (Q) scratch of the pipelined RW = 4 stages (0: not pipelined)
+  int SWPt;                // dense plane pitch of TMA boxes (TW + 2 rw + 4, even)
   int fuseCA;              // 1: candidate value + speculative next value/grad share one stage
   int64_t N;               // H*W*C
   int64_t Ng;              // global element count (Hg*W*C; = N unless a row slab)

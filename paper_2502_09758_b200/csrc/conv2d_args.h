@@ -1,5 +1,6 @@
 // Kernel-argument block of the depthwise 2-D engine (host + device).
 #pragma once
+#include <cuda.h>   // CUtensorMap
 #include "adp_types.h"
 
 namespace adp {
@@ -82,6 +83,9 @@ struct ConvArgs {
   int sflag;               // row-slab CG steps: variant (see CM_SLAB_CG_*)
   unsigned long long* trace;  // optional phase timestamps (CTA 0): [iter][16] %globaltimer ns
   const T* in0; const T* in1; T* out0; T* out1;
+  // TMA descriptors of the plan's workspace images (KS = 9 single-channel
+  // solve kernel): X[0..2], R, P[0] (the next extrapolation point)
+  CUtensorMap tm[5];
 };
 
 template <typename T>
@@ -111,6 +115,8 @@ ConvKernelSet conv_kernels_f64s_rw1();
 ConvKernelSet conv_kernels_f64f_rw1();
 // solve kernels specialised to a 9x9 stencil at RW = 2 (c2), float64
 const void* conv_solve_k9(int fast);
+// the same with TMA tile boxes (dense plane layout, LDS.128 windows)
+const void* conv_solve_k9_tma(int fast);
 // thread bound of the compile-time-stencil solve kernel (the host selects it
 // only for CTAs of at most this many threads)
 constexpr int kSolveKSThreads = 256;

@@ -116,7 +116,7 @@ template <typename T> struct Plain {
 // KS > 0: the stencil size is a compile-time constant (the latency-bound c2
 // solve kernel is instantiated with KS = 9 so it carries no other stencil
 // variant); KS = 0: runtime dispatch over the unrolled sizes + generic loop.
-template <typename T, bool FAST, int RW, int KS = 0>
+template <typename T, bool FAST, int RW, int KS = 0, bool TMA = false>
 struct Conv {
   static_assert((RW & (RW - 1)) == 0, "RW must be a power of two");
   static constexpr int kShift = RW == 1 ? 0 : RW == 2 ? 1 : RW == 4 ? 2 : 3;
@@ -126,8 +126,13 @@ struct Conv {
   int ch, ty, tx;                // this thread's channel, tile row, column group
 
   __device__ __forceinline__ int nC() const { return KS > 0 ? 1 : a.g.C; }
-  __device__ static __forceinline__ int sk(int col) { return RW == 1 ? col : col + (col >> kShift); }
-  __device__ static __forceinline__ int skr(int m) { return RW == 1 ? m : m + (m >> kShift); }
+  // plane column of box column `col` (box column 0 = image column w0 - rw - 1):
+  // skewed (one pad per RW elements) for LDS-fed boxes; dense and shifted by
+  // one for TMA boxes (the TMA box starts at w0 - rw - 2 so the RW = 2 windows
+  // start on 16-byte boundaries: LDS.128 window loads, conflict-free)
+  __device__ static __forceinline__ int sk(int col) { return TMA ? col + 1 : RW == 1 ? col : col + (col >> kShift); }
+  __device__ static __forceinline__ int skr(int m) { return TMA ? m : RW == 1 ? m : m + (m >> kShift); }
+  __device__ __forceinline__ int swp() const { return TMA ? a.g.SWPt : a.g.SWP; }
 
   __device__ explicit Conv(const ConvArgs<T>& a_) : a(a_) {
     const int tpr = a.g.TW / RW;
@@ -147,7 +152,7 @@ struct Conv {
   __device__ __forceinline__ T* pa2() const { return reinterpret_cast<T*>(dsm() + a.g.o_pa2); }
   __device__ __forceinline__ double* tm() const { return reinterpret_cast<double*>(dsm() + a.g.o_tm); }
   __device__ __forceinline__ double* sv() const { return reinterpret_cast<double*>(dsm() + a.g.o_sv); }
-  __device__ __forceinline__ T* plane(int c) const { return pa() + (size_t)c * a.g.SH * a.g.SWP; }
+  __device__ __forceinline__ T* plane(int c) const { return pa() + (size_t)c * a.g.SH * swp(); }
 
   // ---- weights: ws[c][i][j] = kern[i][j][c] (|w| <= eps -> 0), wf flipped
   __device__ void load_weights(const T* kern) {
@@ -202,7 +207,7 @@ struct Conv {
     const int px = (int)(((unsigned long long)e * a.g.magicC) >> 20);
     const int c = e - px * C;
     const int gh = gh0 + sr, gw = gw0 + px;
-    off = c * a.g.SH * a.g.SWP + sr * a.g.SWP + sk(px);
+    off = c * a.g.SH * swp() + sr * swp() + sk(px);
     gi = (gh >= 0 && gh < a.g.H && gw >= 0 && gw < a.g.W) ? ((int64_t)gh * a.g.W + gw) * C + c : -1;
   }
 
@@ -212,7 +217,7 @@ struct Conv {
   static constexpr int kJ = 8;   // lane steps per row handled per pass (rows longer than 256 loop)
   template <class Src>
   __device__ void load_full(int h0, int w0, const Src& src, T* dst_region = nullptr) const {
-    const int C = nC(), H = a.g.H, W = a.g.W, SH = a.g.SH, SWP = a.g.SWP;
+    const int C = nC(), H = a.g.H, W = a.g.W, SH = a.g.SH, SWP = swp();
     const unsigned mC = a.g.magicC;
     const int rowE = (a.g.TW + 2 * a.g.rw + 2) * C, planeSz = SH * SWP;
     const int gh0 = h0 - a.g.rh - 1, gw0 = w0 - a.g.rw - 1;
@@ -306,7 +311,7 @@ struct Conv {
   // global memory), lanes walk the row's interleaved elements.  The caller
   // commits the group and waits before the barrier that publishes it.
   __device__ void load_async(int h0, int w0, const T* x, T* dst) const {
-    const int C = nC(), H = a.g.H, W = a.g.W, SH = a.g.SH, SWP = a.g.SWP;
+    const int C = nC(), H = a.g.H, W = a.g.W, SH = a.g.SH, SWP = swp();
     const unsigned mC = a.g.magicC;
     const int rowE = (a.g.TW + 2 * a.g.rw + 2) * C, planeSz = SH * SWP;
     const int gh0 = h0 - a.g.rh - 1, gw0 = w0 - a.g.rw - 1;
@@ -326,6 +331,57 @@ struct Conv {
   }
   __device__ __forceinline__ T* qs() const { return reinterpret_cast<T*>(dsm() + a.g.o_q); }
 
+  // window of NW box elements starting one past the row base: scalar loads
+  // on the skewed layout; 16-byte loads on the (aligned) dense TMA layout
+  template <int NW>
+  __device__ __forceinline__ void load_win(const T* row, T (&win)[NW]) const {
+    if constexpr (TMA && sizeof(T) == 8 && NW % 2 == 0 && RW % 2 == 0) {
+      const double2* r2 = reinterpret_cast<const double2*>(row + 1);
+#pragma unroll
+      for (int m = 0; m < NW / 2; ++m) {
+        const double2 v = r2[m];
+        win[2 * m] = v.x;
+        win[2 * m + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int m = 0; m < NW; ++m) win[m] = row[skr(1 + m)];
+    }
+  }
+
+  // ---- TMA tile boxes (KS = 9 single-channel kernel): one 2-D tensor copy
+  // per box (cp.async.bulk.tensor, zero fill outside the image), completion on
+  // an mbarrier.  Thread 0 issues; every thread waits on the barrier's phase.
+  __device__ __forceinline__ static unsigned smem_u32(const void* p) {
+    return (unsigned)__cvta_generic_to_shared(p);
+  }
+  __device__ __forceinline__ void tma_box(const CUtensorMap* tm, int h0, int w0, T* dst, unsigned long long* mbar) const {
+    if (threadIdx.x == 0) {
+      const unsigned bar = smem_u32(mbar);
+      const unsigned bytes = (unsigned)(a.g.SH * a.g.SWPt * sizeof(T));
+      // generic-proxy writes (other CTAs' global stores before the grid barrier, this
+      // CTA's earlier reads of dst) ordered before the async-proxy copy
+      asm volatile("fence.proxy.async;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+      asm volatile(
+          "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+              smem_u32(dst)),
+          "l"(tm), "r"(w0 - a.g.rw - 2), "r"(h0 - a.g.rh - 1), "r"(bar)
+          : "memory");
+    }
+  }
+  __device__ __forceinline__ static void tma_wait(unsigned long long* mbar, unsigned phase) {
+    const unsigned bar = smem_u32(mbar);
+    unsigned done = 0;
+    while (!done) {
+      asm volatile(
+          "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(done)
+          : "r"(bar), "r"(phase)
+          : "memory");
+    }
+  }
+
   // ---- register-blocked correlation: RW consecutive outputs (row ty, cols
   // tx*RW..) of the thread's channel plane with stencil w (kh x kw).  Per
   // output the taps are accumulated in row-major order starting from 0.
@@ -335,14 +391,13 @@ struct Conv {
   // order as the generic loop.
   template <int K>
   __device__ __forceinline__ void stencil_k(const T* __restrict__ pl, const T* __restrict__ w, T (&acc)[RW]) const {
-    const int SWP = a.g.SWP;
+    const int SWP = swp();
     const T* base = pl + (ty + 1) * SWP + sk(tx * RW);
 #pragma unroll
     for (int i = 0; i < K; ++i) {
       const T* row = base + i * SWP;
       T win[K + RW - 1];
-#pragma unroll
-      for (int m = 0; m < K + RW - 1; ++m) win[m] = row[skr(1 + m)];
+      load_win<K + RW - 1>(row, win);
 #pragma unroll
       for (int j = 0; j < K; ++j) {
         const T wt = w[i * K + j];
@@ -358,7 +413,7 @@ struct Conv {
   template <int K>
   __device__ __forceinline__ void stencil_k2(const T* __restrict__ pl1, const T* __restrict__ pl2,
                                              const T* __restrict__ w, T (&acc1)[RW], T (&acc2)[RW]) const {
-    const int SWP = a.g.SWP;
+    const int SWP = swp();
     const int b = (ty + 1) * SWP + sk(tx * RW);
 #pragma unroll
     for (int o = 0; o < RW; ++o) acc1[o] = acc2[o] = T(0);
@@ -367,11 +422,8 @@ struct Conv {
       const T* row1 = pl1 + b + i * SWP;
       const T* row2 = pl2 + b + i * SWP;
       T win1[K + RW - 1], win2[K + RW - 1];
-#pragma unroll
-      for (int m = 0; m < K + RW - 1; ++m) {
-        win1[m] = row1[skr(1 + m)];
-        win2[m] = row2[skr(1 + m)];
-      }
+      load_win<K + RW - 1>(row1, win1);
+      load_win<K + RW - 1>(row2, win2);
 #pragma unroll
       for (int j = 0; j < K; ++j) {
         const T wt = w[i * K + j];
@@ -385,7 +437,7 @@ struct Conv {
   }
   // forward taps over two regions; the compile-time-K kernels share the tap loads
   __device__ __forceinline__ void stencil_fwd_pair(const T* pr1, const T* pr2, T (&acc1)[RW], T (&acc2)[RW]) const {
-    const size_t co = (size_t)ch * a.g.SH * a.g.SWP;
+    const size_t co = (size_t)ch * a.g.SH * swp();
     const T* w = ws() + ch * a.g.kh * a.g.kw;
     if constexpr (KS > 0) {
       stencil_k2<KS>(pr1 + co, pr2 + co, w, acc1, acc2);
@@ -399,7 +451,7 @@ struct Conv {
   // unrolled so its window and taps are loaded together.
   template <int K>
   __device__ __forceinline__ void stencil_kr(const T* __restrict__ pl, const T* __restrict__ w, T (&acc)[RW]) const {
-    const int SWP = a.g.SWP;
+    const int SWP = swp();
     const T* base = pl + (ty + 1) * SWP + sk(tx * RW);
 #pragma unroll 1
     for (int i = 0; i < K; ++i) {
@@ -424,7 +476,7 @@ struct Conv {
       stencil_k<KS>(pl, w, acc);
       return;
     }
-    const int kh = a.g.kh, kw = a.g.kw, SWP = a.g.SWP;
+    const int kh = a.g.kh, kw = a.g.kw, SWP = swp();
     if (kh == 9 && kw == 9) {
       stencil_k<9>(pl, w, acc);
       return;
@@ -482,7 +534,7 @@ struct Conv {
 
   // plane value of this thread's channel at tile pixel (r, q)
   __device__ __forceinline__ T fp(int r, int q) const {
-    return plane(ch)[(r + a.g.rh + 1) * a.g.SWP + sk(q + a.g.rw + 1)];
+    return plane(ch)[(r + a.g.rh + 1) * swp() + sk(q + a.g.rw + 1)];
   }
 
   // TV edges are those of the GLOBAL image (a row slab sees its global row
@@ -559,7 +611,7 @@ struct Conv {
   // planes of y resp. xc) into term buffers tb.. (tb = 0 or 3); tileA's TV
   // pass publishes neighbour values through the region `qr` (free by then).
   __device__ __forceinline__ T fpr(const T* pr, int r, int q) const {
-    return pr[(size_t)ch * a.g.SH * a.g.SWP + (r + a.g.rh + 1) * a.g.SWP + sk(q + a.g.rw + 1)];
+    return pr[(size_t)ch * a.g.SH * swp() + (r + a.g.rh + 1) * swp() + sk(q + a.g.rw + 1)];
   }
   __device__ __forceinline__ void tileA(const T* pr, T* qr, int tb, int h0, int w0, const T (&ypre)[RW], T* Rout,
                                         bool tv, T* TV2out, T* TVGout, bool fused, const T* pre_acc = nullptr) {
@@ -572,7 +624,7 @@ struct Conv {
 #pragma unroll
       for (int o = 0; o < RW; ++o) acc[o] = pre_acc[o];
     } else {
-      stencil(pr + (size_t)ch * a.g.SH * a.g.SWP, ws() + ch * a.g.kh * a.g.kw, acc);
+      stencil(pr + (size_t)ch * a.g.SH * swp(), ws() + ch * a.g.kh * a.g.kw, acc);
     }
 #pragma unroll
     for (int o = 0; o < RW; ++o) {
@@ -736,7 +788,7 @@ struct Conv {
                               const T* XPs, T beta, T L, T* Xc, T betaN, T* Yn) {
     const T two = T(2), alpha = T(a.alpha);
     const int H = a.g.H, W = a.g.W;
-    const size_t co = (size_t)ch * a.g.SH * a.g.SWP;
+    const size_t co = (size_t)ch * a.g.SH * swp();
     int tile = blockIdx.x;
     if (tile < a.g.nTiles) {
       int h0, w0;
@@ -837,6 +889,80 @@ struct Conv {
     }
   }
 
+  // Stage B / CA with TMA tile boxes (KS = 9, single channel): R, and then
+  // the candidate x_c and the next extrapolation point y' (materialised here
+  // in Yn, SrcExtrap's exact expression) arrive as 2-D tensor copies on the
+  // mbarriers; the arithmetic is stageB / stageCA's.
+  __device__ void stageB_tma(const CUtensorMap* tmR, bool tv, const T* TVGin, T* Gout, const SumDev* sgg,
+                             const T* Xs, const T* XPs, T beta, T L, T* Xc, T betaN, T* Yn,
+                             unsigned long long* mbar, unsigned& ph) {
+    const T two = T(2), alpha = T(a.alpha);
+    const int H = a.g.H, W = a.g.W;
+    for (int tile = blockIdx.x; tile < a.g.nTiles; tile += gridDim.x) {
+      int h0, w0;
+      tile_origin(tile, h0, w0);
+      __syncthreads();
+      tma_box(tmR, h0, w0, pa(), mbar);
+      const int h = h0 + ty;
+      T tpre[RW], xpre[RW], xppre[RW];
+#pragma unroll
+      for (int o = 0; o < RW; ++o) {
+        const int w = w0 + tx * RW + o;
+        tpre[o] = xpre[o] = xppre[o] = T(0);
+        if (h < H && w < W) {
+          const int64_t i = gidx(h, w, ch);
+          if (tv) tpre[o] = ldcg(TVGin + i);
+          xpre[o] = ldcg(Xs + i);
+          xppre[o] = ldcg(XPs + i);
+        }
+      }
+      tma_wait(mbar, ph);
+      ph ^= 1u;
+      double part = 0.0;
+      T acc[RW];
+      stencil_adj(acc);
+#pragma unroll
+      for (int o = 0; o < RW; ++o) {
+        const int w = w0 + tx * RW + o;
+        if (h < H && w < W) {
+          const int64_t i = gidx(h, w, ch);
+          T gv = two * acc[o];
+          if (tv) gv = gv + alpha * tpre[o];
+          Gout[i] = gv;
+          part += (double)gv * (double)gv;
+          const T xc = (xpre[o] + beta * (xpre[o] - xppre[o])) - gv / L;
+          Xc[i] = xc;
+          Yn[i] = xc + betaN * (xc - xpre[o]);
+        }
+      }
+      if (sgg) tile_partial(*sgg, tile, part);
+    }
+  }
+
+  __device__ void stageCA_tma(const CUtensorMap* tmXc, const CUtensorMap* tmYn, const T* Xold, const T* Gin, bool tv,
+                              T* Rout, T* TVGout, const SumDev* sdot, const SumDev* sfitc, const SumDev* stvc,
+                              const SumDev* sfit2, const SumDev* stv2, unsigned long long* mbar, unsigned* ph) {
+    for (int tile = blockIdx.x; tile < a.g.nTiles; tile += gridDim.x) {
+      int h0, w0;
+      tile_origin(tile, h0, w0);
+      __syncthreads();
+      tma_box(tmXc, h0, w0, pa(), mbar);
+      tma_box(tmYn, h0, w0, pa2(), mbar + 1);
+      T ypre[RW], gpre[RW], xopre[RW];
+      prefetch_c(h0, w0, Gin, Xold, true, ypre, gpre, xopre);
+      tma_wait(mbar, ph[0]);
+      tma_wait(mbar + 1, ph[1]);
+      ph[0] ^= 1u;
+      ph[1] ^= 1u;
+      T acc1[RW], acc2[RW];
+      stencil_fwd_pair(pa(), pa2(), acc1, acc2);
+      const double part = tileC(pa(), h0, w0, ypre, gpre, xopre, nullptr, tv, nullptr, nullptr, true, true, acc1);
+      tileA(pa2(), pa(), 3, h0, w0, ypre, Rout, tv, nullptr, TVGout, true, acc2);   // syncs before reusing pa()
+      tile_partial(*sdot, tile, part);
+      tile_leaves(h0, w0, tv ? 3 : 1, sfitc, stvc, (int)(a.g.Ng / a.g.leafL), 0, sfit2, stv2);
+    }
+  }
+
   // Stage C (value at a candidate): xc = src; rc = B xc - y; TV terms
   // sqrt(d^2+nu^2) - nu (tv_value, regularizers.py:70-72); optional tile
   // partial of g.(xc - xold); xc written to Xout (if non-null).  Fused:
@@ -854,7 +980,7 @@ struct Conv {
 #pragma unroll
       for (int o = 0; o < RW; ++o) acc[o] = pre_acc[o];
     } else {
-      stencil(pr + (size_t)ch * a.g.SH * a.g.SWP, ws() + ch * a.g.kh * a.g.kw, acc);
+      stencil(pr + (size_t)ch * a.g.SH * swp(), ws() + ch * a.g.kh * a.g.kw, acc);
     }
 #pragma unroll
     for (int o = 0; o < RW; ++o) {

@@ -7,4 +7,8 @@ namespace adp {
 const void* conv_solve_k9(int fast) {
   return fast ? (const void*)conv_solve_kernel<double, true, 2, 9> : (const void*)conv_solve_kernel<double, false, 2, 9>;
 }
+const void* conv_solve_k9_tma(int fast) {
+  return fast ? (const void*)conv_solve_kernel<double, true, 2, 9, 512, true>
+              : (const void*)conv_solve_kernel<double, false, 2, 9, 512, true>;
+}
 }  // namespace adp

@@ -4,17 +4,27 @@
 
 namespace adp {
 
-template <typename T, bool FAST, int RW, int KS = 0>
-struct ConvOps : Conv<T, FAST, RW, KS> {
-  using Base = Conv<T, FAST, RW, KS>;
+template <typename T, bool FAST, int RW, int KS = 0, bool TMA = false>
+struct ConvOps : Conv<T, FAST, RW, KS, TMA> {
+  using Base = Conv<T, FAST, RW, KS, TMA>;
   using Base::a;
   GridBarrier gb;
   SumDev* ssm;   // shared-memory copies of a.s_fit .. a.s_tv2 (read at every decision point)
+  unsigned long long* mbar = nullptr;   // TMA: two transaction barriers (one per plane region)
 
   __device__ explicit ConvOps(const ConvArgs<T>& a_) : Base(a_) {
     gb.counter = a_.bar;
     gb.nblocks = gridDim.x;
     gb.target = 0;
+    if constexpr (TMA) {
+      __shared__ __align__(8) unsigned long long sh_mbar[2];
+      mbar = sh_mbar;
+      if (threadIdx.x == 0) {
+        for (int k = 0; k < 2; ++k)
+          asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(Base::smem_u32(sh_mbar + k)) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      }
+    }
     __shared__ SumDev sh_sums[kNumSums];
     static_assert(offsetof(ConvArgs<T>, s_tv2) - offsetof(ConvArgs<T>, s_fit) == (kNumSums - 1) * sizeof(SumDev),
                   "sum descriptors must be contiguous");
@@ -160,9 +170,10 @@ struct ConvOps : Conv<T, FAST, RW, KS> {
 // 255-register file instead of spilling at the 512-thread cap of 128.
 // MAXT < 512: instances for CTAs of at most MAXT threads (c3-c5 run 384),
 // more registers per thread for the same reason.
-template <typename T, bool FAST, int RW, int KS = 0, int MAXT = 512>
+template <typename T, bool FAST, int RW, int KS = 0, int MAXT = 512, bool TMA = false>
 __global__ void __launch_bounds__(KS > 0 ? kSolveKSThreads : MAXT, 1) conv_solve_kernel(const __grid_constant__ ConvArgs<T> a) {
-  ConvOps<T, FAST, RW, KS> E(a);
+  ConvOps<T, FAST, RW, KS, TMA> E(a);
+  unsigned tph[2] = {0u, 0u};   // TMA: mbarrier phases
   const ConvGeom& g = a.g;
   E.load_weights(a.kern);
   const bool tv = (a.alpha != 0.0);
@@ -240,12 +251,19 @@ __global__ void __launch_bounds__(KS > 0 ? kSolveKSThreads : MAXT, 1) conv_solve
         ADP_TRACE(t, 1);
       }
       ADP_TRACE(t, 2);
-      if (pipe) {
-        const double t_next2 = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t_mom * t_mom));   // as in the stage-CA branch
-        const double beta2 = (t_mom - 1.0) / t_next2;
-        E.stageB_pipe(a.R, tv, a.TVG, a.G, &a.s_t0, a.X[ix], a.X[ixp], tb, T(L_try), a.X[ic], T(beta2), a.P[0]);
+      const double t_nextB = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t_mom * t_mom));   // as in the stage-CA branch
+      const double betaB = (t_mom - 1.0) / t_nextB;
+      if constexpr (TMA) {
+        if (spec)
+          E.stageB_tma(&a.tm[3], tv, a.TVG, a.G, &a.s_t0, a.X[ix], a.X[ixp], tb, T(L_try), a.X[ic], T(betaB),
+                       a.P[0], E.mbar, tph[0]);
+        else
+          E.stageB(a.R, tv, a.TVG, a.G, &a.s_t0, a.X[ix], a.X[ixp], tb, T(L_try), a.X[ic]);
       } else {
-        E.stageB(a.R, tv, a.TVG, a.G, &a.s_t0, a.X[ix], a.X[ixp], tb, T(L_try), a.X[ic]);
+        if (pipe)
+          E.stageB_pipe(a.R, tv, a.TVG, a.G, &a.s_t0, a.X[ix], a.X[ixp], tb, T(L_try), a.X[ic], T(betaB), a.P[0]);
+        else
+          E.stageB(a.R, tv, a.TVG, a.G, &a.s_t0, a.X[ix], a.X[ixp], tb, T(L_try), a.X[ic]);
       }
       E.leaves_if_unfused(a.s_fit, a.R, true);
       if (tv) E.leaves_if_unfused(a.s_tv, a.TV2, false);
@@ -260,12 +278,17 @@ __global__ void __launch_bounds__(KS > 0 ? kSolveKSThreads : MAXT, 1) conv_solve
       // next iteration's momentum if this one ends without restart
       const double t_next2 = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t_mom * t_mom));
       const double beta2 = (t_mom - 1.0) / t_next2;
-      if (pipe)
-        E.stageCA_pipe(a.X[ic], a.P[0], a.X[ix], a.G, tv, a.R, a.TVG, &a.s_t1, &a.s_fitc, &a.s_tvc,
-                       par ? &a.s_fit : &a.s_fit2, par ? &a.s_tv : &a.s_tv2);
-      else
-        E.stageCA(a.X[ic], a.X[ix], T(beta2), a.G, tv, a.R, a.TVG, &a.s_t1, &a.s_fitc, &a.s_tvc,
-                  par ? &a.s_fit : &a.s_fit2, par ? &a.s_tv : &a.s_tv2);
+      if constexpr (TMA) {
+        E.stageCA_tma(&a.tm[ic], &a.tm[4], a.X[ix], a.G, tv, a.R, a.TVG, &a.s_t1, &a.s_fitc, &a.s_tvc,
+                      par ? &a.s_fit : &a.s_fit2, par ? &a.s_tv : &a.s_tv2, E.mbar, tph);
+      } else {
+        if (pipe)
+          E.stageCA_pipe(a.X[ic], a.P[0], a.X[ix], a.G, tv, a.R, a.TVG, &a.s_t1, &a.s_fitc, &a.s_tvc,
+                         par ? &a.s_fit : &a.s_fit2, par ? &a.s_tv : &a.s_tv2);
+        else
+          E.stageCA(a.X[ic], a.X[ix], T(beta2), a.G, tv, a.R, a.TVG, &a.s_t1, &a.s_fitc, &a.s_tvc,
+                    par ? &a.s_fit : &a.s_fit2, par ? &a.s_tv : &a.s_tv2);
+      }
       ++vals;
     } else if (a.adaptive) {
       E.value_cand(SrcLin<T>{a.X[ic]}, tv, nullptr, a.G, a.X[ix], &a.s_t1);

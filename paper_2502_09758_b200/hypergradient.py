@@ -130,7 +130,7 @@ def _cached_dev(owner, arr):
     """Device copy of a host array held by `owner` (e.g. y_delta), cached."""
     cache = owner.__dict__.setdefault("_devcache", {})
     key = (id(arr), nat.get_precision()["dtype"], nat.current_device())
-    ver = arr._version if nat.is_torch(arr) else None   # in-place edits of a tensor re-copy
+    ver = arr._version if nat.is_torch(arr) else nat.host_fingerprint(arr)   # in-place edits re-copy
     hit = cache.get(key)
     if hit is None or hit[0] is not arr or hit[1] != ver:
         hit = (arr, ver, nat.to_dev(arr, owner.signal_shape))

@@ -119,3 +119,19 @@ def test_sum_layout_binary_tile_tree():
     assert nl == 5000 and ns == 3 and top == -1
     vals = np.arange(5000, dtype=float)
     assert perfect([perfect(vals[sub_leaf[t]:sub_leaf[t + 1]]) for t in range(ns)]) == vals.sum()
+
+
+def test_host_fingerprint_sees_edits():
+    """Device-copy caches of host arrays (problems.UpperProblem.lower_problem,
+    hypergradient._cached_dev) key on identity + a sampled fingerprint."""
+    import numpy as np
+    from paper_2502_09758_b200 import _native as nat
+    y = np.random.default_rng(0).standard_normal((64, 48, 3))
+    f0 = nat.host_fingerprint(y)
+    assert nat.host_fingerprint(y) == f0
+    y *= 2.0
+    assert nat.host_fingerprint(y) != f0
+    f1 = nat.host_fingerprint(y)
+    y[:] = 0.5
+    assert nat.host_fingerprint(y) != f1
+    assert nat.host_fingerprint(y.copy()) != nat.host_fingerprint(y)   # a new object (address) re-uploads
