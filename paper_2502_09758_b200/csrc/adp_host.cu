@@ -555,8 +555,9 @@ static int conv_plan_init(PlanImpl& P) {
       // TMA tile boxes for the c2 kernel (ADP_TMA=0: the LDS-fed loaders)
       const char* et = getenv("ADP_TMA");
       if (!(et && atoi(et) == 0) && !slab && (size_t)g.SH * g.SWPt <= (size_t)g.SH * g.SWP &&
-          build_tmaps(P) == ADP_OK) {
+          P.smem + 128 <= smem_optin && build_tmaps(P) == ADP_OK) {
         P.tma = 1;
+        P.smem += 128;   // the kernel aligns its dynamic shared-memory base to 128 bytes
         ks.solve = conv_solve_k9_tma(P.d.mode == ADP_MODE_FAST);
       }
     }

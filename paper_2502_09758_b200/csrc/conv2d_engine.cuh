@@ -145,13 +145,24 @@ struct Conv {
   }
 
   // ---- shared-memory views (byte offsets from the dynamic window)
-  __device__ __forceinline__ double* red() const { return reinterpret_cast<double*>(dsm()); }
-  __device__ __forceinline__ T* ws() const { return reinterpret_cast<T*>(dsm() + a.g.o_ws); }
-  __device__ __forceinline__ T* wf() const { return reinterpret_cast<T*>(dsm() + a.g.o_wf); }
-  __device__ __forceinline__ T* pa() const { return reinterpret_cast<T*>(dsm() + a.g.o_pa); }
-  __device__ __forceinline__ T* pa2() const { return reinterpret_cast<T*>(dsm() + a.g.o_pa2); }
-  __device__ __forceinline__ double* tm() const { return reinterpret_cast<double*>(dsm() + a.g.o_tm); }
-  __device__ __forceinline__ double* sv() const { return reinterpret_cast<double*>(dsm() + a.g.o_sv); }
+  // dynamic shared-memory base; TMA kernels shift it to the next 128-byte
+  // boundary (TMA destinations; the host adds 128 bytes to the allocation)
+  __device__ __forceinline__ unsigned char* sbase() const {
+    if constexpr (TMA) {
+      unsigned char* b = dsm();
+      const unsigned o = (unsigned)__cvta_generic_to_shared(b);
+      return b + ((128u - (o & 127u)) & 127u);
+    } else {
+      return dsm();
+    }
+  }
+  __device__ __forceinline__ double* red() const { return reinterpret_cast<double*>(sbase()); }
+  __device__ __forceinline__ T* ws() const { return reinterpret_cast<T*>(sbase() + a.g.o_ws); }
+  __device__ __forceinline__ T* wf() const { return reinterpret_cast<T*>(sbase() + a.g.o_wf); }
+  __device__ __forceinline__ T* pa() const { return reinterpret_cast<T*>(sbase() + a.g.o_pa); }
+  __device__ __forceinline__ T* pa2() const { return reinterpret_cast<T*>(sbase() + a.g.o_pa2); }
+  __device__ __forceinline__ double* tm() const { return reinterpret_cast<double*>(sbase() + a.g.o_tm); }
+  __device__ __forceinline__ double* sv() const { return reinterpret_cast<double*>(sbase() + a.g.o_sv); }
   __device__ __forceinline__ T* plane(int c) const { return pa() + (size_t)c * a.g.SH * swp(); }
 
   // ---- weights: ws[c][i][j] = kern[i][j][c] (|w| <= eps -> 0), wf flipped
@@ -329,7 +340,7 @@ struct Conv {
       }
     }
   }
-  __device__ __forceinline__ T* qs() const { return reinterpret_cast<T*>(dsm() + a.g.o_q); }
+  __device__ __forceinline__ T* qs() const { return reinterpret_cast<T*>(sbase() + a.g.o_q); }
 
   // window of NW box elements starting one past the row base: scalar loads
   // on the skewed layout; 16-byte loads on the (aligned) dense TMA layout
