@@ -336,10 +336,15 @@ def run_native(args):
     for s in range(args.warmup):
         one_step(s, {})
     torch.cuda.synchronize()
+    plan = ups[seeds[0]].lower_problem(ups[seeds[0]].b0).op.plan()
+    flags = plan.flags()
+    # live timing of the dominant kernel: CUDA events around every 16th launch (sampled, so the host-side
+    # event calls stay off the critical path of the timed steps)
+    nat.check(nat.lib().adp_plan_profile(plan.handle, 16), "adp_plan_profile")
     if ws > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    times, units, vals, vgs = [], 0, 0, 0
+    times, units, vals, vgs, launches, dom_ms, dom_n = [], 0, 0, 0, 0, 0.0, 0
     with ClockSampler(local) as clk:
         for s in range(args.warmup, nsteps):
             flush.zero_()
@@ -354,7 +359,11 @@ def run_native(args):
             units += N * r.iters
             vals += stats["value_evals"]
             vgs += stats["vg_evals"]
+            launches += stats["launches"]
+            dom_ms += stats["dominant_ms"]
+            dom_n += stats["dominant_launches"]
     torch.cuda.synchronize()
+    nat.check(nat.lib().adp_plan_profile(plan.handle, 0), "adp_plan_profile")
     if ws > 1:
         dist.barrier()
     t_dev = float(np.sum(times))
@@ -406,11 +415,22 @@ def run_native(args):
            "note": "host float64 NumPy y, x0, kernel in / x~ out through paper_2502_09758_b200.solve_lower "
                    "(wall clock, fresh operator per step)"}
 
-    # ---- roofline of the dominant (only) kernel in the timed region: conv_solve_kernel, one launch per step
+    # ---- roofline.  Persistent solve (c2; ADP_STEP=0): the only kernel in the timed region is
+    # conv_solve_kernel, one launch per step.  Host-stepped solve (c3-c5 default): the dominant kernel
+    # is step_ca_kernel (the candidate's value pass + the speculative stage A at the next
+    # extrapolation point: two stencil passes), timed live with CUDA events on its stream.
     iters_total = units / N
     value_per_it = vals / max(iters_total, 1)
     flop_px_it = 2.0 * K * K * (2.0 + value_per_it) + 50.0    # 6K^2+50 at one value pass
-    achieved_tf = flop_px_it * units / sum(times) / 1e12      # this rank's launches
+    step_total_tf = flop_px_it * units / sum(times) / 1e12     # whole solve (all kernels of the step)
+    if flags["step"] and dom_n:
+        dom_kernel = "step_ca_kernel"
+        dom_flop = (2.0 * 2.0 * K * K + 50.0) * N              # two forward K x K passes + TV terms per launch
+        achieved_tf = dom_flop * dom_n / (dom_ms * 1e-3) / 1e12
+        dom_share = dom_ms * 1e-3 / sum(times)
+    else:
+        dom_kernel, dom_flop, dom_share = "conv_solve_kernel", flop_px_it * units / len(times), 1.0
+        achieved_tf = step_total_tf
     tf = ctypes.c_double()
     ms = ctypes.c_double()
     nat.check(nat.lib().adp_fp64_peak(ctypes.byref(tf), ctypes.byref(ms), nat.stream_ptr()), "fp64 peak")
@@ -428,13 +448,20 @@ def run_native(args):
             "peak_source": "measured live on this GPU: DFMA microbenchmark (adp_fp64_peak, 2 flop/DFMA); "
                            "MEASURED_PEAKS.json has no FP64 entry",
             "peak_nominal_tflops": NOMINAL_FP64_TF,
-            "flop_per_px_it": flop_px_it, "kernel": "conv_solve_kernel",
-            "units_per_launch": units / len(times), "launch_ms": 1e3 * sum(times) / len(times),
+            "kernel": dom_kernel, "flop_per_launch": dom_flop,
+            "launch_ms": (dom_ms / max(dom_n, 1)) if dom_kernel == "step_ca_kernel" else 1e3 * sum(times) / len(times),
+            "kernel_share_of_step": dom_share,
+            "whole_step": {"achieved_tflops": step_total_tf, "flop_per_px_it": flop_px_it,
+                           "frac": step_total_tf / peak,
+                           "note": "all kernels of the timed steps: 2K^2 (2 + value passes per iteration) + 50 flop "
+                                   "per lower pixel-iteration over the device time"},
+            "solve_path": "host-stepped stage kernels (csrc/conv2d_step.cu)" if flags["step"] else
+                          "persistent single-launch kernel" + (" with TMA tile boxes" if flags["tma"] else ""),
             "hbm": {"achieved_gbs": bytes_px_it * units / sum(times) / 1e9, "peak_gbs": hbm,
                     "frac": bytes_px_it * units / sum(times) / 1e9 / hbm, "bytes_per_px_it": bytes_px_it,
                     "peak_source": peak_src}}
     if strict:
-        roof["strict_ceiling"] = {"frac": 2.0 * achieved_tf / peak,
+        roof["strict_ceiling"] = {"frac": 2.0 * achieved_tf / peak, "whole_step_frac": 2.0 * step_total_tf / peak,
                                   "note": "strict mode reproduces scipy.ndimage rounding with DMUL + DADD per tap "
                                           "(2 FP64 issues per multiply-add), so its attainable fraction of the "
                                           "DFMA roof is 0.5; frac here is against that ceiling"}
@@ -445,7 +472,7 @@ def run_native(args):
             "warmup": args.warmup, "ms_per_step": 1e3 * t_dev / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64" if dtype == "float64" else "f32",
             "data": "synthetic (seeded generators of SURVEY.md Appendix A)", "config": cfg,
-            "roofline": roof, "e2e": e2e, "gpu_launches": args.steps, "clocks": clk.summary()}
+            "roofline": roof, "e2e": e2e, "gpu_launches": launches, "clocks": clk.summary()}
 
     # ---- MAID upper iterations / s: c1 (full 60-step run) and c2 (reference 2-D settings)
     if args.maid_steps > 0 and rank == 0:
@@ -556,6 +583,24 @@ def other_configs(args, flush, main_wl):
                  "instances": len(ups), "ms": 1e3 * t,
                  "workload": "8 c3 instances (seeds 0-7) = one GPU's share of 64, 300 AGD iterations each, "
                              "no collectives (weak scaling over GPUs)"}
+    # the same 8 instances on 2 host threads / CUDA streams (one instance's kernels fill the device while the
+    # other waits on its host-side decisions); wall clock with a device-wide synchronisation on both sides
+    import torch
+    from paper_2502_09758_b200 import multigpu
+    serial_x = [nat.to_host(q.x_tilde) for q in rs]
+    multigpu.run_instances(list(range(2)), lambda k: solve(ups[k], 5), streams=2)   # per-thread plans
+    torch.cuda.synchronize()
+    flush.zero_()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rs2, _ = multigpu.run_instances(list(range(len(ups))), lambda k: solve(ups[k], 300), streams=2)
+    torch.cuda.synchronize()
+    t2 = time.perf_counter() - t0
+    out["c4_2streams"] = {"value": sum(u.y_delta.size * q.iters for u, q in zip(ups, rs2)) / t2 / 1e9, "unit": UNIT,
+                          "instances": len(ups), "ms": 1e3 * t2, "identical_to_serial": all(
+                              np.array_equal(a, nat.to_host(b.x_tilde)) for a, b in zip(serial_x, rs2)),
+                          "workload": "c4 share (8 instances, 300 AGD iterations each) on 2 host threads x 2 CUDA "
+                                      "streams, wall clock"}
     for u in ups:
         dev.pop(id(u), None)
     del ups

@@ -118,6 +118,11 @@ typedef struct {
   int32_t power_converged;
   int64_t vg_evals, value_evals, restarts;
   double t_mom, lip_t;  /* AGD state at exit (momentum t; lip_t, or 1 / step for proxgrad) */
+  int64_t launches;     /* kernel launches of the solve (1: the persistent single-launch kernel) */
+  double dominant_ms;   /* with adp_plan_profile(p, 1): summed device time (CUDA events on the launching
+                         * stream) of the dominant kernel (host-stepped solve: the candidate-value +
+                         * speculative-stage-A kernel), and its launch count */
+  int64_t dominant_launches;
 } adp_solve_result;
 
 typedef struct {
@@ -308,6 +313,13 @@ int adp_slab_upper(adp_plan* p, const void* A_kernel, const void* x, const void*
                    void* stream);
 int adp_slab_mixed(adp_plan* p, const adp_lower* lp, const void* x_tilde, const void* q, double* part, void* stream);
 int adp_kgc_groups(adp_plan* p, int32_t* ngroups, int32_t* ntaps);
+/* plan execution flags: bit 0 = TMA tile boxes in the solve kernel (c2), bit 1 = host-stepped
+ * high-occupancy solve_lower (c3-c5: stage kernels one tile per CTA, scalar control on the host) */
+int adp_plan_flags(adp_plan* p, int32_t* flags);
+/* enable (period k >= 1) / disable (0) live timing of the dominant kernel of host-stepped solves:
+ * every k-th iteration's launch is bracketed by CUDA events on its stream (result fields dominant_ms /
+ * dominant_launches = the sampled launches' summed device time and count) */
+int adp_plan_profile(adp_plan* p, int32_t enable);
 int adp_kgc_final(adp_plan* p, const double* part, void* out, double scale, void* stream);
 /* k (<= 8) perfect-tree folds (zero-padded to a power of two, <= 16384 units each) of device unit
  * vectors units[i] (n[i] doubles); results to HOST out[i]; synchronises the stream. */

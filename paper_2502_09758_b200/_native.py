@@ -55,7 +55,8 @@ class SolveResult(ctypes.Structure):
                 ("status", ctypes.c_int32), ("fail_iter", ctypes.c_int32), ("power_iters", ctypes.c_int32),
                 ("power_converged", ctypes.c_int32), ("vg_evals", ctypes.c_int64),
                 ("value_evals", ctypes.c_int64), ("restarts", ctypes.c_int64), ("t_mom", ctypes.c_double),
-                ("lip_t", ctypes.c_double)]
+                ("lip_t", ctypes.c_double), ("launches", ctypes.c_int64), ("dominant_ms", ctypes.c_double),
+                ("dominant_launches", ctypes.c_int64)]
 
 
 class CGResultC(ctypes.Structure):
@@ -123,6 +124,8 @@ SIGNATURES = {
     "adp_slab_upper": (_I, [_P, _P, _P, _P, _P, _P]),
     "adp_slab_mixed": (_I, [_P, ctypes.POINTER(Lower), _P, _P, _P, _P]),
     "adp_kgc_groups": (_I, [_P, ctypes.POINTER(_I), ctypes.POINTER(_I)]),
+    "adp_plan_flags": (_I, [_P, ctypes.POINTER(_I)]),
+    "adp_plan_profile": (_I, [_P, _I]),
     "adp_kgc_final": (_I, [_P, _P, _P, _D, _P]),
     "adp_sum_layout": (_I, [ctypes.c_int64, _I, ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(_I),
                             ctypes.POINTER(_I), _P, ctypes.c_int64, _P, _P, ctypes.c_int64, _P, ctypes.c_int64,
@@ -257,6 +260,12 @@ class Plan:
         out = (ctypes.c_int32 * 10)()
         check(lib().adp_plan_geometry(self.handle, out), "adp_plan_geometry")
         return dict(zip(GEOMETRY_KEYS, (int(v) for v in out)))
+
+    def flags(self) -> dict:
+        """Execution choices of the plan: TMA tile boxes, host-stepped solve."""
+        f = ctypes.c_int32()
+        check(lib().adp_plan_flags(self.handle, ctypes.byref(f)), "adp_plan_flags")
+        return {"tma": bool(f.value & 1), "step": bool(f.value & 2)}
 
 
 _plans: dict = {}

@@ -3,6 +3,7 @@
 // extern "C" ABI declared in include/adp_b200.h.
 #include <cuda_runtime.h>
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstring>
 #include <functional>
@@ -564,6 +565,30 @@ static int conv_plan_init(PlanImpl& P) {
     else if (g.rwb == 4 && g.threads <= kSolveT384 && !(getenv("ADP_T384") && atoi(getenv("ADP_T384")) == 0))
       ks.solve = conv_solve_t384(P.d.dtype, P.d.mode == ADP_MODE_FAST);
   }
+  // host-stepped high-occupancy solve (conv2d_step.cu): float64 RW = 4 plans
+  // with fused leaves, not slabs; ADP_STEP=0 disables, =1 enables for every
+  // eligible plan, default: images of >= 2^18 elements (c3-c5)
+  {
+    const char* ev = getenv("ADP_STEP");
+    const int want = ev ? atoi(ev) : -1;
+    if (want != 0 && P.d.dtype == ADP_DTYPE_F64 && g.rwb == 4 && g.fused && g.fuseCA && !slab &&
+        g.threads <= 384 && (want == 1 || g.N >= (1 << 18))) {
+      const size_t es = (size_t)P.esize;
+      const size_t pa = ((size_t)g.C * g.SH * g.SWP * es + 127) & ~size_t(127);
+      const size_t tm = (size_t)3 * g.TH * g.TW * g.C * sizeof(double);
+      P.step_o_tm = g.o_pa + (int)pa;
+      P.step_smem = (size_t)P.step_o_tm + tm;
+      StepKernels sk = step_kernels(P.d.mode == ADP_MODE_FAST);
+      P.k_extrap = sk.extrap;
+      P.step_smem_b = (size_t)g.o_pa + pa;   // stage B: no term buffers (three CTAs per SM)
+      if (setup_kernel(P, P.k_sb, sk.b, g.threads, P.step_smem_b, g.nTiles) == ADP_OK &&
+          setup_kernel(P, P.k_sca, sk.ca, g.threads, P.step_smem, 2 * g.nTiles) == ADP_OK &&
+          setup_kernel(P, P.k_sc, sk.c, g.threads, P.step_smem, g.nTiles) == ADP_OK &&
+          setup_kernel(P, P.k_sa, sk.a, g.threads, P.step_smem, g.nTiles) == ADP_OK &&
+          setup_kernel(P, P.k_sred, sk.red, g.threads, P.smem, g.nTiles) == ADP_OK)
+        P.step = 1;
+    }
+  }
   const int maxg = g.nTiles;
   if (int e = setup_kernel(P, P.k_solve, ks.solve, g.threads, P.smem, maxg)) return e;
   if (int e = setup_kernel(P, P.k_cg, ks.cg, g.threads, P.smem, maxg)) return e;
@@ -783,6 +808,9 @@ void adp_plan_destroy(adp_plan* p) {
   if (P.h_sres) cudaFreeHost(P.h_sres);
   if (P.h_cres) cudaFreeHost(P.h_cres);
   if (P.h_scal) cudaFreeHost(P.h_scal);
+  if (P.h_flag) cudaFreeHost(P.h_flag);
+  if (P.prof_ev[0]) cudaEventDestroy(P.prof_ev[0]);
+  if (P.prof_ev[1]) cudaEventDestroy(P.prof_ev[1]);
   delete p;
 }
 
@@ -906,6 +934,234 @@ int adp_lower_hess_diag(adp_plan* p, const adp_lower* lp, const void* x, void* o
   return DISPATCH_T(P, conv_misc)(P, CM_HESS_DIAG, lp, nullptr, x, nullptr, out, nullptr, nullptr, STREAM(stream));
 }
 
+// ---------------------------------------------------------------------------
+// Host-stepped solve_lower (adaptive AGD with restart on smoothed TV,
+// lower_solvers.py:104-213) for plans with P.step: the persistent kernel's
+// stages as one-tile-per-CTA kernels (conv2d_step.cu) and its scalar control
+// flow here, expression for expression (conv_solve_kernel), so iterates,
+// decisions and counters are identical to the single-launch solve.
+static int step_launch(PlanImpl& P, KernelInfo& k, ConvArgs<double>& a, cudaStream_t st, bool coop, size_t smem,
+                       int grid) {
+  void* args[] = {&a};
+  if (coop) {
+    CK(cudaMemsetAsync(P.d_bar, 0, sizeof(unsigned int), st));
+    CK(cudaLaunchCooperativeKernel(k.fn, dim3(grid), dim3(P.g.threads), args, smem, st));
+  } else {
+    CK(cudaLaunchKernel(k.fn, dim3(grid), dim3(P.g.threads), args, smem, st));
+  }
+  return ADP_OK;
+}
+
+static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, void* x_out, const adp_solve_args* sa,
+                           adp_solve_result* res, cudaStream_t st) {
+  using T = double;
+  const ConvGeom& g = P.g;
+  ConvArgs<T> base = conv_base<T>(P);
+  set_lower(base, lp);
+  ConvArgs<T> sa_args = base;   // stage kernels: one plane region, term buffers right after it
+  sa_args.g.o_tm = P.step_o_tm;
+  sa_args.g.o_pa2 = P.step_o_tm;   // never addressed with one tile per CTA
+  const double alpha = lp->alpha, nu = lp->nu;
+  const double twoN = 2.0 * (double)g.N;
+  const double tol = sa->eps * sa->mu;
+  long long launches = 0, dom_n = 0;
+  double dom_ms = 0.0;
+  bool prof_now = false;
+  // ---- step size / Lipschitz constant (solve_lower lines 135-140, L_of_b 90-96)
+  double lip, lam = sa->norm_sq;
+  int pit = 0, pconv = 1;
+  if (sa->step_size > 0) {
+    lip = 1.0 / sa->step_size;
+  } else {
+    if (!(sa->norm_sq >= 0.0)) {
+      ConvArgs<T> a = base;
+      a.v0 = (const T*)sa->v0;
+      a.mode = CM_POWER;
+      a.power_max_iters = sa->norm_max_iters;
+      a.power_tol = sa->norm_tol;
+      if (int e = launch_coop(P, P.k_misc, a, st)) return e;
+      if (int e = fetch_scal(P, 3, st)) return e;
+      lam = P.h_scal[0];
+      pconv = (int)P.h_scal[1];
+      pit = (int)P.h_scal[2];
+      ++launches;
+    }
+    lip = 2.0 * lam + alpha * (8.0 / nu);
+  }
+  // ---- x = x_prev = x0 (or the injected state of a P2 lockstep step)
+  T* X[3] = {(T*)P.ws[0], (T*)P.ws[1], (T*)P.ws[2]};
+  T* Yn = (T*)P.ws[10];
+  const size_t nbytes = (size_t)g.N * sizeof(T);
+  CK(cudaMemcpyAsync(X[0], x0, nbytes, cudaMemcpyDeviceToDevice, st));
+  if (sa->x_prev0) CK(cudaMemcpyAsync(X[1], sa->x_prev0, nbytes, cudaMemcpyDeviceToDevice, st));
+  int ix = 0, ixp = sa->x_prev0 ? 1 : 0, ic = sa->x_prev0 ? 2 : 1;
+  double t_mom = sa->t_mom0 > 0.0 ? sa->t_mom0 : 1.0, lip_t = sa->lip_t0 > 0.0 ? sa->lip_t0 : lip;
+  int status = ST_OK, fail_iter = -1, iters = sa->max_iters, converged = 0;
+  double gn = 0.0, h_y = 0.0, beta = 0.0;
+  long long vg = 0, vals = 0, restarts = 0;
+  bool done = false, a_ready = false;
+  int par = 0;
+  const int nT = g.nTiles;
+  if (P.profile && !P.prof_ev[0]) {
+    CK(cudaEventCreate(&P.prof_ev[0]));
+    CK(cudaEventCreate(&P.prof_ev[1]));
+  }
+  if (!P.h_flag) {
+    CK(cudaHostAlloc(&P.h_flag, sizeof(int), cudaHostAllocMapped));
+    *(volatile int*)P.h_flag = 0;
+  }
+  double* d_hscal = nullptr;
+  int* d_hflag = nullptr;
+  CK(cudaHostGetDevicePointer((void**)&d_hscal, P.h_scal, 0));
+  CK(cudaHostGetDevicePointer((void**)&d_hflag, P.h_flag, 0));
+  // the reduction writes its sums and then a sequence number into mapped pinned memory; the host
+  // spins on the number (no stream synchronisation on the decision path), checking for errors
+  auto reduce = [&](int mode, int n) -> int {
+    ConvArgs<T> a = base;
+    a.sflag = mode;
+    a.hscal = d_hscal;
+    a.hflag = d_hflag;
+    a.hseq = ++P.step_seq;
+    if (int e = step_launch(P, P.k_sred, a, st, true, P.smem, P.k_sred.grid)) return e;
+    ++launches;
+    for (long long spin = 0; *(volatile int*)P.h_flag != a.hseq; ++spin) {
+      if ((spin & 0xfffff) == 0xfffff) {
+        const cudaError_t q = cudaStreamQuery(st);
+        if (q != cudaErrorNotReady && q != cudaSuccess) return fail(ADP_ERR_CUDA, cudaGetErrorString(q));
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    (void)n;
+    return ADP_OK;
+  };
+  for (int t = 0; t < sa->max_iters; ++t) {
+    const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t_mom * t_mom));
+    beta = (t_mom - 1.0) / t_next;
+    t_mom = t_next;
+    double L_try = lip_t;
+    if (!a_ready) {   // stage A at y = x + beta (x - x_prev), sums set `par`
+      ConvArgs<T> a = sa_args;
+      a.in0 = X[ix]; a.in1 = X[ixp]; a.sbeta = beta; a.sflag = 1 | (par ? 2 : 0);
+      if (int e = step_launch(P, P.k_sa, a, st, false, P.step_smem, nT)) return e;
+      ++launches;
+    }
+    const double t_next2 = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t_mom * t_mom));   // next momentum, no restart
+    const double beta2 = (t_mom - 1.0) / t_next2;
+    {   // stage B: g, first candidate, next extrapolation point
+      ConvArgs<T> a = sa_args;
+      a.in0 = X[ix]; a.in1 = X[ixp]; a.out0 = X[ic]; a.out1 = Yn;
+      a.sbeta = beta; a.sL = L_try; a.sbetaN = beta2;
+      if (int e = step_launch(P, P.k_sb, a, st, false, P.step_smem_b, nT)) return e;
+      ++launches;
+    }
+    {   // candidate value + restart dot, and the speculative stage A at y' (valid iff the candidate is
+        // accepted without retry or restart; the other sums set), in one launch
+      ConvArgs<T> a = sa_args;
+      a.in0 = X[ic]; a.in1 = X[ix]; a.out1 = Yn; a.sflag = par ? 0 : 2;
+      prof_now = P.profile && (t % P.profile == 0);   // sampled: every P.profile-th iteration
+      if (prof_now) CK(cudaEventRecord(P.prof_ev[0], st));
+      if (int e = step_launch(P, P.k_sca, a, st, false, P.step_smem, 2 * nT)) return e;
+      if (prof_now) CK(cudaEventRecord(P.prof_ev[1], st));
+      ++launches;
+    }
+    ++vg;
+    ++vals;
+    if (int e = reduce(par, 6)) return e;
+    if (prof_now) {   // the reduction followed the timed launch in the stream: both events completed
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, P.prof_ev[0], P.prof_ev[1]));
+      dom_ms += ms;
+      ++dom_n;
+    }
+    const double* o = P.h_scal;
+    const double fit = o[0];
+    h_y = fit + alpha * (o[1] - nu * twoN);
+    gn = sqrt(o[2]);
+    double dot = o[3];
+    double fitc = o[4], tvc = o[5];
+    if (!std::isfinite(gn)) { status = ST_DIVERGED; fail_iter = t; done = true; break; }
+    if (gn <= tol) {
+      // converged: return y (lower_solvers.py:200-201)
+      const int64_t n = g.N;
+      const T* xp = X[ix];
+      const T* xpp = X[ixp];
+      T bb = (T)beta;
+      T* outp = (T*)x_out;
+      int64_t nn = n;
+      void* args[] = {(void*)&xp, (void*)&xpp, (void*)&bb, (void*)&outp, (void*)&nn};
+      CK(cudaLaunchKernel(P.k_extrap, dim3(4 * P.sm_count), dim3(256), args, 0, st));
+      ++launches;
+      iters = t;
+      converged = 1;
+      done = true;
+      break;
+    }
+    int k = 0;
+    while (true) {   // _backtracked_step (lower_solvers.py:170-177)
+      const double val = fitc + alpha * tvc;
+      if (val <= h_y - 0.5 * gn * gn / L_try + 1e-15 * fabs(h_y)) break;
+      L_try *= 2.0;
+      if (++k >= 60) { status = ST_BT_FAIL; fail_iter = t; break; }
+      ConvArgs<T> a = sa_args;
+      a.in0 = X[ix]; a.in1 = X[ixp]; a.out0 = X[ic]; a.sbeta = beta; a.sL = L_try; a.sflag = 1;
+      if (int e = step_launch(P, P.k_sc, a, st, false, P.step_smem, nT)) return e;
+      ++launches;
+      ++vals;
+      if (int e = reduce(2, 3)) return e;
+      fitc = P.h_scal[0]; tvc = P.h_scal[1]; dot = P.h_scal[2];
+    }
+    if (status != ST_OK) { done = true; break; }
+    const double bstep = 1.0 / L_try;
+    lip_t = fmax(1.0 / bstep * 0.9, lip * 1e-8);
+    ixp = ix;
+    ix = ic;
+    const bool restart = dot > 0.0;
+    if (restart) {
+      t_mom = 1.0;
+      ixp = ix;
+      ++restarts;
+    }
+    for (int b = 0; b < 3; ++b)
+      if (b != ix && b != ixp) { ic = b; break; }
+    a_ready = k == 0 && !restart;
+    if (a_ready) par ^= 1;
+  }
+  if (!done) {
+    // max_iters reached: g = lower_grad(p, x) (lower_solvers.py:212-213)
+    ConvArgs<T> a = base;
+    a.mode = CM_GRAD;
+    a.in0 = X[ix];
+    a.out0 = (T*)P.ws[5];
+    if (int e = launch_coop(P, P.k_misc, a, st)) return e;
+    ++launches;
+    if (int e = fetch_scal(P, 2, st)) return e;
+    gn = P.h_scal[1];
+    CK(cudaMemcpyAsync(x_out, X[ix], nbytes, cudaMemcpyDeviceToDevice, st));
+    iters = sa->max_iters;
+    converged = gn <= tol;
+  }
+  CK(cudaStreamSynchronize(st));
+  res->norm_sq = lam;
+  res->lip = lip;
+  res->grad_norm = gn;
+  res->value = h_y;
+  res->iters = iters;
+  res->converged = converged;
+  res->status = status;
+  res->fail_iter = fail_iter;
+  res->power_iters = pit;
+  res->power_converged = pconv;
+  res->vg_evals = vg;
+  res->value_evals = vals;
+  res->restarts = restarts;
+  res->t_mom = t_mom;
+  res->lip_t = lip_t;
+  res->launches = launches;
+  res->dominant_ms = dom_ms;
+  res->dominant_launches = dom_n;
+  return ADP_OK;
+}
+
 int adp_lower_solve(adp_plan* p, const adp_lower* lp, const void* x0, void* x_out, const adp_solve_args* sa,
                     adp_solve_result* res, void* stream) {
   if (int e = check_lower(p, lp)) return e;
@@ -917,8 +1173,14 @@ int adp_lower_solve(adp_plan* p, const adp_lower* lp, const void* x0, void* x_ou
   const bool injected = sa->x_prev0 || sa->t_mom0 > 0 || sa->lip_t0 > 0;
   if (IS_DENSE(p)) {
     if (injected) return fail(ADP_ERR_UNSUPPORTED, "injected AGD state: depthwise 2-D plans only");
-    return dense_solve(P, lp, x0, x_out, sa, res, STREAM(stream));
+    *res = adp_solve_result{};
+    const int e = dense_solve(P, lp, x0, x_out, sa, res, STREAM(stream));
+    res->launches = 1;
+    return e;
   }
+  *res = adp_solve_result{};
+  if (P.step && sa->method == M_AGD && sa->adaptive && lp->alpha != 0.0 && !P.d_trace)
+    return conv_solve_step(P, lp, x0, x_out, sa, res, STREAM(stream));
   auto run = [&](auto tag) -> int {
     using T = decltype(tag);
     ConvArgs<T> a = conv_base<T>(P);
@@ -958,6 +1220,9 @@ int adp_lower_solve(adp_plan* p, const adp_lower* lp, const void* x0, void* x_ou
     res->restarts = o.restarts;
     res->t_mom = o.t_mom;
     res->lip_t = o.lip_t;
+    res->launches = 1;
+    res->dominant_ms = 0.0;
+    res->dominant_launches = 0;
     return ADP_OK;
   };
   return P.d.dtype == ADP_DTYPE_F32 ? run(float()) : run(double());
@@ -1303,6 +1568,20 @@ extern "C" int adp_slab_mixed(adp_plan* p, const adp_lower* lp, const void* x_ti
                                        STREAM(stream)))
     return e;
   return DISPATCH_T(P, conv_kgc)(P, x_tilde, bq, q, resid, nullptr, 2.0, STREAM(stream), part);
+}
+
+// plan execution flags: bit 0 = TMA tile boxes (c2 kernel), bit 1 = host-stepped
+// high-occupancy solve (conv2d_step.cu)
+extern "C" int adp_plan_flags(adp_plan* p, int32_t* flags) {
+  if (!p || !flags) return fail(ADP_ERR_ARG, "null argument");
+  *flags = (p->impl.tma ? 1 : 0) | (p->impl.step ? 2 : 0);
+  return ADP_OK;
+}
+
+extern "C" int adp_plan_profile(adp_plan* p, int32_t enable) {
+  if (!p) return fail(ADP_ERR_ARG, "null plan");
+  p->impl.profile = enable > 0 ? enable : 0;   // sampling period in iterations (1: every launch)
+  return ADP_OK;
 }
 
 extern "C" int adp_kgc_groups(adp_plan* p, int32_t* ngroups, int32_t* ntaps) {

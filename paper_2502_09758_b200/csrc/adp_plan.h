@@ -65,6 +65,16 @@ struct PlanImpl {
   int kgc_groups = 0;
   int kgc_cblocks = 1;
   int tma = 0;                  // KS = 9 solve kernel with TMA tile boxes (tm[] valid)
+  int step = 0;                 // host-stepped high-occupancy solve (conv2d_step.cu) for this plan
+  KernelInfo k_sb, k_sc, k_sa, k_sred, k_sca;
+  size_t step_smem_b = 0;
+  int* h_flag = nullptr;        // mapped pinned: host-stepped solve's reduction-ready sequence number
+  int step_seq = 0;
+  int profile = 0;              // adp_plan_profile: time the dominant kernel of host-stepped solves
+  cudaEvent_t prof_ev[2] = {nullptr, nullptr};
+  const void* k_extrap = nullptr;
+  size_t step_smem = 0;
+  int step_o_tm = 0;
   CUtensorMap tm[5];            // X[0..2], R, P[0]
   // pinned host staging
   SolveOut* h_sres = nullptr;

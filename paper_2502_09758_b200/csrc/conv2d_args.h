@@ -80,6 +80,10 @@ struct ConvArgs {
   int mode;                // misc kernel mode
   int nofloor;             // hess_diag without the 1e-12*max floor (regularizer-only call)
   double sbeta, sL;        // row-slab steps: momentum beta, trial Lipschitz L (or power scale)
+  double sbetaN;           // host-stepped solve: momentum of the next extrapolation point
+  double* hscal;           // host-stepped solve: results also written to mapped pinned host memory,
+  volatile int* hflag;     //   then the sequence number `hseq` to hflag (the host spins on it)
+  int hseq;
   int sflag;               // row-slab CG steps: variant (see CM_SLAB_CG_*)
   unsigned long long* trace;  // optional phase timestamps (CTA 0): [iter][16] %globaltimer ns
   const T* in0; const T* in1; T* out0; T* out1;
@@ -117,6 +121,16 @@ ConvKernelSet conv_kernels_f64f_rw1();
 const void* conv_solve_k9(int fast);
 // the same with TMA tile boxes (dense plane layout, LDS.128 windows)
 const void* conv_solve_k9_tma(int fast);
+// host-stepped solve (conv2d_step.cu): stage kernels, one tile per CTA
+struct StepKernels {
+  const void* b;
+  const void* c;
+  const void* a;
+  const void* red;
+  const void* extrap;
+  const void* ca;
+};
+StepKernels step_kernels(int fast);
 // thread bound of the compile-time-stencil solve kernel (the host selects it
 // only for CTAs of at most this many threads)
 constexpr int kSolveKSThreads = 256;

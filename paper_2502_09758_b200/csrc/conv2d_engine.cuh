@@ -124,6 +124,7 @@ struct Conv {
 
   const ConvArgs<T>& a;
   int ch, ty, tx;                // this thread's channel, tile row, column group
+  int tb0, tbs;                  // stageA / stageC tile walk: first tile, stride (default: the grid)
 
   __device__ __forceinline__ int nC() const { return KS > 0 ? 1 : a.g.C; }
   // plane column of box column `col` (box column 0 = image column w0 - rw - 1):
@@ -134,7 +135,7 @@ struct Conv {
   __device__ static __forceinline__ int skr(int m) { return TMA ? m : RW == 1 ? m : m + (m >> kShift); }
   __device__ __forceinline__ int swp() const { return TMA ? a.g.SWPt : a.g.SWP; }
 
-  __device__ explicit Conv(const ConvArgs<T>& a_) : a(a_) {
+  __device__ explicit Conv(const ConvArgs<T>& a_) : a(a_), tb0(blockIdx.x), tbs(gridDim.x) {
     const int tpr = a.g.TW / RW;
     // KS > 0 instances serve single-channel images only (host check), so the
     // channel index and count are compile-time
@@ -716,7 +717,7 @@ struct Conv {
                          const SumDev* sfit, const SumDev* stv) {
     const int H = a.g.H, W = a.g.W;
     const bool fused = a.g.fused && sfit;
-    for (int tile = blockIdx.x; tile < a.g.nTiles; tile += gridDim.x) {
+    for (int tile = tb0; tile < a.g.nTiles; tile += tbs) {
       int h0, w0;
       tile_origin(tile, h0, w0);
       __syncthreads();
@@ -1046,7 +1047,7 @@ struct Conv {
   __device__ void stageC(const Src& src, T* RCout, bool tv, T* TV2Cout, T* Xout, const T* Gin, const T* Xold,
                          const SumDev* sdot, const SumDev* sfitc, const SumDev* stvc) {
     const bool fused = a.g.fused && sfitc;
-    for (int tile = blockIdx.x; tile < a.g.nTiles; tile += gridDim.x) {
+    for (int tile = tb0; tile < a.g.nTiles; tile += tbs) {
       int h0, w0;
       tile_origin(tile, h0, w0);
       __syncthreads();

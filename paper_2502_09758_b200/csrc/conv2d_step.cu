@@ -1,0 +1,122 @@
+// Host-stepped, high-occupancy lower solve for the large RW = 4 plans (c3,
+// c4, c5): the stages of conv_solve_kernel (adaptive AGD with restart on
+// smoothed TV, lower_solvers.py:180-213) as separate non-cooperative kernels,
+// one tile per CTA and two CTAs per SM, so one CTA's tile loads, epilogues
+// and leaf sums overlap the other's stencil; the deterministic reductions run
+// in a small cooperative kernel and the scalar AGD decisions on the host (the
+// same IEEE double expressions in the same order as the persistent kernel).
+// Every stage computes exactly the persistent kernel's arithmetic (same stage
+// methods, tiles, fused leaves, tile partials and trees), so iterates and
+// decisions are bitwise identical to it.
+#include "conv2d_kernels.cuh"
+
+namespace adp {
+
+template <typename T, bool FAST>
+__global__ void __launch_bounds__(384, 3) step_b_kernel(const __grid_constant__ ConvArgs<T> a) {
+  // g at y (stage B), first candidate x_c = y - g / L -> out0, next
+  // extrapolation point y' = x_c + betaN (x_c - x) -> out1
+  Conv<T, FAST, 4> E(a);
+  E.load_weights(a.kern);
+  E.stageB_pipe(a.R, a.alpha != 0.0, a.TVG, a.G, &a.s_t0, a.in0, a.in1, T(a.sbeta), T(a.sL), a.out0, T(a.sbetaN),
+                a.out1);
+}
+
+template <typename T, bool FAST>
+__global__ void __launch_bounds__(384, 2) step_c_kernel(const __grid_constant__ ConvArgs<T> a) {
+  // value at the candidate (lower_value form) + restart-dot partial
+  // g.(x_c - x).  sflag 0: the first candidate x_c = in0 (stage B wrote it),
+  // x = in1; sflag 1: backtracking retry x_c = y - g / L with y = in0 + beta
+  // (in0 - in1), written to out0, x = in0  (lower_solvers.py:170-177)
+  Conv<T, FAST, 4> E(a);
+  E.load_weights(a.kern);
+  const bool tv = a.alpha != 0.0;
+  if (a.sflag == 0)
+    E.stageC(SrcLin<T>{a.in0}, a.RC, tv, a.TV2C, nullptr, a.G, a.in1, &a.s_t1, &a.s_fitc, &a.s_tvc);
+  else
+    E.stageC(SrcCand<T>{a.in0, a.in1, a.G, T(a.sbeta), T(a.sL)}, a.RC, tv, a.TV2C, a.out0, a.G, a.in0, &a.s_t1,
+             &a.s_fitc, &a.s_tvc);
+}
+
+template <typename T, bool FAST>
+__global__ void __launch_bounds__(384, 2) step_a_kernel(const __grid_constant__ ConvArgs<T> a) {
+  // value + TV gradient terms at a point (stage A): sflag 0: y = in0 (the
+  // materialised y'); 1: y = in0 + beta (in0 - in1).  Sums into s_fit/s_tv
+  // (sflag & 2: the second set s_fit2/s_tv2)
+  Conv<T, FAST, 4> E(a);
+  E.load_weights(a.kern);
+  const bool tv = a.alpha != 0.0;
+  const SumDev* sf = (a.sflag & 2) ? &a.s_fit2 : &a.s_fit;
+  const SumDev* st = (a.sflag & 2) ? &a.s_tv2 : &a.s_tv;
+  if (a.sflag & 1)
+    E.stageA(SrcExtrap<T>{a.in0, a.in1, T(a.sbeta)}, a.R, a.ydat, tv, a.TV2, a.TVG, sf, st);
+  else
+    E.stageA(SrcLin<T>{a.in0}, a.R, a.ydat, tv, a.TV2, a.TVG, sf, st);
+}
+
+// candidate value (as step_c, sflag 0) and speculative stage A at y' = out1
+// (as step_a, sflag 0 / 2 in sL > 0 ? set 2 : set 1) in ONE launch of 2 x nTiles
+// CTAs: the two independent passes share the waves (one tail instead of two)
+template <typename T, bool FAST>
+__global__ void __launch_bounds__(384, 2) step_ca_kernel(const __grid_constant__ ConvArgs<T> a) {
+  Conv<T, FAST, 4> E(a);
+  E.load_weights(a.kern);
+  const bool tv = a.alpha != 0.0;
+  const int nT = a.g.nTiles;
+  if ((int)blockIdx.x < nT) {
+    E.tb0 = blockIdx.x;
+    E.tbs = nT;
+    E.stageC(SrcLin<T>{a.in0}, a.RC, tv, a.TV2C, nullptr, a.G, a.in1, &a.s_t1, &a.s_fitc, &a.s_tvc);
+  } else {
+    E.tb0 = blockIdx.x - nT;
+    E.tbs = nT;
+    const SumDev* sf = (a.sflag & 2) ? &a.s_fit2 : &a.s_fit;
+    const SumDev* st = (a.sflag & 2) ? &a.s_tv2 : &a.s_tv;
+    E.stageA(SrcLin<T>{a.out1}, a.R, a.ydat, tv, a.TV2, a.TVG, sf, st);
+  }
+}
+
+// the deterministic sums of one decision point -> scal[0..k), CTA 0
+template <typename T>
+__global__ void __launch_bounds__(512, 1) step_reduce_kernel(const __grid_constant__ ConvArgs<T> a) {
+  ConvOps<T, false, 4> E(a);
+  double o[6] = {0, 0, 0, 0, 0, 0};
+  const int par = a.sflag & 1;
+  const SumDev* sfit = par ? &a.s_fit2 : &a.s_fit;
+  const SumDev* stv = par ? &a.s_tv2 : &a.s_tv;
+  if ((a.sflag >> 1) == 0) E.reduce({sfit, stv, &a.s_t0, &a.s_t1, &a.s_fitc, &a.s_tvc}, o);
+  else E.reduce({&a.s_fitc, &a.s_tvc, &a.s_t1}, o);
+  if (blockIdx.x == 0 && threadIdx.x < 6) {
+    a.scal[threadIdx.x] = o[threadIdx.x];
+    if (a.hscal) a.hscal[threadIdx.x] = o[threadIdx.x];
+  }
+  if (a.hflag && blockIdx.x == 0) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence_system();   // the results are visible to the host before the flag
+      *a.hflag = a.hseq;
+    }
+  }
+}
+
+// converged: x~ = x + beta (x - x_prev)   (lower_solvers.py:200-201)
+template <typename T>
+__global__ void step_extrap_kernel(const T* x, const T* xp, T beta, T* out, int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const T xv = x[i], xpv = xp[i];
+    out[i] = xv + beta * (xv - xpv);
+  }
+}
+
+StepKernels step_kernels(int fast) {
+  StepKernels k;
+  k.b = fast ? (const void*)step_b_kernel<double, true> : (const void*)step_b_kernel<double, false>;
+  k.c = fast ? (const void*)step_c_kernel<double, true> : (const void*)step_c_kernel<double, false>;
+  k.a = fast ? (const void*)step_a_kernel<double, true> : (const void*)step_a_kernel<double, false>;
+  k.red = (const void*)step_reduce_kernel<double>;
+  k.ca = fast ? (const void*)step_ca_kernel<double, true> : (const void*)step_ca_kernel<double, false>;
+  k.extrap = (const void*)step_extrap_kernel<double>;
+  return k;
+}
+
+}  // namespace adp

@@ -215,7 +215,8 @@ def solve_lower(p: LowerProblem, x0, eps: float, mu: float, max_iters: int = 300
         raise SolveDiverged("backtracking line search failed to find a decreasing step")
     if stats is not None:
         stats.update(vg_evals=int(r.vg_evals), value_evals=int(r.value_evals), restarts=int(r.restarts),
-                     lip=float(r.lip), power_iters=int(r.power_iters))
+                     lip=float(r.lip), power_iters=int(r.power_iters), launches=int(r.launches),
+                     dominant_ms=float(r.dominant_ms), dominant_launches=int(r.dominant_launches))
     gn = float(r.grad_norm)
     return LowerSolveResult(nat.like(out, x0), gn, int(r.iters), gn / mu, bool(r.converged))
 

@@ -36,11 +36,53 @@ def shard_instances(n_items: int, rank: int, world: int) -> list:
     return list(range(rank, n_items, world))
 
 
-def run_instances(seeds, solve_one, timer=None):
-    """Solve every assigned instance in turn; returns (results, seconds)."""
+def run_instances(seeds, solve_one, timer=None, streams: int = 1):
+    """Solve every assigned instance; returns (results in seed order, seconds).
+    streams > 1: that many host threads, each with its own CUDA stream (and,
+    through the per-thread plan cache, its own workspace), take instances
+    from a shared queue, so one instance's kernels fill the device while
+    another waits on its host-side decisions (the host-stepped solve) — the
+    reference's concurrency model for distinct runs.  The
+    C-ABI calls release the GIL (ctypes)."""
     import time
     t0 = time.perf_counter()
-    out = [solve_one(s) for s in seeds]
+    if streams <= 1 or len(seeds) <= 1:
+        out = [solve_one(s) for s in seeds]
+        return out, time.perf_counter() - t0
+    import queue
+    import threading
+
+    import torch
+    dev = torch.cuda.current_device()
+    work = queue.Queue()
+    for k, s in enumerate(seeds):
+        work.put((k, s))
+    out = [None] * len(seeds)
+    errors = []
+
+    def worker():
+        torch.cuda.set_device(dev)
+        st = torch.cuda.Stream()
+        with torch.cuda.stream(st):
+            while True:
+                try:
+                    k, s = work.get_nowait()
+                except queue.Empty:
+                    break
+                try:
+                    out[k] = solve_one(s)
+                except Exception as e:  # noqa: BLE001 - re-raised in the caller
+                    errors.append(e)
+                    break
+            st.synchronize()
+
+    threads = [threading.Thread(target=worker) for _ in range(min(streams, len(seeds)))]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
     return out, time.perf_counter() - t0
 
 

@@ -125,6 +125,8 @@ def test_c4_sharded_runner_equals_single_solves(adp):
         p = up.lower_problem(up.b0)
         return adp.solve_lower(p, up.x0, 1e-14, 10.0, max_iters=20, method="agd", adaptive=True)
     res, _ = multigpu.run_instances(seeds, solve)
-    for s, r in zip(seeds, res):
+    res2, _ = multigpu.run_instances(seeds + [19, 27], solve, streams=2)   # 2 host threads x 2 CUDA streams
+    for s, r, r2 in zip(seeds, res, res2):
         r1 = solve(s)
         assert r.iters == r1.iters and np.array_equal(r.x_tilde, r1.x_tilde) and r.grad_norm == r1.grad_norm
+        assert r2.iters == r1.iters and np.array_equal(r2.x_tilde, r1.x_tilde) and r2.grad_norm == r1.grad_norm

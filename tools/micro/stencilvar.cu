@@ -14,7 +14,9 @@ __device__ __forceinline__ double madd(double a, double x, double w) { return __
 template <int RW>
 __device__ __forceinline__ int sk(int c) { return RW == 1 ? c : c + c / RW; }
 
-template <int TH, int RW, int RH>
+__constant__ double cw[C * K * K];
+
+template <int TH, int RW, int RH, int CW>
 __global__ void __launch_bounds__((TH / RH) * (TW / RW)) stage(const double* __restrict__ x, const double* __restrict__ y,
                                                               const double* __restrict__ kern, double* __restrict__ out) {
   constexpr int SH = TH + 2 * R + 2, SWL = TW + 2 * R + 2, SWP = SWL + SWL / RW + 1;
@@ -61,7 +63,7 @@ __global__ void __launch_bounds__((TH / RH) * (TW / RW)) stage(const double* __r
       if (i < 0 || i >= K) continue;
 #pragma unroll
       for (int j = 0; j < K; ++j) {
-        const double wt = ws[i * K + j];
+        const double wt = CW ? cw[ch * K * K + i * K + j] : ws[i * K + j];
 #pragma unroll
         for (int o = 0; o < RW; ++o) acc[q][o] = madd(acc[q][o], win[o + j], wt);
       }
@@ -76,31 +78,31 @@ __global__ void __launch_bounds__((TH / RH) * (TW / RW)) stage(const double* __r
     }
 }
 
-template <int TH, int RW, int RH>
+template <int TH, int RW, int RH, int CW = 0>
 void run(const double* x, const double* y, const double* k, double* out) {
   constexpr int SH = TH + 2 * R + 2, SWL = TW + 2 * R + 2, SWP = SWL + SWL / RW + 1;
   const size_t smem = (size_t)SH * SWP * sizeof(double);
   const int threads = (TH / RH) * (TW / RW);
-  cudaFuncSetAttribute(stage<TH, RW, RH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaFuncSetAttribute(stage<TH, RW, RH, CW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncAttributes fa;
-  cudaFuncGetAttributes(&fa, stage<TH, RW, RH>);
+  cudaFuncGetAttributes(&fa, stage<TH, RW, RH, CW>);
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, stage<TH, RW, RH>, threads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, stage<TH, RW, RH, CW>, threads, smem);
   const int grid = (H / TH) * (W / TW) * C;
-  for (int w = 0; w < 3; ++w) stage<TH, RW, RH><<<grid, threads, smem>>>(x, y, k, out);
+  for (int w = 0; w < 3; ++w) stage<TH, RW, RH, CW><<<grid, threads, smem>>>(x, y, k, out);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   const int reps = 400;
   cudaEventRecord(e0);
-  for (int r = 0; r < reps; ++r) stage<TH, RW, RH><<<grid, threads, smem>>>(x, y, k, out);
+  for (int r = 0; r < reps; ++r) stage<TH, RW, RH, CW><<<grid, threads, smem>>>(x, y, k, out);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   const double us = 1e3 * ms / reps;
   const double taps = (double)H * W * C * K * K;
-  printf("TH=%2d RW=%d RH=%d threads=%3d regs=%3d CTAs/SM=%2d: %6.2f us/pass %.2f Ttap/s (%s)\n", TH, RW, RH, threads,
+  printf("%s TH=%2d RW=%d RH=%d threads=%3d regs=%3d CTAs/SM=%2d: %6.2f us/pass %.2f Ttap/s (%s)\n", CW ? "const" : "smem ", TH, RW, RH, threads,
          fa.numRegs, nb, us, taps / us / 1e6, cudaGetErrorString(cudaGetLastError()));
 }
 
@@ -123,6 +125,11 @@ int main() {
   for (int w = 0; w < 20; ++w) spin<<<148 * 4, 512>>>(out, 200000);   // clocks up before timing
   cudaDeviceSynchronize();
   run<16, 4, 1>(x, y, k, out);
+  run<16, 4, 1, 1>(x, y, k, out);
+  run<16, 4, 2, 1>(x, y, k, out);
+  run<16, 8, 1, 1>(x, y, k, out);
+  run<16, 2, 4, 1>(x, y, k, out);
+  run<16, 4, 4, 1>(x, y, k, out);
   run<16, 4, 2>(x, y, k, out);
   run<16, 4, 4>(x, y, k, out);
   run<16, 8, 1>(x, y, k, out);
