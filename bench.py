@@ -286,14 +286,20 @@ def load_peaks():
     return {"hbm_gbs": 6650.0}, "fallback (B200_PROFILING.md)"
 
 
-def ncu_traffic(workload, mode, iters):
-    """DRAM bytes per conv_solve_kernel launch from the committed ncu --set full
-    capture of the same workload (profiles/ncu_traffic.json), else None."""
+def ncu_traffic(workload, mode, iters, kernel="conv_solve_kernel"):
+    """DRAM bytes per launch of the dominant kernel from the committed ncu --set
+    full capture of the same workload (profiles/ncu_traffic.json), else None."""
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(tpath) or mode != "strict":
         return None, None
-    ent = json.load(open(tpath)).get(workload)
-    if not ent or ent.get("iters") != iters:
+    tab = json.load(open(tpath))
+    if kernel == "step_ca_kernel":
+        ent = tab.get(f"{workload}_step_ca")
+    else:
+        ent = tab.get(workload)
+        if ent and ent.get("iters") != iters:
+            ent = None
+    if not ent:
         return None, None
     return ent["dram_bytes_per_launch"], ent.get("source")
 
@@ -427,7 +433,7 @@ def run_native(args):
         dom_kernel = "step_ca_kernel"
         dom_flop = (2.0 * 2.0 * K * K + 50.0) * N              # two forward K x K passes + TV terms per launch
         achieved_tf = dom_flop * dom_n / (dom_ms * 1e-3) / 1e12
-        dom_share = dom_ms * 1e-3 / sum(times)
+        dom_share = (dom_ms / dom_n) * 1e-3 * vgs / sum(times)   # one launch per lower iteration (vg evals)
     else:
         dom_kernel, dom_flop, dom_share = "conv_solve_kernel", flop_px_it * units / len(times), 1.0
         achieved_tf = step_total_tf
@@ -438,13 +444,14 @@ def run_native(args):
     bytes_px_it = 48.0 if dtype == "float64" else 24.0
     peaks, peak_src = load_peaks()
     hbm = peaks["hbm_gbs"]
-    traffic, tsrc = ncu_traffic(wl, mode, args.iters)
+    traffic, tsrc = ncu_traffic(wl, mode, args.iters, dom_kernel)
     strict = mode == "strict" and dtype == "float64"
     roof = {"bound": "fp64", "achieved": achieved_tf, "peak": peak, "unit": "TFLOP/s",
             "frac": achieved_tf / peak, "traffic": traffic,
-            "traffic_note": (f"DRAM read+write bytes per conv_solve_kernel launch (one step) from {tsrc}; "
-                             f"algorithmic: {bytes_px_it:.0f} B/px-it = {bytes_px_it * units / len(times) / 1e9:.2f} "
-                             "GB per step" if traffic else "no committed ncu capture for this exact workload"),
+            "traffic_note": (f"DRAM read+write bytes per {dom_kernel} launch from {tsrc}; algorithmic: "
+                             f"{bytes_px_it:.0f} B/px-it = {bytes_px_it * units / len(times) / 1e9:.2f} GB per step "
+                             "(the c3 working set is L2-resident)" if traffic else
+                             "no committed ncu capture for this exact workload"),
             "peak_source": "measured live on this GPU: DFMA microbenchmark (adp_fp64_peak, 2 flop/DFMA); "
                            "MEASURED_PEAKS.json has no FP64 entry",
             "peak_nominal_tflops": NOMINAL_FP64_TF,
