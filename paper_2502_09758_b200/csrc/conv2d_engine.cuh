@@ -125,6 +125,8 @@ struct Conv {
   const ConvArgs<T>& a;
   int ch, ty, tx;                // this thread's channel, tile row, column group
   int tb0, tbs;                  // stageA / stageC tile walk: first tile, stride (default: the grid)
+  bool opsm = false;             // stageA / stageC (fused, float64): epilogue operands staged in the term
+                                 // buffers by asynchronous copies instead of registers held across the stencil
 
   __device__ __forceinline__ int nC() const { return KS > 0 ? 1 : a.g.C; }
   // plane column of box column `col` (box column 0 = image column w0 - rw - 1):
@@ -612,6 +614,30 @@ struct Conv {
   __device__ __forceinline__ void put_term(int buf, int r, int q, double v) const {
     tm()[(size_t)buf * a.g.TH * a.g.TW * nC() + ((size_t)r * a.g.TW + q) * nC() + ch] = v;
   }
+  // opsm: the operand staged in term buffer `buf` for own pixel (r, q), read before that slot's term
+  // is written (same thread); else the prefetched register
+  __device__ __forceinline__ T opv(int buf, int r, int q, const T (&pre)[RW], int o) const {
+    if constexpr (sizeof(T) == 8) {
+      if (opsm) return (T)tm()[(size_t)buf * a.g.TH * a.g.TW * nC() + ((size_t)r * a.g.TW + q) * nC() + ch];
+    }
+    return pre[o];
+  }
+  // asynchronous copy of the tile's own pixels of `src` into term buffer `buf` (rows of TW * C
+  // contiguous doubles, 16-byte copies; rows outside the image zero-filled)
+  __device__ void stage_own(int h0, int w0, const T* src, int buf) const {
+    if constexpr (sizeof(T) == 8) {
+      const int C = nC(), H = a.g.H, W = a.g.W;
+      const int rowE = a.g.TW * C, pairs = rowE >> 1;
+      double* dst = tm() + (size_t)buf * a.g.TH * rowE;
+      for (int k = threadIdx.x; k < a.g.TH * pairs; k += blockDim.x) {
+        const int r = k / pairs, e = (k - r * pairs) * 2;
+        const int h = h0 + r;
+        const int64_t gi = ((int64_t)h * W + w0) * C + e;
+        const int valid = (h < H && w0 * C + e < W * C) ? 16 : 0;
+        cp_async16(dst + (size_t)r * rowE + e, valid ? (const double*)src + gi : (const double*)src, valid);
+      }
+    }
+  }
 
   // =========================================================================
   // Stage A: r = B y - ydat (write R); TV at y: root terms, grad -> TVG
@@ -644,7 +670,7 @@ struct Conv {
       const int w = w0 + q;
       if (h < H && w < W) {
         const int64_t i = gidx(h, w, ch);
-        const T r = acc[o] - ypre[o];
+        const T r = acc[o] - opv(tb + 0, ty, q, ypre, o);
         Rout[i] = r;
         if (fused) put_term(tb + 0, ty, q, (double)(r * r));
       }
@@ -723,12 +749,19 @@ struct Conv {
       __syncthreads();
       const int h = h0 + ty;
       T ypre[RW];   // epilogue operands: issued before the tile box so both share one round trip
+      if (opsm && fused) {
+        stage_own(h0, w0, ydat, 0);
 #pragma unroll
-      for (int o = 0; o < RW; ++o) {
-        const int w = w0 + tx * RW + o;
-        ypre[o] = (h < H && w < W) ? ydat[gidx(h, w, ch)] : T(0);
+        for (int o = 0; o < RW; ++o) ypre[o] = T(0);
+      } else {
+#pragma unroll
+        for (int o = 0; o < RW; ++o) {
+          const int w = w0 + tx * RW + o;
+          ypre[o] = (h < H && w < W) ? ydat[gidx(h, w, ch)] : T(0);
+        }
       }
       load_full(h0, w0, src);
+      if (opsm && fused) cp_async_wait_all();
       __syncthreads();
       tileA(pa(), pa(), 0, h0, w0, ypre, Rout, tv, TV2out, TVGout, fused);
       if (fused) tile_leaves(h0, w0, tv ? 3 : 1, sfit, stv, (int)(a.g.Ng / a.g.leafL));
@@ -1000,7 +1033,8 @@ struct Conv {
       const int w = w0 + q;
       if (h < H && w < W) {
         const int64_t i = gidx(h, w, ch);
-        const T rc = acc[o] - ypre[o];
+        const T yv = opv(0, ty, q, ypre, o), gv = opv(1, ty, q, gpre, o), xov = opv(2, ty, q, xopre, o);
+        const T rc = acc[o] - yv;
         const T xc = fpr(pr, ty, q);
         if (fused) put_term(0, ty, q, (double)(rc * rc));
         else RCout[i] = rc;
@@ -1018,7 +1052,7 @@ struct Conv {
           }
         }
         if (Xout) Xout[i] = xc;
-        if (dot) part += (double)gpre[o] * (double)(xc - xopre[o]);
+        if (dot) part += (double)gv * (double)(xc - xov);
       }
     }
     return part;
@@ -1052,10 +1086,23 @@ struct Conv {
       tile_origin(tile, h0, w0);
       __syncthreads();
       T ypre[RW], gpre[RW], xopre[RW];   // epilogue operands, in flight with the tile box
-      prefetch_c(h0, w0, Gin, Xold, sdot != nullptr, ypre, gpre, xopre);
+      const bool st = opsm && fused && sdot != nullptr;
+      if (st) {
+        stage_own(h0, w0, a.ydat, 0);
+        stage_own(h0, w0, Gin, 1);
+        stage_own(h0, w0, Xold, 2);
+#pragma unroll
+        for (int o = 0; o < RW; ++o) ypre[o] = gpre[o] = xopre[o] = T(0);
+      } else {
+        prefetch_c(h0, w0, Gin, Xold, sdot != nullptr, ypre, gpre, xopre);
+      }
       load_full(h0, w0, src);
+      if (st) cp_async_wait_all();
       __syncthreads();
+      const bool keep = opsm;
+      opsm = st;
       const double part = tileC(pa(), h0, w0, ypre, gpre, xopre, RCout, tv, TV2Cout, Xout, sdot != nullptr, fused);
+      opsm = keep;
       if (sdot) tile_partial(*sdot, tile, part);
       if (fused) tile_leaves(h0, w0, tv ? 3 : 1, sfitc, stvc, (int)(a.g.Ng / a.g.leafL));
     }

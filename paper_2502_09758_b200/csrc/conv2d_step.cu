@@ -29,6 +29,7 @@ __global__ void __launch_bounds__(384, 2) step_c_kernel(const __grid_constant__ 
   // x = in1; sflag 1: backtracking retry x_c = y - g / L with y = in0 + beta
   // (in0 - in1), written to out0, x = in0  (lower_solvers.py:170-177)
   Conv<T, FAST, 4> E(a);
+  E.opsm = true;
   E.load_weights(a.kern);
   const bool tv = a.alpha != 0.0;
   if (a.sflag == 0)
@@ -44,6 +45,7 @@ __global__ void __launch_bounds__(384, 2) step_a_kernel(const __grid_constant__ 
   // materialised y'); 1: y = in0 + beta (in0 - in1).  Sums into s_fit/s_tv
   // (sflag & 2: the second set s_fit2/s_tv2)
   Conv<T, FAST, 4> E(a);
+  E.opsm = true;
   E.load_weights(a.kern);
   const bool tv = a.alpha != 0.0;
   const SumDev* sf = (a.sflag & 2) ? &a.s_fit2 : &a.s_fit;
@@ -60,6 +62,7 @@ __global__ void __launch_bounds__(384, 2) step_a_kernel(const __grid_constant__ 
 template <typename T, bool FAST>
 __global__ void __launch_bounds__(384, 2) step_ca_kernel(const __grid_constant__ ConvArgs<T> a) {
   Conv<T, FAST, 4> E(a);
+  E.opsm = true;
   E.load_weights(a.kern);
   const bool tv = a.alpha != 0.0;
   const int nT = a.g.nTiles;
