@@ -572,7 +572,8 @@ static int conv_plan_init(PlanImpl& P) {
     const char* ev = getenv("ADP_STEP");
     const int want = ev ? atoi(ev) : -1;
     if (want != 0 && P.d.dtype == ADP_DTYPE_F64 && g.rwb == 4 && g.fused && g.fuseCA && !slab &&
-        g.threads <= 384 && (want == 1 || g.N >= (1 << 18))) {
+        g.threads <= 384 && (want == 1 || g.N >= (1 << 18)) && g.kh * g.kw * g.C <= kStepWMax &&
+        g.tpc % 32 == 0) {   // taps as kernel parameters; channel-uniform warps
       const size_t es = (size_t)P.esize;
       const size_t pa = ((size_t)g.C * g.SH * g.SWP * es + 127) & ~size_t(127);
       const size_t tm = (size_t)3 * g.TH * g.TW * g.C * sizeof(double);
@@ -585,8 +586,10 @@ static int conv_plan_init(PlanImpl& P) {
           setup_kernel(P, P.k_sca, sk.ca, g.threads, P.step_smem, 2 * g.nTiles) == ADP_OK &&
           setup_kernel(P, P.k_sc, sk.c, g.threads, P.step_smem, g.nTiles) == ADP_OK &&
           setup_kernel(P, P.k_sa, sk.a, g.threads, P.step_smem, g.nTiles) == ADP_OK &&
-          setup_kernel(P, P.k_sred, sk.red, g.threads, P.smem, g.nTiles) == ADP_OK)
+          setup_kernel(P, P.k_sred, sk.red, g.threads, P.smem, g.nTiles) == ADP_OK) {
+        CK(cudaMallocHost(&P.h_kern, (size_t)g.kh * g.kw * g.C * sizeof(double)));
         P.step = 1;
+      }
     }
   }
   const int maxg = g.nTiles;
@@ -809,6 +812,7 @@ void adp_plan_destroy(adp_plan* p) {
   if (P.h_cres) cudaFreeHost(P.h_cres);
   if (P.h_scal) cudaFreeHost(P.h_scal);
   if (P.h_flag) cudaFreeHost(P.h_flag);
+  if (P.h_kern) cudaFreeHost(P.h_kern);
   if (P.prof_ev[0]) cudaEventDestroy(P.prof_ev[0]);
   if (P.prof_ev[1]) cudaEventDestroy(P.prof_ev[1]);
   delete p;
@@ -941,8 +945,8 @@ int adp_lower_hess_diag(adp_plan* p, const adp_lower* lp, const void* x, void* o
 // flow here, expression for expression (conv_solve_kernel), so iterates,
 // decisions and counters are identical to the single-launch solve.
 static int step_launch(PlanImpl& P, KernelInfo& k, ConvArgs<double>& a, cudaStream_t st, bool coop, size_t smem,
-                       int grid) {
-  void* args[] = {&a};
+                       int grid, const StepW* wt = nullptr) {
+  void* args[] = {&a, (void*)wt};
   if (coop) {
     CK(cudaMemsetAsync(P.d_bar, 0, sizeof(unsigned int), st));
     CK(cudaLaunchCooperativeKernel(k.fn, dim3(grid), dim3(P.g.threads), args, smem, st));
@@ -958,6 +962,18 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
   const ConvGeom& g = P.g;
   ConvArgs<T> base = conv_base<T>(P);
   set_lower(base, lp);
+  // the stage kernels' taps as kernel parameters (StepW): forward [c][i][j] and flipped, ndimage's
+  // |w| <= DBL_EPSILON taps zeroed (Conv::load_weights' rule)
+  const int kk = g.kh * g.kw, nk = kk * g.C;
+  CK(cudaMemcpyAsync(P.h_kern, lp->kernel, (size_t)nk * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int e = 0; e < nk; ++e) {
+    const int c = e % g.C, ij = e / g.C, i = ij / g.kw, j = ij % g.kw;
+    double w = P.h_kern[e];
+    if (!(fabs(w) > 2.220446049250313e-16)) w = 0.0;
+    P.wfwd.w[(c * g.kh + i) * g.kw + j] = w;
+    P.wadj.w[(c * g.kh + (g.kh - 1 - i)) * g.kw + (g.kw - 1 - j)] = w;
+  }
   ConvArgs<T> sa_args = base;   // stage kernels: one plane region, term buffers right after it
   sa_args.g.o_tm = P.step_o_tm;
   sa_args.g.o_pa2 = P.step_o_tm;   // never addressed with one tile per CTA
@@ -1042,7 +1058,7 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
     if (!a_ready) {   // stage A at y = x + beta (x - x_prev), sums set `par`
       ConvArgs<T> a = sa_args;
       a.in0 = X[ix]; a.in1 = X[ixp]; a.sbeta = beta; a.sflag = 1 | (par ? 2 : 0);
-      if (int e = step_launch(P, P.k_sa, a, st, false, P.step_smem, nT)) return e;
+      if (int e = step_launch(P, P.k_sa, a, st, false, P.step_smem, nT, &P.wfwd)) return e;
       ++launches;
     }
     const double t_next2 = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t_mom * t_mom));   // next momentum, no restart
@@ -1051,7 +1067,7 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
       ConvArgs<T> a = sa_args;
       a.in0 = X[ix]; a.in1 = X[ixp]; a.out0 = X[ic]; a.out1 = Yn;
       a.sbeta = beta; a.sL = L_try; a.sbetaN = beta2;
-      if (int e = step_launch(P, P.k_sb, a, st, false, P.step_smem_b, nT)) return e;
+      if (int e = step_launch(P, P.k_sb, a, st, false, P.step_smem_b, nT, &P.wadj)) return e;
       ++launches;
     }
     {   // candidate value + restart dot, and the speculative stage A at y' (valid iff the candidate is
@@ -1060,7 +1076,7 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
       a.in0 = X[ic]; a.in1 = X[ix]; a.out1 = Yn; a.sflag = par ? 0 : 2;
       prof_now = P.profile && (t % P.profile == 0);   // sampled: every P.profile-th iteration
       if (prof_now) CK(cudaEventRecord(P.prof_ev[0], st));
-      if (int e = step_launch(P, P.k_sca, a, st, false, P.step_smem, 2 * nT)) return e;
+      if (int e = step_launch(P, P.k_sca, a, st, false, P.step_smem, 2 * nT, &P.wfwd)) return e;
       if (prof_now) CK(cudaEventRecord(P.prof_ev[1], st));
       ++launches;
     }
@@ -1104,7 +1120,7 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
       if (++k >= 60) { status = ST_BT_FAIL; fail_iter = t; break; }
       ConvArgs<T> a = sa_args;
       a.in0 = X[ix]; a.in1 = X[ixp]; a.out0 = X[ic]; a.sbeta = beta; a.sL = L_try; a.sflag = 1;
-      if (int e = step_launch(P, P.k_sc, a, st, false, P.step_smem, nT)) return e;
+      if (int e = step_launch(P, P.k_sc, a, st, false, P.step_smem, nT, &P.wfwd)) return e;
       ++launches;
       ++vals;
       if (int e = reduce(2, 3)) return e;

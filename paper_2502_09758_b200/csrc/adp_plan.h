@@ -6,6 +6,7 @@
 #include <string>
 #include <vector>
 #include "adp_types.h"
+#include "conv2d_args.h"   // StepW
 #include "../../include/adp_b200.h"
 
 namespace adp {
@@ -75,6 +76,8 @@ struct PlanImpl {
   const void* k_extrap = nullptr;
   size_t step_smem = 0;
   int step_o_tm = 0;
+  double* h_kern = nullptr;     // pinned: the solve's stencil, read back to build the stage kernels' tap sets
+  StepW wfwd{}, wadj{};         // forward / flipped taps (kernel parameters of the stage kernels)
   CUtensorMap tm[5];            // X[0..2], R, P[0]
   // pinned host staging
   SolveOut* h_sres = nullptr;

@@ -92,6 +92,14 @@ struct ConvArgs {
   CUtensorMap tm[5];
 };
 
+// Host-stepped stage kernels: the launch's tap set as a kernel parameter
+// (constant bank 0), channel-major [c][i][j] with ndimage's |w| <= DBL_EPSILON
+// taps zeroed; forward taps for the value passes, flipped for the adjoint.
+constexpr int kStepWMax = 1024;
+struct StepW {
+  double w[kStepWMax];
+};
+
 template <typename T>
 struct KgcArgs {
   ConvGeom g;

@@ -116,7 +116,13 @@ template <typename T> struct Plain {
 // KS > 0: the stencil size is a compile-time constant (the latency-bound c2
 // solve kernel is instantiated with KS = 9 so it carries no other stencil
 // variant); KS = 0: runtime dispatch over the unrolled sizes + generic loop.
-template <typename T, bool FAST, int RW, int KS = 0, bool TMA = false>
+// PW: the stencil taps come from a kernel-parameter array (constant bank 0,
+// the host-stepped stage kernels: StepW) instead of shared memory; warps are
+// channel-uniform (tpc % 32 == 0, host check), so the channel index is moved
+// to a uniform register and every tap is an LDCU into the uniform register
+// file feeding DMUL's second operand: no shared-memory wavefronts or vector
+// registers for the weights, no per-CTA weight staging.
+template <typename T, bool FAST, int RW, int KS = 0, bool TMA = false, bool PW = false>
 struct Conv {
   static_assert((RW & (RW - 1)) == 0, "RW must be a power of two");
   static constexpr int kShift = RW == 1 ? 0 : RW == 2 ? 1 : RW == 4 ? 2 : 3;
@@ -127,6 +133,8 @@ struct Conv {
   int tb0, tbs;                  // stageA / stageC tile walk: first tile, stride (default: the grid)
   bool opsm = false;             // stageA / stageC (fused, float64): epilogue operands staged in the term
                                  // buffers by asynchronous copies instead of registers held across the stencil
+  const T* pw = nullptr;         // PW: the launch's tap set in parameter space ([c][i][j], forward or flipped)
+  int chu = 0;                   // PW: ch in a uniform register
 
   __device__ __forceinline__ int nC() const { return KS > 0 ? 1 : a.g.C; }
   // plane column of box column `col` (box column 0 = image column w0 - rw - 1):
@@ -142,6 +150,7 @@ struct Conv {
     // KS > 0 instances serve single-channel images only (host check), so the
     // channel index and count are compile-time
     ch = KS > 0 ? 0 : (int)(threadIdx.x / a.g.tpc);
+    if constexpr (PW) chu = __reduce_max_sync(0xffffffffu, ch);
     const int r = threadIdx.x - ch * a.g.tpc;
     ty = r / tpr;
     tx = r - ty * tpr;
@@ -167,6 +176,16 @@ struct Conv {
   __device__ __forceinline__ double* tm() const { return reinterpret_cast<double*>(sbase() + a.g.o_tm); }
   __device__ __forceinline__ double* sv() const { return reinterpret_cast<double*>(sbase() + a.g.o_sv); }
   __device__ __forceinline__ T* plane(int c) const { return pa() + (size_t)c * a.g.SH * swp(); }
+  // this thread's channel taps: forward (correlation) and flipped (adjoint);
+  // PW kernels carry exactly one of the two sets, chosen by the host
+  __device__ __forceinline__ const T* wfwd() const {
+    if constexpr (PW) return pw + chu * a.g.kh * a.g.kw;
+    else return ws() + ch * a.g.kh * a.g.kw;
+  }
+  __device__ __forceinline__ const T* wadj() const {
+    if constexpr (PW) return pw + chu * a.g.kh * a.g.kw;
+    else return wf() + ch * a.g.kh * a.g.kw;
+  }
 
   // ---- weights: ws[c][i][j] = kern[i][j][c] (|w| <= eps -> 0), wf flipped
   __device__ void load_weights(const T* kern) {
@@ -452,7 +471,7 @@ struct Conv {
   // forward taps over two regions; the compile-time-K kernels share the tap loads
   __device__ __forceinline__ void stencil_fwd_pair(const T* pr1, const T* pr2, T (&acc1)[RW], T (&acc2)[RW]) const {
     const size_t co = (size_t)ch * a.g.SH * swp();
-    const T* w = ws() + ch * a.g.kh * a.g.kw;
+    const T* w = wfwd();
     if constexpr (KS > 0) {
       stencil_k2<KS>(pr1 + co, pr2 + co, w, acc1, acc2);
     } else {
@@ -540,10 +559,10 @@ struct Conv {
     }
   }
   __device__ __forceinline__ void stencil_fwd(T (&acc)[RW]) const {
-    stencil(plane(ch), ws() + ch * a.g.kh * a.g.kw, acc);
+    stencil(plane(ch), wfwd(), acc);
   }
   __device__ __forceinline__ void stencil_adj(T (&acc)[RW]) const {
-    stencil(plane(ch), wf() + ch * a.g.kh * a.g.kw, acc);
+    stencil(plane(ch), wadj(), acc);
   }
 
   // plane value of this thread's channel at tile pixel (r, q)
@@ -662,7 +681,7 @@ struct Conv {
 #pragma unroll
       for (int o = 0; o < RW; ++o) acc[o] = pre_acc[o];
     } else {
-      stencil(pr + (size_t)ch * a.g.SH * swp(), ws() + ch * a.g.kh * a.g.kw, acc);
+      stencil(pr + (size_t)ch * a.g.SH * swp(), wfwd(), acc);
     }
 #pragma unroll
     for (int o = 0; o < RW; ++o) {
@@ -869,7 +888,7 @@ struct Conv {
       __syncthreads();
       double part = 0.0;
       T acc[RW];
-      stencil(cur + co, wf() + ch * a.g.kh * a.g.kw, acc);
+      stencil(cur + co, wadj(), acc);
 #pragma unroll
       for (int o = 0; o < RW; ++o) {
         const int w = w0 + tx * RW + o;
@@ -1025,7 +1044,7 @@ struct Conv {
 #pragma unroll
       for (int o = 0; o < RW; ++o) acc[o] = pre_acc[o];
     } else {
-      stencil(pr + (size_t)ch * a.g.SH * swp(), ws() + ch * a.g.kh * a.g.kw, acc);
+      stencil(pr + (size_t)ch * a.g.SH * swp(), wfwd(), acc);
     }
 #pragma unroll
     for (int o = 0; o < RW; ++o) {

@@ -8,29 +8,32 @@
 // Every stage computes exactly the persistent kernel's arithmetic (same stage
 // methods, tiles, fused leaves, tile partials and trees), so iterates and
 // decisions are bitwise identical to it.
+// Taps: a StepW kernel parameter (see Conv's PW), not shared memory.
 #include "conv2d_kernels.cuh"
 
 namespace adp {
 
 template <typename T, bool FAST>
-__global__ void __launch_bounds__(384, 3) step_b_kernel(const __grid_constant__ ConvArgs<T> a) {
+__global__ void __launch_bounds__(384, 3) step_b_kernel(const __grid_constant__ ConvArgs<T> a,
+                                                            const __grid_constant__ StepW wt) {
   // g at y (stage B), first candidate x_c = y - g / L -> out0, next
-  // extrapolation point y' = x_c + betaN (x_c - x) -> out1
-  Conv<T, FAST, 4> E(a);
-  E.load_weights(a.kern);
+  // extrapolation point y' = x_c + betaN (x_c - x) -> out1; wt: flipped taps
+  Conv<T, FAST, 4, 0, false, true> E(a);
+  E.pw = wt.w;
   E.stageB_pipe(a.R, a.alpha != 0.0, a.TVG, a.G, &a.s_t0, a.in0, a.in1, T(a.sbeta), T(a.sL), a.out0, T(a.sbetaN),
                 a.out1);
 }
 
 template <typename T, bool FAST>
-__global__ void __launch_bounds__(384, 2) step_c_kernel(const __grid_constant__ ConvArgs<T> a) {
+__global__ void __launch_bounds__(384, 2) step_c_kernel(const __grid_constant__ ConvArgs<T> a,
+                                                            const __grid_constant__ StepW wt) {
   // value at the candidate (lower_value form) + restart-dot partial
   // g.(x_c - x).  sflag 0: the first candidate x_c = in0 (stage B wrote it),
   // x = in1; sflag 1: backtracking retry x_c = y - g / L with y = in0 + beta
   // (in0 - in1), written to out0, x = in0  (lower_solvers.py:170-177)
-  Conv<T, FAST, 4> E(a);
+  Conv<T, FAST, 4, 0, false, true> E(a);   // wt: forward taps
   E.opsm = true;
-  E.load_weights(a.kern);
+  E.pw = wt.w;
   const bool tv = a.alpha != 0.0;
   if (a.sflag == 0)
     E.stageC(SrcLin<T>{a.in0}, a.RC, tv, a.TV2C, nullptr, a.G, a.in1, &a.s_t1, &a.s_fitc, &a.s_tvc);
@@ -40,13 +43,14 @@ __global__ void __launch_bounds__(384, 2) step_c_kernel(const __grid_constant__ 
 }
 
 template <typename T, bool FAST>
-__global__ void __launch_bounds__(384, 2) step_a_kernel(const __grid_constant__ ConvArgs<T> a) {
+__global__ void __launch_bounds__(384, 2) step_a_kernel(const __grid_constant__ ConvArgs<T> a,
+                                                            const __grid_constant__ StepW wt) {
   // value + TV gradient terms at a point (stage A): sflag 0: y = in0 (the
   // materialised y'); 1: y = in0 + beta (in0 - in1).  Sums into s_fit/s_tv
   // (sflag & 2: the second set s_fit2/s_tv2)
-  Conv<T, FAST, 4> E(a);
+  Conv<T, FAST, 4, 0, false, true> E(a);   // wt: forward taps
   E.opsm = true;
-  E.load_weights(a.kern);
+  E.pw = wt.w;
   const bool tv = a.alpha != 0.0;
   const SumDev* sf = (a.sflag & 2) ? &a.s_fit2 : &a.s_fit;
   const SumDev* st = (a.sflag & 2) ? &a.s_tv2 : &a.s_tv;
@@ -60,10 +64,11 @@ __global__ void __launch_bounds__(384, 2) step_a_kernel(const __grid_constant__ 
 // (as step_a, sflag 0 / 2 in sL > 0 ? set 2 : set 1) in ONE launch of 2 x nTiles
 // CTAs: the two independent passes share the waves (one tail instead of two)
 template <typename T, bool FAST>
-__global__ void __launch_bounds__(384, 2) step_ca_kernel(const __grid_constant__ ConvArgs<T> a) {
-  Conv<T, FAST, 4> E(a);
+__global__ void __launch_bounds__(384, 2) step_ca_kernel(const __grid_constant__ ConvArgs<T> a,
+                                                            const __grid_constant__ StepW wt) {
+  Conv<T, FAST, 4, 0, false, true> E(a);   // wt: forward taps
   E.opsm = true;
-  E.load_weights(a.kern);
+  E.pw = wt.w;
   const bool tv = a.alpha != 0.0;
   const int nT = a.g.nTiles;
   if ((int)blockIdx.x < nT) {
