@@ -62,25 +62,45 @@ __global__ void __launch_bounds__(384, 2) step_a_kernel(const __grid_constant__ 
 
 // candidate value (as step_c, sflag 0) and speculative stage A at y' = out1
 // (as step_a, sflag 0 / 2 in sL > 0 ? set 2 : set 1) in ONE launch of 2 x nTiles
-// CTAs: the two independent passes share the waves (one tail instead of two)
+// CTAs: the two independent passes share the waves (one tail instead of two).
+// Both halves run ONE code path up to the end of the stencil (epilogue operands
+// and the tile box as asynchronous copies, then the forward taps), so the
+// kernel carries a single copy of the unrolled stencil (instruction-cache
+// footprint); the epilogues are stageC's / stageA's (tileC / tileA on the
+// precomputed accumulators: the same arithmetic).
 template <typename T, bool FAST>
 __global__ void __launch_bounds__(384, 2) step_ca_kernel(const __grid_constant__ ConvArgs<T> a,
                                                             const __grid_constant__ StepW wt) {
   Conv<T, FAST, 4, 0, false, true> E(a);   // wt: forward taps
-  E.opsm = true;
   E.pw = wt.w;
   const bool tv = a.alpha != 0.0;
   const int nT = a.g.nTiles;
-  if ((int)blockIdx.x < nT) {
-    E.tb0 = blockIdx.x;
-    E.tbs = nT;
-    E.stageC(SrcLin<T>{a.in0}, a.RC, tv, a.TV2C, nullptr, a.G, a.in1, &a.s_t1, &a.s_fitc, &a.s_tvc);
+  const bool isC = (int)blockIdx.x < nT;
+  const int tile = isC ? (int)blockIdx.x : (int)blockIdx.x - nT;
+  int h0, w0;
+  E.tile_origin(tile, h0, w0);
+  E.stage_own(h0, w0, a.ydat, 0);
+  if (isC) {
+    E.stage_own(h0, w0, a.G, 1);
+    E.stage_own(h0, w0, a.in1, 2);
+  }
+  E.load_async(h0, w0, isC ? a.in0 : a.out1, E.pa());
+  cp_async_wait_all();
+  __syncthreads();
+  T acc[4];
+  E.stencil(E.pa() + (size_t)E.ch * a.g.SH * E.swp(), E.wfwd(), acc);
+  const T z[4] = {T(0), T(0), T(0), T(0)};
+  E.opsm = true;
+  const int koff = (int)(a.g.Ng / a.g.leafL);
+  if (isC) {
+    const double part = E.tileC(E.pa(), h0, w0, z, z, z, a.RC, tv, a.TV2C, nullptr, true, true, acc);
+    E.tile_partial(a.s_t1, tile, part);
+    E.tile_leaves(h0, w0, tv ? 3 : 1, &a.s_fitc, &a.s_tvc, koff);
   } else {
-    E.tb0 = blockIdx.x - nT;
-    E.tbs = nT;
     const SumDev* sf = (a.sflag & 2) ? &a.s_fit2 : &a.s_fit;
     const SumDev* st = (a.sflag & 2) ? &a.s_tv2 : &a.s_tv;
-    E.stageA(SrcLin<T>{a.out1}, a.R, a.ydat, tv, a.TV2, a.TVG, sf, st);
+    E.tileA(E.pa(), E.pa(), 0, h0, w0, z, a.R, tv, a.TV2, a.TVG, true, acc);
+    E.tile_leaves(h0, w0, tv ? 3 : 1, sf, st, koff);
   }
 }
 
