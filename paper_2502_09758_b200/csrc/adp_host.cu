@@ -581,7 +581,7 @@ static int conv_plan_init(PlanImpl& P) {
       P.step_smem = (size_t)P.step_o_tm + tm;
       StepKernels sk = step_kernels(P.d.mode == ADP_MODE_FAST);
       P.k_extrap = sk.extrap;
-      P.step_smem_b = (size_t)g.o_pa + pa;   // stage B: no term buffers (three CTAs per SM)
+      P.step_smem_b = sk.b_ep == 2 ? P.step_smem : (size_t)g.o_pa + pa;   // stage B: no term buffers (three CTAs per SM)
       if (setup_kernel(P, P.k_sb, sk.b, g.threads, P.step_smem_b, g.nTiles) == ADP_OK &&
           setup_kernel(P, P.k_sca, sk.ca, g.threads, P.step_smem, 2 * g.nTiles) == ADP_OK &&
           setup_kernel(P, P.k_sc, sk.c, g.threads, P.step_smem, g.nTiles) == ADP_OK &&

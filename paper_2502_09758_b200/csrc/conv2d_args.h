@@ -137,6 +137,7 @@ struct StepKernels {
   const void* red;
   const void* extrap;
   const void* ca;
+  int b_ep;        // stage-B epilogue operand variant (2: term buffers, two CTAs per SM)
 };
 StepKernels step_kernels(int fast);
 // thread bound of the compile-time-stencil solve kernel (the host selects it

@@ -9,19 +9,86 @@
 // methods, tiles, fused leaves, tile partials and trees), so iterates and
 // decisions are bitwise identical to it.
 // Taps: a StepW kernel parameter (see Conv's PW), not shared memory.
+#include <cstdlib>
 #include "conv2d_kernels.cuh"
 
 namespace adp {
 
-template <typename T, bool FAST>
-__global__ void __launch_bounds__(384, 3) step_b_kernel(const __grid_constant__ ConvArgs<T> a,
-                                                            const __grid_constant__ StepW wt) {
-  // g at y (stage B), first candidate x_c = y - g / L -> out0, next
-  // extrapolation point y' = x_c + betaN (x_c - x) -> out1; wt: flipped taps
+// Stage B on one tile (stageB_pipe's arithmetic, expression for expression):
+// g = 2 B^T r + alpha tvg -> G, tile partial of g.g, the first candidate
+// x_c = (x + beta (x - x_prev)) - g / L -> out0 and the next extrapolation
+// point y' = x_c + betaN (x_c - x) -> out1.  wt: flipped taps.  EP selects
+// where the epilogue operands (tvg, x, x_prev) come from: 0 registers loaded
+// before the stencil, 1 registers loaded after it, 2 term buffers filled by
+// asynchronous copies with the tile box (two CTAs per SM instead of three;
+// the default: c3 4.86 / 4.83 / 4.99 Gpx-it/s for EP = 0 / 1 / 2).
+template <typename T, bool FAST, int EP>
+__global__ void __launch_bounds__(384, EP == 2 ? 2 : 3) step_b_kernel(const __grid_constant__ ConvArgs<T> a,
+                                                                      const __grid_constant__ StepW wt) {
   Conv<T, FAST, 4, 0, false, true> E(a);
   E.pw = wt.w;
-  E.stageB_pipe(a.R, a.alpha != 0.0, a.TVG, a.G, &a.s_t0, a.in0, a.in1, T(a.sbeta), T(a.sL), a.out0, T(a.sbetaN),
-                a.out1);
+  const bool tv = a.alpha != 0.0;
+  const T two = T(2), alpha = T(a.alpha), beta = T(a.sbeta), L = T(a.sL), betaN = T(a.sbetaN);
+  const int H = a.g.H, W = a.g.W;
+  const int tile = blockIdx.x;
+  int h0, w0;
+  E.tile_origin(tile, h0, w0);
+  if (EP == 2) {
+    if (tv) E.stage_own(h0, w0, a.TVG, 0);
+    E.stage_own(h0, w0, a.in0, 1);
+    E.stage_own(h0, w0, a.in1, 2);
+  }
+  E.load_async(h0, w0, a.R, E.pa());
+  cp_commit();
+  const int h = h0 + E.ty;
+  T tpre[4], xpre[4], xppre[4];
+  auto fetch = [&]() {
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {
+      const int w = w0 + E.tx * 4 + o;
+      tpre[o] = xpre[o] = xppre[o] = T(0);
+      if (h < H && w < W) {
+        const int64_t i = E.gidx(h, w, E.ch);
+        if (tv) tpre[o] = ldcg(a.TVG + i);
+        xpre[o] = ldcg(a.in0 + i);
+        xppre[o] = ldcg(a.in1 + i);
+      }
+    }
+  };
+  if (EP == 0) fetch();
+  cp_wait<0>();
+  __syncthreads();
+  T acc[4];
+  E.stencil(E.pa() + (size_t)E.ch * a.g.SH * E.swp(), E.wadj(), acc);
+  if (EP == 1) fetch();
+  double part = 0.0;
+#pragma unroll
+  for (int o = 0; o < 4; ++o) {
+    const int q = E.tx * 4 + o;
+    const int w = w0 + q;
+    if (h < H && w < W) {
+      const int64_t i = E.gidx(h, w, E.ch);
+      T tg, xv, xpv;
+      if (EP == 2) {
+        E.opsm = true;
+        tg = tv ? E.opv(0, E.ty, q, tpre, o) : T(0);
+        xv = E.opv(1, E.ty, q, xpre, o);
+        xpv = E.opv(2, E.ty, q, xppre, o);
+      } else {
+        tg = tpre[o];
+        xv = xpre[o];
+        xpv = xppre[o];
+      }
+      T gv = two * acc[o];
+      if (tv) gv = gv + alpha * tg;
+      a.G[i] = gv;
+      part += (double)gv * (double)gv;
+      const T xc = (xv + beta * (xv - xpv)) - gv / L;
+      a.out0[i] = xc;
+      a.out1[i] = xc + betaN * (xc - xv);
+    }
+  }
+  E.tile_partial(a.s_t0, tile, part);
 }
 
 template <typename T, bool FAST>
@@ -138,7 +205,12 @@ __global__ void step_extrap_kernel(const T* x, const T* xp, T beta, T* out, int6
 
 StepKernels step_kernels(int fast) {
   StepKernels k;
-  k.b = fast ? (const void*)step_b_kernel<double, true> : (const void*)step_b_kernel<double, false>;
+  const char* ev = getenv("ADP_SB");   // stage-B epilogue operand variant (see step_b_kernel)
+  const int ep = ev ? atoi(ev) : 2;
+  k.b_ep = ep;
+  if (ep == 1) k.b = fast ? (const void*)step_b_kernel<double, true, 1> : (const void*)step_b_kernel<double, false, 1>;
+  else if (ep == 2) k.b = fast ? (const void*)step_b_kernel<double, true, 2> : (const void*)step_b_kernel<double, false, 2>;
+  else k.b = fast ? (const void*)step_b_kernel<double, true, 0> : (const void*)step_b_kernel<double, false, 0>;
   k.c = fast ? (const void*)step_c_kernel<double, true> : (const void*)step_c_kernel<double, false>;
   k.a = fast ? (const void*)step_a_kernel<double, true> : (const void*)step_a_kernel<double, false>;
   k.red = (const void*)step_reduce_kernel<double>;
