@@ -314,7 +314,8 @@ int adp_slab_upper(adp_plan* p, const void* A_kernel, const void* x, const void*
 int adp_slab_mixed(adp_plan* p, const adp_lower* lp, const void* x_tilde, const void* q, double* part, void* stream);
 int adp_kgc_groups(adp_plan* p, int32_t* ngroups, int32_t* ntaps);
 /* plan execution flags: bit 0 = TMA tile boxes in the solve kernel (c2), bit 1 = host-stepped
- * high-occupancy solve_lower (c3-c5: stage kernels one tile per CTA, scalar control on the host) */
+ * high-occupancy solve_lower (c3-c5: stage kernels one tile per CTA, scalar control on the host),
+ * bit 2 = its decision sums folded inside the stage kernels (no reduction launch; csrc/step_tail.h) */
 int adp_plan_flags(adp_plan* p, int32_t* flags);
 /* enable (period k >= 1) / disable (0) live timing of the dominant kernel of host-stepped solves:
  * every k-th iteration's launch is bracketed by CUDA events on its stream (result fields dominant_ms /

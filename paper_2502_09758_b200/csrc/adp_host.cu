@@ -589,6 +589,26 @@ static int conv_plan_init(PlanImpl& P) {
           setup_kernel(P, P.k_sred, sk.red, g.threads, P.smem, g.nTiles) == ADP_OK) {
         CK(cudaMallocHost(&P.h_kern, (size_t)g.kh * g.kw * g.C * sizeof(double)));
         P.step = 1;
+        // in-kernel decision sums (step_tail.h): whole tiles, tile rows = power-of-two runs of the
+        // perfect sum trees, every fold within one register pass (<= 1024 units); ADP_TAIL=0 disables
+        auto pow2 = [](int64_t v) { return v > 0 && (v & (v - 1)) == 0; };
+        const int64_t GL = (int64_t)g.TH * g.rowL;
+        const char* et = getenv("ADP_TAIL");
+        if (!(et && atoi(et) == 0) && g.H % g.TH == 0 && g.W % g.TW == 0 && pow2(GL) && GL <= 1024 &&
+            pow2(g.tilesW) && g.tilesW <= 1024 && pow2(g.tilesH) && 2 * g.tilesH <= 1024 && P.s_fit.regular &&
+            P.s_tv.regular && P.s_t0.regular && (int64_t)P.s_fit.nLeaves == GL * g.tilesH &&
+            (int64_t)P.s_tv.nLeaves == 2 * GL * g.tilesH && g.threads >= 192) {
+          const size_t nsub = (size_t)11 * g.tilesH * sizeof(double);
+          const size_t ncnt = (size_t)(2 * g.tilesH + 1) * sizeof(unsigned int);
+          CK(cudaMalloc(&P.d_tail, nsub + ncnt));
+          CK(cudaMemset(P.d_tail, 0, nsub + ncnt));
+          P.tail.sub = (double*)P.d_tail;
+          P.tail.cnt = (unsigned int*)((char*)P.d_tail + nsub);
+          P.tail.on = 1;
+          P.tail.nG = g.tilesH;
+          P.tail.GL = (int)GL;
+          P.tail.tW = g.tilesW;
+        }
       }
     }
   }
@@ -808,6 +828,7 @@ void adp_plan_destroy(adp_plan* p) {
   if (P.d.layout == ADP_LAYOUT_DENSE1D) dense_plan_free(P);
   if (P.dmem) cudaFree(P.dmem);
   if (P.d_zero) cudaFree(P.d_zero);
+  if (P.d_tail) cudaFree(P.d_tail);
   if (P.h_sres) cudaFreeHost(P.h_sres);
   if (P.h_cres) cudaFreeHost(P.h_cres);
   if (P.h_scal) cudaFreeHost(P.h_scal);
@@ -945,8 +966,8 @@ int adp_lower_hess_diag(adp_plan* p, const adp_lower* lp, const void* x, void* o
 // flow here, expression for expression (conv_solve_kernel), so iterates,
 // decisions and counters are identical to the single-launch solve.
 static int step_launch(PlanImpl& P, KernelInfo& k, ConvArgs<double>& a, cudaStream_t st, bool coop, size_t smem,
-                       int grid, const StepW* wt = nullptr) {
-  void* args[] = {&a, (void*)wt};
+                       int grid, const StepW* wt = nullptr, const StepTail* tl = nullptr) {
+  void* args[] = {&a, (void*)wt, (void*)tl};
   if (coop) {
     CK(cudaMemsetAsync(P.d_bar, 0, sizeof(unsigned int), st));
     CK(cudaLaunchCooperativeKernel(k.fn, dim3(grid), dim3(P.g.threads), args, smem, st));
@@ -982,7 +1003,7 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
   const double tol = sa->eps * sa->mu;
   long long launches = 0, dom_n = 0;
   double dom_ms = 0.0;
-  bool prof_now = false;
+  bool prof_now = false, prof_pending = false;
   // ---- step size / Lipschitz constant (solve_lower lines 135-140, L_of_b 90-96)
   double lip, lam = sa->norm_sq;
   int pit = 0, pconv = 1;
@@ -1032,6 +1053,16 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
   CK(cudaHostGetDevicePointer((void**)&d_hflag, P.h_flag, 0));
   // the reduction writes its sums and then a sequence number into mapped pinned memory; the host
   // spins on the number (no stream synchronisation on the decision path), checking for errors
+  auto wait_flag = [&](int seq) -> int {
+    for (long long spin = 0; *(volatile int*)P.h_flag != seq; ++spin) {
+      if ((spin & 0xfffff) == 0xfffff) {
+        const cudaError_t q = cudaStreamQuery(st);
+        if (q != cudaErrorNotReady && q != cudaSuccess) return fail(ADP_ERR_CUDA, cudaGetErrorString(q));
+      }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    return ADP_OK;
+  };
   auto reduce = [&](int mode, int n) -> int {
     ConvArgs<T> a = base;
     a.sflag = mode;
@@ -1040,15 +1071,8 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
     a.hseq = ++P.step_seq;
     if (int e = step_launch(P, P.k_sred, a, st, true, P.smem, P.k_sred.grid)) return e;
     ++launches;
-    for (long long spin = 0; *(volatile int*)P.h_flag != a.hseq; ++spin) {
-      if ((spin & 0xfffff) == 0xfffff) {
-        const cudaError_t q = cudaStreamQuery(st);
-        if (q != cudaErrorNotReady && q != cudaSuccess) return fail(ADP_ERR_CUDA, cudaGetErrorString(q));
-      }
-    }
-    std::atomic_thread_fence(std::memory_order_acquire);
     (void)n;
-    return ADP_OK;
+    return wait_flag(a.hseq);
   };
   for (int t = 0; t < sa->max_iters; ++t) {
     const double t_next = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t_mom * t_mom));
@@ -1058,7 +1082,9 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
     if (!a_ready) {   // stage A at y = x + beta (x - x_prev), sums set `par`
       ConvArgs<T> a = sa_args;
       a.in0 = X[ix]; a.in1 = X[ixp]; a.sbeta = beta; a.sflag = 1 | (par ? 2 : 0);
-      if (int e = step_launch(P, P.k_sa, a, st, false, P.step_smem, nT, &P.wfwd)) return e;
+      StepTail tl = P.tail;
+      tl.setA = par;
+      if (int e = step_launch(P, P.k_sa, a, st, false, P.step_smem, nT, &P.wfwd, &tl)) return e;
       ++launches;
     }
     const double t_next2 = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t_mom * t_mom));   // next momentum, no restart
@@ -1074,20 +1100,40 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
         // accepted without retry or restart; the other sums set), in one launch
       ConvArgs<T> a = sa_args;
       a.in0 = X[ic]; a.in1 = X[ix]; a.out1 = Yn; a.sflag = par ? 0 : 2;
-      prof_now = P.profile && (t % P.profile == 0);   // sampled: every P.profile-th iteration
+      if (prof_pending) {   // the sampled launch of an earlier iteration has completed (stream order)
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, P.prof_ev[0], P.prof_ev[1]) == cudaSuccess) {
+          dom_ms += ms;
+          ++dom_n;
+          prof_pending = false;
+        } else {
+          (void)cudaGetLastError();   // not ready yet: keep the events for a later iteration
+        }
+      }
+      prof_now = P.profile && (t % P.profile == 0) && !prof_pending;   // sampled: every P.profile-th iteration
+      StepTail tl = P.tail;
+      tl.setA = par ? 0 : 1;   // the speculative stage A writes the other (fit, tv) set
+      tl.setR = par;
+      if (tl.on) {   // the candidate half's last tile row publishes the six sums (step_tail.h)
+        a.hscal = d_hscal;
+        a.hflag = d_hflag;
+        a.hseq = ++P.step_seq;
+      }
       if (prof_now) CK(cudaEventRecord(P.prof_ev[0], st));
-      if (int e = step_launch(P, P.k_sca, a, st, false, P.step_smem, 2 * nT, &P.wfwd)) return e;
-      if (prof_now) CK(cudaEventRecord(P.prof_ev[1], st));
+      if (int e = step_launch(P, P.k_sca, a, st, false, P.step_smem, 2 * nT, &P.wfwd, &tl)) return e;
+      if (prof_now) {
+        CK(cudaEventRecord(P.prof_ev[1], st));
+        prof_pending = true;
+      }
       ++launches;
+      if (tl.on) {
+        if (int e = wait_flag(a.hseq)) return e;
+      }
     }
     ++vg;
     ++vals;
-    if (int e = reduce(par, 6)) return e;
-    if (prof_now) {   // the reduction followed the timed launch in the stream: both events completed
-      float ms = 0.f;
-      CK(cudaEventElapsedTime(&ms, P.prof_ev[0], P.prof_ev[1]));
-      dom_ms += ms;
-      ++dom_n;
+    if (!P.tail.on) {
+      if (int e = reduce(par, 6)) return e;
     }
     const double* o = P.h_scal;
     const double fit = o[0];
@@ -1119,12 +1165,28 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
       L_try *= 2.0;
       if (++k >= 60) { status = ST_BT_FAIL; fail_iter = t; break; }
       ConvArgs<T> a = sa_args;
-      a.in0 = X[ix]; a.in1 = X[ixp]; a.out0 = X[ic]; a.sbeta = beta; a.sL = L_try; a.sflag = 1;
-      if (int e = step_launch(P, P.k_sc, a, st, false, P.step_smem, nT, &P.wfwd)) return e;
+      a.in0 = X[ix]; a.in1 = X[ixp]; a.out0 = X[ic]; a.sbeta = beta; a.sL = L_try; a.sbetaN = beta2;
+      a.sflag = par ? 0 : 2;   // the set the speculative stage A writes (as in the first candidate's launch)
+      StepTail tl = P.tail;
+      tl.setA = par ? 0 : 1;
+      tl.setR = par;
+      if (tl.on) {
+        a.hscal = d_hscal;
+        a.hflag = d_hflag;
+        a.hseq = ++P.step_seq;
+      }
+      // in-kernel sums: the retry's value pass and the speculative stage A at its next extrapolation
+      // point share one launch; otherwise the value pass alone, then the reduction launch
+      if (int e = step_launch(P, P.k_sc, a, st, false, P.step_smem, tl.on ? 2 * nT : nT, &P.wfwd, &tl)) return e;
       ++launches;
       ++vals;
-      if (int e = reduce(2, 3)) return e;
-      fitc = P.h_scal[0]; tvc = P.h_scal[1]; dot = P.h_scal[2];
+      if (tl.on) {
+        if (int e = wait_flag(a.hseq)) return e;
+        fitc = P.h_scal[4]; tvc = P.h_scal[5]; dot = P.h_scal[3];
+      } else {
+        if (int e = reduce(2, 3)) return e;
+        fitc = P.h_scal[0]; tvc = P.h_scal[1]; dot = P.h_scal[2];
+      }
     }
     if (status != ST_OK) { done = true; break; }
     const double bstep = 1.0 / L_try;
@@ -1139,7 +1201,7 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
     }
     for (int b = 0; b < 3; ++b)
       if (b != ix && b != ixp) { ic = b; break; }
-    a_ready = k == 0 && !restart;
+    a_ready = (k == 0 || P.tail.on) && !restart;   // an accepted retry carried its own speculative stage A
     if (a_ready) par ^= 1;
   }
   if (!done) {
@@ -1157,6 +1219,12 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
     converged = gn <= tol;
   }
   CK(cudaStreamSynchronize(st));
+  if (prof_pending) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, P.prof_ev[0], P.prof_ev[1]));
+    dom_ms += ms;
+    ++dom_n;
+  }
   res->norm_sq = lam;
   res->lip = lip;
   res->grad_norm = gn;
@@ -1590,7 +1658,7 @@ extern "C" int adp_slab_mixed(adp_plan* p, const adp_lower* lp, const void* x_ti
 // high-occupancy solve (conv2d_step.cu)
 extern "C" int adp_plan_flags(adp_plan* p, int32_t* flags) {
   if (!p || !flags) return fail(ADP_ERR_ARG, "null argument");
-  *flags = (p->impl.tma ? 1 : 0) | (p->impl.step ? 2 : 0);
+  *flags = (p->impl.tma ? 1 : 0) | (p->impl.step ? 2 : 0) | (p->impl.step && p->impl.tail.on ? 4 : 0);
   return ADP_OK;
 }
 

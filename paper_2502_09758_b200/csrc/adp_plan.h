@@ -7,6 +7,7 @@
 #include <vector>
 #include "adp_types.h"
 #include "conv2d_args.h"   // StepW
+#include "step_tail.h"
 #include "../../include/adp_b200.h"
 
 namespace adp {
@@ -78,6 +79,8 @@ struct PlanImpl {
   int step_o_tm = 0;
   double* h_kern = nullptr;     // pinned: the solve's stencil, read back to build the stage kernels' tap sets
   StepW wfwd{}, wadj{};         // forward / flipped taps (kernel parameters of the stage kernels)
+  StepTail tail{};              // in-kernel decision sums of the host-stepped solve (tail.on: geometry allows it)
+  void* d_tail = nullptr;       // sub-values + tickets
   CUtensorMap tm[5];            // X[0..2], R, P[0]
   // pinned host staging
   SolveOut* h_sres = nullptr;

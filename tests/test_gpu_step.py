@@ -12,8 +12,9 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-def _solve(adp, nat, up, iters, step):
+def _solve(adp, nat, up, iters, step, tail=True):
     os.environ["ADP_STEP"] = "1" if step else "0"
+    os.environ["ADP_TAIL"] = "1" if tail else "0"
     try:
         nat.clear_plans()
         p = up.lower_problem(up.b0)
@@ -23,6 +24,7 @@ def _solve(adp, nat, up, iters, step):
         return r, st, p.op._norm_sq, flags
     finally:
         os.environ.pop("ADP_STEP", None)
+        os.environ.pop("ADP_TAIL", None)
         nat.clear_plans()
 
 
@@ -34,9 +36,27 @@ def test_step_solve_equals_persistent(adp, cfg, size, iters):
     r0, s0, n0, _ = _solve(adp, nat, up, iters, False)
     r1, s1, n1, f1 = _solve(adp, nat, up, iters, True)
     assert f1["step"] == (cfg == "c3")     # c5-geometry plans (K = 31) keep the persistent kernel
+    assert f1["tail"] == (cfg == "c3")     # decision sums folded inside the stage kernels
     assert n1 == n0 and r1.iters == r0.iters and r1.grad_norm == r0.grad_norm
     assert {k: s1[k] for k in ("vg_evals", "value_evals", "restarts", "lip", "power_iters")} == \
         {k: s0[k] for k in ("vg_evals", "value_evals", "restarts", "lip", "power_iters")}
+    assert np.array_equal(r1.x_tilde, r0.x_tilde)
+
+
+def test_step_tail_equals_reduce_kernel(adp):
+    """In-kernel decision sums (step_tail.h) vs the separate reduction launch: same trees, bitwise,
+    over a run with backtracking retries."""
+    from paper_2502_09758_b200 import _native as nat
+    from paper_2502_09758_b200 import configs
+    up = configs.CONFIGS["c3"](3, size=512)
+    r0, s0, n0, f0 = _solve(adp, nat, up, 150, True, tail=False)
+    r1, s1, n1, f1 = _solve(adp, nat, up, 150, True, tail=True)
+    assert f0["step"] and not f0["tail"] and f1["tail"]
+    assert s1["value_evals"] > s1["vg_evals"]          # retries happened
+    assert n1 == n0 and r1.iters == r0.iters and r1.grad_norm == r0.grad_norm
+    assert {k: s1[k] for k in ("vg_evals", "value_evals", "restarts", "lip")} == \
+        {k: s0[k] for k in ("vg_evals", "value_evals", "restarts", "lip")}
+    assert s1["launches"] < s0["launches"]
     assert np.array_equal(r1.x_tilde, r0.x_tilde)
 
 
