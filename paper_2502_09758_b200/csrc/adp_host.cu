@@ -572,7 +572,7 @@ static int conv_plan_init(PlanImpl& P) {
     const char* ev = getenv("ADP_STEP");
     const int want = ev ? atoi(ev) : -1;
     if (want != 0 && P.d.dtype == ADP_DTYPE_F64 && g.rwb == 4 && g.fused && g.fuseCA && !slab &&
-        g.threads <= 384 && (want == 1 || g.N >= (1 << 18)) && g.kh * g.kw * g.C <= kStepWMax &&
+        g.threads <= 384 && (want == 1 || g.N >= (1 << 18)) && ((g.kh * g.kw + 1) & ~1) * g.C <= kStepWMax &&
         g.tpc % 32 == 0) {   // taps as kernel parameters; channel-uniform warps
       const size_t es = (size_t)P.esize;
       const size_t pa = ((size_t)g.C * g.SH * g.SWP * es + 127) & ~size_t(127);
@@ -985,15 +985,15 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
   set_lower(base, lp);
   // the stage kernels' taps as kernel parameters (StepW): forward [c][i][j] and flipped, ndimage's
   // |w| <= DBL_EPSILON taps zeroed (Conv::load_weights' rule)
-  const int kk = g.kh * g.kw, nk = kk * g.C;
+  const int kk = g.kh * g.kw, nk = kk * g.C, kkp = (kk + 1) & ~1;   // channel blocks padded to even
   CK(cudaMemcpyAsync(P.h_kern, lp->kernel, (size_t)nk * sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
   for (int e = 0; e < nk; ++e) {
     const int c = e % g.C, ij = e / g.C, i = ij / g.kw, j = ij % g.kw;
     double w = P.h_kern[e];
     if (!(fabs(w) > 2.220446049250313e-16)) w = 0.0;
-    P.wfwd.w[(c * g.kh + i) * g.kw + j] = w;
-    P.wadj.w[(c * g.kh + (g.kh - 1 - i)) * g.kw + (g.kw - 1 - j)] = w;
+    P.wfwd.w[c * kkp + i * g.kw + j] = w;
+    P.wadj.w[c * kkp + (g.kh - 1 - i) * g.kw + (g.kw - 1 - j)] = w;
   }
   ConvArgs<T> sa_args = base;   // stage kernels: one plane region, term buffers right after it
   sa_args.g.o_tm = P.step_o_tm;

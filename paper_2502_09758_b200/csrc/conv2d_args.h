@@ -95,8 +95,9 @@ struct ConvArgs {
 // Host-stepped stage kernels: the launch's tap set as a kernel parameter
 // (constant bank 0), channel-major [c][i][j] with ndimage's |w| <= DBL_EPSILON
 // taps zeroed; forward taps for the value passes, flipped for the adjoint.
+// Channel blocks are padded to an even tap count (16-byte aligned tap pairs).
 constexpr int kStepWMax = 1024;
-struct StepW {
+struct alignas(16) StepW {
   double w[kStepWMax];
 };
 

@@ -178,12 +178,13 @@ struct Conv {
   __device__ __forceinline__ T* plane(int c) const { return pa() + (size_t)c * a.g.SH * swp(); }
   // this thread's channel taps: forward (correlation) and flipped (adjoint);
   // PW kernels carry exactly one of the two sets, chosen by the host
+  // (PW: channel blocks padded to an even tap count, so tap pairs are 16-byte aligned)
   __device__ __forceinline__ const T* wfwd() const {
-    if constexpr (PW) return pw + chu * a.g.kh * a.g.kw;
+    if constexpr (PW) return pw + chu * ((a.g.kh * a.g.kw + 1) & ~1);
     else return ws() + ch * a.g.kh * a.g.kw;
   }
   __device__ __forceinline__ const T* wadj() const {
-    if constexpr (PW) return pw + chu * a.g.kh * a.g.kw;
+    if constexpr (PW) return pw + chu * ((a.g.kh * a.g.kw + 1) & ~1);
     else return wf() + ch * a.g.kh * a.g.kw;
   }
 
@@ -349,16 +350,42 @@ struct Conv {
     const int rowE = (a.g.TW + 2 * a.g.rw + 2) * C, planeSz = SH * SWP;
     const int gh0 = h0 - a.g.rh - 1, gw0 = w0 - a.g.rw - 1;
     const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int sr = threadIdx.x >> 5; sr < SH; sr += nw) {
-      const int gh = gh0 + sr;
-      const bool rowok = gh >= 0 && gh < H;
-      const int64_t rowbase = ((int64_t)(rowok ? gh : 0) * W + gw0) * C;
-      T* drow = dst + sr * SWP;
-      for (int e = lane; e < rowE; e += 32) {
+    const unsigned sdst = (unsigned)__cvta_generic_to_shared(dst);
+    for (int e0 = 0; e0 < rowE; e0 += 32 * kJ) {
+      // the lane's (up to kJ) elements of a box row: their plane offsets and column validity are
+      // the same for every row, so the de-interleave arithmetic runs once per pass, not per element
+      unsigned soff[kJ];
+      unsigned inb = 0, okc = 0;
+#pragma unroll
+      for (int j = 0; j < kJ; ++j) {
+        const int e = e0 + lane + 32 * j;
         const int px = C == 1 ? e : (int)(((unsigned long long)(unsigned)e * mC) >> 20);
         const int c = e - px * C;
-        const bool ok = rowok && (unsigned)(gw0 + px) < (unsigned)W;
-        cp_async_el(drow + c * planeSz + sk(px), ok ? x + rowbase + e : x, ok);
+        soff[j] = (unsigned)((c * planeSz + sk(px)) * (int)sizeof(T));
+        if (e < rowE) inb |= 1u << j;
+        if (e < rowE && (unsigned)(gw0 + px) < (unsigned)W) okc |= 1u << j;
+      }
+      for (int sr = threadIdx.x >> 5; sr < SH; sr += nw) {
+        const int gh = gh0 + sr;
+        const bool rowok = gh >= 0 && gh < H;
+        const T* grow = x + ((int64_t)(rowok ? gh : 0) * W + gw0) * C + (e0 + lane);
+        const unsigned srow = sdst + (unsigned)(sr * SWP * (int)sizeof(T));
+        const unsigned okr = rowok ? okc : 0u;
+#pragma unroll
+        for (int j = 0; j < kJ; ++j) {
+          if ((inb >> j) & 1u) {
+            const bool ok = (okr >> j) & 1u;
+            const T* src = ok ? grow + 32 * j : x;
+            if (sizeof(T) == 8)
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(srow + soff[j]), "l"(src),
+                           "r"(ok ? 8 : 0)
+                           : "memory");
+            else
+              asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(srow + soff[j]), "l"(src),
+                           "r"(ok ? 4 : 0)
+                           : "memory");
+          }
+        }
       }
     }
   }
@@ -440,6 +467,31 @@ struct Conv {
     }
   }
 
+  // PW form of stencil_k: the taps are read from parameter space as 16-byte pairs (flattened
+  // row-major tap index t: pair t >> 1; the channel blocks are padded to an even tap count), half
+  // the uniform loads of the scalar form.  Same tap order.
+  template <int K>
+  __device__ __forceinline__ void stencil_kp(const T* __restrict__ pl, const T* __restrict__ w, T (&acc)[RW]) const {
+    static_assert(sizeof(T) == 8, "parameter-space taps: float64 only");
+    const int SWP = swp();
+    const T* base = pl + (ty + 1) * SWP + sk(tx * RW);
+    const double2* w2 = reinterpret_cast<const double2*>(w);
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+      const T* row = base + i * SWP;
+      T win[K + RW - 1];
+      load_win<K + RW - 1>(row, win);
+#pragma unroll
+      for (int j = 0; j < K; ++j) {
+        const int t = i * K + j;
+        const double2 wp = w2[t >> 1];
+        const T wt = (t & 1) ? wp.y : wp.x;
+#pragma unroll
+        for (int o = 0; o < RW; ++o) acc[o] = madd<FAST>(acc[o], win[o + j], wt);
+      }
+    }
+  }
+
   // Two planes through the same compile-time K x K taps (the fused candidate
   // stage): each tap is loaded once for both accumulations; per output the
   // order is exactly stencil_k's.
@@ -511,11 +563,13 @@ struct Conv {
     }
     const int kh = a.g.kh, kw = a.g.kw, SWP = swp();
     if (kh == 9 && kw == 9) {
-      stencil_k<9>(pl, w, acc);
+      if constexpr (PW) stencil_kp<9>(pl, w, acc);
+      else stencil_k<9>(pl, w, acc);
       return;
     }
     if (kh == 15 && kw == 15) {
-      stencil_k<15>(pl, w, acc);
+      if constexpr (PW) stencil_kp<15>(pl, w, acc);
+      else stencil_k<15>(pl, w, acc);
       return;
     }
     if (kh == 31 && kw == 31) {
@@ -641,21 +695,41 @@ struct Conv {
     }
     return pre[o];
   }
-  // asynchronous copy of the tile's own pixels of `src` into term buffer `buf` (rows of TW * C
-  // contiguous doubles, 16-byte copies; rows outside the image zero-filled)
-  __device__ void stage_own(int h0, int w0, const T* src, int buf) const {
+  // asynchronous copies of the tile's own pixels of NB arrays into term buffers buf0.. (rows of TW * C
+  // contiguous doubles, 16-byte copies; rows outside the image zero-filled).  One index computation
+  // (a single integer division per thread) serves all NB arrays.
+  template <int NB>
+  __device__ void stage_own_n(int h0, int w0, const T* const (&src)[NB], int buf0) const {
     if constexpr (sizeof(T) == 8) {
-      const int C = nC(), H = a.g.H, W = a.g.W;
+      const int C = nC(), H = a.g.H, W = a.g.W, TH = a.g.TH;
       const int rowE = a.g.TW * C, pairs = rowE >> 1;
-      double* dst = tm() + (size_t)buf * a.g.TH * rowE;
-      for (int k = threadIdx.x; k < a.g.TH * pairs; k += blockDim.x) {
-        const int r = k / pairs, e = (k - r * pairs) * 2;
-        const int h = h0 + r;
+      const int BD = blockDim.x;
+      const int dr = BD / pairs, de = BD - dr * pairs;
+      int r = threadIdx.x / pairs, p = threadIdx.x - r * pairs;
+      const unsigned bufB = (unsigned)(TH * rowE * 8);
+      const unsigned d0 = (unsigned)__cvta_generic_to_shared(tm()) + (unsigned)buf0 * bufB;
+      while (r < TH) {
+        const int h = h0 + r, e = 2 * p;
         const int64_t gi = ((int64_t)h * W + w0) * C + e;
         const int valid = (h < H && w0 * C + e < W * C) ? 16 : 0;
-        cp_async16(dst + (size_t)r * rowE + e, valid ? (const double*)src + gi : (const double*)src, valid);
+        const unsigned d = d0 + (unsigned)((r * rowE + e) * 8);
+#pragma unroll
+        for (int b = 0; b < NB; ++b)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d + b * bufB),
+                       "l"(valid ? (const double*)src[b] + gi : (const double*)src[b]), "r"(valid)
+                       : "memory");
+        r += dr;
+        p += de;
+        if (p >= pairs) {
+          p -= pairs;
+          ++r;
+        }
       }
     }
+  }
+  __device__ void stage_own(int h0, int w0, const T* src, int buf) const {
+    const T* const one[1] = {src};
+    stage_own_n<1>(h0, w0, one, buf);
   }
 
   // =========================================================================

@@ -153,9 +153,13 @@ __global__ void __launch_bounds__(384, EP == 2 ? 2 : 3) step_b_kernel(const __gr
   int h0, w0;
   E.tile_origin(tile, h0, w0);
   if (EP == 2) {
-    if (tv) E.stage_own(h0, w0, a.TVG, 0);
-    E.stage_own(h0, w0, a.in0, 1);
-    E.stage_own(h0, w0, a.in1, 2);
+    if (tv) {
+      const T* const ops[3] = {a.TVG, a.in0, a.in1};
+      E.template stage_own_n<3>(h0, w0, ops, 0);
+    } else {
+      const T* const ops[2] = {a.in0, a.in1};
+      E.template stage_own_n<2>(h0, w0, ops, 1);
+    }
   }
   E.load_async(h0, w0, a.R, E.pa());
   cp_commit();
@@ -292,10 +296,11 @@ __global__ void __launch_bounds__(384, 2) step_ca_kernel(const __grid_constant__
   const int tile = isC ? (int)blockIdx.x : (int)blockIdx.x - nT;
   int h0, w0;
   E.tile_origin(tile, h0, w0);
-  E.stage_own(h0, w0, a.ydat, 0);
   if (isC) {
-    E.stage_own(h0, w0, a.G, 1);
-    E.stage_own(h0, w0, a.in1, 2);
+    const T* const ops[3] = {a.ydat, a.G, a.in1};
+    E.template stage_own_n<3>(h0, w0, ops, 0);
+  } else {
+    E.stage_own(h0, w0, a.ydat, 0);
   }
   E.load_async(h0, w0, isC ? a.in0 : a.out1, E.pa());
   cp_async_wait_all();
