@@ -579,7 +579,7 @@ static int conv_plan_init(PlanImpl& P) {
       const size_t tm = (size_t)3 * g.TH * g.TW * g.C * sizeof(double);
       P.step_o_tm = g.o_pa + (int)pa;
       P.step_smem = (size_t)P.step_o_tm + tm;
-      StepKernels sk = step_kernels(P.d.mode == ADP_MODE_FAST);
+      StepKernels sk = step_kernels(P.d.mode == ADP_MODE_FAST, g.kh == g.kw ? g.kh : 0);
       P.k_extrap = sk.extrap;
       P.step_smem_b = sk.b_ep == 2 ? P.step_smem : (size_t)g.o_pa + pa;   // stage B: no term buffers (three CTAs per SM)
       if (setup_kernel(P, P.k_sb, sk.b, g.threads, P.step_smem_b, g.nTiles) == ADP_OK &&
@@ -599,7 +599,7 @@ static int conv_plan_init(PlanImpl& P) {
             P.s_tv.regular && P.s_t0.regular && (int64_t)P.s_fit.nLeaves == GL * g.tilesH &&
             (int64_t)P.s_tv.nLeaves == 2 * GL * g.tilesH && g.threads >= 192) {
           const size_t nsub = (size_t)11 * g.tilesH * sizeof(double);
-          const size_t ncnt = (size_t)(2 * g.tilesH + 1) * sizeof(unsigned int);
+          const size_t ncnt = 64;
           CK(cudaMalloc(&P.d_tail, nsub + ncnt));
           CK(cudaMemset(P.d_tail, 0, nsub + ncnt));
           P.tail.sub = (double*)P.d_tail;
@@ -608,6 +608,8 @@ static int conv_plan_init(PlanImpl& P) {
           P.tail.nG = g.tilesH;
           P.tail.GL = (int)GL;
           P.tail.tW = g.tilesW;
+          P.tail.gpr = std::min(g.tilesH, 8);   // tile rows per reducer CTA
+          P.tail.nR = g.tilesH / P.tail.gpr;
         }
       }
     }
@@ -972,7 +974,21 @@ static int step_launch(PlanImpl& P, KernelInfo& k, ConvArgs<double>& a, cudaStre
     CK(cudaMemsetAsync(P.d_bar, 0, sizeof(unsigned int), st));
     CK(cudaLaunchCooperativeKernel(k.fn, dim3(grid), dim3(P.g.threads), args, smem, st));
   } else {
-    CK(cudaLaunchKernel(k.fn, dim3(grid), dim3(P.g.threads), args, smem, st));
+    // programmatic dependent launch: the stage kernel's CTAs may become resident while the previous
+    // stage kernel drains (it signals at its start); they wait (griddepcontrol.wait) for that grid's
+    // completion before touching its data, so only launch latency and index set-up overlap.  ADP_PDL=0: off
+    static const bool pdl = !(getenv("ADP_PDL") && atoi(getenv("ADP_PDL")) == 0);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(P.g.threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    CK(cudaLaunchKernelExC(&cfg, k.fn, args));
   }
   return ADP_OK;
 }
@@ -1031,6 +1047,13 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
   const size_t nbytes = (size_t)g.N * sizeof(T);
   CK(cudaMemcpyAsync(X[0], x0, nbytes, cudaMemcpyDeviceToDevice, st));
   if (sa->x_prev0) CK(cudaMemcpyAsync(X[1], sa->x_prev0, nbytes, cudaMemcpyDeviceToDevice, st));
+  if (P.tail.on) {
+    // the candidate half's sum units start unwritten (all-ones pattern, step_tail.h); the reducers
+    // reset what they read, so this covers units left by other kernels of the plan
+    CK(cudaMemsetAsync(P.s_fitc.leaf_vals, 0xFF, (size_t)P.s_fitc.nLeaves * sizeof(double), st));
+    CK(cudaMemsetAsync(P.s_tvc.leaf_vals, 0xFF, (size_t)P.s_tvc.nLeaves * sizeof(double), st));
+    CK(cudaMemsetAsync(P.s_t1.leaf_vals, 0xFF, (size_t)g.nTiles * sizeof(double), st));
+  }
   int ix = 0, ixp = sa->x_prev0 ? 1 : 0, ic = sa->x_prev0 ? 2 : 1;
   double t_mom = sa->t_mom0 > 0.0 ? sa->t_mom0 : 1.0, lip_t = sa->lip_t0 > 0.0 ? sa->lip_t0 : lip;
   int status = ST_OK, fail_iter = -1, iters = sa->max_iters, converged = 0;
@@ -1082,9 +1105,7 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
     if (!a_ready) {   // stage A at y = x + beta (x - x_prev), sums set `par`
       ConvArgs<T> a = sa_args;
       a.in0 = X[ix]; a.in1 = X[ixp]; a.sbeta = beta; a.sflag = 1 | (par ? 2 : 0);
-      StepTail tl = P.tail;
-      tl.setA = par;
-      if (int e = step_launch(P, P.k_sa, a, st, false, P.step_smem, nT, &P.wfwd, &tl)) return e;
+      if (int e = step_launch(P, P.k_sa, a, st, false, P.step_smem, nT, &P.wfwd)) return e;
       ++launches;
     }
     const double t_next2 = 0.5 * (1.0 + sqrt(1.0 + 4.0 * t_mom * t_mom));   // next momentum, no restart
@@ -1112,15 +1133,15 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
       }
       prof_now = P.profile && (t % P.profile == 0) && !prof_pending;   // sampled: every P.profile-th iteration
       StepTail tl = P.tail;
-      tl.setA = par ? 0 : 1;   // the speculative stage A writes the other (fit, tv) set
-      tl.setR = par;
-      if (tl.on) {   // the candidate half's last tile row publishes the six sums (step_tail.h)
+      tl.setR = par;   // (the speculative stage A writes the other (fit, tv) set)
+      if (tl.on) {   // reducer CTAs publish the six sums (step_tail.h)
         a.hscal = d_hscal;
         a.hflag = d_hflag;
         a.hseq = ++P.step_seq;
       }
       if (prof_now) CK(cudaEventRecord(P.prof_ev[0], st));
-      if (int e = step_launch(P, P.k_sca, a, st, false, P.step_smem, 2 * nT, &P.wfwd, &tl)) return e;
+      if (int e = step_launch(P, P.k_sca, a, st, false, P.step_smem, 2 * nT + (tl.on ? tl.nR : 0), &P.wfwd, &tl))
+        return e;
       if (prof_now) {
         CK(cudaEventRecord(P.prof_ev[1], st));
         prof_pending = true;
@@ -1168,7 +1189,6 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
       a.in0 = X[ix]; a.in1 = X[ixp]; a.out0 = X[ic]; a.sbeta = beta; a.sL = L_try; a.sbetaN = beta2;
       a.sflag = par ? 0 : 2;   // the set the speculative stage A writes (as in the first candidate's launch)
       StepTail tl = P.tail;
-      tl.setA = par ? 0 : 1;
       tl.setR = par;
       if (tl.on) {
         a.hscal = d_hscal;
@@ -1177,7 +1197,8 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
       }
       // in-kernel sums: the retry's value pass and the speculative stage A at its next extrapolation
       // point share one launch; otherwise the value pass alone, then the reduction launch
-      if (int e = step_launch(P, P.k_sc, a, st, false, P.step_smem, tl.on ? 2 * nT : nT, &P.wfwd, &tl)) return e;
+      if (int e = step_launch(P, P.k_sc, a, st, false, P.step_smem, tl.on ? 2 * nT + tl.nR : nT, &P.wfwd, &tl))
+        return e;
       ++launches;
       ++vals;
       if (tl.on) {

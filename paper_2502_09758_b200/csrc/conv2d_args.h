@@ -140,7 +140,8 @@ struct StepKernels {
   const void* ca;
   int b_ep;        // stage-B epilogue operand variant (2: term buffers, two CTAs per SM)
 };
-StepKernels step_kernels(int fast);
+// k: the plan's stencil size when square (instances specialised to 15 x 15 exist), else 0
+StepKernels step_kernels(int fast, int k);
 // thread bound of the compile-time-stencil solve kernel (the host selects it
 // only for CTAs of at most this many threads)
 constexpr int kSolveKSThreads = 256;

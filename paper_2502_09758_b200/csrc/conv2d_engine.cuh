@@ -122,7 +122,10 @@ template <typename T> struct Plain {
 // to a uniform register and every tap is an LDCU into the uniform register
 // file feeding DMUL's second operand: no shared-memory wavefronts or vector
 // registers for the weights, no per-CTA weight staging.
-template <typename T, bool FAST, int RW, int KS = 0, bool TMA = false, bool PW = false>
+// KD > 0 (host-stepped stage kernels): the kernel serves KD x KD stencils only (any channel count),
+// so it carries one stencil variant; KU: rows of that stencil unrolled per loop iteration (KD % KU == 0;
+// KU == KD: straight-line code) -- the instruction footprint of the hot path against the instruction caches.
+template <typename T, bool FAST, int RW, int KS = 0, bool TMA = false, bool PW = false, int KD = 0, int KU = 0>
 struct Conv {
   static_assert((RW & (RW - 1)) == 0, "RW must be a power of two");
   static constexpr int kShift = RW == 1 ? 0 : RW == 2 ? 1 : RW == 4 ? 2 : 3;
@@ -492,6 +495,31 @@ struct Conv {
     }
   }
 
+  // K x K taps with the row loop unrolled U rows at a time (K % U == 0), taps from parameter space
+  // (scalar uniform loads, row index in a uniform register).  Same tap order as stencil_k.
+  template <int K, int U>
+  __device__ __forceinline__ void stencil_ku(const T* __restrict__ pl, const T* __restrict__ w, T (&acc)[RW]) const {
+    static_assert(K % U == 0, "row unroll must divide the stencil height");
+    const int SWP = swp();
+    const T* base = pl + (ty + 1) * SWP + sk(tx * RW);
+#pragma unroll 1
+    for (int i0 = 0; i0 < K; i0 += U) {
+#pragma unroll
+      for (int ii = 0; ii < U; ++ii) {
+        const T* row = base + (i0 + ii) * SWP;
+        const T* wr = w + (i0 + ii) * K;
+        T win[K + RW - 1];
+        load_win<K + RW - 1>(row, win);
+#pragma unroll
+        for (int j = 0; j < K; ++j) {
+          const T wt = wr[j];
+#pragma unroll
+          for (int o = 0; o < RW; ++o) acc[o] = madd<FAST>(acc[o], win[o + j], wt);
+        }
+      }
+    }
+  }
+
   // Two planes through the same compile-time K x K taps (the fused candidate
   // stage): each tap is loaded once for both accumulations; per output the
   // order is exactly stencil_k's.
@@ -559,6 +587,12 @@ struct Conv {
     for (int o = 0; o < RW; ++o) acc[o] = T(0);
     if constexpr (KS > 0) {
       stencil_k<KS>(pl, w, acc);
+      return;
+    }
+    if constexpr (KD > 0) {   // the host selected this instance for KD x KD stencils
+      if constexpr (KU > 0 && KU < KD) stencil_ku<KD, KU>(pl, w, acc);
+      else if constexpr (PW) stencil_kp<KD>(pl, w, acc);
+      else stencil_k<KD>(pl, w, acc);
       return;
     }
     const int kh = a.g.kh, kw = a.g.kw, SWP = swp();

@@ -15,11 +15,36 @@
 
 namespace adp {
 
+// Programmatic dependent launch (see step_launch): let the next stage kernel's CTAs become resident,
+// then wait until the previous grid has completed and its writes are visible.  Every stage kernel
+// calls this before its first global-memory access.
+__device__ __forceinline__ void pdl_sync() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+// A leaf unit that may still be unwritten: the candidate half's leaves and tile partials are
+// pre-set to an all-ones NaN pattern (never produced by the arithmetic: the hardware's NaN results
+// are canonical), each is one 8-byte store, so reading anything else means reading the unit.  No
+// fence, ticket or barrier on the producers' side.
+__device__ __forceinline__ double ld_unit(const double* p, bool poll) {
+  unsigned long long b;
+  asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(b) : "l"(p) : "memory");
+  if (poll) {
+    while (b == ~0ull) {
+      __nanosleep(100);
+      asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(b) : "l"(p) : "memory");
+    }
+  }
+  return __longlong_as_double((long long)b);
+}
+
 // Perfect-tree folds of K runs of units read from L2 (n[i] <= 4 T units, T the largest power of two
 // <= blockDim): reduce_k's register path -- chunks of <= 4 contiguous units per folding thread, zero
 // padding to the next power of two, xor-shuffles, then the warp partials.  out valid in every thread.
-template <int K>
-__device__ __forceinline__ void fold_many(const double* const (&src)[K], const int (&n)[K], double (&out)[K],
+// Runs i < NP are polled (ld_unit) and reset to the unwritten pattern once read.
+template <int K, int NP>
+__device__ __forceinline__ void fold_many(double* const (&src)[K], const int (&n)[K], double (&out)[K],
                                           double* red) {
   const int BD = blockDim.x, lgT = 31 - __clz(BD), T = 1 << lgT;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = BD >> 5;
@@ -33,7 +58,9 @@ __device__ __forceinline__ void fold_many(const double* const (&src)[K], const i
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
       const int e = e0 + m;
-      v[m] = (m < chunk && e < n[i] && (int)threadIdx.x < T) ? ldcg(src[i] + e) : 0.0;
+      const bool act = m < chunk && e < n[i] && (int)threadIdx.x < T;
+      v[m] = act ? ld_unit(src[i] + e, i < NP) : 0.0;
+      if (i < NP && act) src[i][e] = __longlong_as_double(-1LL);
     }
     root[i] = chunk == 1 ? v[0] : chunk == 2 ? v[0] + v[1] : (v[0] + v[1]) + (v[2] + v[3]);
   }
@@ -57,70 +84,165 @@ __device__ __forceinline__ void fold_many(const double* const (&src)[K], const i
   __syncthreads();
 }
 
-// Tail of a leaf-producing stage CTA (see step_tail.h): ticket of the tile row; its last CTA folds the
-// row's leaves; candidate half (isC): the last tile row folds all six sums and publishes them to the host.
-// sf / st: the (fit, tv) sums the stage-A pass of this launch wrote (isC false).
-template <class Eng, typename T>
-__device__ __forceinline__ void tail_fold(Eng& E, const ConvArgs<T>& a, const StepTail& tl, bool isC, int tile,
-                                          const SumDev* sf, const SumDev* st) {
+// One warp folds one aligned run of <= 32 units of a sum (a subtree of the perfect pairwise tree:
+// xor-shuffles 1..16, zero beyond n) -- four such tasks in flight per warp so the L2 round trips
+// overlap; polled units (see ld_unit) are waited for and reset.  Lane 0 returns the subtree root.
+struct WarpTask {
+  double* p;   // first unit of the 32-run (nullptr: no task)
+  int n;       // units in the run (<= 32)
+};
+template <bool POLL>
+__device__ __forceinline__ void warp_fold4(const WarpTask (&t)[4], double (&out)[4]) {
+  const int lane = threadIdx.x & 31;
+  unsigned long long b[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    b[u] = 0ull;
+    if (t[u].p && lane < t[u].n) asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(b[u]) : "l"(t[u].p + lane) : "memory");
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    if (POLL && t[u].p && lane < t[u].n) {
+      while (b[u] == ~0ull) {
+        __nanosleep(64);
+        asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(b[u]) : "l"(t[u].p + lane) : "memory");
+      }
+      t[u].p[lane] = __longlong_as_double(-1LL);   // unwritten again for the next launch
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) out[u] = __longlong_as_double((long long)b[u]);
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1)
+#pragma unroll
+    for (int u = 0; u < 4; ++u) out[u] = out[u] + __shfl_xor_sync(kFull, out[u], o);
+}
+
+// Reducer CTA `rid` of a candidate-value launch (see step_tail.h): folds the tile rows
+// [rid * gpr, (rid + 1) * gpr) of the decision sums into sub-values -- the candidate half's leaves
+// and tile partials are polled as they arrive -- takes a ticket, and the last reducer folds the
+// sub-values and publishes the sums to the host.  retry: the candidate's three sums only (the others
+// were delivered by the first candidate's launch and their sub-values are still in place).
+// Runs of a group, in this order: polled leaf runs (fitc, tvc, tvc'), plain leaf runs (fit, tv, tv'),
+// polled tile run (t1), plain tile run (t0).
+// (inlined: a real call in the stage kernels costs the hot path its register allocation -- measured)
+template <typename T>
+__device__ __forceinline__ void tail_reduce(double* red, const ConvArgs<T>& a, const StepTail& tl, int rid, bool retry) {
   __shared__ int s_last;
-  const int grp = E.tile_row(tile);
   const int GL = tl.GL, tW = tl.tW, nG = tl.nG;
-  unsigned int* cnt = tl.cnt + (isC ? 0 : nG) + grp;
-  // the CTA's leaves / partial are ordered before the ticket by the barrier and thread 0's
-  // (cumulative) fence; the folding CTA reads them from L2 (ldcg) after its own fence + barrier
+  const int koff = (int)(a.g.Ng / a.g.leafL);
+  const SumDev* sf = tl.setR ? &a.s_fit2 : &a.s_fit;
+  const SumDev* st = tl.setR ? &a.s_tv2 : &a.s_tv;
+  const int g0 = rid * tl.gpr, ng = min(nG, g0 + tl.gpr) - g0;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  const int segL = (GL + 31) >> 5, segT = (tW + 31) >> 5;     // 32-unit tasks per leaf / tile run
+  const int nrl = retry ? 3 : 6, nrt = retry ? 1 : 2;          // leaf / tile runs per group
+  double* partL = red;                                         // [ng][nrl][segL]
+  double* partT = red + (size_t)tl.gpr * 6 * segL;             // [ng][nrt][segT]
+  auto leaf_run = [&](int gi, int k) -> double* {
+    const size_t lo = (size_t)(g0 + gi) * GL;
+    switch (k) {
+      case 0: return a.s_fitc.leaf_vals + lo;
+      case 1: return a.s_tvc.leaf_vals + lo;
+      case 2: return a.s_tvc.leaf_vals + koff + lo;
+      case 3: return sf->leaf_vals + lo;
+      case 4: return st->leaf_vals + lo;
+      default: return st->leaf_vals + koff + lo;
+    }
+  };
+  // polled tasks first (they may wait), the plain ones behind them
+  const int ntl = ng * nrl * segL;
+  for (int base = warp; base < ntl; base += 4 * nw) {
+    WarpTask tp[4], tq[4];
+    int idp[4], idq[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int id = base + u * nw;
+      tp[u].p = tq[u].p = nullptr;
+      tp[u].n = tq[u].n = 0;
+      idp[u] = idq[u] = -1;
+      if (id < ntl) {
+        const int gi = id / (nrl * segL), rem = id - gi * (nrl * segL), k = rem / segL, sg = rem - k * segL;
+        WarpTask w;
+        w.p = leaf_run(gi, k) + 32 * sg;
+        w.n = min(32, GL - 32 * sg);
+        if (k < 3) { tp[u] = w; idp[u] = id; } else { tq[u] = w; idq[u] = id; }
+      }
+    }
+    double op[4], oq[4];
+    warp_fold4<true>(tp, op);
+    warp_fold4<false>(tq, oq);
+    if (lane == 0) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (idp[u] >= 0) partL[idp[u]] = op[u];
+        if (idq[u] >= 0) partL[idq[u]] = oq[u];
+      }
+    }
+  }
+  const int ntt = ng * nrt * segT;
+  for (int base = warp; base < ntt; base += 4 * nw) {
+    WarpTask tp[4], tq[4];
+    int idp[4], idq[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int id = base + u * nw;
+      tp[u].p = tq[u].p = nullptr;
+      tp[u].n = tq[u].n = 0;
+      idp[u] = idq[u] = -1;
+      if (id < ntt) {
+        const int gi = id / (nrt * segT), rem = id - gi * (nrt * segT), k = rem / segT, sg = rem - k * segT;
+        WarpTask w;
+        w.p = (k == 0 ? a.s_t1.leaf_vals : a.s_t0.leaf_vals) + (size_t)(g0 + gi) * tW + 32 * sg;
+        w.n = min(32, tW - 32 * sg);
+        if (k == 0) { tp[u] = w; idp[u] = id; } else { tq[u] = w; idq[u] = id; }
+      }
+    }
+    double op[4], oq[4];
+    warp_fold4<true>(tp, op);
+    warp_fold4<false>(tq, oq);
+    if (lane == 0) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        if (idp[u] >= 0) partT[idp[u]] = op[u];
+        if (idq[u] >= 0) partT[idq[u]] = oq[u];
+      }
+    }
+  }
+  __syncthreads();
+  // one thread per run: the perfect tree over its 32-unit subtree roots -> sub-value
+  for (int j = threadIdx.x; j < ng * (nrl + nrt); j += blockDim.x) {
+    const bool leaf = j < ng * nrl;
+    const int jj = leaf ? j : j - ng * nrl;
+    const int per = leaf ? nrl : nrt, seg = leaf ? segL : segT;
+    const int gi = jj / per, k = jj - gi * per;
+    const double* c = (leaf ? partL : partT) + (size_t)jj * seg;
+    const double v = seg == 1 ? c[0] : fold_pow2(c, seg);
+    const int grp = g0 + gi;
+    int o;
+    if (leaf) o = k == 0 ? tl.o_fitc() + grp : k == 1 ? tl.o_tvc() + grp : k == 2 ? tl.o_tvc() + nG + grp
+                  : k == 3 ? tl.o_fit() + grp : k == 4 ? tl.o_tv() + grp : tl.o_tv() + nG + grp;
+    else o = k == 0 ? tl.o_t1() + grp : tl.o_t0() + grp;
+    tl.sub[o] = v;
+  }
+  __threadfence();
+  // ticket among the reducers: thread 0 wrote this reducer's sub-values; its fence orders them
+  // before the ticket, the last reducer reads them from L2 after its own fence + barrier
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
-    s_last = atomicAdd(cnt, 1u) == (unsigned)tW - 1;
+    s_last = atomicAdd(tl.cnt, 1u) == (unsigned)tl.nR - 1;
     __threadfence();
   }
   __syncthreads();
   if (!s_last) return;
-  double* red = E.tm();   // the term buffers are free by now
-  const int koff = (int)(a.g.Ng / a.g.leafL);
-  if (!isC) {
-    const double* src[3] = {sf->leaf_vals + (size_t)grp * GL, st->leaf_vals + (size_t)grp * GL,
-                            st->leaf_vals + koff + (size_t)grp * GL};
-    const int n[3] = {GL, GL, GL};
-    double o[3];
-    fold_many<3>(src, n, o, red);
-    if (threadIdx.x == 0) {
-      tl.sub[tl.o_fit(tl.setA) + grp] = o[0];
-      tl.sub[tl.o_tv(tl.setA) + grp] = o[1];
-      tl.sub[tl.o_tv(tl.setA) + nG + grp] = o[2];
-      *cnt = 0;
-    }
-    return;
-  }
-  {
-    const double* src[5] = {a.s_fitc.leaf_vals + (size_t)grp * GL, a.s_tvc.leaf_vals + (size_t)grp * GL,
-                            a.s_tvc.leaf_vals + koff + (size_t)grp * GL, a.s_t1.leaf_vals + (size_t)grp * tW,
-                            a.s_t0.leaf_vals + (size_t)grp * tW};
-    const int n[5] = {GL, GL, GL, tW, tW};
-    double o[5];
-    fold_many<5>(src, n, o, red);
-    if (threadIdx.x == 0) {
-      tl.sub[tl.o_fitc() + grp] = o[0];
-      tl.sub[tl.o_tvc() + grp] = o[1];
-      tl.sub[tl.o_tvc() + nG + grp] = o[2];
-      tl.sub[tl.o_t1() + grp] = o[3];
-      tl.sub[tl.o_t0() + grp] = o[4];
-      *cnt = 0;
-      __threadfence();
-      s_last = atomicAdd(tl.cnt + 2 * nG, 1u) == (unsigned)nG - 1;
-      __threadfence();
-    }
-  }
-  __syncthreads();
-  if (!s_last) return;
-  const double* src[6] = {tl.sub + tl.o_fit(tl.setR), tl.sub + tl.o_tv(tl.setR), tl.sub + tl.o_t0(),
-                          tl.sub + tl.o_t1(),         tl.sub + tl.o_fitc(),      tl.sub + tl.o_tvc()};
+  double* src[6] = {tl.sub + tl.o_fit(),  tl.sub + tl.o_tv(),   tl.sub + tl.o_t0(),
+                    tl.sub + tl.o_t1(),   tl.sub + tl.o_fitc(), tl.sub + tl.o_tvc()};
   const int n[6] = {nG, 2 * nG, nG, nG, nG, 2 * nG};
   double o[6];
-  fold_many<6>(src, n, o, red);
+  fold_many<6, 0>(src, n, o, red);
   if (threadIdx.x == 0) {
-    tl.cnt[2 * nG] = 0;
+    *tl.cnt = 0;
 #pragma unroll
     for (int i = 0; i < 6; ++i) {
       a.scal[i] = o[i];
@@ -136,15 +258,15 @@ __device__ __forceinline__ void tail_fold(Eng& E, const ConvArgs<T>& a, const St
 // Stage B on one tile (stageB_pipe's arithmetic, expression for expression):
 // g = 2 B^T r + alpha tvg -> G, tile partial of g.g, the first candidate
 // x_c = (x + beta (x - x_prev)) - g / L -> out0 and the next extrapolation
-// point y' = x_c + betaN (x_c - x) -> out1.  wt: flipped taps.  EP selects
-// where the epilogue operands (tvg, x, x_prev) come from: 0 registers loaded
-// before the stencil, 1 registers loaded after it, 2 term buffers filled by
-// asynchronous copies with the tile box (two CTAs per SM instead of three;
-// the default: c3 4.86 / 4.83 / 4.99 Gpx-it/s for EP = 0 / 1 / 2).
-template <typename T, bool FAST, int EP>
-__global__ void __launch_bounds__(384, EP == 2 ? 2 : 3) step_b_kernel(const __grid_constant__ ConvArgs<T> a,
-                                                                      const __grid_constant__ StepW wt) {
-  Conv<T, FAST, 4, 0, false, true> E(a);
+// point y' = x_c + betaN (x_c - x) -> out1.  wt: flipped taps.  The epilogue
+// operands (tvg, x, x_prev) are staged in the term buffers by asynchronous copies
+// issued with the tile box (two CTAs per SM; measured against operands held in
+// registers across the stencil or loaded after it, three CTAs per SM: c3 4.99 vs
+// 4.86 / 4.83 Gpx-it/s).
+template <typename T, bool FAST, int KD, int KU>
+__global__ void __launch_bounds__(384, 2) step_b_kernel(const __grid_constant__ ConvArgs<T> a,
+                                                         const __grid_constant__ StepW wt) {
+  Conv<T, FAST, 4, 0, false, true, KD, KU> E(a);
   E.pw = wt.w;
   const bool tv = a.alpha != 0.0;
   const T two = T(2), alpha = T(a.alpha), beta = T(a.sbeta), L = T(a.sL), betaN = T(a.sbetaN);
@@ -152,38 +274,23 @@ __global__ void __launch_bounds__(384, EP == 2 ? 2 : 3) step_b_kernel(const __gr
   const int tile = blockIdx.x;
   int h0, w0;
   E.tile_origin(tile, h0, w0);
-  if (EP == 2) {
-    if (tv) {
-      const T* const ops[3] = {a.TVG, a.in0, a.in1};
-      E.template stage_own_n<3>(h0, w0, ops, 0);
-    } else {
-      const T* const ops[2] = {a.in0, a.in1};
-      E.template stage_own_n<2>(h0, w0, ops, 1);
-    }
+  pdl_sync();
+  if (tv) {
+    const T* const ops[3] = {a.TVG, a.in0, a.in1};
+    E.template stage_own_n<3>(h0, w0, ops, 0);
+  } else {
+    const T* const ops[2] = {a.in0, a.in1};
+    E.template stage_own_n<2>(h0, w0, ops, 1);
   }
   E.load_async(h0, w0, a.R, E.pa());
   cp_commit();
   const int h = h0 + E.ty;
-  T tpre[4], xpre[4], xppre[4];
-  auto fetch = [&]() {
-#pragma unroll
-    for (int o = 0; o < 4; ++o) {
-      const int w = w0 + E.tx * 4 + o;
-      tpre[o] = xpre[o] = xppre[o] = T(0);
-      if (h < H && w < W) {
-        const int64_t i = E.gidx(h, w, E.ch);
-        if (tv) tpre[o] = ldcg(a.TVG + i);
-        xpre[o] = ldcg(a.in0 + i);
-        xppre[o] = ldcg(a.in1 + i);
-      }
-    }
-  };
-  if (EP == 0) fetch();
   cp_wait<0>();
   __syncthreads();
   T acc[4];
   E.stencil(E.pa() + (size_t)E.ch * a.g.SH * E.swp(), E.wadj(), acc);
-  if (EP == 1) fetch();
+  const T z[4] = {T(0), T(0), T(0), T(0)};
+  E.opsm = true;
   double part = 0.0;
 #pragma unroll
   for (int o = 0; o < 4; ++o) {
@@ -191,17 +298,9 @@ __global__ void __launch_bounds__(384, EP == 2 ? 2 : 3) step_b_kernel(const __gr
     const int w = w0 + q;
     if (h < H && w < W) {
       const int64_t i = E.gidx(h, w, E.ch);
-      T tg, xv, xpv;
-      if (EP == 2) {
-        E.opsm = true;
-        tg = tv ? E.opv(0, E.ty, q, tpre, o) : T(0);
-        xv = E.opv(1, E.ty, q, xpre, o);
-        xpv = E.opv(2, E.ty, q, xppre, o);
-      } else {
-        tg = tpre[o];
-        xv = xpre[o];
-        xpv = xppre[o];
-      }
+      const T tg = tv ? E.opv(0, E.ty, q, z, o) : T(0);
+      const T xv = E.opv(1, E.ty, q, z, o);
+      const T xpv = E.opv(2, E.ty, q, z, o);
       T gv = two * acc[o];
       if (tv) gv = gv + alpha * tg;
       a.G[i] = gv;
@@ -227,9 +326,9 @@ template <typename T> struct SrcCandExtrap {
 
 // Backtracking retry (lower_solvers.py:170-177): CTAs [0, nTiles): the value at x_c = y - g / L with
 // y = in0 + beta (in0 - in1) (lower_value form, x_c -> out0) + the restart-dot partial g.(x_c - in0);
-// CTAs [nTiles, 2 nTiles) (launched only with the in-kernel decision sums): the speculative stage A at
-// the retry's next extrapolation point (sums set: sflag & 2), so an accepted retry needs no separate
-// stage-A launch.
+// with the in-kernel decision sums (step_tail.h) the grid continues with tl.nR reducer CTAs and nTiles
+// CTAs of the speculative stage A at the retry's next extrapolation point (sums set: sflag & 2), so an
+// accepted retry needs no separate stage-A launch.
 template <typename T, bool FAST>
 __global__ void __launch_bounds__(384, 2) step_c_kernel(const __grid_constant__ ConvArgs<T> a,
                                                             const __grid_constant__ StepW wt,
@@ -238,28 +337,29 @@ __global__ void __launch_bounds__(384, 2) step_c_kernel(const __grid_constant__ 
   E.opsm = true;
   E.pw = wt.w;
   const bool tv = a.alpha != 0.0;
-  const int nT = a.g.nTiles;
-  const bool isC = (int)blockIdx.x < nT;
-  const int tile = isC ? (int)blockIdx.x : (int)blockIdx.x - nT;
+  const int nT = a.g.nTiles, nR = tl.on ? tl.nR : 0;
+  const int b = (int)blockIdx.x;
+  const bool isC = b < nT, isR = !isC && b < nT + nR;
+  const int tile = isC ? b : b - nT - nR;
   E.tb0 = tile;       // the stage loops run this one tile
   E.tbs = nT;
-  if (isC) {
+  pdl_sync();
+  if (isR) {
+    tail_reduce(E.tm(), a, tl, b - nT, true);
+  } else if (isC) {
     E.stageC(SrcCand<T>{a.in0, a.in1, a.G, T(a.sbeta), T(a.sL)}, a.RC, tv, a.TV2C, a.out0, a.G, a.in0, &a.s_t1,
              &a.s_fitc, &a.s_tvc);
-    if (tl.on) tail_fold(E, a, tl, true, tile, nullptr, nullptr);
   } else {
     const SumDev* sf = (a.sflag & 2) ? &a.s_fit2 : &a.s_fit;
     const SumDev* st = (a.sflag & 2) ? &a.s_tv2 : &a.s_tv;
     E.stageA(SrcCandExtrap<T>{a.in0, a.in1, a.G, T(a.sbeta), T(a.sL), T(a.sbetaN)}, a.R, a.ydat, tv, a.TV2, a.TVG,
              sf, st);
-    if (tl.on) tail_fold(E, a, tl, false, tile, sf, st);
   }
 }
 
 template <typename T, bool FAST>
 __global__ void __launch_bounds__(384, 2) step_a_kernel(const __grid_constant__ ConvArgs<T> a,
-                                                            const __grid_constant__ StepW wt,
-                                                            const __grid_constant__ StepTail tl) {
+                                                            const __grid_constant__ StepW wt) {
   // value + TV gradient terms at a point (stage A): sflag 0: y = in0 (the
   // materialised y'); 1: y = in0 + beta (in0 - in1).  Sums into s_fit/s_tv
   // (sflag & 2: the second set s_fit2/s_tv2)
@@ -269,33 +369,41 @@ __global__ void __launch_bounds__(384, 2) step_a_kernel(const __grid_constant__ 
   const bool tv = a.alpha != 0.0;
   const SumDev* sf = (a.sflag & 2) ? &a.s_fit2 : &a.s_fit;
   const SumDev* st = (a.sflag & 2) ? &a.s_tv2 : &a.s_tv;
+  pdl_sync();
   if (a.sflag & 1)
     E.stageA(SrcExtrap<T>{a.in0, a.in1, T(a.sbeta)}, a.R, a.ydat, tv, a.TV2, a.TVG, sf, st);
   else
     E.stageA(SrcLin<T>{a.in0}, a.R, a.ydat, tv, a.TV2, a.TVG, sf, st);
-  if (tl.on) tail_fold(E, a, tl, false, (int)blockIdx.x, sf, st);   // one tile per CTA
 }
 
 // candidate value (as step_c, sflag 0) and speculative stage A at y' = out1
 // (as step_a, sflag 0 / 2 in sL > 0 ? set 2 : set 1) in ONE launch of 2 x nTiles
-// CTAs: the two independent passes share the waves (one tail instead of two).
+// CTAs (+ the reducer CTAs of step_tail.h between the halves): the two independent
+// passes share the waves (one tail instead of two).
 // Both halves run ONE code path up to the end of the stencil (epilogue operands
 // and the tile box as asynchronous copies, then the forward taps), so the
 // kernel carries a single copy of the unrolled stencil (instruction-cache
 // footprint); the epilogues are stageC's / stageA's (tileC / tileA on the
 // precomputed accumulators: the same arithmetic).
-template <typename T, bool FAST>
+template <typename T, bool FAST, int KD, int KU>
 __global__ void __launch_bounds__(384, 2) step_ca_kernel(const __grid_constant__ ConvArgs<T> a,
                                                             const __grid_constant__ StepW wt,
                                                             const __grid_constant__ StepTail tl) {
-  Conv<T, FAST, 4, 0, false, true> E(a);   // wt: forward taps
+  Conv<T, FAST, 4, 0, false, true, KD, KU> E(a);   // wt: forward taps
   E.pw = wt.w;
   const bool tv = a.alpha != 0.0;
-  const int nT = a.g.nTiles;
-  const bool isC = (int)blockIdx.x < nT;
-  const int tile = isC ? (int)blockIdx.x : (int)blockIdx.x - nT;
+  const int nT = a.g.nTiles, nR = tl.on ? tl.nR : 0;
+  const int b = (int)blockIdx.x;
+  const bool isC = b < nT;
+  if (!isC && b < nT + nR) {   // reducer CTAs sit between the two halves (step_tail.h)
+    pdl_sync();
+    tail_reduce(E.tm(), a, tl, b - nT, false);
+    return;
+  }
+  const int tile = isC ? b : b - nT - nR;
   int h0, w0;
   E.tile_origin(tile, h0, w0);
+  pdl_sync();
   if (isC) {
     const T* const ops[3] = {a.ydat, a.G, a.in1};
     E.template stage_own_n<3>(h0, w0, ops, 0);
@@ -314,13 +422,11 @@ __global__ void __launch_bounds__(384, 2) step_ca_kernel(const __grid_constant__
     const double part = E.tileC(E.pa(), h0, w0, z, z, z, a.RC, tv, a.TV2C, nullptr, true, true, acc);
     E.tile_partial(a.s_t1, tile, part);
     E.tile_leaves(h0, w0, tv ? 3 : 1, &a.s_fitc, &a.s_tvc, koff);
-    if (tl.on) tail_fold(E, a, tl, true, tile, nullptr, nullptr);
   } else {
     const SumDev* sf = (a.sflag & 2) ? &a.s_fit2 : &a.s_fit;
     const SumDev* st = (a.sflag & 2) ? &a.s_tv2 : &a.s_tv;
     E.tileA(E.pa(), E.pa(), 0, h0, w0, z, a.R, tv, a.TV2, a.TVG, true, acc);
     E.tile_leaves(h0, w0, tv ? 3 : 1, sf, st, koff);
-    if (tl.on) tail_fold(E, a, tl, false, tile, sf, st);
   }
 }
 
@@ -356,18 +462,28 @@ __global__ void step_extrap_kernel(const T* x, const T* xp, T beta, T* out, int6
   }
 }
 
-StepKernels step_kernels(int fast) {
+template <int KD, int KU>
+static void pick_bca(StepKernels& k, int fast) {
+  k.b = fast ? (const void*)step_b_kernel<double, true, KD, KU> : (const void*)step_b_kernel<double, false, KD, KU>;
+  k.ca = fast ? (const void*)step_ca_kernel<double, true, KD, KU> : (const void*)step_ca_kernel<double, false, KD, KU>;
+}
+
+StepKernels step_kernels(int fast, int ksz) {
   StepKernels k;
-  const char* ev = getenv("ADP_SB");   // stage-B epilogue operand variant (see step_b_kernel)
-  const int ep = ev ? atoi(ev) : 2;
-  k.b_ep = ep;
-  if (ep == 1) k.b = fast ? (const void*)step_b_kernel<double, true, 1> : (const void*)step_b_kernel<double, false, 1>;
-  else if (ep == 2) k.b = fast ? (const void*)step_b_kernel<double, true, 2> : (const void*)step_b_kernel<double, false, 2>;
-  else k.b = fast ? (const void*)step_b_kernel<double, true, 0> : (const void*)step_b_kernel<double, false, 0>;
+  k.b_ep = 2;
+  // the two hot kernels (stage B, candidate value + speculative stage A) have instances that carry
+  // the 15 x 15 stencil only; ADP_SU: its rows per loop iteration (default 5; 15: straight-line code, whose instruction
+  // footprint costs the candidate kernel 9 us per launch)
+  const char* ev = getenv("ADP_SU");
+  const int su = ev ? atoi(ev) : 5;
+  if (ksz == 15 && su == 1) pick_bca<15, 1>(k, fast);
+  else if (ksz == 15 && su == 3) pick_bca<15, 3>(k, fast);
+  else if (ksz == 15 && su == 5) pick_bca<15, 5>(k, fast);
+  else if (ksz == 15 && su != 0) pick_bca<15, 15>(k, fast);
+  else pick_bca<0, 0>(k, fast);
   k.c = fast ? (const void*)step_c_kernel<double, true> : (const void*)step_c_kernel<double, false>;
   k.a = fast ? (const void*)step_a_kernel<double, true> : (const void*)step_a_kernel<double, false>;
   k.red = (const void*)step_reduce_kernel<double>;
-  k.ca = fast ? (const void*)step_ca_kernel<double, true> : (const void*)step_ca_kernel<double, false>;
   k.extrap = (const void*)step_extrap_kernel<double>;
   return k;
 }
