@@ -581,6 +581,7 @@ static int conv_plan_init(PlanImpl& P) {
       P.step_smem = (size_t)P.step_o_tm + tm;
       StepKernels sk = step_kernels(P.d.mode == ADP_MODE_FAST, g.kh == g.kw ? g.kh : 0);
       P.k_extrap = sk.extrap;
+      P.k_cand = sk.cand;
       P.step_smem_b = sk.b_ep == 2 ? P.step_smem : (size_t)g.o_pa + pa;   // stage B: no term buffers (three CTAs per SM)
       if (setup_kernel(P, P.k_sb, sk.b, g.threads, P.step_smem_b, g.nTiles) == ADP_OK &&
           setup_kernel(P, P.k_sca, sk.ca, g.threads, P.step_smem, 2 * g.nTiles) == ADP_OK &&
@@ -1185,26 +1186,39 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
       if (val <= h_y - 0.5 * gn * gn / L_try + 1e-15 * fabs(h_y)) break;
       L_try *= 2.0;
       if (++k >= 60) { status = ST_BT_FAIL; fail_iter = t; break; }
-      ConvArgs<T> a = sa_args;
-      a.in0 = X[ix]; a.in1 = X[ixp]; a.out0 = X[ic]; a.sbeta = beta; a.sL = L_try; a.sbetaN = beta2;
-      a.sflag = par ? 0 : 2;   // the set the speculative stage A writes (as in the first candidate's launch)
-      StepTail tl = P.tail;
-      tl.setR = par;
-      if (tl.on) {
+      if (P.tail.on) {
+        // in-kernel sums: the retry's candidate and next extrapolation point are materialised
+        // elementwise, then the candidate-value + speculative stage-A launch runs as for the first
+        // candidate (its reducers fold all six sums again; the first three are unchanged)
+        {
+          const T* xp_ = X[ix]; const T* xpp_ = X[ixp]; const T* gp_ = (const T*)P.ws[5];
+          T b_ = (T)beta, L_ = (T)L_try, bn_ = (T)beta2;
+          T* o0 = X[ic]; T* o1 = Yn;
+          int64_t nn = g.N;
+          void* cargs[] = {(void*)&xp_, (void*)&xpp_, (void*)&gp_, (void*)&b_, (void*)&L_, (void*)&bn_,
+                           (void*)&o0, (void*)&o1, (void*)&nn};
+          CK(cudaLaunchKernel(P.k_cand, dim3(4 * P.sm_count), dim3(256), cargs, 0, st));
+          ++launches;
+        }
+        ConvArgs<T> a = sa_args;
+        a.in0 = X[ic]; a.in1 = X[ix]; a.out1 = Yn; a.sflag = par ? 0 : 2;
+        StepTail tl = P.tail;
+        tl.setR = par;
         a.hscal = d_hscal;
         a.hflag = d_hflag;
         a.hseq = ++P.step_seq;
-      }
-      // in-kernel sums: the retry's value pass and the speculative stage A at its next extrapolation
-      // point share one launch; otherwise the value pass alone, then the reduction launch
-      if (int e = step_launch(P, P.k_sc, a, st, false, P.step_smem, tl.on ? 2 * nT + tl.nR : nT, &P.wfwd, &tl))
-        return e;
-      ++launches;
-      ++vals;
-      if (tl.on) {
+        if (int e = step_launch(P, P.k_sca, a, st, false, P.step_smem, 2 * nT + tl.nR, &P.wfwd, &tl)) return e;
+        ++launches;
+        ++vals;
         if (int e = wait_flag(a.hseq)) return e;
         fitc = P.h_scal[4]; tvc = P.h_scal[5]; dot = P.h_scal[3];
       } else {
+        ConvArgs<T> a = sa_args;
+        a.in0 = X[ix]; a.in1 = X[ixp]; a.out0 = X[ic]; a.sbeta = beta; a.sL = L_try; a.sflag = 1;
+        StepTail tl = P.tail;
+        if (int e = step_launch(P, P.k_sc, a, st, false, P.step_smem, nT, &P.wfwd, &tl)) return e;
+        ++launches;
+        ++vals;
         if (int e = reduce(2, 3)) return e;
         fitc = P.h_scal[0]; tvc = P.h_scal[1]; dot = P.h_scal[2];
       }

@@ -75,6 +75,7 @@ struct PlanImpl {
   int profile = 0;              // adp_plan_profile: time the dominant kernel of host-stepped solves
   cudaEvent_t prof_ev[2] = {nullptr, nullptr};
   const void* k_extrap = nullptr;
+  const void* k_cand = nullptr;
   size_t step_smem = 0;
   int step_o_tm = 0;
   double* h_kern = nullptr;     // pinned: the solve's stencil, read back to build the stage kernels' tap sets

@@ -138,6 +138,7 @@ struct StepKernels {
   const void* red;
   const void* extrap;
   const void* ca;
+  const void* cand;   // elementwise backtracking-retry candidate + its next extrapolation point
   int b_ep;        // stage-B epilogue operand variant (2: term buffers, two CTAs per SM)
 };
 // k: the plan's stencil size when square (instances specialised to 15 x 15 exist), else 0

@@ -127,7 +127,8 @@ __device__ __forceinline__ void warp_fold4(const WarpTask (&t)[4], double (&out)
 // polled tile run (t1), plain tile run (t0).
 // (inlined: a real call in the stage kernels costs the hot path its register allocation -- measured)
 template <typename T>
-__device__ __forceinline__ void tail_reduce(double* red, const ConvArgs<T>& a, const StepTail& tl, int rid, bool retry) {
+__device__ __forceinline__ void tail_reduce(double* red, const ConvArgs<T>& a, const StepTail& tl, int rid) {
+  constexpr bool retry = false;   // a retry re-runs the candidate-value launch: all six sums are in place
   __shared__ int s_last;
   const int GL = tl.GL, tW = tl.tW, nG = tl.nG;
   const int koff = (int)(a.g.Ng / a.g.leafL);
@@ -345,7 +346,7 @@ __global__ void __launch_bounds__(384, 2) step_c_kernel(const __grid_constant__ 
   E.tbs = nT;
   pdl_sync();
   if (isR) {
-    tail_reduce(E.tm(), a, tl, b - nT, true);
+    tail_reduce(E.tm(), a, tl, b - nT);
   } else if (isC) {
     E.stageC(SrcCand<T>{a.in0, a.in1, a.G, T(a.sbeta), T(a.sL)}, a.RC, tv, a.TV2C, a.out0, a.G, a.in0, &a.s_t1,
              &a.s_fitc, &a.s_tvc);
@@ -397,7 +398,7 @@ __global__ void __launch_bounds__(384, 2) step_ca_kernel(const __grid_constant__
   const bool isC = b < nT;
   if (!isC && b < nT + nR) {   // reducer CTAs sit between the two halves (step_tail.h)
     pdl_sync();
-    tail_reduce(E.tm(), a, tl, b - nT, false);
+    tail_reduce(E.tm(), a, tl, b - nT);
     return;
   }
   const int tile = isC ? b : b - nT - nR;
@@ -453,6 +454,21 @@ __global__ void __launch_bounds__(512, 1) step_reduce_kernel(const __grid_consta
   }
 }
 
+// backtracking retry (lower_solvers.py:170-177), elementwise: the candidate at the doubled L,
+// x_c = (x + beta (x - x_prev)) - g / L -> out0, and its next extrapolation point
+// y'' = x_c + betaN (x_c - x) -> out1 (step_b_kernel's expressions); the candidate-value kernel then
+// runs on them exactly as for the first candidate.
+template <typename T>
+__global__ void step_cand_kernel(const T* x, const T* xp, const T* g, T beta, T L, T betaN, T* out0, T* out1,
+                                 int64_t n) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const T xv = ldcg(x + i), xpv = ldcg(xp + i), gv = ldcg(g + i);
+    const T xc = (xv + beta * (xv - xpv)) - gv / L;
+    out0[i] = xc;
+    out1[i] = xc + betaN * (xc - xv);
+  }
+}
+
 // converged: x~ = x + beta (x - x_prev)   (lower_solvers.py:200-201)
 template <typename T>
 __global__ void step_extrap_kernel(const T* x, const T* xp, T beta, T* out, int64_t n) {
@@ -485,6 +501,7 @@ StepKernels step_kernels(int fast, int ksz) {
   k.a = fast ? (const void*)step_a_kernel<double, true> : (const void*)step_a_kernel<double, false>;
   k.red = (const void*)step_reduce_kernel<double>;
   k.extrap = (const void*)step_extrap_kernel<double>;
+  k.cand = (const void*)step_cand_kernel<double>;
   return k;
 }
 
