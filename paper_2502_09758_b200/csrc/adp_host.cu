@@ -598,7 +598,7 @@ static int conv_plan_init(PlanImpl& P) {
         if (!(et && atoi(et) == 0) && g.H % g.TH == 0 && g.W % g.TW == 0 && pow2(GL) && GL <= 1024 &&
             pow2(g.tilesW) && g.tilesW <= 1024 && pow2(g.tilesH) && 2 * g.tilesH <= 1024 && P.s_fit.regular &&
             P.s_tv.regular && P.s_t0.regular && (int64_t)P.s_fit.nLeaves == GL * g.tilesH &&
-            (int64_t)P.s_tv.nLeaves == 2 * GL * g.tilesH && g.threads >= 192) {
+            (int64_t)P.s_tv.nLeaves == 2 * GL * g.tilesH && g.threads >= 64) {
           const size_t nsub = (size_t)11 * g.tilesH * sizeof(double);
           const size_t ncnt = 64;
           CK(cudaMalloc(&P.d_tail, nsub + ncnt));

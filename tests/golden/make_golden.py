@@ -333,6 +333,50 @@ def maid2d_p4():
     save("maid2d_p4.npz", **out)
 
 
+def _maid3_run(tag, perturb_seed):
+    """One reference maid_run on a reduced c3 (64x64x3, the c3 generator's 15x15 line-Gaussian truth
+    shared by the channels, isotropic initial kernel, the reference 2-D MAID settings, 2 accepted
+    upper steps); perturb_seed > 0: y_delta * (1 + 1e-15 N(0, 1))."""
+    from adp import metrics_io as MI
+    from paper_2502_09758_b200 import configs as C
+
+    def ref_blur(x, kernel):
+        return O.ConvOperator(O.Kernel(kernel.data, O.DEPTHWISE2D), x.shape).apply(x)
+    up3 = C.config3(0, size=64, blur_fn=ref_blur)
+    y = np.array(up3.y_delta)
+    if perturb_seed:
+        y = y * (1.0 + 1e-15 * np.random.default_rng(2000 + perturb_seed).standard_normal(y.shape))
+    ref3 = P.UpperProblem(name="c3s", A=O.ConvOperator(O.Kernel(up3.a.data, O.DEPTHWISE2D), y.shape),
+                          a=O.Kernel(up3.a.data, O.DEPTHWISE2D), y_delta=y, beta=0.3, alpha=0.6,
+                          reg=R.SmoothedTV(1e-4), b0=O.Kernel(up3.b0.data, O.DEPTHWISE2D), x0=y.copy(),
+                          mu_floor=10.0, lower_method="agd", lower_max_iters=1200, lower_adaptive=True)
+    cfg = M.MAIDConfig(eps0=0.25, delta0=0.25, alpha0=2e-5, max_bt=2, cg_max_iters=100, max_upper_iters=2)
+    b, x, tr = M.maid_run(ref3, cfg)
+    out = {f"{tag}_{f}": np.asarray(getattr(tr, f)) for f in
+           ("loss", "grad_norm", "eps", "delta", "alpha", "lower_iters_cum", "cg_iters_cum")}
+    out[f"{tag}_final"] = tr.final_loss
+    out[f"{tag}_psnr"] = MI.psnr(x, up3.ground_truth)
+    out[f"{tag}_b"] = b.data
+    if not perturb_seed:
+        out["y_delta"] = y
+        out["x_true"] = up3.ground_truth
+        out["a"] = up3.a.data
+        out["b0"] = up3.b0.data
+    return out
+
+
+def maid3_p4():
+    """P4 full-run fixture for an RGB 15x15 (c3 / c4 type) MAID run: the reference run plus three
+    1e-15-perturbed replicas."""
+    import multiprocessing as mp
+    with mp.get_context("fork").Pool(4) as pool:
+        parts = pool.starmap(_maid3_run, [("ref", 0), ("rep1", 1), ("rep2", 2), ("rep3", 3)])
+    out = {}
+    for d in parts:
+        out.update(d)
+    save("maid3_p4.npz", **out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:
         for name in sys.argv[1:]:
