@@ -571,9 +571,10 @@ static int conv_plan_init(PlanImpl& P) {
   {
     const char* ev = getenv("ADP_STEP");
     const int want = ev ? atoi(ev) : -1;
-    if (want != 0 && P.d.dtype == ADP_DTYPE_F64 && g.rwb == 4 && g.fused && g.fuseCA && !slab &&
-        g.threads <= 384 && (want == 1 || g.N >= (1 << 18)) && ((g.kh * g.kw + 1) & ~1) * g.C <= kStepWMax &&
-        g.tpc % 32 == 0) {   // taps as kernel parameters; channel-uniform warps
+    if (want != 0 && P.d.dtype == ADP_DTYPE_F64 && g.rwb == 4 && g.fused && !slab &&
+        g.threads <= 384 && (want == 1 || g.N >= (1 << 18)) &&
+        ((g.kh * g.kw + 1) & ~1) * g.C <= ((g.kh == 31 && g.kw == 31) ? kStepWMax : kStepWSmall) &&
+        g.tpc % 32 == 0) {   // taps as kernel parameters (the 31 x 31 instances take the large block); channel-uniform warps
       const size_t es = (size_t)P.esize;
       const size_t pa = ((size_t)g.C * g.SH * g.SWP * es + 127) & ~size_t(127);
       const size_t tm = (size_t)3 * g.TH * g.TW * g.C * sizeof(double);
@@ -969,7 +970,7 @@ int adp_lower_hess_diag(adp_plan* p, const adp_lower* lp, const void* x, void* o
 // flow here, expression for expression (conv_solve_kernel), so iterates,
 // decisions and counters are identical to the single-launch solve.
 static int step_launch(PlanImpl& P, KernelInfo& k, ConvArgs<double>& a, cudaStream_t st, bool coop, size_t smem,
-                       int grid, const StepW* wt = nullptr, const StepTail* tl = nullptr) {
+                       int grid, const StepWL* wt = nullptr, const StepTail* tl = nullptr) {
   void* args[] = {&a, (void*)wt, (void*)tl};
   if (coop) {
     CK(cudaMemsetAsync(P.d_bar, 0, sizeof(unsigned int), st));

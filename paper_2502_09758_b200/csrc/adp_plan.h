@@ -79,7 +79,8 @@ struct PlanImpl {
   size_t step_smem = 0;
   int step_o_tm = 0;
   double* h_kern = nullptr;     // pinned: the solve's stencil, read back to build the stage kernels' tap sets
-  StepW wfwd{}, wadj{};         // forward / flipped taps (kernel parameters of the stage kernels)
+  StepWL wfwd{}, wadj{};        // forward / flipped taps (kernel parameters of the stage kernels; the
+                                // instances for stencils of <= kStepWSmall taps read the first part only)
   StepTail tail{};              // in-kernel decision sums of the host-stepped solve (tail.on: geometry allows it)
   void* d_tail = nullptr;       // sub-values + tickets
   CUtensorMap tm[5];            // X[0..2], R, P[0]

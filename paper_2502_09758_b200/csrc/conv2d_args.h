@@ -96,10 +96,16 @@ struct ConvArgs {
 // (constant bank 0), channel-major [c][i][j] with ndimage's |w| <= DBL_EPSILON
 // taps zeroed; forward taps for the value passes, flipped for the adjoint.
 // Channel blocks are padded to an even tap count (16-byte aligned tap pairs).
-constexpr int kStepWMax = 1024;
-struct alignas(16) StepW {
-  double w[kStepWMax];
+// Two capacities: StepW (stencils up to 1024 padded taps: c2-c4) and StepWL (31 x 31 x 3: c5), so the
+// common launches do not carry the large block; the host fills a StepWL and passes its address to either.
+constexpr int kStepWSmall = 1024;
+constexpr int kStepWMax = 3072;
+template <int N>
+struct alignas(16) StepWT {
+  double w[N];
 };
+using StepW = StepWT<kStepWSmall>;
+using StepWL = StepWT<kStepWMax>;
 
 template <typename T>
 struct KgcArgs {

@@ -264,9 +264,9 @@ __device__ __forceinline__ void tail_reduce(double* red, const ConvArgs<T>& a, c
 // issued with the tile box (two CTAs per SM; measured against operands held in
 // registers across the stencil or loaded after it, three CTAs per SM: c3 4.99 vs
 // 4.86 / 4.83 Gpx-it/s).
-template <typename T, bool FAST, int KD, int KU>
+template <typename T, bool FAST, int KD, int KU, class WT>
 __global__ void __launch_bounds__(384, 2) step_b_kernel(const __grid_constant__ ConvArgs<T> a,
-                                                         const __grid_constant__ StepW wt) {
+                                                         const __grid_constant__ WT wt) {
   Conv<T, FAST, 4, 0, false, true, KD, KU> E(a);
   E.pw = wt.w;
   const bool tv = a.alpha != 0.0;
@@ -330,11 +330,11 @@ template <typename T> struct SrcCandExtrap {
 // with the in-kernel decision sums (step_tail.h) the grid continues with tl.nR reducer CTAs and nTiles
 // CTAs of the speculative stage A at the retry's next extrapolation point (sums set: sflag & 2), so an
 // accepted retry needs no separate stage-A launch.
-template <typename T, bool FAST>
+template <typename T, bool FAST, int KD, int KU, class WT>
 __global__ void __launch_bounds__(384, 2) step_c_kernel(const __grid_constant__ ConvArgs<T> a,
-                                                            const __grid_constant__ StepW wt,
+                                                            const __grid_constant__ WT wt,
                                                             const __grid_constant__ StepTail tl) {
-  Conv<T, FAST, 4, 0, false, true> E(a);   // wt: forward taps
+  Conv<T, FAST, 4, 0, false, true, KD, KU> E(a);   // wt: forward taps
   E.opsm = true;
   E.pw = wt.w;
   const bool tv = a.alpha != 0.0;
@@ -358,13 +358,13 @@ __global__ void __launch_bounds__(384, 2) step_c_kernel(const __grid_constant__ 
   }
 }
 
-template <typename T, bool FAST>
+template <typename T, bool FAST, int KD, int KU, class WT>
 __global__ void __launch_bounds__(384, 2) step_a_kernel(const __grid_constant__ ConvArgs<T> a,
-                                                            const __grid_constant__ StepW wt) {
+                                                            const __grid_constant__ WT wt) {
   // value + TV gradient terms at a point (stage A): sflag 0: y = in0 (the
   // materialised y'); 1: y = in0 + beta (in0 - in1).  Sums into s_fit/s_tv
   // (sflag & 2: the second set s_fit2/s_tv2)
-  Conv<T, FAST, 4, 0, false, true> E(a);   // wt: forward taps
+  Conv<T, FAST, 4, 0, false, true, KD, KU> E(a);   // wt: forward taps
   E.opsm = true;
   E.pw = wt.w;
   const bool tv = a.alpha != 0.0;
@@ -386,9 +386,9 @@ __global__ void __launch_bounds__(384, 2) step_a_kernel(const __grid_constant__ 
 // kernel carries a single copy of the unrolled stencil (instruction-cache
 // footprint); the epilogues are stageC's / stageA's (tileC / tileA on the
 // precomputed accumulators: the same arithmetic).
-template <typename T, bool FAST, int KD, int KU>
+template <typename T, bool FAST, int KD, int KU, class WT>
 __global__ void __launch_bounds__(384, 2) step_ca_kernel(const __grid_constant__ ConvArgs<T> a,
-                                                            const __grid_constant__ StepW wt,
+                                                            const __grid_constant__ WT wt,
                                                             const __grid_constant__ StepTail tl) {
   Conv<T, FAST, 4, 0, false, true, KD, KU> E(a);   // wt: forward taps
   E.pw = wt.w;
@@ -478,27 +478,28 @@ __global__ void step_extrap_kernel(const T* x, const T* xp, T beta, T* out, int6
   }
 }
 
-template <int KD, int KU>
-static void pick_bca(StepKernels& k, int fast) {
-  k.b = fast ? (const void*)step_b_kernel<double, true, KD, KU> : (const void*)step_b_kernel<double, false, KD, KU>;
-  k.ca = fast ? (const void*)step_ca_kernel<double, true, KD, KU> : (const void*)step_ca_kernel<double, false, KD, KU>;
+template <int KD, int KU, class WT>
+static void pick(StepKernels& k, int fast) {
+  k.b = fast ? (const void*)step_b_kernel<double, true, KD, KU, WT> : (const void*)step_b_kernel<double, false, KD, KU, WT>;
+  k.ca = fast ? (const void*)step_ca_kernel<double, true, KD, KU, WT>
+              : (const void*)step_ca_kernel<double, false, KD, KU, WT>;
+  k.a = fast ? (const void*)step_a_kernel<double, true, KD, KU, WT> : (const void*)step_a_kernel<double, false, KD, KU, WT>;
+  k.c = fast ? (const void*)step_c_kernel<double, true, KD, KU, WT> : (const void*)step_c_kernel<double, false, KD, KU, WT>;
 }
 
 StepKernels step_kernels(int fast, int ksz) {
   StepKernels k;
   k.b_ep = 2;
-  // the two hot kernels (stage B, candidate value + speculative stage A) have instances that carry
-  // the 15 x 15 stencil only; ADP_SU: its rows per loop iteration (default 5; 15: straight-line code, whose instruction
-  // footprint costs the candidate kernel 9 us per launch)
+  // instances that carry one stencil size only: 15 x 15 (c3, c4) with the row loop unrolled 5 rows at a
+  // time (ADP_SU=15: straight-line code, whose instruction footprint costs the candidate kernel 9 us per
+  // launch; ADP_SU=0: the generic multi-stencil instances) and 31 x 31 (c5: one row per iteration, the
+  // large tap block); everything else runs the generic instances
   const char* ev = getenv("ADP_SU");
   const int su = ev ? atoi(ev) : 5;
-  if (ksz == 15 && su == 1) pick_bca<15, 1>(k, fast);
-  else if (ksz == 15 && su == 3) pick_bca<15, 3>(k, fast);
-  else if (ksz == 15 && su == 5) pick_bca<15, 5>(k, fast);
-  else if (ksz == 15 && su != 0) pick_bca<15, 15>(k, fast);
-  else pick_bca<0, 0>(k, fast);
-  k.c = fast ? (const void*)step_c_kernel<double, true> : (const void*)step_c_kernel<double, false>;
-  k.a = fast ? (const void*)step_a_kernel<double, true> : (const void*)step_a_kernel<double, false>;
+  if (ksz == 15 && su == 15) pick<15, 15, StepW>(k, fast);
+  else if (ksz == 15 && su != 0) pick<15, 5, StepW>(k, fast);
+  else if (ksz == 31) pick<31, 1, StepWL>(k, fast);
+  else pick<0, 0, StepW>(k, fast);
   k.red = (const void*)step_reduce_kernel<double>;
   k.extrap = (const void*)step_extrap_kernel<double>;
   k.cand = (const void*)step_cand_kernel<double>;

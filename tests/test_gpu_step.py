@@ -35,8 +35,8 @@ def test_step_solve_equals_persistent(adp, cfg, size, iters):
     up = configs.CONFIGS[cfg](0, size=size)
     r0, s0, n0, _ = _solve(adp, nat, up, iters, False)
     r1, s1, n1, f1 = _solve(adp, nat, up, iters, True)
-    assert f1["step"] == (cfg == "c3")     # c5-geometry plans (K = 31) keep the persistent kernel
-    assert f1["tail"] == (cfg == "c3")     # decision sums folded inside the stage kernels
+    assert f1["step"] and f1["tail"]       # c3 (15 x 15) and c5-geometry (31 x 31) plans: stage kernels with
+                                           # the decision sums folded inside them
     assert n1 == n0 and r1.iters == r0.iters and r1.grad_norm == r0.grad_norm
     assert {k: s1[k] for k in ("vg_evals", "value_evals", "restarts", "lip", "power_iters")} == \
         {k: s0[k] for k in ("vg_evals", "value_evals", "restarts", "lip", "power_iters")}
