@@ -552,11 +552,16 @@ def other_configs(args, flush, main_wl):
     """Side lines, device time, power iteration included (fresh operator per
     solve, as MAID calls it): c2 (256x256x1), c4 (8 c3 instances = one GPU's
     share of 64), c1 IFT, c5 (one 4096x4096x3 image, K = 31) direct and FFT."""
+    import ctypes
+
     import paper_2502_09758_b200 as adp
     from paper_2502_09758_b200 import _native as nat
     from paper_2502_09758_b200 import configs
     out = {}
     eps, mu = 1e-14, 10.0
+    tf_, ms_ = ctypes.c_double(), ctypes.c_double()
+    nat.check(nat.lib().adp_fp64_peak(ctypes.byref(tf_), ctypes.byref(ms_), nat.stream_ptr()), "fp64 peak")
+    fp64_peak = tf_.value   # measured DFMA TFLOP/s (2 flop per DFMA)
 
     dev = {}   # x0 and the output buffer stay resident in HBM (inputs resident before the timed region)
 
@@ -630,6 +635,19 @@ def other_configs(args, flush, main_wl):
                  "ms_per_solve": 1e3 * t, "stats": {k: st5.get(k) for k in ("power_iters", "vg_evals", "value_evals")},
                  "workload": f"{args.c5_size}x{args.c5_size}x3, 31x31 Gaussian, {args.c5_iters} AGD iterations "
                              "(+ power iteration), one GPU"}
+    # steady state of the direct c5 solve: a second solve 30 iterations longer, the difference per iteration
+    # (the 10-iteration line above carries the power iteration for L(b))
+    flush.zero_()
+    r2, t2 = _timed(lambda: solve(up5, args.c5_iters + 30))
+    if r2.iters > r.iters:
+        per = (t2 - t) / (r2.iters - r.iters)
+        out["c5"]["steady_state"] = {"ms_per_iter": 1e3 * per, "value": up5.y_delta.size / per / 1e9, "unit": UNIT,
+                                     "flop_per_px_it": 2 * 31 * 31 * 3 + 50,
+                                     "strict_ceiling_frac": (2 * 31 * 31 * 3 + 50) * up5.y_delta.size / per / 1e12
+                                     / (0.5 * fp64_peak) if fp64_peak else None,
+                                     "note": "solve of c5_iters + 30 iterations minus the solve above, per iteration; "
+                                             "flop: three 31x31 strict stencils (1.0 value passes) + epilogues; "
+                                             "ceiling: half the measured DFMA rate (DMUL + DADD per tap)"}
     out["c5_fft"] = c5_fft(args, up5, solve, flush)
     return out
 
