@@ -591,6 +591,7 @@ static int conv_plan_init(PlanImpl& P) {
           setup_kernel(P, P.k_sred, sk.red, g.threads, P.smem, g.nTiles) == ADP_OK) {
         CK(cudaMallocHost(&P.h_kern, (size_t)g.kh * g.kw * g.C * sizeof(double)));
         P.step = 1;
+        P.pdl = !(getenv("ADP_PDL") && atoi(getenv("ADP_PDL")) == 0);
         // in-kernel decision sums (step_tail.h): whole tiles, tile rows = power-of-two runs of the
         // perfect sum trees, every fold within one register pass (<= 1024 units); ADP_TAIL=0 disables
         auto pow2 = [](int64_t v) { return v > 0 && (v & (v - 1)) == 0; };
@@ -979,7 +980,7 @@ static int step_launch(PlanImpl& P, KernelInfo& k, ConvArgs<double>& a, cudaStre
     // programmatic dependent launch: the stage kernel's CTAs may become resident while the previous
     // stage kernel drains (it signals at its start); they wait (griddepcontrol.wait) for that grid's
     // completion before touching its data, so only launch latency and index set-up overlap.  ADP_PDL=0: off
-    static const bool pdl = !(getenv("ADP_PDL") && atoi(getenv("ADP_PDL")) == 0);
+    const bool pdl = P.pdl;   // read at plan creation
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(P.g.threads);

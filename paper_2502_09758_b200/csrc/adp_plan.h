@@ -81,6 +81,7 @@ struct PlanImpl {
   double* h_kern = nullptr;     // pinned: the solve's stencil, read back to build the stage kernels' tap sets
   StepWL wfwd{}, wadj{};        // forward / flipped taps (kernel parameters of the stage kernels; the
                                 // instances for stencils of <= kStepWSmall taps read the first part only)
+  bool pdl = true;              // stage kernels launched with programmatic stream serialization (ADP_PDL=0: off)
   StepTail tail{};              // in-kernel decision sums of the host-stepped solve (tail.on: geometry allows it)
   void* d_tail = nullptr;       // sub-values + tickets
   CUtensorMap tm[5];            // X[0..2], R, P[0]

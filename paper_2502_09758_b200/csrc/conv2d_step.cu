@@ -23,6 +23,9 @@ __device__ __forceinline__ void pdl_sync() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
+// polls before a reducer gives up on a unit (>= 64 ns each: about two seconds)
+constexpr unsigned kPollMax = 1u << 25;
+
 // A leaf unit that may still be unwritten: the candidate half's leaves and tile partials are
 // pre-set to an all-ones NaN pattern (never produced by the arithmetic: the hardware's NaN results
 // are canonical), each is one 8-byte store, so reading anything else means reading the unit.  No
@@ -31,7 +34,11 @@ __device__ __forceinline__ double ld_unit(const double* p, bool poll) {
   unsigned long long b;
   asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(b) : "l"(p) : "memory");
   if (poll) {
-    while (b == ~0ull) {
+    for (unsigned spins = 0; b == ~0ull; ++spins) {
+      if (spins > kPollMax) {   // never written (cannot happen for a completed producer grid): fail, do not hang
+        b = 0x7ff8000000000000ull;
+        break;
+      }
       __nanosleep(100);
       asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(b) : "l"(p) : "memory");
     }
@@ -103,7 +110,11 @@ __device__ __forceinline__ void warp_fold4(const WarpTask (&t)[4], double (&out)
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     if (POLL && t[u].p && lane < t[u].n) {
-      while (b[u] == ~0ull) {
+      for (unsigned spins = 0; b[u] == ~0ull; ++spins) {
+        if (spins > kPollMax) {   // see ld_unit: a NaN sum makes the host report a diverged solve
+          b[u] = 0x7ff8000000000000ull;
+          break;
+        }
         __nanosleep(64);
         asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(b[u]) : "l"(t[u].p + lane) : "memory");
       }

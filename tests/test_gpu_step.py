@@ -60,6 +60,28 @@ def test_step_tail_equals_reduce_kernel(adp):
     assert np.array_equal(r1.x_tilde, r0.x_tilde)
 
 
+@pytest.mark.parametrize("env", [{"ADP_SU": "0"}, {"ADP_SU": "15"}, {"ADP_PDL": "0"}])
+def test_step_kernel_variants_bitwise(adp, env):
+    """The stage-kernel variants -- generic multi-stencil instances, straight-line 15 x 15 taps, launches
+    without programmatic stream serialization -- give the default path's iterates bit for bit."""
+    from paper_2502_09758_b200 import _native as nat
+    from paper_2502_09758_b200 import configs
+    up = configs.CONFIGS["c3"](1, size=256)
+    r0, s0, n0, f0 = _solve(adp, nat, up, 80, True)
+    for k, v in env.items():
+        os.environ[k] = v
+    try:
+        r1, s1, n1, f1 = _solve(adp, nat, up, 80, True)
+    finally:
+        for k in env:
+            os.environ.pop(k, None)
+    assert f0["step"] and f1["step"] and f1["tail"]
+    assert n1 == n0 and r1.iters == r0.iters and r1.grad_norm == r0.grad_norm
+    assert {k: s1[k] for k in ("vg_evals", "value_evals", "restarts", "lip")} == \
+        {k: s0[k] for k in ("vg_evals", "value_evals", "restarts", "lip")}
+    assert np.array_equal(r1.x_tilde, r0.x_tilde)
+
+
 def test_step_lockstep_c3(adp, orc):
     """P2 at c3 through the host-stepped path: bitwise vs the oracle."""
     from paper_2502_09758_b200 import _native as nat
