@@ -39,6 +39,7 @@
 #include <math.h>
 #include <stdint.h>
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -60,6 +61,9 @@ constexpr double kInvT2 = 1.0 / (512.0 * 512.0);   // exact power of two
 
 struct Geo {
   int H, W, C, kh, kw, rh, rw, Vh, Vw, ntY, ntX, ntiles, npairs;
+  // chunked stencil passes (see stencil()): this launch covers the global tile pairs pair0.., whose
+  // scratch slots are spair0.. of an S laid out with spairs pairs per channel
+  int pair0, spair0, spairs;
 };
 
 // ---------------------------------------------------------------------------
@@ -233,9 +237,10 @@ __global__ void __launch_bounds__(256, FFT_ROW_MINB) row_fwd_kernel(const __grid
   double dot = 0.0;
   if (A.mode == 0) {
     int h0a, w0a, h0b = 0, w0b = 0;
-    tile_origin(g, 2 * p, h0a, w0a);
-    const bool hasb = 2 * p + 1 < g.ntiles;
-    if (hasb) tile_origin(g, 2 * p + 1, h0b, w0b);
+    const int pg = p + g.pair0;   // global pair
+    tile_origin(g, 2 * pg, h0a, w0a);
+    const bool hasb = 2 * pg + 1 < g.ntiles;
+    if (hasb) tile_origin(g, 2 * pg + 1, h0b, w0b);
     const int ha = h0a - g.rh + row, hb = h0b - g.rh + row;
     const bool rowa = ha >= 0 && ha < g.H, rowb = hasb && hb >= 0 && hb < g.H;
     const bool vrow = row >= g.rh && row - g.rh < g.Vh;     // valid-region row of both tiles
@@ -251,7 +256,7 @@ __global__ void __launch_bounds__(256, FFT_ROW_MINB) row_fwd_kernel(const __grid
     }
     if (A.pro == P_STEP) {
       const double s = block_sum(dot, red);
-      if (threadIdx.x == 0) A.part[blockIdx.x] = s;
+      if (threadIdx.x == 0) A.part[blockIdx.x + g.pair0 * (T / RROWS) * g.C] = s;   // global CTA index
     }
   } else if (A.mode == 2) {   // kgc: the tiles' own valid-region pixels v[h0 + a, w0 + b] (zero elsewhere)
     int h0a, w0a, h0b = 0, w0b = 0;
@@ -281,7 +286,7 @@ __global__ void __launch_bounds__(256, FFT_ROW_MINB) row_fwd_kernel(const __grid
     }
   }
   fft512_reg<false>(v, sm + rr * kPadB, j, A.tw);
-  double2* S = A.S + (((int64_t)c * g.npairs + p) * T + row) * T;
+  double2* S = A.S + (((int64_t)c * g.spairs + g.spair0 + p) * T + row) * T;
 #pragma unroll
   for (int r = 0; r < 8; ++r) S[j + 64 * r] = v[r];
 }
@@ -309,7 +314,7 @@ __global__ void __launch_bounds__(64 * CCOLS, FFT_COL_MINB) col_kernel(const __g
   block_coords(T / CCOLS, A.g.C, p, strip, c);
   const int bi = threadIdx.x % CCOLS, j = threadIdx.x / CCOLS;
   const int col = strip * CCOLS + bi;
-  double2* S = A.S + ((int64_t)c * A.npairs + p) * T * T + col;
+  double2* S = A.S + ((int64_t)c * A.npairs + A.g.spair0 + p) * T * T + col;
   double2 v[8];
 #pragma unroll
   for (int r = 0; r < 8; ++r) v[r] = S[(int64_t)(j + 64 * r) * T];
@@ -463,7 +468,7 @@ __global__ void __launch_bounds__(256, FFT_ROW_MINB) row_inv_kernel(const __grid
   int p, rg, c;
   block_coords(T / RROWS, g.C, p, rg, c);
   const int j = threadIdx.x & 63, rr = threadIdx.x >> 6, row = rg * RROWS + rr;
-  const double2* S = A.S + (((int64_t)c * g.npairs + p) * T + row) * T;
+  const double2* S = A.S + (((int64_t)c * g.spairs + g.spair0 + p) * T + row) * T;
   double2 v[8];
 #pragma unroll
   for (int r = 0; r < 8; ++r) v[r] = S[j + 64 * r];
@@ -471,7 +476,7 @@ __global__ void __launch_bounds__(256, FFT_ROW_MINB) row_inv_kernel(const __grid
   double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll 1
   for (int half = 0; half < 2; ++half) {
-    const int t = 2 * p + half;
+    const int t = 2 * (p + g.pair0) + half;
     if (t >= g.ntiles || row >= g.Vh) break;
     int h0, w0;
     tile_origin(g, t, h0, w0);
@@ -544,8 +549,9 @@ __global__ void __launch_bounds__(256, FFT_ROW_MINB) row_inv_kernel(const __grid
     const double s0 = block_sum(acc0, red);
     const double s1 = block_sum(acc1, red);
     if (threadIdx.x == 0) {
-      A.part[2 * blockIdx.x] = s0;
-      A.part[2 * blockIdx.x + 1] = s1;
+      const int cta = blockIdx.x + g.pair0 * (T / RROWS) * g.C;   // global CTA index
+      A.part[2 * cta] = s0;
+      A.part[2 * cta + 1] = s1;
     }
   }
 }
@@ -738,6 +744,7 @@ using namespace adp::fft;
 
 struct adp_fft_plan {
   Geo g;
+  int chunk = 0;               // tile pairs per chunk of the stencil passes (0: whole image)
   int64_t N = 0;
   double2* S = nullptr;        // (C, npairs, T, T)
   double2* spec = nullptr;     // (2, C, T, T): [0] apply, [1] adjoint
@@ -774,6 +781,7 @@ int build_spectra(adp_fft_plan* P, const double* kern, cudaStream_t st) {
   const Geo& g = P->g;
   Geo kg = g;
   kg.npairs = 2;   // S slots: pair 0 = kernel, pair 1 = flipped kernel
+  kg.spairs = 2;
   RowArgs ra{kg, nullptr, P->S, P->tw, 1, kern, P_NONE, nullptr, nullptr, 0.0, nullptr, nullptr};
   row_fwd_kernel<<<2 * (T / RROWS) * g.C, 256, 0, st>>>(ra);
   ColArgs ca{kg, P->S, nullptr, P->spec, P->tw, 1, 2};
@@ -792,16 +800,41 @@ struct ProArgs {
 
 // One stencil: out/epilogue from (the prologue of) x with the apply (adj = 0) or adjoint (adj = 1)
 // spectrum; K3 partials to part3 (2 per CTA) when non-NULL, K1 partials (P_STEP) to P->partK1.
+// Optional (ADP_FFT_PB > 0, off by default: measured slower, see the plan set-up): the passes run over
+// chunks of P->chunk tile pairs (row pass, column pass, inverse rows per chunk) through ONE chunk-sized
+// scratch region, so the complex scratch of a chunk (12 MB per pair at C = 3) is written, transformed
+// and consumed while it is L2-resident instead of making three round trips to HBM.  Partial sums are indexed by the global CTA, so the results are those of the unchunked
+// passes bit for bit.  A stencil whose inverse-row epilogue reads neighbours of the iterate its own
+// row-pass prologue stores (the candidate's value pass) runs the row pass over the whole image first
+// (the later chunks' tiles must exist), then the other two passes per chunk.
 int stencil(adp_fft_plan* P, int adj, const double* x, const ProArgs& pa, int epi, double* out, const double* y,
             const double* xp, double alpha, double nu, double* part3, cudaStream_t st) {
-  const Geo& g = P->g;
-  const int rgrid = g.npairs * (T / RROWS) * g.C;
-  RowArgs ra{g, x, P->S, P->tw, 0, nullptr, pa.pro, pa.x2, pa.xold, pa.coef, pa.wout, P->partK1};
-  row_fwd_kernel<<<rgrid, 256, 0, st>>>(ra);
-  ColArgs ca{g, P->S, P->spec + (size_t)adj * g.C * T * T, nullptr, P->tw, 0, g.npairs};
-  col_kernel<<<g.npairs * (T / CCOLS) * g.C, 64 * CCOLS, 0, st>>>(ca);
-  InvArgs ia{g, P->S, P->tw, out, y, xp, alpha, nu, epi, part3, P->cgbuf[5], P->cgbuf[6]};
-  row_inv_kernel<<<rgrid, 256, 0, st>>>(ia);
+  Geo g = P->g;
+  const int PB = P->chunk > 0 ? std::min(P->chunk, g.npairs) : g.npairs;
+  const bool reads_nb = epi == E_VALUE || epi == E_GRAD || epi == E_HESS || epi == E_HESSRES;
+  const bool hazard = pa.wout != nullptr && reads_nb && xp == pa.wout && PB < g.npairs;
+  const double2* spec = P->spec + (size_t)adj * g.C * T * T;
+  if (hazard) {
+    g.pair0 = g.spair0 = 0;
+    g.spairs = g.npairs;
+    RowArgs ra{g, x, P->S, P->tw, 0, nullptr, pa.pro, pa.x2, pa.xold, pa.coef, pa.wout, P->partK1};
+    row_fwd_kernel<<<g.npairs * (T / RROWS) * g.C, 256, 0, st>>>(ra);
+  }
+  for (int p0 = 0; p0 < g.npairs; p0 += PB) {
+    const int np = std::min(PB, g.npairs - p0);
+    g.pair0 = p0;
+    g.spair0 = hazard ? p0 : 0;
+    g.spairs = hazard ? g.npairs : PB;
+    const int rgrid = np * (T / RROWS) * g.C;
+    if (!hazard) {
+      RowArgs ra{g, x, P->S, P->tw, 0, nullptr, pa.pro, pa.x2, pa.xold, pa.coef, pa.wout, P->partK1};
+      row_fwd_kernel<<<rgrid, 256, 0, st>>>(ra);
+    }
+    ColArgs ca{g, P->S, spec, nullptr, P->tw, 0, g.spairs};
+    col_kernel<<<np * (T / CCOLS) * g.C, 64 * CCOLS, 0, st>>>(ca);
+    InvArgs ia{g, P->S, P->tw, out, y, xp, alpha, nu, epi, part3, P->cgbuf[5], P->cgbuf[6]};
+    row_inv_kernel<<<rgrid, 256, 0, st>>>(ia);
+  }
   return check_launch("fft stencil");
 }
 
@@ -947,6 +980,16 @@ extern "C" int adp_fft_plan_create(adp_fft_plan** out, int32_t H, int32_t W, int
   g.ntY = (H + g.Vh - 1) / g.Vh; g.ntX = (W + g.Vw - 1) / g.Vw;
   g.ntiles = g.ntY * g.ntX;
   g.npairs = (g.ntiles + 1) / 2;
+  g.pair0 = g.spair0 = 0;
+  g.spairs = g.npairs;
+  {
+    // tile pairs per chunk of the stencil passes (see stencil()); default 0: whole-image passes -- the
+    // chunked, L2-resident order measured slower on B200 (c5 stencil 1.05 ms whole-image, 1.15 / 1.26 /
+    // 1.56 ms at 12 / 6 / 2 pairs per chunk: the passes are issue-latency bound, not HBM bound, and the
+    // extra kernel boundaries cost more than the scratch traffic saves; profiles/r02zf_fft_chunks.txt)
+    const char* ev = getenv("ADP_FFT_PB");
+    P->chunk = ev ? atoi(ev) : 0;
+  }
   P->N = (int64_t)H * W * C;
   // >= 2 pair slots: the spectrum setup transforms the kernel and its flip together
   const size_t sbytes = (size_t)C * std::max(2, g.npairs) * T * T * sizeof(double2);
