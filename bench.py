@@ -504,6 +504,19 @@ def run_native(args):
                       "cg_iters_cum": tr.cg_iters_cum[-1] if len(tr) else 0,
                       "workload": f"c2: 256x256x1, reference 2-D MAID settings, first {args.maid_steps} "
                                   "accepted upper steps, wall clock"}
+        # c3 (the main line's instance): first 2 accepted upper steps of the same 2-D MAID settings
+        cfg3 = configs.maid_config("c3")
+        cfg3.max_upper_iters = min(2, args.maid_steps)
+        up3 = configs.config3(0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        _, _, tr3 = adp.maid_run(up3, cfg3)
+        dt3 = time.perf_counter() - t0
+        maid["c3"] = {"value": len(tr3) / dt3, "accepted": len(tr3), "seconds": dt3,
+                      "lower_iters_cum": tr3.lower_iters_cum[-1] if len(tr3) else 0,
+                      "cg_iters_cum": tr3.cg_iters_cum[-1] if len(tr3) else 0,
+                      "workload": f"c3: 512x512x3, 15x15, reference 2-D MAID settings, first {cfg3.max_upper_iters} "
+                                  "accepted upper steps, wall clock"}
         if not args.no_cpu and ws == 1:
             v, n, d = cpu_maid_c1()
             maid["c1"]["cpu_oracle"] = {"value": v, "accepted": n, "seconds": d, "cores": 1}
