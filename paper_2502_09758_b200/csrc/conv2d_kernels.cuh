@@ -174,6 +174,10 @@ template <typename T, bool FAST, int RW, int KS = 0, int MAXT = 512, bool TMA = 
 __global__ void __launch_bounds__(KS > 0 ? kSolveKSThreads : MAXT, 1) conv_solve_kernel(const __grid_constant__ ConvArgs<T> a) {
   ConvOps<T, FAST, RW, KS, TMA> E(a);
   unsigned tph[2] = {0u, 0u};   // TMA: mbarrier phases
+  if constexpr (TMA) {
+    // the five tile-box descriptors into the descriptor cache before the first box needs them
+    if (threadIdx.x < 5) asm volatile("prefetch.tensormap [%0];" ::"l"(&a.tm[threadIdx.x]) : "memory");
+  }
   const ConvGeom& g = a.g;
   E.load_weights(a.kern);
   const bool tv = (a.alpha != 0.0);
