@@ -1217,8 +1217,7 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
       } else {
         ConvArgs<T> a = sa_args;
         a.in0 = X[ix]; a.in1 = X[ixp]; a.out0 = X[ic]; a.sbeta = beta; a.sL = L_try; a.sflag = 1;
-        StepTail tl = P.tail;
-        if (int e = step_launch(P, P.k_sc, a, st, false, P.step_smem, nT, &P.wfwd, &tl)) return e;
+        if (int e = step_launch(P, P.k_sc, a, st, false, P.step_smem, nT, &P.wfwd)) return e;
         ++launches;
         ++vals;
         if (int e = reduce(2, 3)) return e;

@@ -132,14 +132,13 @@ __device__ __forceinline__ void warp_fold4(const WarpTask (&t)[4], double (&out)
 // Reducer CTA `rid` of a candidate-value launch (see step_tail.h): folds the tile rows
 // [rid * gpr, (rid + 1) * gpr) of the decision sums into sub-values -- the candidate half's leaves
 // and tile partials are polled as they arrive -- takes a ticket, and the last reducer folds the
-// sub-values and publishes the sums to the host.  retry: the candidate's three sums only (the others
-// were delivered by the first candidate's launch and their sub-values are still in place).
+// sub-values and publishes the sums to the host.  (A backtracking retry re-runs the same launch: the
+// three sums at the extrapolation point are folded again, unchanged.)
 // Runs of a group, in this order: polled leaf runs (fitc, tvc, tvc'), plain leaf runs (fit, tv, tv'),
 // polled tile run (t1), plain tile run (t0).
 // (inlined: a real call in the stage kernels costs the hot path its register allocation -- measured)
 template <typename T>
 __device__ __forceinline__ void tail_reduce(double* red, const ConvArgs<T>& a, const StepTail& tl, int rid) {
-  constexpr bool retry = false;   // a retry re-runs the candidate-value launch: all six sums are in place
   __shared__ int s_last;
   const int GL = tl.GL, tW = tl.tW, nG = tl.nG;
   const int koff = (int)(a.g.Ng / a.g.leafL);
@@ -148,7 +147,7 @@ __device__ __forceinline__ void tail_reduce(double* red, const ConvArgs<T>& a, c
   const int g0 = rid * tl.gpr, ng = min(nG, g0 + tl.gpr) - g0;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const int segL = (GL + 31) >> 5, segT = (tW + 31) >> 5;     // 32-unit tasks per leaf / tile run
-  const int nrl = retry ? 3 : 6, nrt = retry ? 1 : 2;          // leaf / tile runs per group
+  constexpr int nrl = 6, nrt = 2;                              // leaf / tile runs per group
   double* partL = red;                                         // [ng][nrl][segL]
   double* partT = red + (size_t)tl.gpr * 6 * segL;             // [ng][nrt][segT]
   auto leaf_run = [&](int gi, int k) -> double* {
@@ -325,48 +324,20 @@ __global__ void __launch_bounds__(384, 2) step_b_kernel(const __grid_constant__ 
   E.tile_partial(a.s_t0, tile, part);
 }
 
-// the next extrapolation point of a backtracking retry: y'' = x_c + betaN (x_c - x) with
-// x_c = (x + beta (x - x_prev)) - g / L   (step_b_kernel's expressions for out0 / out1)
-template <typename T> struct SrcCandExtrap {
-  const T* x; const T* xp; const T* g; T beta; T L; T betaN;
-  __device__ T operator()(int64_t i) const {
-    const T a = ldcg(x + i), b = ldcg(xp + i);
-    const T xc = (a + beta * (a - b)) - ldcg(g + i) / L;
-    return xc + betaN * (xc - a);
-  }
-};
-
-// Backtracking retry (lower_solvers.py:170-177): CTAs [0, nTiles): the value at x_c = y - g / L with
-// y = in0 + beta (in0 - in1) (lower_value form, x_c -> out0) + the restart-dot partial g.(x_c - in0);
-// with the in-kernel decision sums (step_tail.h) the grid continues with tl.nR reducer CTAs and nTiles
-// CTAs of the speculative stage A at the retry's next extrapolation point (sums set: sflag & 2), so an
-// accepted retry needs no separate stage-A launch.
+// Backtracking retry without the in-kernel decision sums (ADP_TAIL=0 or a geometry the reducers do not
+// cover; lower_solvers.py:170-177): the value at x_c = y - g / L with y = in0 + beta (in0 - in1)
+// (lower_value form, x_c -> out0) + the restart-dot partial g.(x_c - in0); step_reduce_kernel follows.
+// (With the in-kernel sums a retry is step_cand_kernel + the regular step_ca_kernel launch.)
 template <typename T, bool FAST, int KD, int KU, class WT>
 __global__ void __launch_bounds__(384, 2) step_c_kernel(const __grid_constant__ ConvArgs<T> a,
-                                                            const __grid_constant__ WT wt,
-                                                            const __grid_constant__ StepTail tl) {
+                                                            const __grid_constant__ WT wt) {
   Conv<T, FAST, 4, 0, false, true, KD, KU> E(a);   // wt: forward taps
   E.opsm = true;
   E.pw = wt.w;
   const bool tv = a.alpha != 0.0;
-  const int nT = a.g.nTiles, nR = tl.on ? tl.nR : 0;
-  const int b = (int)blockIdx.x;
-  const bool isC = b < nT, isR = !isC && b < nT + nR;
-  const int tile = isC ? b : b - nT - nR;
-  E.tb0 = tile;       // the stage loops run this one tile
-  E.tbs = nT;
   pdl_sync();
-  if (isR) {
-    tail_reduce(E.tm(), a, tl, b - nT);
-  } else if (isC) {
-    E.stageC(SrcCand<T>{a.in0, a.in1, a.G, T(a.sbeta), T(a.sL)}, a.RC, tv, a.TV2C, a.out0, a.G, a.in0, &a.s_t1,
-             &a.s_fitc, &a.s_tvc);
-  } else {
-    const SumDev* sf = (a.sflag & 2) ? &a.s_fit2 : &a.s_fit;
-    const SumDev* st = (a.sflag & 2) ? &a.s_tv2 : &a.s_tv;
-    E.stageA(SrcCandExtrap<T>{a.in0, a.in1, a.G, T(a.sbeta), T(a.sL), T(a.sbetaN)}, a.R, a.ydat, tv, a.TV2, a.TVG,
-             sf, st);
-  }
+  E.stageC(SrcCand<T>{a.in0, a.in1, a.G, T(a.sbeta), T(a.sL)}, a.RC, tv, a.TV2C, a.out0, a.G, a.in0, &a.s_t1,
+           &a.s_fitc, &a.s_tvc);
 }
 
 template <typename T, bool FAST, int KD, int KU, class WT>
