@@ -603,10 +603,15 @@ static int conv_plan_init(PlanImpl& P) {
             (int64_t)P.s_tv.nLeaves == 2 * GL * g.tilesH && g.threads >= 64) {
           const size_t nsub = (size_t)11 * g.tilesH * sizeof(double);
           const size_t ncnt = 64;
-          CK(cudaMalloc(&P.d_tail, nsub + ncnt));
-          CK(cudaMemset(P.d_tail, 0, nsub + ncnt));
+          const size_t nflag = (size_t)g.nTiles * sizeof(unsigned int);
+          CK(cudaMalloc(&P.d_tail, nsub + ncnt + nflag));
+          CK(cudaMemset(P.d_tail, 0, nsub + ncnt + nflag));
           P.tail.sub = (double*)P.d_tail;
           P.tail.cnt = (unsigned int*)((char*)P.d_tail + nsub);
+          // the candidate launch overlaps the stage-B launch's last wave (per-tile completion flags,
+          // conv2d_step.cu); needs programmatic dependent launch; ADP_OVL=0: off
+          const char* eo = getenv("ADP_OVL");
+          if (P.pdl && !(eo && atoi(eo) == 0)) P.d_tflag = (unsigned int*)((char*)P.d_tail + nsub + ncnt);
           P.tail.on = 1;
           P.tail.nG = g.tilesH;
           P.tail.GL = (int)GL;
@@ -1117,6 +1122,7 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
       ConvArgs<T> a = sa_args;
       a.in0 = X[ix]; a.in1 = X[ixp]; a.out0 = X[ic]; a.out1 = Yn;
       a.sbeta = beta; a.sL = L_try; a.sbetaN = beta2;
+      a.tflag = P.d_tflag; a.tseq = ++P.tile_seq;
       if (int e = step_launch(P, P.k_sb, a, st, false, P.step_smem_b, nT, &P.wadj)) return e;
       ++launches;
     }
@@ -1134,9 +1140,12 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
           (void)cudaGetLastError();   // not ready yet: keep the events for a later iteration
         }
       }
-      prof_now = P.profile && (t % P.profile == 0) && !prof_pending;   // sampled: every P.profile-th iteration
       StepTail tl = P.tail;
       tl.setR = par;   // (the speculative stage A writes the other (fit, tv) set)
+      // overlap with the stage-B launch just queued (not for the sampled, event-bracketed launch)
+      prof_now = P.profile && (t % P.profile == 0) && !prof_pending;   // sampled: every P.profile-th iteration
+      tl.ovl = tl.on && P.d_tflag && !prof_now;
+      a.tflag = P.d_tflag; a.tseq = P.tile_seq;
       if (tl.on) {   // reducer CTAs publish the six sums (step_tail.h)
         a.hscal = d_hscal;
         a.hflag = d_hflag;

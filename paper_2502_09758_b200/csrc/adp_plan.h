@@ -83,7 +83,9 @@ struct PlanImpl {
                                 // instances for stencils of <= kStepWSmall taps read the first part only)
   bool pdl = true;              // stage kernels launched with programmatic stream serialization (ADP_PDL=0: off)
   StepTail tail{};              // in-kernel decision sums of the host-stepped solve (tail.on: geometry allows it)
-  void* d_tail = nullptr;       // sub-values + tickets
+  void* d_tail = nullptr;       // sub-values + tickets + per-tile stage-B completion flags
+  unsigned int* d_tflag = nullptr;   // the flags (NULL: the candidate launch does not overlap stage B)
+  unsigned int tile_seq = 0;    // sequence number of the last stage-B launch
   CUtensorMap tm[5];            // X[0..2], R, P[0]
   // pinned host staging
   SolveOut* h_sres = nullptr;

@@ -85,6 +85,8 @@ struct ConvArgs {
   volatile int* hflag;     //   then the sequence number `hseq` to hflag (the host spins on it)
   int hseq;
   int sflag;               // row-slab CG steps: variant (see CM_SLAB_CG_*)
+  unsigned int* tflag;     // host-stepped solve: per-tile completion flags of the stage-B launch (value tseq),
+  unsigned int tseq;       //   polled by the overlapping candidate launch (conv2d_step.cu); NULL: off
   unsigned long long* trace;  // optional phase timestamps (CTA 0): [iter][16] %globaltimer ns
   const T* in0; const T* in1; T* out0; T* out1;
   // TMA descriptors of the plan's workspace images (KS = 9 single-channel

@@ -23,6 +23,38 @@ __device__ __forceinline__ void pdl_sync() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
 }
 
+// Overlap of the candidate launch with the stage-B launch before it.  Stage B's CTAs signal
+// launch_dependents at their start, so the candidate launch's first CTAs become resident while stage
+// B's last wave (512 tiles on 296 CTA slots at c3: a quarter of the slots idle) still runs.  Instead
+// of waiting for the whole stage-B grid (griddepcontrol.wait) they wait for the stage-B tiles they
+// read: every stage-B CTA publishes its tile's sequence number with a release store after its last
+// global write, a candidate / stage-A CTA acquires the flags of its tile's 3 x 3 neighbourhood (the
+// halo of the box it loads -- also every stage-B tile that reads the R tile a stage-A CTA overwrites),
+// a reducer the flags of its tile rows (the g.g tile partials).  Dependents are only scheduled once
+// every stage-B CTA has started, so a waiting CTA never holds a slot a stage-B CTA needs.
+__device__ __forceinline__ void tile_done(unsigned int* flag, int tile, unsigned int seq) {
+  __syncthreads();   // the CTA's global writes before thread 0's release (cumulative)
+  if (threadIdx.x == 0) asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag + tile), "r"(seq) : "memory");
+}
+__device__ __forceinline__ void tile_wait_one(const unsigned int* flag, int tile, unsigned int seq) {
+  unsigned int v;
+  for (unsigned spins = 0;; ++spins) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(flag + tile) : "memory");
+    if ((int)(v - seq) >= 0 || spins > (1u << 24)) break;   // (gives up after seconds: cannot happen for a launched grid)
+    __nanosleep(64);
+  }
+}
+// threads 0..8: the 3 x 3 tile neighbourhood of `tile`; the barrier orders every later load of the CTA
+__device__ __forceinline__ void tile_wait_3x3(const unsigned int* flag, unsigned int seq, int tile, int tilesW,
+                                              int tilesH, int trow) {
+  if (threadIdx.x < 9) {
+    const int dr = (int)threadIdx.x / 3 - 1, dc = (int)threadIdx.x % 3 - 1;
+    const int r = trow + dr, c = tile - trow * tilesW + dc;
+    if (r >= 0 && r < tilesH && c >= 0 && c < tilesW) tile_wait_one(flag, r * tilesW + c, seq);
+  }
+  __syncthreads();
+}
+
 // polls before a reducer gives up on a unit (>= 64 ns each: about two seconds)
 constexpr unsigned kPollMax = 1u << 25;
 
@@ -322,6 +354,7 @@ __global__ void __launch_bounds__(384, 2) step_b_kernel(const __grid_constant__ 
     }
   }
   E.tile_partial(a.s_t0, tile, part);
+  if (a.tflag) tile_done(a.tflag, tile, a.tseq);
 }
 
 // Backtracking retry without the in-kernel decision sums (ADP_TAIL=0 or a geometry the reducers do not
@@ -378,15 +411,28 @@ __global__ void __launch_bounds__(384, 2) step_ca_kernel(const __grid_constant__
   const int nT = a.g.nTiles, nR = tl.on ? tl.nR : 0;
   const int b = (int)blockIdx.x;
   const bool isC = b < nT;
+  const bool ovl = tl.ovl && a.tflag;
   if (!isC && b < nT + nR) {   // reducer CTAs sit between the two halves (step_tail.h)
-    pdl_sync();
+    if (ovl) {
+      asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+      const int rid = b - nT, t0 = rid * tl.gpr * tl.tW, t1 = min(nT, t0 + tl.gpr * tl.tW);
+      for (int t = t0 + (int)threadIdx.x; t < t1; t += blockDim.x) tile_wait_one(a.tflag, t, a.tseq);
+      __syncthreads();
+    } else {
+      pdl_sync();
+    }
     tail_reduce(E.tm(), a, tl, b - nT);
     return;
   }
   const int tile = isC ? b : b - nT - nR;
   int h0, w0;
   E.tile_origin(tile, h0, w0);
-  pdl_sync();
+  if (ovl) {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    tile_wait_3x3(a.tflag, a.tseq, tile, a.g.tilesW, a.g.tilesH, E.tile_row(tile));
+  } else {
+    pdl_sync();
+  }
   if (isC) {
     const T* const ops[3] = {a.ydat, a.G, a.in1};
     E.template stage_own_n<3>(h0, w0, ops, 0);

@@ -28,6 +28,8 @@ struct StepTail {
   int nR;               // reducer CTAs of a launch
   int gpr;              // groups per reducer
   int setR;             // (fit, tv) set the decision of this launch reads: 0 / 1
+  int ovl;              // 1: this launch overlaps the stage-B launch before it: no grid dependency wait, every
+                        //    CTA waits for the stage-B tiles it reads (ConvArgs::tflag / tseq) instead
   // sub-value offsets (doubles)
   __host__ __device__ int o_fit() const { return 0; }
   __host__ __device__ int o_tv() const { return 2 * nG; }
