@@ -603,7 +603,7 @@ static int conv_plan_init(PlanImpl& P) {
             (int64_t)P.s_tv.nLeaves == 2 * GL * g.tilesH && g.threads >= 64) {
           const size_t nsub = (size_t)11 * g.tilesH * sizeof(double);
           const size_t ncnt = 64;
-          const size_t nflag = (size_t)g.nTiles * sizeof(unsigned int);
+          const size_t nflag = (size_t)2 * g.nTiles * sizeof(unsigned int);   // stage-B tiles, stage-A tiles
           CK(cudaMalloc(&P.d_tail, nsub + ncnt + nflag));
           CK(cudaMemset(P.d_tail, 0, nsub + ncnt + nflag));
           P.tail.sub = (double*)P.d_tail;
@@ -612,6 +612,9 @@ static int conv_plan_init(PlanImpl& P) {
           // conv2d_step.cu); needs programmatic dependent launch; ADP_OVL=0: off
           const char* eo = getenv("ADP_OVL");
           if (P.pdl && !(eo && atoi(eo) == 0)) P.d_tflag = (unsigned int*)((char*)P.d_tail + nsub + ncnt);
+          // ADP_OVL=2: stage B also overlaps the candidate launch's last wave (stage-A tile flags); measured
+          // and left off: the stage-A CTAs' release costs what the overlap gains (117.9 vs 117.8 us at c3)
+          P.ovl_b = eo && atoi(eo) == 2;
           P.tail.on = 1;
           P.tail.nG = g.tilesH;
           P.tail.GL = (int)GL;
@@ -1068,6 +1071,7 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
   double gn = 0.0, h_y = 0.0, beta = 0.0;
   long long vg = 0, vals = 0, restarts = 0;
   bool done = false, a_ready = false;
+  unsigned int last_aseq = 0;   // != 0: the last launch queued is a candidate launch publishing its stage-A tiles
   int par = 0;
   const int nT = g.nTiles;
   if (P.profile && !P.prof_ev[0]) {
@@ -1113,6 +1117,7 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
     if (!a_ready) {   // stage A at y = x + beta (x - x_prev), sums set `par`
       ConvArgs<T> a = sa_args;
       a.in0 = X[ix]; a.in1 = X[ixp]; a.sbeta = beta; a.sflag = 1 | (par ? 2 : 0);
+      last_aseq = 0;
       if (int e = step_launch(P, P.k_sa, a, st, false, P.step_smem, nT, &P.wfwd)) return e;
       ++launches;
     }
@@ -1123,6 +1128,9 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
       a.in0 = X[ix]; a.in1 = X[ixp]; a.out0 = X[ic]; a.out1 = Yn;
       a.sbeta = beta; a.sL = L_try; a.sbetaN = beta2;
       a.tflag = P.d_tflag; a.tseq = ++P.tile_seq;
+      // directly after a candidate launch whose speculative stage A is this launch's input: overlap it
+      if (P.d_tflag && a_ready && last_aseq) { a.sflag = 1; a.hseq = (int)last_aseq; }
+      last_aseq = 0;
       if (int e = step_launch(P, P.k_sb, a, st, false, P.step_smem_b, nT, &P.wadj)) return e;
       ++launches;
     }
@@ -1146,6 +1154,7 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
       prof_now = P.profile && (t % P.profile == 0) && !prof_pending;   // sampled: every P.profile-th iteration
       tl.ovl = tl.on && P.d_tflag && !prof_now;
       a.tflag = P.d_tflag; a.tseq = P.tile_seq;
+      if (tl.on && P.d_tflag && P.ovl_b && !prof_now) last_aseq = tl.aseq = ++P.a_seq ? P.a_seq : ++P.a_seq;
       if (tl.on) {   // reducer CTAs publish the six sums (step_tail.h)
         a.hscal = d_hscal;
         a.hflag = d_hflag;
@@ -1215,6 +1224,8 @@ static int conv_solve_step(PlanImpl& P, const adp_lower* lp, const void* x0, voi
         a.in0 = X[ic]; a.in1 = X[ix]; a.out1 = Yn; a.sflag = par ? 0 : 2;
         StepTail tl = P.tail;
         tl.setR = par;
+        a.tflag = P.d_tflag;
+        if (P.d_tflag && P.ovl_b) last_aseq = tl.aseq = ++P.a_seq ? P.a_seq : ++P.a_seq;
         a.hscal = d_hscal;
         a.hflag = d_hflag;
         a.hseq = ++P.step_seq;

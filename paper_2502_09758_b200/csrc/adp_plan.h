@@ -86,6 +86,8 @@ struct PlanImpl {
   void* d_tail = nullptr;       // sub-values + tickets + per-tile stage-B completion flags
   unsigned int* d_tflag = nullptr;   // the flags (NULL: the candidate launch does not overlap stage B)
   unsigned int tile_seq = 0;    // sequence number of the last stage-B launch
+  unsigned int a_seq = 0;       // ... of the last candidate launch publishing its stage-A tiles
+  bool ovl_b = false;           // stage B overlaps the candidate launch's last wave too (ADP_OVL=2)
   CUtensorMap tm[5];            // X[0..2], R, P[0]
   // pinned host staging
   SolveOut* h_sres = nullptr;

@@ -317,7 +317,15 @@ __global__ void __launch_bounds__(384, 2) step_b_kernel(const __grid_constant__ 
   const int tile = blockIdx.x;
   int h0, w0;
   E.tile_origin(tile, h0, w0);
-  pdl_sync();
+  if (a.tflag && (a.sflag & 1)) {
+    // this launch follows a candidate launch whose speculative stage A is its input: overlap that
+    // launch's last wave (one CTA slot per SM idle at c3), waiting for the stage-A tiles whose R this
+    // tile's box reads -- the same tiles read the y' tile this CTA overwrites -- instead of the grid
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    tile_wait_3x3(a.tflag + a.g.nTiles, (unsigned)a.hseq, tile, a.g.tilesW, a.g.tilesH, E.tile_row(tile));
+  } else {
+    pdl_sync();
+  }
   if (tv) {
     const T* const ops[3] = {a.TVG, a.in0, a.in1};
     E.template stage_own_n<3>(h0, w0, ops, 0);
@@ -456,6 +464,7 @@ __global__ void __launch_bounds__(384, 2) step_ca_kernel(const __grid_constant__
     const SumDev* st = (a.sflag & 2) ? &a.s_tv2 : &a.s_tv;
     E.tileA(E.pa(), E.pa(), 0, h0, w0, z, a.R, tv, a.TV2, a.TVG, true, acc);
     E.tile_leaves(h0, w0, tv ? 3 : 1, sf, st, koff);
+    if (a.tflag && tl.aseq) tile_done(a.tflag + nT, tile, tl.aseq);
   }
 }
 

@@ -30,6 +30,8 @@ struct StepTail {
   int setR;             // (fit, tv) set the decision of this launch reads: 0 / 1
   int ovl;              // 1: this launch overlaps the stage-B launch before it: no grid dependency wait, every
                         //    CTA waits for the stage-B tiles it reads (ConvArgs::tflag / tseq) instead
+  unsigned int aseq;    // != 0: the stage-A half publishes its tiles' completion (flags tflag + nTiles, this
+                        //    value) for a stage-B launch that overlaps this launch's last wave
   // sub-value offsets (doubles)
   __host__ __device__ int o_fit() const { return 0; }
   __host__ __device__ int o_tv() const { return 2 * nG; }
