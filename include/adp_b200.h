@@ -315,7 +315,10 @@ int adp_slab_mixed(adp_plan* p, const adp_lower* lp, const void* x_tilde, const 
 int adp_kgc_groups(adp_plan* p, int32_t* ngroups, int32_t* ntaps);
 /* plan execution flags: bit 0 = TMA tile boxes in the solve kernel (c2), bit 1 = host-stepped
  * high-occupancy solve_lower (c3-c5: stage kernels one tile per CTA, scalar control on the host),
- * bit 2 = its decision sums folded inside the stage kernels (no reduction launch; csrc/step_tail.h) */
+ * bit 2 = its decision sums folded inside the stage kernels (no reduction launch; csrc/step_tail.h),
+ * bit 3 = its candidate launch overlaps the stage-B launch's last wave (per-tile completion flags
+ * instead of the grid dependency; ADP_OVL=0: off), bit 4 = stage B overlaps the candidate launch's
+ * last wave as well (ADP_OVL=2; measured, off by default) */
 int adp_plan_flags(adp_plan* p, int32_t* flags);
 /* enable (period k >= 1) / disable (0) live timing of the dominant kernel of host-stepped solves:
  * every k-th iteration's launch is bracketed by CUDA events on its stream (result fields dominant_ms /

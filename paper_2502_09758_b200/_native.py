@@ -262,10 +262,13 @@ class Plan:
         return dict(zip(GEOMETRY_KEYS, (int(v) for v in out)))
 
     def flags(self) -> dict:
-        """Execution choices of the plan: TMA tile boxes, host-stepped solve, in-kernel decision sums."""
+        """Execution choices of the plan: TMA tile boxes, host-stepped solve, in-kernel decision sums,
+        candidate launch overlapping stage B's last wave (tile flags), stage B overlapping the candidate
+        launch's (opt-in)."""
         f = ctypes.c_int32()
         check(lib().adp_plan_flags(self.handle, ctypes.byref(f)), "adp_plan_flags")
-        return {"tma": bool(f.value & 1), "step": bool(f.value & 2), "tail": bool(f.value & 4)}
+        return {"tma": bool(f.value & 1), "step": bool(f.value & 2), "tail": bool(f.value & 4),
+                "ovl": bool(f.value & 8), "ovl_b": bool(f.value & 16)}
 
 
 _plans: dict = {}

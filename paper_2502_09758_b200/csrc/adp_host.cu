@@ -1714,7 +1714,8 @@ extern "C" int adp_slab_mixed(adp_plan* p, const adp_lower* lp, const void* x_ti
 // high-occupancy solve (conv2d_step.cu)
 extern "C" int adp_plan_flags(adp_plan* p, int32_t* flags) {
   if (!p || !flags) return fail(ADP_ERR_ARG, "null argument");
-  *flags = (p->impl.tma ? 1 : 0) | (p->impl.step ? 2 : 0) | (p->impl.step && p->impl.tail.on ? 4 : 0);
+  *flags = (p->impl.tma ? 1 : 0) | (p->impl.step ? 2 : 0) | (p->impl.step && p->impl.tail.on ? 4 : 0) |
+           (p->impl.step && p->impl.d_tflag ? 8 : 0) | (p->impl.step && p->impl.d_tflag && p->impl.ovl_b ? 16 : 0);
   return ADP_OK;
 }
 

@@ -60,10 +60,12 @@ def test_step_tail_equals_reduce_kernel(adp):
     assert np.array_equal(r1.x_tilde, r0.x_tilde)
 
 
-@pytest.mark.parametrize("env", [{"ADP_SU": "0"}, {"ADP_SU": "15"}, {"ADP_PDL": "0"}])
+@pytest.mark.parametrize("env", [{"ADP_SU": "0"}, {"ADP_SU": "15"}, {"ADP_PDL": "0"}, {"ADP_OVL": "0"},
+                                 {"ADP_OVL": "2"}])
 def test_step_kernel_variants_bitwise(adp, env):
     """The stage-kernel variants -- generic multi-stencil instances, straight-line 15 x 15 taps, launches
-    without programmatic stream serialization -- give the default path's iterates bit for bit."""
+    without programmatic stream serialization, without / with more of the tile-flag overlap between the
+    stage-B and candidate launches -- give the default path's iterates bit for bit."""
     from paper_2502_09758_b200 import _native as nat
     from paper_2502_09758_b200 import configs
     up = configs.CONFIGS["c3"](1, size=256)
@@ -75,7 +77,9 @@ def test_step_kernel_variants_bitwise(adp, env):
     finally:
         for k in env:
             os.environ.pop(k, None)
-    assert f0["step"] and f1["step"] and f1["tail"]
+    assert f0["step"] and f1["step"] and f1["tail"] and f0["ovl"]
+    if "ADP_OVL" in env:
+        assert f1["ovl"] == (env["ADP_OVL"] != "0") and f1["ovl_b"] == (env["ADP_OVL"] == "2")
     assert n1 == n0 and r1.iters == r0.iters and r1.grad_norm == r0.grad_norm
     assert {k: s1[k] for k in ("vg_evals", "value_evals", "restarts", "lip")} == \
         {k: s0[k] for k in ("vg_evals", "value_evals", "restarts", "lip")}
