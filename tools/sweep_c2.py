@@ -26,6 +26,8 @@ key = (nat.LAYOUT_DEPTHWISE2D, tuple(up.x0.shape), (9, 9))
 tiles = [(0, 0), (2, 128), (4, 128), (8, 128), (1, 256), (2, 256), (4, 256), (1, 128)]
 if os.environ.get("ADP_RW") == "1":
     tiles = [(2, 128), (4, 128), (1, 256), (2, 256), (1, 128)]
+if os.environ.get("ADP_RW") == "4":   # host-stepped stage kernels on c2 (with ADP_STEP=1)
+    tiles = [(0, 0), (4, 128), (8, 64), (8, 128), (16, 64), (4, 64), (2, 128), (16, 32)]
 for tile in tiles:
     nat.set_tile(key, tile)
     nat.clear_plans()
@@ -43,6 +45,6 @@ for tile in tiles:
             e1.record()
             torch.cuda.synchronize()
             ts.append(e0.elapsed_time(e1) * 1e3 / r.iters)
-        print(f"tile {tile} geo {geo}: {min(ts):.2f} us/iter")
+        print(f"tile {tile} geo {geo} flags {p.op.plan().flags()}: {min(ts):.2f} us/iter", flush=True)
     except Exception as ex:  # noqa: BLE001
         print(f"tile {tile}: {ex}")
