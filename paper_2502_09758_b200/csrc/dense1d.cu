@@ -8,7 +8,14 @@
 // shared memory and updated redundantly and identically, so the only data
 // exchanged per GEMV is the row results (B v) or the per-CTA column
 // partials (B^T u), each followed by one grid barrier.
+// Grids of <= 16 CTAs whose state fits (c1: n = 256, 16 CTAs) run as ONE
+// thread-block cluster: every CTA stores its row results / column partials
+// straight into all CTAs' shared memory (distributed shared memory) and the
+// exchange ends with a cluster barrier -- no global round trip, no grid
+// barrier; same arithmetic in the same order (bitwise equal to the grid path,
+// tests/test_gpu_dense_cluster.py).
 #include <cuda_runtime.h>
+#include <cooperative_groups.h>
 #include <algorithm>
 #include <cstring>
 #include <string>
@@ -17,6 +24,7 @@
 #include "dense1d_args.h"
 
 namespace adp {
+namespace cg = cooperative_groups;
 
 enum DenseMode : int {
   DM_APPLY = 0, DM_ADJOINT, DM_GRAM, DM_VALUE, DM_VG, DM_GRAD, DM_HV, DM_HDIAG, DM_UPPER, DM_POWER, DM_MIXED,
@@ -24,6 +32,39 @@ enum DenseMode : int {
 };
 
 constexpr int kDenseVecs = 12;
+
+// np_leaf_warp (adp_device.cuh: NumPy's pairwise leaf, n <= 128) with the terms evaluated by all 32
+// lanes at once -- lane (k, g) computes rows g, g + 4, g + 8, g + 12 of accumulator k -- and only the
+// ordered additions r[k] += a[8 m + k] left as a serial chain fed by shuffles.  The dense engine's sums
+// are latency chains of a few hundred elements whose terms hold square roots: evaluating them inside
+// the 8-lane chain cost 1.8 us per sum.  Same additions in the same order: bitwise equal.
+template <class Src>
+__device__ __forceinline__ double np_leaf_warp32(const Src& src, int64_t s, int n) {
+  const int lane = threadIdx.x & 31;
+  if (n < 8 || n > 128) return np_leaf_warp(src, s, n);
+  const int nfull = n - (n % 8), M = nfull >> 3;   // rows of 8 terms
+  const int k = lane & 7, g = lane >> 3;
+  double v[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int m = g + 4 * j;
+    v[j] = m < M ? src(s + 8 * m + k) : 0.0;
+  }
+  double acc = 0.0;
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const double x = __shfl_sync(kFull, v[m >> 2], k + 8 * (m & 3));   // row m of accumulator k
+    if (m == 0) acc = x;
+    else if (m < M) acc = acc + x;
+  }
+  double t = acc + __shfl_down_sync(kFull, acc, 1);
+  t = t + __shfl_down_sync(kFull, t, 2);
+  t = t + __shfl_down_sync(kFull, t, 4);
+  if (lane == 0) {
+    for (int i = nfull; i < n; ++i) t = t + src(s + i);
+  }
+  return t;
+}
 
 template <typename T>
 struct Dense {
@@ -34,7 +75,13 @@ struct Dense {
   T* v[kDenseVecs];
   double* sv;
   double* red;
+  int64_t* lstart;  // smem copy of s_n.leaf_start
+  int* sprog;       // smem copy of s_n's tree program
   int rb;           // rowbuf ping-pong index
+  bool cl;          // single-cluster launch: exchanges through distributed shared memory
+  T* rowv[2];       // cluster: this CTA's copy of the gathered row results (ping-pong)
+  double* partv[2]; // cluster: [G][n] column partials of all CTAs (ping-pong)
+  int pb;
 
   __device__ Dense(const DenseArgs<T>& a_, unsigned char* smem) : a(a_) {
     gb.counter = a.bar;
@@ -48,6 +95,14 @@ struct Dense {
     off += 64 * sizeof(double);
     sv = reinterpret_cast<double*>(smem + off);
     off += (size_t)(2 * a.s_n.nLeaves + 2) * sizeof(double);
+    // the sum's leaf starts and tree program, read on every npsum: cached in shared memory (each sum
+    // was a chain of four dependent global loads before)
+    lstart = reinterpret_cast<int64_t*>(smem + off);
+    off += (size_t)(a.s_n.nLeaves + 1) * sizeof(int64_t);
+    sprog = reinterpret_cast<int*>(smem + off);
+    off += (size_t)a.plen * sizeof(int);
+    for (int k = threadIdx.x; k <= a.s_n.nLeaves; k += blockDim.x) lstart[k] = a.s_n.leaf_start[k];
+    for (int k = threadIdx.x; k < a.plen; k += blockDim.x) sprog[k] = a.s_n.progs[a.s_n.top_prog + k];
     off = (off + 15) & ~size_t(15);
     for (int k = 0; k < kDenseVecs; ++k) {
       if (a.gvec) {   // large n: this CTA's private copies in global memory (L1/L2-resident)
@@ -65,7 +120,28 @@ struct Dense {
       Bs = a.B + (int64_t)r0 * n;
     }
     rb = 0;
+    cl = a.cluster != 0;
+    pb = 0;
+    if (cl) {
+      if (a.b_smem) off += (size_t)a.rows_per * n * sizeof(T);
+      off = (off + 15) & ~size_t(15);
+      for (int k = 0; k < 2; ++k) {
+        rowv[k] = reinterpret_cast<T*>(smem + off);
+        off += ((size_t)n * sizeof(T) + 15) & ~size_t(15);
+      }
+      for (int k = 0; k < 2; ++k) {
+        partv[k] = reinterpret_cast<double*>(smem + off);
+        off += (size_t)gridDim.x * n * sizeof(double);
+      }
+      cg::this_cluster().sync();   // every CTA of the cluster runs before anyone writes into its shared memory
+    }
     __syncthreads();
+  }
+
+  // the barrier that ends an exchange (after gemv_rows / gemvT_partial / gram_partial)
+  __device__ __forceinline__ void xsync() {
+    if (cl) cg::this_cluster().sync();   // arrive.release + wait.acquire: the remote shared-memory stores are visible
+    else gb.sync();
   }
 
   __device__ __forceinline__ T* rowbuf() { return a.rowbuf + (size_t)rb * n; }
@@ -73,50 +149,79 @@ struct Dense {
   // own rows of (B u) (- sub) -> rowbuf[rb]; warp per row, fixed lane order
   __device__ void gemv_rows(const T* u, const T* sub) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    T* out = rowbuf();
+    T* out = cl ? rowv[rb] : rowbuf();
+    cg::cluster_group cluster = cg::this_cluster();
     for (int i = r0 + warp; i < r1; i += nw) {
       const T* row = Bs + (int64_t)(i - r0) * n;
       T acc = T(0);
       for (int k = lane; k < n; k += 32) acc = acc + row[k] * u[k];
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) acc = acc + __shfl_xor_sync(kFull, acc, o);
-      if (lane == 0) out[i] = sub ? acc - sub[i] : acc;
+      const T val = sub ? acc - sub[i] : acc;   // (every lane holds the sum)
+      if (cl) {
+        if (lane < (int)gridDim.x) cluster.map_shared_rank(out, lane)[i] = val;   // lane c -> CTA c's copy
+      } else if (lane == 0) {
+        out[i] = val;
+      }
     }
   }
   // after a barrier: dst = full rowbuf; flip the ping-pong buffer
   __device__ void gather_rows(T* dst) {
-    const T* src = rowbuf();
-    for (int k = threadIdx.x; k < n; k += blockDim.x) dst[k] = ldcg(src + k);
+    if (cl) {
+      const T* src = rowv[rb];
+      for (int k = threadIdx.x; k < n; k += blockDim.x) dst[k] = src[k];
+    } else {
+      const T* src = rowbuf();
+      for (int k = threadIdx.x; k < n; k += blockDim.x) dst[k] = ldcg(src + k);
+    }
     rb ^= 1;
     __syncthreads();
   }
+  // this CTA's column partial j -> part[cta][j] (global), or into every CTA's partv (cluster)
+  __device__ __forceinline__ void put_part(int j, double v) {
+    if (cl) {
+      cg::cluster_group cluster = cg::this_cluster();
+      double* mine = partv[pb] + (size_t)blockIdx.x * n + j;
+      for (int c = 0; c < (int)gridDim.x; ++c) *cluster.map_shared_rank(mine, c) = v;
+    } else {
+      a.part[(size_t)blockIdx.x * n + j] = v;
+    }
+  }
   // part[cta][j] = sum_{i in own rows} B[i][j] * u[i]
   __device__ void gemvT_partial(const T* u) {
-    double* p = a.part + (size_t)blockIdx.x * n;
     for (int j = threadIdx.x; j < n; j += blockDim.x) {
       T acc = T(0);
       for (int i = r0; i < r1; ++i) acc = acc + Bs[(int64_t)(i - r0) * n + j] * u[i];
-      p[j] = (double)acc;
+      put_part(j, (double)acc);
     }
   }
   // column sums of squares over own rows (gram_diag partial)
   __device__ void gram_partial() {
-    double* p = a.part + (size_t)blockIdx.x * n;
     for (int j = threadIdx.x; j < n; j += blockDim.x) {
       T acc = T(0);
       for (int i = r0; i < r1; ++i) {
         const T b = Bs[(int64_t)(i - r0) * n + j];
         acc = acc + b * b;
       }
-      p[j] = (double)acc;
+      put_part(j, (double)acc);
     }
   }
   // after a barrier: dst[j] = scale * sum_c part[c][j]  (fixed CTA order)
   __device__ void gemvT_finish(T* dst, T scale) {
-    for (int j = threadIdx.x; j < n; j += blockDim.x) {
-      T s = T(0);
-      for (int c = 0; c < gridDim.x; ++c) s = s + T(ldcg(a.part + (size_t)c * n + j));
-      dst[j] = scale * s;
+    if (cl) {
+      const double* p = partv[pb];
+      for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        T s = T(0);
+        for (int c = 0; c < gridDim.x; ++c) s = s + T(p[(size_t)c * n + j]);
+        dst[j] = scale * s;
+      }
+      pb ^= 1;
+    } else {
+      for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        T s = T(0);
+        for (int c = 0; c < gridDim.x; ++c) s = s + T(ldcg(a.part + (size_t)c * n + j));
+        dst[j] = scale * s;
+      }
     }
     __syncthreads();
   }
@@ -127,13 +232,13 @@ struct Dense {
     const SumDev& s = a.s_n;
     const int wpb = blockDim.x >> 5;
     for (int l = threadIdx.x >> 5; l < s.nLeaves; l += wpb) {
-      const int64_t st = s.leaf_start[l];
-      const int len = (int)(s.leaf_start[l + 1] - st);
-      const double r = np_leaf_warp(f, st, len);
+      const int64_t st = lstart[l];
+      const int len = (int)(lstart[l + 1] - st);
+      const double r = np_leaf_warp32(f, st, len);
       if ((threadIdx.x & 31) == 0) sv[l] = r;
     }
     __syncthreads();
-    return eval_prog(s.progs + s.top_prog, sv);
+    return eval_prog(sprog, sv);
   }
   // ddot-type sum (fixed thread-strided order then block tree)
   template <class F>
@@ -181,13 +286,13 @@ struct Dense {
       }
     } else {
       gemv_rows(x, a.ydat);
-      gb.sync();
+      xsync();
       T* r = v[4];
       gather_rows(r);
       val = npsum([&](int64_t k) { const T t = r[k]; return (double)(t * t); });
       if (gout) {
         gemvT_partial(r);
-        gb.sync();
+        xsync();
         gemvT_finish(gout, T(2));
       }
     }
@@ -206,11 +311,11 @@ struct Dense {
       __syncthreads();
     } else {
       gemv_rows(u, nullptr);
-      gb.sync();
+      xsync();
       T* bu = v[4];
       gather_rows(bu);
       gemvT_partial(bu);
-      gb.sync();
+      xsync();
       gemvT_finish(out, T(2));
     }
     if (a.alpha != 0.0) {
@@ -239,10 +344,10 @@ struct Dense {
     for (int it = 0; it < max_iters; ++it) {
       iters = it + 1;
       gemv_rows(vv, nullptr);
-      gb.sync();
+      xsync();
       gather_rows(u);
       gemvT_partial(u);
-      gb.sync();
+      xsync();
       gemvT_finish(w, T(1));
       const double lam_new = sqrt(dsum([&](int k) { const double t = w[k]; return t * t; }));
       if (lam_new == 0.0) { lam = 0.0; conv = 1; break; }
@@ -381,7 +486,7 @@ __device__ void dense_hess_diag(Dense<T>& E, const T* xt, T* d) {
     __syncthreads();
   } else {
     E.gram_partial();
-    E.gb.sync();
+    E.xsync();
     E.gemvT_finish(d, T(2));   // 2.0 * gram_diag
   }
   if (a.alpha != 0.0) {
@@ -496,20 +601,20 @@ __global__ void __launch_bounds__(256) dense_misc_kernel(const __grid_constant__
     case DM_APPLY:
       load(U, a.in0);
       E.gemv_rows(U, nullptr);
-      E.gb.sync();
+      E.xsync();
       E.gather_rows(V);
       store(a.out0, V);
       break;
     case DM_ADJOINT:
       load(U, a.in0);
       E.gemvT_partial(U);
-      E.gb.sync();
+      E.xsync();
       E.gemvT_finish(V, T(1));
       store(a.out0, V);
       break;
     case DM_GRAM:
       E.gram_partial();
-      E.gb.sync();
+      E.xsync();
       E.gemvT_finish(V, T(1));
       store(a.out0, V);
       break;
@@ -544,11 +649,11 @@ __global__ void __launch_bounds__(256) dense_misc_kernel(const __grid_constant__
     case DM_UPPER: {
       load(U, a.in0);
       E.gemv_rows(U, a.ydat);
-      E.gb.sync();
+      E.xsync();
       E.gather_rows(V);
       const double fit = E.npsum([&](int64_t k) { const T t = V[k]; return (double)(t * t); });
       E.gemvT_partial(V);
-      E.gb.sync();
+      E.xsync();
       E.gemvT_finish(W, T(2));
       const double gn = sqrt(E.dsum([&](int k) { const double t = W[k]; return t * t; }));
       if (a.out0) store(a.out0, W);
@@ -566,10 +671,10 @@ __global__ void __launch_bounds__(256) dense_misc_kernel(const __grid_constant__
       load(U, a.in0);   // x~
       load(V, a.in1);   // q
       E.gemv_rows(U, a.ydat);
-      E.gb.sync();
+      E.xsync();
       E.gather_rows(W);  // residual
       E.gemv_rows(V, nullptr);
-      E.gb.sync();
+      E.xsync();
       E.gather_rows(Z);  // B q
       for (int i = E.r0; i < E.r1; ++i)
         for (int j = threadIdx.x; j < n; j += blockDim.x)
@@ -593,11 +698,11 @@ __global__ void __launch_bounds__(256) dense_misc_kernel(const __grid_constant__
       const T step = T(a.pstep), thr = T(a.pthr), c2al2 = T((2.0 * a.alpha) * a.l2);
       for (int it = 0; it < a.piters; ++it) {
         E.gemv_rows(x, a.ydat);
-        E.gb.sync();
+        E.xsync();
         T* r = E.v[4];
         E.gather_rows(r);
         E.gemvT_partial(r);
-        E.gb.sync();
+        E.xsync();
         E.gemvT_finish(V, T(2));
         for (int k = threadIdx.x; k < n; k += blockDim.x) {
           const T g = V[k] + c2al2 * x[k];
@@ -639,6 +744,8 @@ DenseKernelSet dense_kernels_f32() {
 int dense_fail(int code, const char* m);  // adp_host.cu
 
 struct DenseState {
+  int cluster;       // the grid is one thread-block cluster (distributed-shared-memory exchanges)
+  int plen;          // words of the top sum program
   int G, rows_per, b_smem;
   size_t smem;
   void* d_gvec;      // large n: replicated vectors in global memory
@@ -670,7 +777,10 @@ int dense_plan_init(PlanImpl& P) {
   build_sum(S->sn, n, true, pool, false);   // in-CTA program evaluation (signal-length vectors)
   if (S->sn.nSub != 1) return dense_fail(ADP_ERR_UNSUPPORTED, "dense1d signal too long");
   const size_t es = (size_t)P.esize;
+  const int* tw = pool.words.data() + S->sn.top_prog;
+  S->plen = 3 + (tw[2] + 1) + 2 * tw[1];   // nL, nI, nLev, level bounds, left / right children
   size_t base = 64 * sizeof(double) + (size_t)(2 * S->sn.nLeaves + 2) * sizeof(double);
+  base += (size_t)(S->sn.nLeaves + 1) * sizeof(int64_t) + (size_t)S->plen * sizeof(int);
   base = (base + 15) & ~size_t(15);
   const size_t vecs = (size_t)kDenseVecs * (((size_t)n * es + 15) & ~size_t(15));
   const bool gvec = base + vecs > (size_t)optin;   // large n: vectors in global memory instead of smem
@@ -686,6 +796,18 @@ int dense_plan_init(PlanImpl& P) {
   S->smem = base + (S->b_smem ? bslice : 0);
   S->G = G;
   S->rows_per = rows_per;
+  // one thread-block cluster (<= 16 CTAs; > 8 is the non-portable size) when the vectors and the B slice are in
+  // shared memory and the exchange buffers fit next to them; ADP_DENSE_CLUSTER=0: the cooperative grid
+  S->cluster = 0;
+  {
+    const char* ev = getenv("ADP_DENSE_CLUSTER");
+    size_t cs = (S->smem + 15) & ~size_t(15);
+    cs += 2 * (((size_t)n * es + 15) & ~size_t(15)) + 2 * (size_t)G * n * sizeof(double);
+    if (!(ev && atoi(ev) == 0) && G >= 2 && G <= 16 && !gvec && S->b_smem && cs <= (size_t)optin) {
+      S->cluster = 1;
+      S->smem = cs;
+    }
+  }
   DCK(cudaMalloc(&S->d_progs, pool.words.size() * sizeof(int)));
   DCK(cudaMemcpy(S->d_progs, pool.words.data(), pool.words.size() * sizeof(int), cudaMemcpyHostToDevice));
   DCK(cudaMalloc(&S->d_leaf, S->sn.leaf_start.size() * sizeof(int64_t)));
@@ -705,8 +827,31 @@ int dense_plan_init(PlanImpl& P) {
   DenseKernelSet k = P.d.dtype == ADP_DTYPE_F32 ? dense_kernels_f32() : dense_kernels_f64();
   const void* fns[3] = {k.solve, k.cg, k.misc};
   KernelInfo* kis[3] = {&S->ks, &S->kc, &S->km};
+  for (int i = 0; i < 3; ++i) DCK(cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+  for (int i = 0; i < 3 && S->cluster; ++i) {   // can one cluster of G CTAs be scheduled?  else the cooperative grid
+    if (G > 8 && cudaFuncSetAttribute(fns[i], cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess) {
+      (void)cudaGetLastError();
+      S->cluster = 0;
+      break;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = S->smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = G;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nc = 0;
+    if (cudaOccupancyMaxActiveClusters(&nc, fns[i], &cfg) != cudaSuccess || nc < 1) {
+      (void)cudaGetLastError();
+      S->cluster = 0;
+    }
+  }
   for (int i = 0; i < 3; ++i) {
-    DCK(cudaFuncSetAttribute(fns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     int nb = 0;
     DCK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fns[i], 256, S->smem));
     if (nb * P.sm_count < G) return dense_fail(ADP_ERR_UNSUPPORTED, "dense grid not co-resident");
@@ -744,6 +889,8 @@ static DenseArgs<T> dense_base(PlanImpl& P) {
   a.part = S->d_part;
   a.gvec = (T*)S->d_gvec;
   a.vpitch = S->vpitch;
+  a.cluster = S->cluster;
+  a.plen = S->plen;
   a.s_n.nLeaves = S->sn.nLeaves;
   a.s_n.nSub = 1;
   a.s_n.sub_own0 = 0;
@@ -777,8 +924,24 @@ static void dense_set_lower(DenseArgs<T>& a, const adp_lower* lp) {
 template <typename T>
 static int dense_launch(PlanImpl& P, KernelInfo& k, DenseArgs<T>& a, cudaStream_t st) {
   DenseState* S = (DenseState*)P.ws[0];
-  DCK(cudaMemsetAsync(P.d_bar, 0, sizeof(unsigned int), st));
   void* args[] = {&a};
+  if (S->cluster) {   // the whole grid is one cluster: no grid barrier, no counter
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(k.grid);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = S->smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = k.grid;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    DCK(cudaLaunchKernelExC(&cfg, k.fn, args));
+    return ADP_OK;
+  }
+  DCK(cudaMemsetAsync(P.d_bar, 0, sizeof(unsigned int), st));
   DCK(cudaLaunchCooperativeKernel(k.fn, dim3(k.grid), dim3(256), args, S->smem, st));
   return ADP_OK;
 }

@@ -32,6 +32,10 @@ struct DenseArgs {
   T* gvec;                       // non-null: the replicated vectors live in global memory (large n),
                                  //   CTA b's kDenseVecs vectors at gvec + (b * kDenseVecs + k) * vpitch
   int64_t vpitch;
+  int plen;                      // words of the sum program s_n (cached in shared memory with the leaf starts)
+  int cluster;                   // 1: the grid is ONE thread-block cluster (n <= 256: c1): GEMV row results and
+                                 //    B^T partials are exchanged through distributed shared memory and
+                                 //    cluster barriers instead of global memory and the grid barrier
 };
 
 struct DenseKernelSet {
