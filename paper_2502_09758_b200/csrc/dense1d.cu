@@ -74,6 +74,7 @@ struct Dense {
   const T* Bs;      // row slice (smem) or global rows
   T* v[kDenseVecs];
   double* sv;
+  double* sv2;
   double* red;
   int64_t* lstart;  // smem copy of s_n.leaf_start
   int* sprog;       // smem copy of s_n's tree program
@@ -94,6 +95,8 @@ struct Dense {
     red = reinterpret_cast<double*>(smem);
     off += 64 * sizeof(double);
     sv = reinterpret_cast<double*>(smem + off);
+    off += (size_t)(2 * a.s_n.nLeaves + 2) * sizeof(double);
+    sv2 = reinterpret_cast<double*>(smem + off);   // second tree workspace (two sums folded in one pass)
     off += (size_t)(2 * a.s_n.nLeaves + 2) * sizeof(double);
     // the sum's leaf starts and tree program, read on every npsum: cached in shared memory (each sum
     // was a chain of four dependent global loads before)
@@ -138,6 +141,15 @@ struct Dense {
     __syncthreads();
   }
 
+  // split form of xsync(): local work placed between the two runs inside the cluster barrier's latency
+  // (the grid barrier has no split form: it all happens in xwait)
+  __device__ __forceinline__ void xarrive() {
+    if (cl) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  }
+  __device__ __forceinline__ void xwait() {
+    if (cl) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    else gb.sync();
+  }
   // the barrier that ends an exchange (after gemv_rows / gemvT_partial / gram_partial)
   __device__ __forceinline__ void xsync() {
     if (cl) cg::this_cluster().sync();   // arrive.release + wait.acquire: the remote shared-memory stores are visible
@@ -240,6 +252,37 @@ struct Dense {
     __syncthreads();
     return eval_prog(sprog, sv);
   }
+  // two sums in one pass (their leaves on different warps, one barrier, both trees folded level by level
+  // together): each bitwise npsum's value
+  template <class F0, class F1>
+  __device__ void npsum2(const F0& f0, const F1& f1, double& o0, double& o1) {
+    const int nL = a.s_n.nLeaves;
+    const int wpb = blockDim.x >> 5;
+    for (int l = threadIdx.x >> 5; l < 2 * nL; l += wpb) {
+      const int w = l >= nL, ll = l - w * nL;
+      const int64_t st = lstart[ll];
+      const int len = (int)(lstart[ll + 1] - st);
+      const double r = w ? np_leaf_warp32(f1, st, len) : np_leaf_warp32(f0, st, len);
+      if ((threadIdx.x & 31) == 0) (w ? sv2 : sv)[ll] = r;
+    }
+    __syncthreads();
+    const int* prog = sprog;
+    const int nI = prog[1], nLev = prog[2];
+    const int* lev = prog + 3;
+    const int* left = lev + nLev + 1;
+    const int* right = left + nI;
+    for (int lv = 0; lv < nLev; ++lv) {
+      const int b0 = lev[lv], b1 = lev[lv + 1];
+      for (int k = b0 + threadIdx.x; k < b1; k += blockDim.x) {
+        sv[nL + k] = sv[left[k]] + sv[right[k]];
+        sv2[nL + k] = sv2[left[k]] + sv2[right[k]];
+      }
+      __syncthreads();
+    }
+    o0 = nI ? sv[nL + nI - 1] : sv[0];
+    o1 = nI ? sv2[nL + nI - 1] : sv2[0];
+    __syncthreads();
+  }
   // ddot-type sum (fixed thread-strided order then block tree)
   template <class F>
   __device__ double dsum(const F& f) {
@@ -250,14 +293,17 @@ struct Dense {
 
   // ---- smoothed elastic net pieces (regularizers.py:75-134)
   __device__ double reg_value(const T* x) {
-    const double s1 = npsum([&](int64_t k) { const T t = x[k]; return (double)(t * t); });
-    double val = a.l2 * s1;
     if (a.l1 > 0) {
       const T nu = T(a.nu), nu2 = nu * nu;
-      const double s2 = npsum([&](int64_t k) { const T t = x[k]; return (double)(sqrt(t * t + nu2) - nu); });
+      double s1, s2;
+      npsum2([&](int64_t k) { const T t = x[k]; return (double)(t * t); },
+             [&](int64_t k) { const T t = x[k]; return (double)(sqrt(t * t + nu2) - nu); }, s1, s2);
+      double val = a.l2 * s1;
       val = val + a.l1 * s2;
+      return val;
     }
-    return val;
+    const double s1 = npsum([&](int64_t k) { const T t = x[k]; return (double)(t * t); });
+    return a.l2 * s1;
   }
   // g[k] = g[k] + alpha * grad J(x)[k]
   __device__ void add_reg_grad(T* g, const T* x) {
@@ -278,27 +324,34 @@ struct Dense {
   // value (and optionally gradient) of the lower problem at x (smem).
   // r into v[4]; g into gout (if non-null).  Uses barriers.
   __device__ double value_grad(const T* x, T* gout, bool vg_form) {
-    double val = 0.0;
+    double val = 0.0, rv = 0.0;
+    const bool need_reg = !vg_form || a.alpha != 0.0;
     if (a.reg_only) {
       if (gout) {
         for (int k = threadIdx.x; k < n; k += blockDim.x) gout[k] = T(0);
         __syncthreads();
       }
+      if (need_reg) rv = reg_value(x);
     } else {
+      // the sums that need no remote data run between the arrive and the wait of the exchange barriers
       gemv_rows(x, a.ydat);
-      xsync();
+      xarrive();
+      if (need_reg) rv = reg_value(x);
+      xwait();
       T* r = v[4];
       gather_rows(r);
-      val = npsum([&](int64_t k) { const T t = r[k]; return (double)(t * t); });
       if (gout) {
         gemvT_partial(r);
-        xsync();
+        xarrive();
+        val = npsum([&](int64_t k) { const T t = r[k]; return (double)(t * t); });
+        xwait();
         gemvT_finish(gout, T(2));
+      } else {
+        val = npsum([&](int64_t k) { const T t = r[k]; return (double)(t * t); });
       }
     }
-    if (!vg_form || a.alpha != 0.0) {
-      const double rv = reg_value(x);
-      val = vg_form ? val + a.alpha * rv : val + a.alpha * rv;
+    if (need_reg) {
+      val = val + a.alpha * rv;
       if (gout && a.alpha != 0.0) add_reg_grad(gout, x);
     }
     return val;
@@ -779,7 +832,7 @@ int dense_plan_init(PlanImpl& P) {
   const size_t es = (size_t)P.esize;
   const int* tw = pool.words.data() + S->sn.top_prog;
   S->plen = 3 + (tw[2] + 1) + 2 * tw[1];   // nL, nI, nLev, level bounds, left / right children
-  size_t base = 64 * sizeof(double) + (size_t)(2 * S->sn.nLeaves + 2) * sizeof(double);
+  size_t base = 64 * sizeof(double) + 2 * (size_t)(2 * S->sn.nLeaves + 2) * sizeof(double);
   base += (size_t)(S->sn.nLeaves + 1) * sizeof(int64_t) + (size_t)S->plen * sizeof(int);
   base = (base + 15) & ~size_t(15);
   const size_t vecs = (size_t)kDenseVecs * (((size_t)n * es + 15) & ~size_t(15));
